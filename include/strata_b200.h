@@ -1,0 +1,184 @@
+/* strata_b200.h — C ABI of the B200-native composable-format sparse operator path.
+ *
+ * Drop-in boundary for the reference `strata` kit's hot path (paths relative to
+ * /root/reference/proj).  Every entry point lists the reference interface it replaces.
+ * Conventions:
+ *   - plain pointers and sizes only; no torch / C++ types;
+ *   - device pointers are caller-owned device memory; only handles are freed here;
+ *   - every call returns 0 (STRATA_OK) or the reference ErrKind ordinal + 1
+ *     (include/strata/common.hpp:36-45), or STRATA_ERR_CUDA; strata_last_error() gives
+ *     the message (thread-local), mirroring strata::Error{kind, what()};
+ *   - calls are ordered on the caller's stream (`stream` is a cudaStream_t, may be NULL
+ *     for the legacy default stream); the only host synchronisations are inside the
+ *     *_decompose / *_from_csr planners (to size allocations) and the *_host e2e entry
+ *     points.
+ * There is no CPU fallback: without a visible sm_100 device every compute call fails with
+ * STRATA_ERR_CUDA.
+ */
+#ifndef STRATA_B200_H
+#define STRATA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: ErrKind ordinal + 1 (common.hpp:36-45) ------------------------- */
+enum {
+  STRATA_OK = 0,
+  STRATA_ERR_VALIDATION = 1,
+  STRATA_ERR_SCHEDULE = 2,
+  STRATA_ERR_LOWERING = 3,
+  STRATA_ERR_CAPACITY = 4,
+  STRATA_ERR_LOOKUP = 5,
+  STRATA_ERR_USAGE = 6,
+  STRATA_ERR_EXEC = 7,
+  STRATA_ERR_INTERNAL = 8,
+  STRATA_ERR_CUDA = 9 /* no reference analogue: CUDA runtime / device failure */
+};
+
+/* Message of the last failing call on this thread (never NULL). */
+const char* strata_last_error(void);
+/* ABI version (major*10000 + minor*100 + patch). */
+int strata_abi_version(void);
+/* 1 if a device usable by this library (sm_100) is visible, else 0 (sets last error). */
+int strata_device_ok(void);
+
+/* ---- synthetic inputs (host) --------------------------------------------------------
+ * Replaces: CooMatrix generate_matrix(kind, n, m, density, band, block, avg_degree, seed)
+ *           (driver.hpp:84-85, driver.cpp:365-416) followed by build_csr(m) with F32 values
+ *           (storage.cpp:89-124).  Same libstdc++ <random> calls in the same order, so the
+ *           graph is identical to the reference's; emitted directly as CSR.
+ * The returned arrays are owned by the handle (host memory). */
+typedef struct strata_csr_host strata_csr_host;
+int strata_generate_csr(const char* kind, int64_t n, int64_t m, double density, int64_t band,
+                        int64_t block, double avg_degree, uint64_t seed, strata_csr_host** out);
+int strata_csr_host_info(const strata_csr_host* h, int64_t* rows, int64_t* cols, int64_t* nnz);
+const int32_t* strata_csr_host_indptr(const strata_csr_host* h);
+const int32_t* strata_csr_host_indices(const strata_csr_host* h);
+const float* strata_csr_host_values(const strata_csr_host* h);
+int strata_csr_host_destroy(strata_csr_host* h);
+/* Dense operand as the reference tuner/driver seeds it: mt19937(seed), uniform_int(-3,3),
+ * row-major (tune.cpp:108-111, driver.cpp:320-321).  `out` is host float[count]. */
+int strata_dense_int(int64_t count, uint64_t seed, float* out);
+
+/* ---- hyb(c, k) decomposition (device) ------------------------------------------------
+ * Replaces: HybDecomposition decompose_hyb(const TensorStorage& csr, int c, int k,
+ *           const std::string& prefix)          (storage.hpp:131-132, storage.cpp:271-334)
+ *           std::vector<FormatRewriteRule> hyb_rules(csr, c, k, name)
+ *                                               (transform.hpp:102-103, transform.cpp:525-557)
+ * Input CSR (indptr[rows+1], indices[nnz], values[nnz] f32) is DEVICE memory.  The handle
+ * owns the device-resident ELL parts.  Parts are numbered exactly like
+ * HybDecomposition::parts: partition-major, bucket ascending, empty (p,b) omitted. */
+typedef struct strata_hyb strata_hyb;
+int strata_hyb_decompose(const int32_t* indptr, const int32_t* indices, const float* values,
+                         int64_t rows, int64_t cols, int64_t nnz, int c, int k, void* stream,
+                         strata_hyb** out);
+/* hyb_auto_k (storage.hpp:173, storage.cpp:561-565). */
+int strata_hyb_auto_k(int64_t rows, int64_t nnz);
+int strata_hyb_num_parts(const strata_hyb* h, int* nparts);
+/* EllBucketPart fields (storage.hpp:84-91) + the ELL storage's nnz / pad_slots. */
+int strata_hyb_part_info(const strata_hyb* h, int part, int* partition, int* bucket,
+                         int64_t* width, int64_t* nrows, int64_t* nnz, int64_t* pad_slots,
+                         int64_t* col_lo, int64_t* col_hi);
+/* Bit-exact readback of one part's arrays into HOST buffers, by the reference's layout:
+ * I_indptr[2] = {0, nrows}; I_indices[nrows]; J_indices[nrows*width]; values[nrows*width]
+ * (build_ell_bucket, storage.cpp:229-269).  Any pointer may be NULL to skip it. */
+int strata_hyb_part_read(const strata_hyb* h, int part, int32_t* I_indptr, int32_t* I_indices,
+                         int32_t* J_indices, float* values);
+/* Device views of one part (owned by the handle; valid until destroy). */
+int strata_hyb_part_device(const strata_hyb* h, int part, const int32_t** I_indices,
+                           const int32_t** J_indices, const float** values);
+/* HybDecomposition::padding_ratio (storage.cpp:332, :559). */
+int strata_hyb_padding_ratio(const strata_hyb* h, double* ratio);
+int strata_hyb_dims(const strata_hyb* h, int64_t* rows, int64_t* cols, int* c, int* k);
+int strata_hyb_destroy(strata_hyb* h);
+/* SpMM schedule of this decomposition: ELL slots, virtual-warp chunks, split runs crossing
+ * chunk boundaries, rows with no entry, and how many kernels one strata_spmm_hyb_f32 call
+ * launches (used by bench.py to report gpu_launches). */
+int strata_hyb_schedule_info(const strata_hyb* h, int64_t* slots, int64_t* chunks,
+                             int64_t* crossing_runs, int64_t* empty_rows, int* launches_per_spmm);
+
+/* ---- hyb SpMM (device) ---------------------------------------------------------------
+ * Replaces: Pipeline::run_dense() / interpret(stage3, bindings) for
+ *           build_matrix_pipeline(KernelOp::SpMM, m, d, F32, "hyb:c=..,k=..")
+ *           (driver.cpp:163-217, interp.cpp:564-622; nest = SURVEY Appendix B).
+ * X[cols][d] f32 row-major, Y[rows][d] f32 row-major (overwritten: the reference
+ * zero-initialises outputs, interp.cpp:584-587).  Deterministic: identical bits on every
+ * run.  Exact (bitwise equal to the reference) whenever every partial sum is exactly
+ * representable in f32, e.g. the reference's integer operands; otherwise within
+ * |x-y| <= 1e-5*max(|x|,|y|,1) of the F64 pipeline (driver.cpp:124-144). */
+int strata_spmm_hyb_f32(const strata_hyb* h, const float* X, float* Y, int64_t d, void* stream);
+/* End-to-end form: X and Y are HOST buffers (pinned for full PCIe speed); copies in and out
+ * are inside the call, which returns after Y is on the host. */
+int strata_spmm_hyb_f32_host(const strata_hyb* h, const float* X_host, float* Y_host, int64_t d,
+                             void* stream);
+
+/* ---- CSR SpMM (device, row-split baseline form of the same op) ---------------------
+ * Replaces: build_matrix_pipeline(SpMM, ..., "csr") + interpret. */
+int strata_spmm_csr_f32(const int32_t* indptr, const int32_t* indices, const float* A,
+                        const float* X, float* Y, int64_t rows, int64_t cols, int64_t d,
+                        void* stream);
+
+/* ---- SDDMM (device) -----------------------------------------------------------------
+ * Replaces: build_matrix_pipeline(KernelOp::SDDMM, m, d, F32, "csr") + interpret
+ *           (kernels.cpp:110-136: B[ij] = sum_k A[ij]*X[i,k]*Y[k,j]).
+ * X[rows][d]; Y[d][cols] (the reference's {"K","Jd"} layout, kernels.cpp:122);
+ * B[nnz] positional in CSR order (overwritten). */
+int strata_sddmm_csr_f32(const int32_t* indptr, const int32_t* indices, const float* A,
+                         const float* X, const float* Y, float* B, int64_t rows, int64_t cols,
+                         int64_t nnz, int64_t d, void* stream);
+
+/* ---- BSR (device) ---------------------------------------------------------------------
+ * Replaces: TensorStorage csr_to_bsr(csr, b, prefix) (storage.hpp:117, storage.cpp:138-188)
+ *           and bsr_rule (transform.cpp:466-483).  Dims are padded up to multiples of b
+ *           (driver.cpp:69-78).  Values converted to bf16 for the tensor-core SpMM and kept
+ *           in f32 for bit-exact readback. */
+typedef struct strata_bsr strata_bsr;
+int strata_bsr_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
+                        int64_t rows, int64_t cols, int64_t nnz, int64_t b, void* stream,
+                        strata_bsr** out);
+/* mb = padded_rows/b, nb = padded_cols/b. */
+int strata_bsr_info(const strata_bsr* h, int64_t* mb, int64_t* nb, int64_t* b, int64_t* nblocks,
+                    int64_t* pad_slots);
+/* HOST readback: JO_indptr[mb+1], JO_indices[nblocks], values[nblocks*b*b] (f32). */
+int strata_bsr_read(const strata_bsr* h, int32_t* jo_indptr, int32_t* jo_indices, float* values);
+int strata_bsr_destroy(strata_bsr* h);
+/* BSR SpMM on tcgen05 tensor cores: Y[mb*b][d] (f32, overwritten) = A_bsr(bf16) * X
+ * (X[nb*b][d] bf16 row-major).  Requires b == 32 and d % 16 == 0 (16 <= d <= 256). */
+int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int64_t d,
+                         void* stream);
+
+/* ---- ELL (device) ---------------------------------------------------------------------
+ * Replaces: csr_to_ell(csr, w, prefix) (storage.hpp:124, storage.cpp:190-227).
+ * Output device arrays J_indices[rows*w], values[rows*w] (caller-allocated).  Fails with
+ * STRATA_ERR_CAPACITY (message names the row, like the reference) when a row exceeds w. */
+int strata_ell_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
+                        int64_t rows, int64_t cols, int64_t w, int32_t* J_indices,
+                        float* ell_values, void* stream);
+
+/* ---- RGMS / RGCN (device) -----------------------------------------------------------
+ * Replaces: build_rgms_pipeline(relations, d_in, d_out, F32, "hyb"/"csr") + interpret
+ *           (driver.cpp:241-314, kernels.cpp:138-167):
+ *           Y[i,l] = sum_r sum_j A[r,i,j] * sum_k X[j,k] * W[r,k,l].
+ * The relation-major edge list is the RelSparse layout (kernels.cpp:19-62) flattened:
+ * rel_ptr[R+1] (edges of relation r are [rel_ptr[r], rel_ptr[r+1])), dst[nnz] (row i),
+ * src[nnz] (col j), A[nnz] f32.  X[n][d_in] bf16, W[R][d_in][d_out] bf16, Y[m][d_out] f32
+ * (overwritten).  Per-relation gather -> tcgen05 GEMM (W_r in smem) -> scatter.
+ * Requires d_in % 16 == 0, d_in <= 64, d_out % 16 == 0, d_out <= 256. */
+int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, const int32_t* src,
+                     const float* A, int64_t R, int64_t m, int64_t n, int64_t nnz,
+                     const void* X_bf16, const void* W_bf16, float* Y, int64_t d_in,
+                     int64_t d_out, void* stream);
+
+/* ---- multi-GPU helpers (host logic, no device work) -----------------------------------
+ * Row-partition into `parts` contiguous row ranges balanced by nnz: cut p is the first row
+ * r with indptr[r] >= nnz*p/parts (binary search on the HOST indptr).  bounds[parts+1]. */
+int strata_partition_rows(const int32_t* indptr_host, int64_t rows, int parts, int64_t* bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STRATA_B200_H */

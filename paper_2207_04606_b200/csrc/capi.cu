@@ -1,0 +1,336 @@
+// capi.cu — the extern "C" boundary (include/strata_b200.h).
+//
+// Error behaviour mirrors the reference: strata::Error{ErrKind, msg} (common.hpp:36-53)
+// becomes "return ErrKind ordinal + 1" plus a thread-local message; CUDA failures are
+// STRATA_ERR_CUDA.  No entry point has a CPU fallback.
+#include <algorithm>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "capi_internal.h"
+
+using namespace strata_b200;
+
+struct strata_csr_host : CsrHost {};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return STRATA_OK;
+  } catch (const ApiError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return STRATA_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return STRATA_ERR_INTERNAL;
+  }
+}
+
+void require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw ApiError(code, msg);
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// The kernels are compiled for sm_100a only; fail loudly anywhere else.
+void require_device() {
+  int dev = 0;
+  STRATA_CUDA_CHECK(cudaGetDevice(&dev));
+  int major = 0, minor = 0;
+  STRATA_CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  STRATA_CUDA_CHECK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (major != 10 || minor != 0)
+    throw ApiError(STRATA_ERR_CUDA, "strata_b200 kernels are built for sm_100a; device is sm_" +
+                                        std::to_string(major * 10 + minor));
+}
+
+const strata_hyb_impl& hyb_of(const strata_hyb* h) {
+  require(h != nullptr, STRATA_ERR_USAGE, "null hyb handle");
+  return *h;
+}
+
+}  // namespace
+
+namespace strata_b200 {
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+}  // namespace strata_b200
+
+extern "C" {
+
+const char* strata_last_error(void) { return g_last_error.c_str(); }
+
+int strata_abi_version(void) { return 100; }
+
+int strata_device_ok(void) {
+  return guard([] { require_device(); }) == STRATA_OK ? 1 : 0;
+}
+
+// ---- synthetic inputs ----------------------------------------------------------------
+int strata_generate_csr(const char* kind, int64_t n, int64_t m, double density, int64_t band,
+                        int64_t block, double avg_degree, uint64_t seed, strata_csr_host** out) {
+  return guard([&] {
+    require(kind && out, STRATA_ERR_USAGE, "null argument");
+    require(n >= 0 && m >= 0, STRATA_ERR_USAGE, "matrix dims must be >= 0");
+    auto* h = new strata_csr_host();
+    try {
+      generate_csr(kind, n, m, density, band, block, avg_degree, seed, *h);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int strata_csr_host_info(const strata_csr_host* h, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  return guard([&] {
+    require(h, STRATA_ERR_USAGE, "null handle");
+    if (rows) *rows = h->rows;
+    if (cols) *cols = h->cols;
+    if (nnz) *nnz = h->nnz;
+  });
+}
+const int32_t* strata_csr_host_indptr(const strata_csr_host* h) { return h ? h->indptr.data() : nullptr; }
+const int32_t* strata_csr_host_indices(const strata_csr_host* h) { return h ? h->indices.data() : nullptr; }
+const float* strata_csr_host_values(const strata_csr_host* h) { return h ? h->values.data() : nullptr; }
+int strata_csr_host_destroy(strata_csr_host* h) {
+  delete h;
+  return STRATA_OK;
+}
+
+int strata_dense_int(int64_t count, uint64_t seed, float* out) {
+  return guard([&] {
+    require(count >= 0 && (count == 0 || out), STRATA_ERR_USAGE, "bad dense_int arguments");
+    dense_int(count, seed, out);
+  });
+}
+
+// ---- hyb -------------------------------------------------------------------------------
+int strata_hyb_auto_k(int64_t rows, int64_t nnz) {
+  if (rows == 0 || nnz == 0) return 0;  // storage.cpp:561-565
+  int64_t avg = (nnz + rows - 1) / rows;
+  int k = 0;
+  for (int64_t v = 1; v < std::max<int64_t>(1, avg); v <<= 1) ++k;
+  return k;
+}
+
+int strata_hyb_decompose(const int32_t* indptr, const int32_t* indices, const float* values,
+                         int64_t rows, int64_t cols, int64_t nnz, int c, int k, void* stream,
+                         strata_hyb** out) {
+  return guard([&] {
+    require(out != nullptr, STRATA_ERR_USAGE, "null output handle");
+    if (c < 1 || k < 0) throw ApiError(STRATA_ERR_USAGE, "hyb requires c >= 1 and k >= 0");
+    require(k <= 30, STRATA_ERR_USAGE, "hyb requires k <= 30");
+    require(rows >= 0 && cols >= 0 && nnz >= 0, STRATA_ERR_USAGE, "negative dims");
+    require(nnz <= INT32_MAX && rows < INT32_MAX && cols <= INT32_MAX, STRATA_ERR_CAPACITY,
+            "CSR exceeds int32 index range");
+    require(rows == 0 || indptr, STRATA_ERR_USAGE, "null indptr");
+    require(nnz == 0 || (indices && values), STRATA_ERR_USAGE, "null CSR arrays");
+    require_device();
+    auto* h = new strata_hyb();
+    try {
+      STRATA_CUDA_CHECK(cudaGetDevice(&h->device));
+      h->rows = rows;
+      h->cols = cols;
+      h->nnz = nnz;
+      h->c = c;
+      h->k = k;
+      hyb_decompose_device(*h, indptr, indices, values, as_stream(stream));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int strata_hyb_num_parts(const strata_hyb* h, int* nparts) {
+  return guard([&] { *nparts = static_cast<int>(hyb_of(h).parts.size()); });
+}
+
+int strata_hyb_part_info(const strata_hyb* h, int part, int* partition, int* bucket,
+                         int64_t* width, int64_t* nrows, int64_t* nnz, int64_t* pad_slots,
+                         int64_t* col_lo, int64_t* col_hi) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    require(part >= 0 && part < static_cast<int>(H.parts.size()), STRATA_ERR_LOOKUP,
+            "hyb part index out of range");
+    const HybPart& P = H.parts[part];
+    if (partition) *partition = P.partition;
+    if (bucket) *bucket = P.bucket;
+    if (width) *width = P.width;
+    if (nrows) *nrows = P.nrows;
+    if (nnz) *nnz = P.nnz;
+    if (pad_slots) *pad_slots = P.pad_slots;
+    if (col_lo) *col_lo = P.col_lo;
+    if (col_hi) *col_hi = P.col_hi;
+  });
+}
+
+int strata_hyb_part_read(const strata_hyb* h, int part, int32_t* I_indptr, int32_t* I_indices,
+                         int32_t* J_indices, float* values) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    require(part >= 0 && part < static_cast<int>(H.parts.size()), STRATA_ERR_LOOKUP,
+            "hyb part index out of range");
+    const HybPart& P = H.parts[part];
+    if (I_indptr) {
+      I_indptr[0] = 0;
+      I_indptr[1] = static_cast<int32_t>(P.nrows);
+    }
+    if (I_indices)
+      STRATA_CUDA_CHECK(cudaMemcpy(I_indices, H.I.p + P.row_off, sizeof(int32_t) * P.nrows,
+                                   cudaMemcpyDeviceToHost));
+    if (J_indices)
+      STRATA_CUDA_CHECK(cudaMemcpy(J_indices, H.J.p + P.slot_off,
+                                   sizeof(int32_t) * P.nrows * P.width, cudaMemcpyDeviceToHost));
+    if (values)
+      STRATA_CUDA_CHECK(cudaMemcpy(values, H.V.p + P.slot_off, sizeof(float) * P.nrows * P.width,
+                                   cudaMemcpyDeviceToHost));
+  });
+}
+
+int strata_hyb_part_device(const strata_hyb* h, int part, const int32_t** I_indices,
+                           const int32_t** J_indices, const float** values) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    require(part >= 0 && part < static_cast<int>(H.parts.size()), STRATA_ERR_LOOKUP,
+            "hyb part index out of range");
+    const HybPart& P = H.parts[part];
+    if (I_indices) *I_indices = H.I.p + P.row_off;
+    if (J_indices) *J_indices = H.J.p + P.slot_off;
+    if (values) *values = H.V.p + P.slot_off;
+  });
+}
+
+int strata_hyb_padding_ratio(const strata_hyb* h, double* ratio) {
+  return guard([&] { *ratio = hyb_of(h).padding_ratio; });
+}
+
+int strata_hyb_dims(const strata_hyb* h, int64_t* rows, int64_t* cols, int* c, int* k) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    if (rows) *rows = H.rows;
+    if (cols) *cols = H.cols;
+    if (c) *c = H.c;
+    if (k) *k = H.k;
+  });
+}
+
+int strata_hyb_schedule_info(const strata_hyb* h, int64_t* slots, int64_t* chunks,
+                             int64_t* crossing_runs, int64_t* empty_rows, int* launches_per_spmm) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    int64_t sl = 0, ch = 0, ru = 0;
+    int partitions = 0, prev = -1;
+    for (const auto& P : H.parts) {
+      sl += P.nrows * P.width;
+      ch += P.nchunks;
+      ru += P.nruns;
+      if (P.partition != prev) ++partitions;
+      prev = P.partition;
+    }
+    int launches = partitions;  // one spmm_hyb_kernel per column partition
+    for (int p = 0, i = 0; i < static_cast<int>(H.parts.size()); ++p) {
+      bool runs = false;
+      const int part_id = H.parts[i].partition;
+      for (; i < static_cast<int>(H.parts.size()) && H.parts[i].partition == part_id; ++i)
+        runs |= H.parts[i].nruns > 0;
+      launches += runs ? 1 : 0;  // spmm_fixup_kernel
+    }
+    if (H.c == 1 && H.n_empty > 0) launches += 1;  // zero_rows_kernel (c > 1 uses a memset)
+    if (slots) *slots = sl;
+    if (chunks) *chunks = ch;
+    if (crossing_runs) *crossing_runs = ru;
+    if (empty_rows) *empty_rows = H.n_empty;
+    if (launches_per_spmm) *launches_per_spmm = launches;
+  });
+}
+
+int strata_hyb_destroy(strata_hyb* h) {
+  delete h;
+  return STRATA_OK;
+}
+
+// ---- SpMM / SDDMM ----------------------------------------------------------------------
+int strata_spmm_hyb_f32(const strata_hyb* h, const float* X, float* Y, int64_t d, void* stream) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    require(d >= 1, STRATA_ERR_USAGE, "spmm: d must be >= 1");
+    require((H.cols == 0 || X) && (H.rows == 0 || Y), STRATA_ERR_USAGE, "null operand");
+    require_device();
+    spmm_hyb_launch(H, X, Y, d, as_stream(stream));
+  });
+}
+
+int strata_spmm_hyb_f32_host(const strata_hyb* h, const float* X_host, float* Y_host, int64_t d,
+                             void* stream) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    require(d >= 1, STRATA_ERR_USAGE, "spmm: d must be >= 1");
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    const size_t xn = static_cast<size_t>(H.cols) * d, yn = static_cast<size_t>(H.rows) * d;
+    if (H.stage_x.n < xn) H.stage_x.alloc(xn);
+    if (H.stage_y.n < yn) H.stage_y.alloc(yn);
+    if (xn) STRATA_CUDA_CHECK(cudaMemcpyAsync(H.stage_x.p, X_host, xn * 4, cudaMemcpyHostToDevice, s));
+    spmm_hyb_launch(H, H.stage_x.p, H.stage_y.p, d, s);
+    if (yn) STRATA_CUDA_CHECK(cudaMemcpyAsync(Y_host, H.stage_y.p, yn * 4, cudaMemcpyDeviceToHost, s));
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int strata_spmm_csr_f32(const int32_t* indptr, const int32_t* indices, const float* A,
+                        const float* X, float* Y, int64_t rows, int64_t cols, int64_t d,
+                        void* stream) {
+  return guard([&] {
+    (void)cols;
+    require(d >= 1, STRATA_ERR_USAGE, "spmm: d must be >= 1");
+    require_device();
+    spmm_csr_launch(indptr, indices, A, X, Y, rows, d, as_stream(stream));
+  });
+}
+
+int strata_sddmm_csr_f32(const int32_t* indptr, const int32_t* indices, const float* A,
+                         const float* X, const float* Y, float* B, int64_t rows, int64_t cols,
+                         int64_t nnz, int64_t d, void* stream) {
+  return guard([&] {
+    require(d >= 1, STRATA_ERR_USAGE, "sddmm: d must be >= 1");
+    require(nnz <= INT32_MAX, STRATA_ERR_CAPACITY, "nnz exceeds int32 index range");
+    require_device();
+    sddmm_csr_launch(indptr, indices, A, X, Y, B, rows, cols, nnz, d, as_stream(stream));
+  });
+}
+
+// ---- multi-GPU host helper ---------------------------------------------------------------
+int strata_partition_rows(const int32_t* indptr_host, int64_t rows, int parts, int64_t* bounds) {
+  return guard([&] {
+    require(parts >= 1 && bounds && (rows == 0 || indptr_host), STRATA_ERR_USAGE,
+            "bad partition arguments");
+    const int64_t nnz = rows > 0 ? indptr_host[rows] : 0;
+    bounds[0] = 0;
+    for (int p = 1; p < parts; ++p) {
+      const int64_t target = (nnz * p) / parts;  // first row r with indptr[r] >= target
+      const int32_t* it = std::lower_bound(indptr_host, indptr_host + rows + 1, target,
+                                           [](int32_t a, int64_t v) { return a < v; });
+      bounds[p] = std::max<int64_t>(bounds[p - 1], std::min<int64_t>(rows, it - indptr_host));
+    }
+    bounds[parts] = rows;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// capi_internal.h — host-side internals shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/strata_b200.h"
+
+namespace strata_b200 {
+
+// Mirrors strata::Error{ErrKind, msg} (common.hpp:47-53); `code` is the ErrKind ordinal + 1.
+struct ApiError : std::runtime_error {
+  ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+  int code;
+};
+
+#define STRATA_CUDA_CHECK(expr)                                                          \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::strata_b200::ApiError(STRATA_ERR_CUDA, std::string(#expr) + ": " +         \
+                                                         cudaGetErrorString(e_));        \
+  } while (0)
+
+struct CsrHost {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  std::vector<int32_t> indptr, indices;
+  std::vector<float> values;
+};
+
+void generate_csr(const std::string& kind, int64_t n, int64_t m, double density, int64_t band,
+                  int64_t block, double avg_degree, uint64_t seed, CsrHost& out);
+void dense_int(int64_t count, uint64_t seed, float* out);
+
+// RAII device buffer (stream-ordered free is not needed: handles are destroyed by the
+// caller after its stream work completes, as with the reference's value semantics).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    reset();
+    p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  void alloc(size_t count) {
+    reset();
+    n = count;
+    if (count) STRATA_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { reset(); }
+};
+
+// One non-empty (partition, bucket) ELL part — EllBucketPart (storage.hpp:84-91).
+struct HybPart {
+  int partition = 0, bucket = 0;
+  int64_t width = 1, nrows = 0, nnz = 0, pad_slots = 0, col_lo = 0, col_hi = 0;
+  int64_t row_off = 0;   // into the concatenated I_indices
+  int64_t slot_off = 0;  // into the concatenated J_indices / values
+  // SpMM schedule: rows per chunk (power of two) and the crossing-run list for the split part
+  int rpc_log2 = 0;
+  int64_t nchunks = 0;
+  bool may_split = false;
+  int64_t nruns = 0;     // split runs that cross chunk boundaries
+  int64_t run_off = 0;   // into run_start / run_end
+  int64_t carry_off = 0; // in chunks, into the carry buffer
+};
+
+// Device-resident hyb decomposition.  Layout in HBM: all parts concatenated
+// in part order — one I array (int32), one J array (int32) and one value array (f32) — so the
+// whole decomposition is three allocations and one SpMM launch covers every part.
+struct strata_hyb_impl {
+  int device = 0;
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int c = 1, k = 0;
+  double padding_ratio = 0.0;
+  std::vector<HybPart> parts;
+  DevBuf<int32_t> I, J;
+  DevBuf<float> V;
+  DevBuf<int32_t> empty_rows;  // rows with no stored entry (zeroed by SpMM when c == 1)
+  int64_t n_empty = 0;
+  DevBuf<long long> run_start, run_end;  // per crossing run: first / last chunk (part-local)
+  int64_t total_chunks_carry = 0;      // chunks of split parts (carry buffer rows)
+  mutable DevBuf<float> carry;         // [total_chunks_carry][2][d] scratch, grown on demand
+  mutable int64_t carry_d = 0;
+  mutable DevBuf<float> stage_x, stage_y;  // e2e staging
+};
+
+// Kernel launchers (defined in .cu files).
+void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32_t* indices,
+                          const float* values, cudaStream_t s);
+void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t d,
+                     cudaStream_t s);
+void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,
+                     const float* X, float* Y, int64_t rows, int64_t d, cudaStream_t s);
+void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,
+                      const float* X, const float* Y, float* B, int64_t rows, int64_t cols,
+                      int64_t nnz, int64_t d, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace strata_b200
+
+struct strata_hyb : strata_b200::strata_hyb_impl {};

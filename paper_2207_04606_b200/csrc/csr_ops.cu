@@ -1,0 +1,244 @@
+// csr_ops.cu — CSR SDDMM (the reference's fused nest) and the row-split CSR SpMM baseline.
+//
+// SDDMM (kernels.cpp:110-136, fused by sparse_fuse at :135; stage-III nest in SURVEY
+// Appendix B):  B[ij] = sum_k A[ij] * X[i*d + k] * Y[k*n + J[ij]]   with Y stored [d][n].
+//
+// Design:
+//  * Y's [d][n] layout makes the per-non-zero operand a strided column; it is transposed once
+//    per call into a row-major Yt[n][d] workspace (d*n*8 bytes of traffic, tiny next to the
+//    nnz*d gathers) so every gather is one coalesced 128-bit access per lane;
+//  * work is split by non-zeros, not rows (power-law rows range over 4+ orders of magnitude):
+//    each virtual warp (L = d/4 lanes) takes a fixed 256-non-zero chunk, finds its first row
+//    with one binary search on indptr (the reference does one per non-zero, lower.cpp:375-402),
+//    and walks rows forward;
+//  * per group of L non-zeros each lane forms partial dot products over its 4 features, then
+//    a butterfly reduce-scatter (L-1 shuffles for L results, PAPER.md:442's two-stage
+//    reduction) leaves non-zero t's full dot product in lane t, which scales by A and stores
+//    B coalesced.
+#include <algorithm>
+
+#include "capi_internal.h"
+#include "common.cuh"
+
+namespace strata_b200 {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kNnzPerChunk = 256;
+
+__global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                 long long rows, long long cols) {
+  // in[rows][cols] -> out[cols][rows]
+  __shared__ float tile[32][33];
+  const long long c0 = static_cast<long long>(blockIdx.x) * 32, r0 = static_cast<long long>(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const long long r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = __ldcs(in + r * cols + c);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const long long c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+template <int L>
+__device__ __forceinline__ float reduce_scatter(float (&v)[L], int lane, unsigned mask) {
+#pragma unroll
+  for (int w = L / 2; w >= 1; w >>= 1) {
+    const bool hi = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = hi ? v[i] : v[i + w];
+      const float keep = hi ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(mask, send, w, L);
+    }
+  }
+  return v[0];
+}
+
+template <int L>
+__global__ void __launch_bounds__(kBlock)
+sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+             const float* __restrict__ A, const float* __restrict__ X,
+             const float* __restrict__ Yt, float* __restrict__ B, long long rows, long long nnz,
+             long long d) {
+  constexpr int U = 8;
+  const int wl = threadIdx.x & 31;
+  const int lane = threadIdx.x & (L - 1);
+  const int vbase = wl & ~(L - 1);
+  const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << vbase);
+  const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
+  const long long e0 = vw * kNnzPerChunk;
+  if (e0 >= nnz) return;
+  const long long e1 = llmin(e0 + kNnzPerChunk, nnz);
+
+  // Row of e0: last row r with indptr[r] <= e0 (the reference's LocateSegment, once per chunk).
+  long long lo = 0, hi = rows;
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) >> 1;
+    if (__ldg(indptr + mid) <= e0) lo = mid; else hi = mid - 1;
+  }
+  long long row = lo;  // walks forward with the group
+  long long xrow = -1;
+  float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  for (long long g = e0; g < e1; g += L) {
+    const long long e = g + lane;
+    const bool in = e < e1;
+    const int32_t col = in ? ld_stream(indices + e) : 0;
+    const float av = in ? ld_stream(A + e) : 0.f;
+    // Row of each lane's non-zero (skips empty rows).
+    long long my_row = row;
+    if (in) while (__ldg(indptr + my_row + 1) <= e) ++my_row;
+    float part[L];
+#pragma unroll
+    for (int u0 = 0; u0 < L; u0 += U) {
+      float4 yv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t cu = __shfl_sync(vmask, col, u0 + u, L);
+        yv[u] = (g + u0 + u < e1) ? ld_gather4(reinterpret_cast<const float4*>(Yt + static_cast<long long>(cu) * d) + lane)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long ru = __shfl_sync(vmask, my_row, u0 + u, L);
+        if (g + u0 + u < e1 && ru != xrow) {
+          x = ld_gather4(reinterpret_cast<const float4*>(X + ru * d) + lane);
+          xrow = ru;
+        }
+        part[u0 + u] = x.x * yv[u].x + x.y * yv[u].y + x.z * yv[u].z + x.w * yv[u].w;
+      }
+    }
+    row = __shfl_sync(vmask, my_row, L - 1, L);
+    const float dot = reduce_scatter<L>(part, lane, vmask);
+    if (in) st_stream(B + e, av * dot);
+  }
+}
+
+// Fallback for feature sizes the vectorised kernel does not cover: one thread per non-zero.
+__global__ void sddmm_scalar_kernel(const int32_t* __restrict__ indptr,
+                                    const int32_t* __restrict__ indices,
+                                    const float* __restrict__ A, const float* __restrict__ X,
+                                    const float* __restrict__ Yt, float* __restrict__ B,
+                                    long long rows, long long nnz, long long d) {
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long lo = 0, hi = rows;
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) >> 1;
+      if (indptr[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const float* x = X + lo * d;
+    const float* y = Yt + static_cast<long long>(indices[e]) * d;
+    float s = 0.f;
+    for (long long k = 0; k < d; ++k) s = fmaf(x[k], y[k], s);
+    B[e] = A[e] * s;
+  }
+}
+
+// Row-split CSR SpMM: one virtual warp per row (the "csr" format of the reference pipeline).
+template <int L>
+__global__ void __launch_bounds__(kBlock)
+spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                const float* __restrict__ A, const float* __restrict__ X, float* __restrict__ Y,
+                long long rows, long long d) {
+  constexpr int U = 8;
+  const int wl = threadIdx.x & 31;
+  const int lane = threadIdx.x & (L - 1);
+  const int vbase = wl & ~(L - 1);
+  const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << vbase);
+  const long long r = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
+  if (r >= rows) return;
+  const long long q0 = __ldg(indptr + r), q1 = __ldg(indptr + r + 1);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long g = q0; g < q1; g += L) {
+    const long long q = g + lane;
+    const int32_t col = q < q1 ? ld_stream(indices + q) : 0;
+    const float val = q < q1 ? ld_stream(A + q) : 0.f;
+    const int n = static_cast<int>(llmin(L, q1 - g));
+    for (int u0 = 0; u0 < n; u0 += U) {
+      float4 xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t cu = __shfl_sync(vmask, col, (u0 + u) & (L - 1), L);
+        if (u0 + u < n) xv[u] = ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(cu) * d) + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float vu = __shfl_sync(vmask, val, (u0 + u) & (L - 1), L);
+        if (u0 + u < n) fma4(acc, vu, xv[u]);
+      }
+    }
+  }
+  st_stream4(reinterpret_cast<float4*>(Y + r * d) + lane, acc);
+}
+
+__global__ void spmm_csr_scalar_kernel(const int32_t* __restrict__ indptr,
+                                       const int32_t* __restrict__ indices,
+                                       const float* __restrict__ A, const float* __restrict__ X,
+                                       float* __restrict__ Y, long long rows, long long d) {
+  const long long r = blockIdx.x;
+  if (r >= rows) return;
+  for (long long f = threadIdx.x; f < d; f += blockDim.x) {
+    float acc = 0.f;
+    for (long long q = indptr[r]; q < indptr[r + 1]; ++q)
+      acc = fmaf(A[q], X[static_cast<long long>(indices[q]) * d + f], acc);
+    Y[r * d + f] = acc;
+  }
+}
+
+}  // namespace
+
+void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,
+                      const float* X, const float* Y, float* B, int64_t rows, int64_t cols,
+                      int64_t nnz, int64_t d, cudaStream_t s) {
+  if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "sddmm: d must be >= 1");
+  if (nnz == 0) return;
+  float* Yt = nullptr;
+  STRATA_CUDA_CHECK(cudaMallocAsync(&Yt, sizeof(float) * cols * d, s));
+  {
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((d + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(Y, Yt, d, cols);
+    STRATA_CUDA_CHECK(cudaGetLastError());
+  }
+  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0;
+  const long long chunks = (nnz + kNnzPerChunk - 1) / kNnzPerChunk;
+  auto blocks_for = [&](int L) {
+    return static_cast<unsigned>((chunks * L + kBlock - 1) / kBlock);
+  };
+  if (aligned && d == 32)
+    sddmm_kernel<8><<<blocks_for(8), kBlock, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  else if (aligned && d == 64)
+    sddmm_kernel<16><<<blocks_for(16), kBlock, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  else if (aligned && d == 128)
+    sddmm_kernel<32><<<blocks_for(32), kBlock, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  else {
+    const unsigned blocks = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, 148 * 32));
+    sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  }
+  STRATA_CUDA_CHECK(cudaGetLastError());
+  STRATA_CUDA_CHECK(cudaFreeAsync(Yt, s));
+}
+
+void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,
+                     const float* X, float* Y, int64_t rows, int64_t d, cudaStream_t s) {
+  if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "spmm: d must be >= 1");
+  if (rows == 0) return;
+  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(Y) % 16 == 0;
+  auto blocks_for = [&](int L) { return static_cast<unsigned>((rows * L + kBlock - 1) / kBlock); };
+  if (aligned && d == 32)
+    spmm_csr_kernel<8><<<blocks_for(8), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  else if (aligned && d == 64)
+    spmm_csr_kernel<16><<<blocks_for(16), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  else if (aligned && d == 128)
+    spmm_csr_kernel<32><<<blocks_for(32), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  else
+    spmm_csr_scalar_kernel<<<static_cast<unsigned>(rows), 128, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  STRATA_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace strata_b200

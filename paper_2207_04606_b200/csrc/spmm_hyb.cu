@@ -1,0 +1,369 @@
+// spmm_hyb.cu — hyb SpMM on sm_100a CUDA cores (HBM-bound gather kernel).
+//
+// Computes the reference's decomposed SpMM (kernels.cpp:85-108 through decompose_format,
+// transform.cpp:215-388; stage-III nest in SURVEY Appendix B):
+//   for each part (p, b) in rule order, for each ELL row r, slot s < 2^b, k < d:
+//     Y[I[r]*d + k] += A[r*2^b + s] * X[J[r*2^b + s]*d + k]
+//
+// Design:
+//  * one launch covers every part of a column partition ("horizontal fusion");
+//  * work unit = chunk of ~256 consecutive ELL slots (whole rows) per *virtual warp* (VW) of
+//    L = min(32, d/4) lanes; lane l owns float4 column groups l, l+L, ... of the feature row,
+//    so every gathered X row is one fully coalesced 128-bit access per lane;
+//  * index/value tiles are loaded L slots at a time (coalesced, streaming), pad slots are
+//    detected with the reference's own rule (a slot repeating the previous column of the same
+//    segment, storage.cpp:484/528) and skipped, and up to U real-slot gathers are issued before
+//    any is consumed (U x 16 B in flight per lane) to hide HBM latency;
+//  * each output row is produced by exactly one VW with a plain streaming store, except the
+//    rows that decompose_hyb split into several bucket-k segments (storage.cpp:301-309) and
+//    whose segment run crosses a chunk boundary: those chunks write their partial row to a
+//    carry buffer and spmm_fixup_kernel sums the carries of each run in chunk order with a
+//    fixed-shape tree.  No atomics, so the result is bitwise reproducible run to run.
+//  * c > 1: partitions are launched in order and accumulate (Y zeroed first), which keeps
+//    the reference's per-row accumulation order across partitions (ascending columns).
+#include <algorithm>
+
+#include "capi_internal.h"
+#include "common.cuh"
+
+namespace strata_b200 {
+
+namespace {
+
+constexpr int kMaxParts = 32;
+constexpr int kBlock = 256;
+
+struct SpmmPartDev {
+  long long slot_off, row_off, nrows, chunk_begin, nchunks, carry_off;
+  int b, rpc_log2, may_split, pad_;
+};
+
+struct SpmmArgs {
+  const int32_t* I;
+  const int32_t* J;
+  const float* V;
+  const float* X;
+  float* Y;
+  float* carry;
+  long long d;
+  long long total_chunks;
+  int nparts;
+  int accumulate;
+  SpmmPartDev parts[kMaxParts];
+};
+
+template <int VEC, bool kScalar>
+struct Frag {
+  float4 v[VEC];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+};
+
+// Gather one X row fragment owned by this lane.
+template <int L, int VEC, bool kScalar>
+__device__ __forceinline__ void gather(Frag<VEC, kScalar>& f, const float* __restrict__ X,
+                                       long long col, long long d, int lane, long long feat0) {
+  if constexpr (kScalar) {
+    const long long fi = feat0 + lane;
+    f.v[0].x = fi < d ? ld_gather(X + col * d + fi) : 0.f;
+  } else {
+    const float4* xp = reinterpret_cast<const float4*>(X + col * d) + lane;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) f.v[i] = ld_gather4(xp + i * L);
+  }
+}
+
+template <int VEC, bool kScalar>
+__device__ __forceinline__ void fma_frag(Frag<VEC, kScalar>& acc, float a,
+                                         const Frag<VEC, kScalar>& x) {
+  if constexpr (kScalar) {
+    acc.v[0].x = fmaf(a, x.v[0].x, acc.v[0].x);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) fma4(acc.v[i], a, x.v[i]);
+  }
+}
+
+// Write (or accumulate into) one output row fragment.
+template <int L, int VEC, bool kScalar>
+__device__ __forceinline__ void put_row(float* __restrict__ row, const Frag<VEC, kScalar>& acc,
+                                        long long d, int lane, long long feat0, bool accumulate) {
+  if constexpr (kScalar) {
+    const long long fi = feat0 + lane;
+    if (fi < d) {
+      float v = acc.v[0].x;
+      if (accumulate) v += row[fi];
+      row[fi] = v;
+    }
+  } else {
+    float4* rp = reinterpret_cast<float4*>(row) + lane;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      float4 v = acc.v[i];
+      if (accumulate) v = add4(v, rp[i * L]);
+      st_stream4(rp + i * L, v);
+    }
+  }
+}
+
+template <int L, int VEC, bool kScalar>
+__global__ void __launch_bounds__(kBlock) spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
+  constexpr int U = kScalar ? 8 : (VEC == 1 ? 8 : (VEC == 2 ? 4 : 2));
+  const int wl = threadIdx.x & 31;
+  const int lane = threadIdx.x & (L - 1);
+  const int vbase = wl & ~(L - 1);
+  const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << vbase);
+  const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
+  if (vw >= a.total_chunks) return;
+  const long long feat0 = kScalar ? static_cast<long long>(blockIdx.y) * 32 : 0;
+
+  int pi = 0;
+  while (pi + 1 < a.nparts && vw >= a.parts[pi + 1].chunk_begin) ++pi;
+  const SpmmPartDev& P = a.parts[pi];
+  const int b = P.b;
+  const long long wmask = (1ll << b) - 1;
+  const long long c = vw - P.chunk_begin;
+  const long long r0 = c << P.rpc_log2;
+  const long long r1 = llmin(r0 + (1ll << P.rpc_log2), P.nrows);
+  const int32_t* __restrict__ Ip = a.I + P.row_off;
+  const int32_t* __restrict__ Jp = a.J + P.slot_off;
+  const float* __restrict__ Vp = a.V + P.slot_off;
+  const long long d = a.d;
+  const bool split = P.may_split != 0;
+  bool head_cont = false, tail_cont = false;
+  if (split) {
+    head_cont = c > 0 && __ldg(Ip + r0 - 1) == __ldg(Ip + r0);
+    tail_cont = c + 1 < P.nchunks && __ldg(Ip + r1 - 1) == __ldg(Ip + r1);
+  }
+
+  Frag<VEC, kScalar> acc;
+  acc.zero();
+  long long cur_row = -1;
+  int32_t cur_dest = -1;
+  bool first_group = true;
+
+  auto flush = [&](bool is_final) {
+    float* out;
+    bool accum = a.accumulate != 0;
+    if (split && first_group && head_cont) {
+      out = a.carry + ((P.carry_off + c) * 2 + 0) * d;
+      accum = false;
+    } else if (split && is_final && tail_cont) {
+      out = a.carry + ((P.carry_off + c) * 2 + 1) * d;
+      accum = false;
+    } else {
+      const int32_t dest = split ? cur_dest : __ldg(Ip + cur_row);
+      out = a.Y + static_cast<long long>(dest) * d;
+    }
+    put_row<L, VEC, kScalar>(out, acc, d, lane, feat0, accum);
+    acc.zero();
+    first_group = false;
+  };
+
+  const long long s_end = r1 << b;
+  int32_t last_col = 0;
+  for (long long g = r0 << b; g < s_end; g += L) {
+    const long long t = g + lane;
+    const bool in = t < s_end;
+    int32_t col = 0;
+    float val = 0.f;
+    if (in) {
+      col = ld_stream(Jp + t);
+      val = ld_stream(Vp + t);
+    }
+    int32_t prev = __shfl_up_sync(vmask, col, 1, L);
+    if (lane == 0) prev = last_col;
+    const bool pad = in && (t & wmask) != 0 && col == prev;
+    unsigned real = __ballot_sync(vmask, in && !pad);
+    if constexpr (L < 32) real = (real >> vbase) & ((1u << L) - 1u);
+    last_col = __shfl_sync(vmask, col, L - 1, L);
+
+    while (real) {
+      int sl[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ok[u] = real != 0;
+        sl[u] = ok[u] ? __ffs(real) - 1 : 0;
+        real &= real - 1u;
+      }
+      Frag<VEC, kScalar> xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t cu = __shfl_sync(vmask, col, sl[u], L);
+        if (ok[u]) gather<L, VEC, kScalar>(xv[u], a.X, cu, d, lane, feat0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float vu = __shfl_sync(vmask, val, sl[u], L);
+        if (ok[u]) {
+          const long long row = (g + sl[u]) >> b;
+          if (row != cur_row) {
+            if (split) {
+              const int32_t dest = __ldg(Ip + row);
+              if (cur_row >= 0 && dest != cur_dest) flush(false);
+              cur_dest = dest;
+            } else if (cur_row >= 0) {
+              flush(false);
+            }
+            cur_row = row;
+          }
+          fma_frag(acc, vu, xv[u]);
+        }
+      }
+    }
+  }
+  if (cur_row >= 0) flush(true);
+}
+
+// One CTA per crossing split run: Y[row] (+)= carry_tail[ca] + sum_{ca<c<=cb} carry_head[c].
+// Fixed grouping (G groups of chunks, combined in group order) -> deterministic.
+struct FixPartDev {
+  long long row_off, carry_off, run_off, nruns;
+  int rpc_log2, pad_;
+};
+struct FixArgs {
+  const int32_t* I;
+  const long long* run_start;
+  const long long* run_end;
+  const float* carry;
+  float* Y;
+  long long d;
+  int nparts;
+  int accumulate;
+  FixPartDev parts[kMaxParts];
+};
+
+__global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const __grid_constant__ FixArgs a) {
+  __shared__ float part_sum[kBlock];
+  const long long j = blockIdx.x;
+  int pi = 0;
+  while (pi + 1 < a.nparts && j >= a.parts[pi + 1].run_off) ++pi;
+  const FixPartDev& P = a.parts[pi];
+  const long long ca = a.run_start[j], cb = a.run_end[j];
+  const int32_t row = a.I[P.row_off + ((ca + 1) << P.rpc_log2) - 1];
+  const long long d = a.d;
+  const int dcap = static_cast<int>(llmin(d, kBlock));
+  const int G = kBlock / dcap;
+  const int grp = threadIdx.x / dcap;
+  const int fl = threadIdx.x % dcap;
+  for (long long fb = 0; fb < d; fb += dcap) {
+    const long long f = fb + fl;
+    const bool active = grp < G && f < d;
+    float s = 0.f;
+    if (active)
+      for (long long cc = ca + 1 + grp; cc <= cb; cc += G)
+        s += a.carry[((P.carry_off + cc) * 2 + 0) * d + f];
+    part_sum[threadIdx.x] = s;
+    __syncthreads();
+    if (grp == 0 && f < d) {
+      float tot = a.carry[((P.carry_off + ca) * 2 + 1) * d + f];
+      for (int g = 0; g < G; ++g) tot += part_sum[g * dcap + fl];
+      float* y = a.Y + static_cast<long long>(row) * d + f;
+      *y = a.accumulate ? *y + tot : tot;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void zero_rows_kernel(const int32_t* __restrict__ rows, long long n, float* Y,
+                                 long long d) {
+  const long long total = n * d;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = e / d, f = e - r * d;
+    Y[static_cast<long long>(rows[r]) * d + f] = 0.f;
+  }
+}
+
+template <int L, int VEC, bool kScalar>
+void launch_variant(const SpmmArgs& args, long long total_chunks, long long d, cudaStream_t s) {
+  const long long threads = total_chunks * L;
+  const unsigned blocks = static_cast<unsigned>((threads + kBlock - 1) / kBlock);
+  dim3 grid(blocks, kScalar ? static_cast<unsigned>((d + 31) / 32) : 1u);
+  spmm_hyb_kernel<L, VEC, kScalar><<<grid, kBlock, 0, s>>>(args);
+}
+
+}  // namespace
+
+void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t d,
+                     cudaStream_t s) {
+  if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "spmm: d must be >= 1");
+  const bool aligned = (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+  // Variant: lanes per VW (L) and float4s per lane (VEC).
+  int L = 32, VEC = 1;
+  bool scalar = true;
+  if (aligned) {
+    if (d == 32) { L = 8; scalar = false; }
+    else if (d == 64) { L = 16; scalar = false; }
+    else if (d == 128) { L = 32; scalar = false; }
+    else if (d == 256) { L = 32; VEC = 2; scalar = false; }
+    else if (d == 512) { L = 32; VEC = 4; scalar = false; }
+  }
+
+  if (h.carry_d != d && h.total_chunks_carry > 0) {
+    h.carry.alloc(static_cast<size_t>(h.total_chunks_carry) * 2 * d);
+    h.carry_d = d;
+  }
+  if (h.c > 1 && h.rows > 0)
+    STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * h.rows * d, s));
+  else if (h.n_empty > 0) {
+    const long long total = h.n_empty * d;
+    const unsigned blocks = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 4096));
+    zero_rows_kernel<<<blocks, 256, 0, s>>>(h.empty_rows.p, h.n_empty, Y, d);
+    STRATA_CUDA_CHECK(cudaGetLastError());
+  }
+
+  // One launch (plus one fix-up) per column partition, partitions in order.
+  size_t pi = 0;
+  while (pi < h.parts.size()) {
+    const int part_id = h.parts[pi].partition;
+    SpmmArgs args{};
+    FixArgs fx{};
+    args.I = h.I.p; args.J = h.J.p; args.V = h.V.p; args.X = X; args.Y = Y;
+    args.carry = h.carry.p; args.d = d; args.accumulate = h.c > 1;
+    fx.I = h.I.p; fx.run_start = h.run_start.p; fx.run_end = h.run_end.p; fx.carry = h.carry.p;
+    fx.Y = Y; fx.d = d; fx.accumulate = h.c > 1;
+    long long chunks = 0, runs = 0, run_base = -1;
+    int np = 0, nf = 0;
+    for (; pi < h.parts.size() && h.parts[pi].partition == part_id; ++pi) {
+      const HybPart& P = h.parts[pi];
+      if (np >= kMaxParts) throw ApiError(STRATA_ERR_USAGE, "spmm: too many buckets per partition");
+      SpmmPartDev& q = args.parts[np++];
+      q.slot_off = P.slot_off; q.row_off = P.row_off; q.nrows = P.nrows;
+      q.chunk_begin = chunks; q.nchunks = P.nchunks; q.carry_off = P.carry_off;
+      q.b = P.bucket; q.rpc_log2 = P.rpc_log2; q.may_split = P.may_split;
+      chunks += P.nchunks;
+      if (P.nruns > 0) {
+        if (run_base < 0) run_base = P.run_off;
+        FixPartDev& f = fx.parts[nf++];
+        f.row_off = P.row_off; f.carry_off = P.carry_off; f.run_off = P.run_off - run_base;
+        f.nruns = P.nruns; f.rpc_log2 = P.rpc_log2;
+        runs += P.nruns;
+      }
+    }
+    args.nparts = np;
+    args.total_chunks = chunks;
+    if (chunks > 0) {
+      if (scalar) launch_variant<32, 1, true>(args, chunks, d, s);
+      else if (L == 8) launch_variant<8, 1, false>(args, chunks, d, s);
+      else if (L == 16) launch_variant<16, 1, false>(args, chunks, d, s);
+      else if (VEC == 1) launch_variant<32, 1, false>(args, chunks, d, s);
+      else if (VEC == 2) launch_variant<32, 2, false>(args, chunks, d, s);
+      else launch_variant<32, 4, false>(args, chunks, d, s);
+      STRATA_CUDA_CHECK(cudaGetLastError());
+    }
+    if (runs > 0) {
+      fx.nparts = nf;
+      fx.run_start = h.run_start.p + run_base;
+      fx.run_end = h.run_end.p + run_base;
+      spmm_fixup_kernel<<<static_cast<unsigned>(runs), kBlock, 0, s>>>(fx);
+      STRATA_CUDA_CHECK(cudaGetLastError());
+    }
+  }
+}
+
+}  // namespace strata_b200
