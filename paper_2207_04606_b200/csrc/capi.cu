@@ -245,13 +245,8 @@ int strata_hyb_schedule_info(const strata_hyb* h, int64_t* slots, int64_t* chunk
       prev = P.partition;
     }
     int launches = partitions;  // one spmm_hyb_kernel per column partition
-    for (int p = 0, i = 0; i < static_cast<int>(H.parts.size()); ++p) {
-      bool runs = false;
-      const int part_id = H.parts[i].partition;
-      for (; i < static_cast<int>(H.parts.size()) && H.parts[i].partition == part_id; ++i)
-        runs |= H.parts[i].nruns > 0;
-      launches += runs ? 1 : 0;  // spmm_fixup_kernel
-    }
+    for (const auto& R : H.fix_ranges)  // fix-up level 1 / level 2 per partition
+      launches += (R.tile_end > R.tile_begin ? 1 : 0) + (R.run_end > R.run_begin ? 1 : 0);
     if (H.c == 1 && H.n_empty > 0) launches += 1;  // zero_rows_kernel (c > 1 uses a memset)
     if (slots) *slots = sl;
     if (chunks) *chunks = ch;

@@ -65,6 +65,25 @@ struct DevBuf {
   ~DevBuf() { reset(); }
 };
 
+// Fix-up plan entries (see spmm_hyb.cu).  A crossing run's contributions are, in chunk
+// order, the tail carry of its first chunk and the head carries of the following chunks.
+constexpr int kFixTile = 32;  // contributions summed by one level-1 CTA
+struct FixTile {
+  long long carry0;  // carry row (chunk index incl. carry_off) of contribution 0
+  long long out;     // >= 0: Y row (run fits one tile); < 0: -(level-2 slot + 1)
+  int count;         // contributions in this tile
+  int first_slot;    // carry slot of contribution 0 (1 = tail carry of the run's first chunk)
+};
+struct FixRun {
+  long long l2_first;  // first level-2 slot of this run
+  long long row;       // Y row
+  int ntiles, pad_;
+};
+struct FixRange {
+  int partition;
+  long long tile_begin, tile_end, run_begin, run_end;
+};
+
 // One non-empty (partition, bucket) ELL part — EllBucketPart (storage.hpp:84-91).
 struct HybPart {
   int partition = 0, bucket = 0;
@@ -76,7 +95,6 @@ struct HybPart {
   int64_t nchunks = 0;
   bool may_split = false;
   int64_t nruns = 0;     // split runs that cross chunk boundaries
-  int64_t run_off = 0;   // into run_start / run_end
   int64_t carry_off = 0; // in chunks, into the carry buffer
 };
 
@@ -93,9 +111,15 @@ struct strata_hyb_impl {
   DevBuf<float> V;
   DevBuf<int32_t> empty_rows;  // rows with no stored entry (zeroed by SpMM when c == 1)
   int64_t n_empty = 0;
-  DevBuf<long long> run_start, run_end;  // per crossing run: first / last chunk (part-local)
   int64_t total_chunks_carry = 0;      // chunks of split parts (carry buffer rows)
+  // Fix-up plan for split runs crossing chunk boundaries (two-level fixed-shape tree):
+  // level 1 sums <= kFixTile consecutive carries per tile, level 2 sums a run's tiles.
+  DevBuf<FixTile> fix_tiles;
+  DevBuf<FixRun> fix_runs;
+  std::vector<FixRange> fix_ranges;    // per column partition, in partition order
+  int64_t l2_slots = 0;
   mutable DevBuf<float> carry;         // [total_chunks_carry][2][d] scratch, grown on demand
+  mutable DevBuf<float> carry_l2;      // [l2_slots][d]
   mutable int64_t carry_d = 0;
   mutable DevBuf<float> stage_x, stage_y;  // e2e staging
 };

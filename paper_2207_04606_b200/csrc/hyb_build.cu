@@ -186,7 +186,7 @@ hyb_fill_kernel(const int32_t* __restrict__ indices, const float* __restrict__ v
                 const long long* __restrict__ seg_src, const int32_t* __restrict__ seg_len,
                 int32_t* __restrict__ J, float* __restrict__ V, long long total_slots,
                 const FillPart* __restrict__ parts, int nparts) {
-  __shared__ FillPart sp[64];
+  extern __shared__ FillPart sp[];  // [nparts]
   for (int p = threadIdx.x; p < nparts; p += blockDim.x) sp[p] = parts[p];
   __syncthreads();
   for (long long slot = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -293,7 +293,6 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
     slots += P.nrows * P.width;
     h.parts.push_back(P);
   }
-  if (h.parts.size() > 64) throw ApiError(STRATA_ERR_USAGE, "hyb: more than 64 non-empty parts");
   h.padding_ratio = slots == 0 ? 0.0 : static_cast<double>(pads) / static_cast<double>(slots);
 
   h.I.alloc(total_segs);
@@ -315,7 +314,9 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
     STRATA_CUDA_CHECK(cudaMemcpyAsync(dfp.p, fp.data(), fp.size() * sizeof(FillPart),
                                       cudaMemcpyHostToDevice, s));
     const long long blocks = std::min<long long>((slot_cursor + 255) / 256, 148LL * 64);
-    hyb_fill_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(hyb_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(std::max<size_t>(fp.size() * sizeof(FillPart), 1))));
+    hyb_fill_kernel<<<static_cast<unsigned>(blocks), 256, fp.size() * sizeof(FillPart), s>>>(
         indices, values, seg_src.p, seg_len.p, h.J.p, h.V.p, slot_cursor, dfp.p,
         static_cast<int>(fp.size()));
     STRATA_CUDA_CHECK(cudaGetLastError());
@@ -323,16 +324,20 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
   }
 
   // SpMM schedule.
-  std::vector<long long> all_start, all_end;
-  int64_t carry_chunks = 0;
+  std::vector<FixTile> tiles;
+  std::vector<FixRun> runs;
+  h.fix_ranges.clear();
+  int64_t carry_chunks = 0, l2_slots = 0;
   for (auto& P : h.parts) {
     P.rpc_log2 = std::max(0, 8 - P.bucket);  // kSlotsPerChunk = 256 slots per chunk
     static_assert(kSlotsPerChunk == 256, "rpc rule assumes 256-slot chunks");
     P.nchunks = (P.nrows + (int64_t{1} << P.rpc_log2) - 1) >> P.rpc_log2;
     P.may_split = (P.bucket == k);  // only bucket k may hold several segments of one row
     P.nruns = 0;
-    P.run_off = static_cast<int64_t>(all_start.size());
     P.carry_off = 0;
+    if (h.fix_ranges.empty() || h.fix_ranges.back().partition != P.partition)
+      h.fix_ranges.push_back({P.partition, (long long)tiles.size(), (long long)tiles.size(),
+                              (long long)runs.size(), (long long)runs.size()});
     if (!P.may_split || P.nchunks < 2) continue;
     DevBuf<unsigned char> fs(P.nchunks), fe(P.nchunks);
     cross_flags_kernel<<<static_cast<unsigned>((P.nchunks + 255) / 256), 256, 0, s>>>(
@@ -355,23 +360,45 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
     P.nruns = hn[0];
     P.carry_off = carry_chunks;
     carry_chunks += P.nchunks;
-    if (P.nruns) {
-      std::vector<long long> a(P.nruns), b(P.nruns);
-      STRATA_CUDA_CHECK(cudaMemcpy(a.data(), rs.p, P.nruns * sizeof(long long), cudaMemcpyDeviceToHost));
-      STRATA_CUDA_CHECK(cudaMemcpy(b.data(), re.p, P.nruns * sizeof(long long), cudaMemcpyDeviceToHost));
-      all_start.insert(all_start.end(), a.begin(), a.end());
-      all_end.insert(all_end.end(), b.begin(), b.end());
+    if (!P.nruns) continue;
+    std::vector<long long> a(P.nruns), b(P.nruns);
+    std::vector<int32_t> Ih(P.nrows);
+    STRATA_CUDA_CHECK(cudaMemcpy(a.data(), rs.p, P.nruns * sizeof(long long), cudaMemcpyDeviceToHost));
+    STRATA_CUDA_CHECK(cudaMemcpy(b.data(), re.p, P.nruns * sizeof(long long), cudaMemcpyDeviceToHost));
+    STRATA_CUDA_CHECK(cudaMemcpy(Ih.data(), h.I.p + P.row_off, P.nrows * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost));
+    for (long long j = 0; j < P.nruns; ++j) {
+      // Run j: chunks a[j]..b[j]; contributions in order = tail carry of a[j], then the head
+      // carries of a[j]+1 .. b[j].  Its output row is the last row of chunk a[j].
+      const long long ca = a[j], n = b[j] - a[j] + 1;
+      const long long row = Ih[((ca + 1) << P.rpc_log2) - 1];
+      const long long nt = (n + kFixTile - 1) / kFixTile;
+      for (long long u = 0; u < nt; ++u) {
+        FixTile t;
+        t.carry0 = P.carry_off + ca + u * kFixTile;
+        t.count = static_cast<int>(std::min<long long>(kFixTile, n - u * kFixTile));
+        t.first_slot = u == 0 ? 1 : 0;
+        t.out = nt == 1 ? row : -(l2_slots + u + 1);
+        tiles.push_back(t);
+      }
+      if (nt > 1) {
+        runs.push_back({l2_slots, row, static_cast<int>(nt), 0});
+        l2_slots += nt;
+      }
     }
+    h.fix_ranges.back().tile_end = static_cast<long long>(tiles.size());
+    h.fix_ranges.back().run_end = static_cast<long long>(runs.size());
   }
   h.total_chunks_carry = carry_chunks;
-  h.run_start.alloc(all_start.size());
-  h.run_end.alloc(all_end.size());
-  if (!all_start.empty()) {
-    STRATA_CUDA_CHECK(cudaMemcpy(h.run_start.p, all_start.data(), all_start.size() * sizeof(long long),
+  h.l2_slots = l2_slots;
+  h.fix_tiles.alloc(tiles.size());
+  h.fix_runs.alloc(runs.size());
+  if (!tiles.empty())
+    STRATA_CUDA_CHECK(cudaMemcpy(h.fix_tiles.p, tiles.data(), tiles.size() * sizeof(FixTile),
                                  cudaMemcpyHostToDevice));
-    STRATA_CUDA_CHECK(cudaMemcpy(h.run_end.p, all_end.data(), all_end.size() * sizeof(long long),
+  if (!runs.empty())
+    STRATA_CUDA_CHECK(cudaMemcpy(h.fix_runs.p, runs.data(), runs.size() * sizeof(FixRun),
                                  cudaMemcpyHostToDevice));
-  }
 }
 
 }  // namespace strata_b200

@@ -218,54 +218,77 @@ __global__ void __launch_bounds__(kBlock) spmm_hyb_kernel(const __grid_constant_
   if (cur_row >= 0) flush(true);
 }
 
-// One CTA per crossing split run: Y[row] (+)= carry_tail[ca] + sum_{ca<c<=cb} carry_head[c].
-// Fixed grouping (G groups of chunks, combined in group order) -> deterministic.
-struct FixPartDev {
-  long long row_off, carry_off, run_off, nruns;
-  int rpc_log2, pad_;
-};
-struct FixArgs {
-  const int32_t* I;
-  const long long* run_start;
-  const long long* run_end;
-  const float* carry;
-  float* Y;
-  long long d;
-  int nparts;
-  int accumulate;
-  FixPartDev parts[kMaxParts];
-};
+// Fix-up of split runs that cross chunk boundaries: a deterministic two-level tree.
+//   level 1 (spmm_fixup_tiles_kernel): one CTA per tile of <= kFixTile consecutive carries of
+//     one run; G thread groups take contributions g, g+G, ... (8 loads in flight per thread),
+//     then the groups are combined in group order.  Runs that fit one tile write Y directly.
+//   level 2 (spmm_fixup_runs_kernel): one CTA per longer run sums its tile partials the same
+//     way.  Fixed shapes and orders => bitwise reproducible; no atomics.
+constexpr int kFixBlock = 128;
 
-__global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const __grid_constant__ FixArgs a) {
-  __shared__ float part_sum[kBlock];
-  const long long j = blockIdx.x;
-  int pi = 0;
-  while (pi + 1 < a.nparts && j >= a.parts[pi + 1].run_off) ++pi;
-  const FixPartDev& P = a.parts[pi];
-  const long long ca = a.run_start[j], cb = a.run_end[j];
-  const int32_t row = a.I[P.row_off + ((ca + 1) << P.rpc_log2) - 1];
-  const long long d = a.d;
-  const int dcap = static_cast<int>(llmin(d, kBlock));
-  const int G = kBlock / dcap;
-  const int grp = threadIdx.x / dcap;
-  const int fl = threadIdx.x % dcap;
-  for (long long fb = 0; fb < d; fb += dcap) {
-    const long long f = fb + fl;
-    const bool active = grp < G && f < d;
-    float s = 0.f;
-    if (active)
-      for (long long cc = ca + 1 + grp; cc <= cb; cc += G)
-        s += a.carry[((P.carry_off + cc) * 2 + 0) * d + f];
-    part_sum[threadIdx.x] = s;
+template <int V>  // V = 4: float4 lanes (d % 4 == 0); V = 1: scalar
+__device__ __forceinline__ void fix_reduce(const float* __restrict__ src, long long first_row,
+                                           int count, int first_slot, bool two_slot, float* out,
+                                           long long d, bool accumulate) {
+  __shared__ float4 part[kFixBlock];
+  const long long dv = d / V;
+  const int rt = static_cast<int>(llmin(dv, kFixBlock));  // threads per feature row
+  const int G = kFixBlock / rt;
+  const int g = threadIdx.x / rt;
+  for (long long fb = 0; fb < dv; fb += rt) {
+    const long long f = fb + threadIdx.x % rt;
+    const bool active = g < G && f < dv;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (active) {
+      for (int q0 = g; q0 < count; q0 += 8 * G) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = q0 + u * G;
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < count) {
+            const long long r = two_slot ? (first_row + q) * 2 + (q == 0 ? first_slot : 0)
+                                         : first_row + q;
+            if constexpr (V == 4) v[u] = reinterpret_cast<const float4*>(src + r * d)[f];
+            else v[u].x = src[r * d + f];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = add4(acc, v[u]);
+      }
+    }
+    part[threadIdx.x] = acc;
     __syncthreads();
-    if (grp == 0 && f < d) {
-      float tot = a.carry[((P.carry_off + ca) * 2 + 1) * d + f];
-      for (int g = 0; g < G; ++g) tot += part_sum[g * dcap + fl];
-      float* y = a.Y + static_cast<long long>(row) * d + f;
-      *y = a.accumulate ? *y + tot : tot;
+    if (g == 0 && f < dv) {
+      float4 tot = part[threadIdx.x];
+      for (int gg = 1; gg < G; ++gg) tot = add4(tot, part[gg * rt + threadIdx.x]);
+      if constexpr (V == 4) {
+        float4* o = reinterpret_cast<float4*>(out) + f;
+        if (accumulate) tot = add4(tot, *o);
+        *o = tot;
+      } else {
+        out[f] = accumulate ? out[f] + tot.x : tot.x;
+      }
     }
     __syncthreads();
   }
+}
+
+template <int V>
+__global__ void __launch_bounds__(kFixBlock)
+spmm_fixup_tiles_kernel(const FixTile* __restrict__ tiles, const float* __restrict__ carry,
+                        float* __restrict__ l2, float* __restrict__ Y, long long d, int accumulate) {
+  const FixTile t = tiles[blockIdx.x];
+  float* out = t.out >= 0 ? Y + t.out * d : l2 + (-t.out - 1) * d;
+  fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, out, d, t.out >= 0 && accumulate);
+}
+
+template <int V>
+__global__ void __launch_bounds__(kFixBlock)
+spmm_fixup_runs_kernel(const FixRun* __restrict__ runs, const float* __restrict__ l2,
+                       float* __restrict__ Y, long long d, int accumulate) {
+  const FixRun r = runs[blockIdx.x];
+  fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, Y + r.row * d, d, accumulate != 0);
 }
 
 __global__ void zero_rows_kernel(const int32_t* __restrict__ rows, long long n, float* Y,
@@ -304,8 +327,9 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
     else if (d == 512) { L = 32; VEC = 4; scalar = false; }
   }
 
-  if (h.carry_d != d && h.total_chunks_carry > 0) {
+  if (h.carry_d != d) {
     h.carry.alloc(static_cast<size_t>(h.total_chunks_carry) * 2 * d);
+    h.carry_l2.alloc(static_cast<size_t>(h.l2_slots) * d);
     h.carry_d = d;
   }
   if (h.c > 1 && h.rows > 0)
@@ -317,18 +341,16 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
 
-  // One launch (plus one fix-up) per column partition, partitions in order.
-  size_t pi = 0;
+  // One launch (plus the fix-up pair) per column partition, partitions in order.
+  size_t pi = 0, fr = 0;
+  const bool vec4 = d % 4 == 0;
   while (pi < h.parts.size()) {
     const int part_id = h.parts[pi].partition;
     SpmmArgs args{};
-    FixArgs fx{};
     args.I = h.I.p; args.J = h.J.p; args.V = h.V.p; args.X = X; args.Y = Y;
     args.carry = h.carry.p; args.d = d; args.accumulate = h.c > 1;
-    fx.I = h.I.p; fx.run_start = h.run_start.p; fx.run_end = h.run_end.p; fx.carry = h.carry.p;
-    fx.Y = Y; fx.d = d; fx.accumulate = h.c > 1;
-    long long chunks = 0, runs = 0, run_base = -1;
-    int np = 0, nf = 0;
+    long long chunks = 0;
+    int np = 0;
     for (; pi < h.parts.size() && h.parts[pi].partition == part_id; ++pi) {
       const HybPart& P = h.parts[pi];
       if (np >= kMaxParts) throw ApiError(STRATA_ERR_USAGE, "spmm: too many buckets per partition");
@@ -337,13 +359,6 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
       q.chunk_begin = chunks; q.nchunks = P.nchunks; q.carry_off = P.carry_off;
       q.b = P.bucket; q.rpc_log2 = P.rpc_log2; q.may_split = P.may_split;
       chunks += P.nchunks;
-      if (P.nruns > 0) {
-        if (run_base < 0) run_base = P.run_off;
-        FixPartDev& f = fx.parts[nf++];
-        f.row_off = P.row_off; f.carry_off = P.carry_off; f.run_off = P.run_off - run_base;
-        f.nruns = P.nruns; f.rpc_log2 = P.rpc_log2;
-        runs += P.nruns;
-      }
     }
     args.nparts = np;
     args.total_chunks = chunks;
@@ -356,12 +371,28 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
       else launch_variant<32, 4, false>(args, chunks, d, s);
       STRATA_CUDA_CHECK(cudaGetLastError());
     }
-    if (runs > 0) {
-      fx.nparts = nf;
-      fx.run_start = h.run_start.p + run_base;
-      fx.run_end = h.run_end.p + run_base;
-      spmm_fixup_kernel<<<static_cast<unsigned>(runs), kBlock, 0, s>>>(fx);
-      STRATA_CUDA_CHECK(cudaGetLastError());
+    while (fr < h.fix_ranges.size() && h.fix_ranges[fr].partition < part_id) ++fr;
+    if (fr < h.fix_ranges.size() && h.fix_ranges[fr].partition == part_id) {
+      const FixRange& R = h.fix_ranges[fr];
+      const long long nt = R.tile_end - R.tile_begin, nr = R.run_end - R.run_begin;
+      if (nt > 0) {
+        if (vec4)
+          spmm_fixup_tiles_kernel<4><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
+              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, d, h.c > 1);
+        else
+          spmm_fixup_tiles_kernel<1><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
+              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, d, h.c > 1);
+        STRATA_CUDA_CHECK(cudaGetLastError());
+      }
+      if (nr > 0) {
+        if (vec4)
+          spmm_fixup_runs_kernel<4><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
+              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, d, h.c > 1);
+        else
+          spmm_fixup_runs_kernel<1><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
+              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, d, h.c > 1);
+        STRATA_CUDA_CHECK(cudaGetLastError());
+      }
     }
   }
 }
