@@ -59,6 +59,10 @@ int strata_csr_host_info(const strata_csr_host* h, int64_t* rows, int64_t* cols,
 const int32_t* strata_csr_host_indptr(const strata_csr_host* h);
 const int32_t* strata_csr_host_indices(const strata_csr_host* h);
 const float* strata_csr_host_values(const strata_csr_host* h);
+/* powerlaw only: the generator's triplet order as rows (out[rows]); the reference's COO lists
+ * row out[0]'s entries first, then out[1]'s, ... (driver.cpp:400-411).  Consumers that walk
+ * the triplets, e.g. the RGCN relation split (strata_cli.cpp:70-82), replay it from this. */
+int strata_csr_host_row_order(const strata_csr_host* h, int32_t* out);
 int strata_csr_host_destroy(strata_csr_host* h);
 /* Dense operand as the reference tuner/driver seeds it: mt19937(seed), uniform_int(-3,3),
  * row-major (tune.cpp:108-111, driver.cpp:320-321).  `out` is host float[count]. */

@@ -62,6 +62,7 @@ _sig("strata_csr_host_indptr", vp, vp)
 _sig("strata_csr_host_indices", vp, vp)
 _sig("strata_csr_host_values", vp, vp)
 _sig("strata_csr_host_destroy", C.c_int, vp)
+_sig("strata_csr_host_row_order", C.c_int, vp, vp)
 _sig("strata_dense_int", C.c_int, i64, C.c_uint64, vp)
 _sig("strata_hyb_decompose", C.c_int, vp, vp, vp, i64, i64, i64, C.c_int, C.c_int, vp,
      C.POINTER(vp))
@@ -92,7 +93,8 @@ _sig("strata_partition_rows", C.c_int, vp, i64, C.c_int, vp)
 EXPORTED = [
     "strata_last_error", "strata_abi_version", "strata_device_ok", "strata_generate_csr",
     "strata_csr_host_info", "strata_csr_host_indptr", "strata_csr_host_indices",
-    "strata_csr_host_values", "strata_csr_host_destroy", "strata_dense_int",
+    "strata_csr_host_values", "strata_csr_host_destroy", "strata_csr_host_row_order",
+    "strata_dense_int",
     "strata_hyb_decompose", "strata_hyb_auto_k", "strata_hyb_num_parts", "strata_hyb_part_info",
     "strata_hyb_part_read", "strata_hyb_part_device", "strata_hyb_padding_ratio",
     "strata_hyb_dims", "strata_hyb_destroy", "strata_hyb_schedule_info", "strata_spmm_hyb_f32", "strata_spmm_hyb_f32_host",

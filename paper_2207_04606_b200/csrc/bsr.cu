@@ -1,0 +1,384 @@
+// bsr.cu — device csr_to_bsr and the tcgen05 (UMMA) BSR SpMM.
+//
+// csr_to_bsr (storage.cpp:138-188): per block row the sorted unique block columns, then every
+// CSR entry scattered into its b x b block (row-major inside the block).  Device version:
+// block-column keys -> cub segmented sort per block row (a block row's entries are one
+// contiguous CSR range) -> per-block-row unique count -> scan -> JO_indices -> scatter with a
+// binary search of the block column, exactly like the reference's lower_bound.
+//
+// BSR SpMM (bsr_rule, transform.cpp:466-483; lowered nest in SURVEY Appendix B):
+//   Y[(io*b+ii)*d + f] = sum_jo sum_ji A_bsr[jo][ii][ji] * X[(JO_idx[jo]*b + ji)*d + f]
+// One CTA per block row.  Per block the tensor core computes the transposed product
+//   D[f][ii] += sum_ji X[jb*b + ji][f] * A_blk[ii][ji]
+// i.e. M = d (feature tile of 64 or 128), N = b = 32, K = b = 32 (two K=16 bf16 steps), with the
+// X tile as the MN-major A operand (X rows are feature-contiguous, so no transpose is needed)
+// and the block as the K-major B operand.  Accumulation over the block row stays in TMEM
+// (f32); a 4-stage cp.async ring streams block/X tiles while the MMAs of earlier blocks run,
+// and tcgen05.commit -> mbarrier recycles stages.  Epilogue: tcgen05.ld -> registers -> Y.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cuda_bf16.h>
+
+#include "capi_internal.h"
+#include "common.cuh"
+#include "tc_common.cuh"
+
+using namespace strata_b200;
+
+struct strata_bsr {
+  int device = 0;
+  int64_t rows = 0, cols = 0, nnz = 0, b = 0, mb = 0, nb = 0, nblocks = 0, pad_slots = 0;
+  DevBuf<int32_t> indptr, indices;
+  DevBuf<float> values;           // f32, bit-exact readback
+  DevBuf<__nv_bfloat16> vals_bf;  // tensor-core operand
+};
+
+namespace {
+
+__global__ void block_keys_kernel(const int32_t* __restrict__ indices, long long nnz, int b,
+                                  int32_t* __restrict__ keys) {
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < nnz;
+       q += static_cast<long long>(gridDim.x) * blockDim.x)
+    keys[q] = indices[q] / b;
+}
+
+__global__ void seg_bounds_kernel(const int32_t* __restrict__ indptr, long long rows, int b,
+                                  long long mb, int32_t* __restrict__ beg, int32_t* __restrict__ end) {
+  const long long br = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (br >= mb) return;
+  beg[br] = indptr[min64(br * b, rows)];
+  end[br] = indptr[min64((br + 1) * b, rows)];
+}
+
+// Unique block columns of each block row (keys sorted within the row's segment).
+template <bool kWrite>
+__global__ void __launch_bounds__(256)
+bsr_unique_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ beg,
+                  const int32_t* __restrict__ end, long long* __restrict__ cnt,
+                  const long long* __restrict__ off, int32_t* __restrict__ jo_indices) {
+  using Scan = cub::BlockScan<int, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ long long running;
+  const long long br = blockIdx.x;
+  const long long q0 = beg[br], q1 = end[br];
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  for (long long base = q0; base < q1; base += 256) {
+    const long long q = base + threadIdx.x;
+    const int is_new = q < q1 && (q == q0 || keys[q] != keys[q - 1]);
+    int rank, total;
+    Scan(tmp).ExclusiveSum(is_new, rank, total);
+    if (kWrite && is_new) jo_indices[off[br] + running + rank] = keys[q];
+    __syncthreads();
+    if (threadIdx.x == 0) running += total;
+    __syncthreads();
+  }
+  if (!kWrite && threadIdx.x == 0) cnt[br] = running;
+}
+
+// One warp per CSR row: place each entry in its block (storage.cpp:175-183).
+__global__ void bsr_scatter_kernel(const int32_t* __restrict__ indptr,
+                                   const int32_t* __restrict__ indices,
+                                   const float* __restrict__ values, long long rows, int b,
+                                   const int32_t* __restrict__ jo_indptr,
+                                   const int32_t* __restrict__ jo_indices, float* __restrict__ bv,
+                                   __nv_bfloat16* __restrict__ bvh) {
+  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (i >= rows) return;
+  const long long br = i / b;
+  const int lo0 = jo_indptr[br], hi0 = jo_indptr[br + 1];
+  for (long long q = indptr[i] + lane; q < indptr[i + 1]; q += 32) {
+    const int32_t j = indices[q];
+    const int32_t bc = j / b;
+    int lo = lo0, hi = hi0;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (jo_indices[mid] < bc) lo = mid + 1; else hi = mid;
+    }
+    const long long pos = static_cast<long long>(lo) * b * b + (i % b) * b + (j % b);
+    bv[pos] = values[q];
+    bvh[pos] = __float2bfloat16_rn(values[q]);
+  }
+}
+
+// ---- tensor-core SpMM ---------------------------------------------------------------------
+constexpr int kB = 32;        // block size served by the tensor-core path
+constexpr int kStages = 4;
+constexpr int kThreads = 128;
+
+template <int D>  // feature count, 64 or a multiple of 128 (<= 512)
+__global__ void __launch_bounds__(kThreads)
+bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restrict__ jo_indices,
+                   const __nv_bfloat16* __restrict__ bvals, const __nv_bfloat16* __restrict__ X,
+                   float* __restrict__ Y) {
+  constexpr int kM = D == 64 ? 64 : 128;         // UMMA M (feature tile)
+  constexpr int kTiles = D / kM;                  // feature tiles
+  constexpr int kCols = kTiles * kB < 32 ? 32 : kTiles * kB;  // TMEM columns (pow2 >= 32)
+  constexpr int kAB = kB * kB * 2;                // block bytes (B operand)
+  constexpr int kXB = kB * D * 2;                 // X tile bytes (A operand)
+  constexpr int kStageB = kAB + kXB;
+  constexpr uint32_t kIdesc = tc::make_idesc_bf16(kM, kB, /*A MN-major*/ true, /*B K-major*/ false);
+  static_assert(D == 64 || (D % 128 == 0 && D <= 512), "unsupported feature size");
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[kStages];
+  __shared__ uint32_t tmem_slot;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long br = blockIdx.x;
+  const int q0 = jo_indptr[br], nblk = jo_indptr[br + 1] - q0;
+
+  if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) tc::mbar_init(&mbar[s], 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_slot;
+
+  // Stage loader: block (K-major B operand) and X tile (MN-major A operand), 16 B chunks.
+  auto load_stage = [&](int j, int s) {
+    uint8_t* sa = smem + s * kStageB;  // block
+    uint8_t* sx = sa + kAB;            // X tile
+    const int q = q0 + j;
+    const __nv_bfloat16* gb = bvals + static_cast<long long>(q) * kB * kB;
+    for (int c = tid; c < kB * kB / 8; c += kThreads) {  // chunk c: row ii = c/4, k-group c%4
+      const int ii = c >> 2, kg = c & 3;
+      tc::cp_async16(sa + (ii >> 3) * 512 + kg * 128 + (ii & 7) * 16, gb + ii * kB + kg * 8);
+    }
+    const long long row0 = static_cast<long long>(jo_indices[q]) * kB;
+    for (int c = tid; c < kB * D / 8; c += kThreads) {  // chunk c: X row ji, feature group fg
+      const int ji = c / (D / 8), fg = c % (D / 8);
+      tc::cp_async16(sx + fg * 512 + (ji >> 3) * 128 + (ji & 7) * 16,
+                     X + (row0 + ji) * D + fg * 8);
+    }
+  };
+
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nblk) load_stage(s, s);
+    tc::cp_async_commit();
+  }
+  for (int j = 0; j < nblk; ++j) {
+    const int s = j % kStages;
+    const int jn = j + kStages - 1;
+    if (jn < nblk) {
+      if (j >= 1) tc::mbar_wait(&mbar[(j - 1) % kStages], ((j - 1) / kStages) & 1);
+      load_stage(jn, jn % kStages);
+    }
+    tc::cp_async_commit();
+    tc::cp_async_wait<kStages - 1>();
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+      const uint32_t sa = tc::smem_u32(smem + s * kStageB);
+      const uint32_t sx = sa + kAB;
+#pragma unroll
+      for (int t = 0; t < kTiles; ++t) {
+#pragma unroll
+        for (int kk = 0; kk < kB / 16; ++kk) {
+          // A = X tile (MN-major): feature tile t starts kM/8 feature groups * 512 B later.
+          const uint64_t adesc = tc::make_desc(sx + t * (kM / 8) * 512 + kk * 256, 128, 512);
+          const uint64_t bdesc = tc::make_desc(sa + kk * 256, 128, 512);
+          tc::mma_bf16(tmem + t * kB, adesc, bdesc, kIdesc, j > 0 || kk > 0);
+        }
+      }
+      tc::mma_commit(&mbar[s]);
+    }
+  }
+
+  float* yrow = Y + br * kB * D;
+  if (nblk > 0) {
+    const int jl = nblk - 1;
+    tc::mbar_wait(&mbar[jl % kStages], (jl / kStages) & 1);
+    tc::fence_after_sync();
+#pragma unroll
+    for (int t = 0; t < kTiles; ++t) {
+      uint32_t r[32];
+      tc::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + t * kB, r);
+      tc::tmem_ld_wait();
+      // M = 128: TMEM lane = feature row.  M = 64: rows 16w..16w+15 live in lanes 32w..32w+15.
+      const int f = kM == 128 ? t * 128 + warp * 32 + lane : warp * 16 + lane;
+      if (kM == 128 || lane < 16) {
+#pragma unroll
+        for (int ii = 0; ii < kB; ++ii) yrow[ii * D + f] = __uint_as_float(r[ii]);
+      }
+    }
+  } else {
+    for (int e = tid; e < kB * D; e += kThreads) yrow[e] = 0.f;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<kCols>(tmem);
+}
+
+template <int D>
+void launch_bsr(const strata_bsr& h, const __nv_bfloat16* X, float* Y, cudaStream_t s) {
+  constexpr int smem = kStages * (kB * kB * 2 + kB * D * 2);
+  STRATA_CUDA_CHECK(cudaFuncSetAttribute(bsr_spmm_tc_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  bsr_spmm_tc_kernel<D><<<static_cast<unsigned>(h.mb), kThreads, smem, s>>>(
+      h.indptr.p, h.indices.p, h.vals_bf.p, X, Y);
+  STRATA_CUDA_CHECK(cudaGetLastError());
+}
+
+void require_device_bsr() {
+  int dev = 0, major = 0;
+  STRATA_CUDA_CHECK(cudaGetDevice(&dev));
+  STRATA_CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) throw ApiError(STRATA_ERR_CUDA, "strata_b200 kernels are built for sm_100a");
+}
+
+template <class F>
+int guard_bsr(F&& f) {
+  try {
+    f();
+    return STRATA_OK;
+  } catch (const ApiError& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return STRATA_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int strata_bsr_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
+                        int64_t rows, int64_t cols, int64_t nnz, int64_t b, void* stream,
+                        strata_bsr** out) {
+  return guard_bsr([&] {
+    if (b < 1) throw ApiError(STRATA_ERR_USAGE, "block size must be >= 1");  // storage.cpp:139
+    if (!out) throw ApiError(STRATA_ERR_USAGE, "null output handle");
+    if (nnz > INT32_MAX || rows >= INT32_MAX) throw ApiError(STRATA_ERR_CAPACITY, "CSR exceeds int32");
+    require_device_bsr();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto* h = new strata_bsr();
+    try {
+      STRATA_CUDA_CHECK(cudaGetDevice(&h->device));
+      h->rows = rows; h->cols = cols; h->nnz = nnz; h->b = b;
+      h->mb = (rows + b - 1) / b;
+      h->nb = (cols + b - 1) / b;
+      h->indptr.alloc(h->mb + 1);
+      DevBuf<int32_t> keys(std::max<int64_t>(nnz, 1)), sorted(std::max<int64_t>(nnz, 1));
+      DevBuf<int32_t> beg(std::max<int64_t>(h->mb, 1)), end(std::max<int64_t>(h->mb, 1));
+      DevBuf<long long> cnt(h->mb + 1), off(h->mb + 1);
+      STRATA_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, cnt.n * sizeof(long long), s));
+      if (h->mb > 0) {
+        seg_bounds_kernel<<<static_cast<unsigned>((h->mb + 255) / 256), 256, 0, s>>>(
+            indptr, rows, static_cast<int>(b), h->mb, beg.p, end.p);
+        if (nnz > 0) {
+          block_keys_kernel<<<static_cast<unsigned>(std::min<int64_t>((nnz + 255) / 256, 8192)), 256, 0, s>>>(
+              indices, nnz, static_cast<int>(b), keys.p);
+          size_t tb = 0;
+          cub::DeviceSegmentedSort::SortKeys(nullptr, tb, keys.p, sorted.p, nnz, h->mb, beg.p, end.p, s);
+          DevBuf<unsigned char> tmp(tb);
+          cub::DeviceSegmentedSort::SortKeys(tmp.p, tb, keys.p, sorted.p, nnz, h->mb, beg.p, end.p, s);
+          bsr_unique_kernel<false><<<static_cast<unsigned>(h->mb), 256, 0, s>>>(
+              sorted.p, beg.p, end.p, cnt.p, nullptr, nullptr);
+        }
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, h->mb + 1, s);
+        DevBuf<unsigned char> tmp(tb);
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, h->mb + 1, s);
+        STRATA_CUDA_CHECK(cudaGetLastError());
+      }
+      long long total = 0;
+      if (h->mb > 0)
+        STRATA_CUDA_CHECK(cudaMemcpyAsync(&total, off.p + h->mb, sizeof(long long),
+                                          cudaMemcpyDeviceToHost, s));
+      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (total * b * b > INT32_MAX * 16ll) throw ApiError(STRATA_ERR_CAPACITY, "BSR too large");
+      h->nblocks = total;
+      h->pad_slots = total * b * b - nnz;  // storage.cpp:186
+      // JO_indptr as int32 (reference IntArray)
+      std::vector<long long> hoff(h->mb + 1);
+      if (h->mb > 0)
+        STRATA_CUDA_CHECK(cudaMemcpy(hoff.data(), off.p, (h->mb + 1) * sizeof(long long),
+                                     cudaMemcpyDeviceToHost));
+      std::vector<int32_t> hptr(h->mb + 1, 0);
+      for (int64_t i = 0; i <= h->mb; ++i) hptr[i] = static_cast<int32_t>(hoff[i]);
+      STRATA_CUDA_CHECK(cudaMemcpy(h->indptr.p, hptr.data(), hptr.size() * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice));
+      h->indices.alloc(total);
+      h->values.alloc(total * b * b);
+      h->vals_bf.alloc(total * b * b);
+      if (total > 0) {
+        STRATA_CUDA_CHECK(cudaMemsetAsync(h->values.p, 0, total * b * b * sizeof(float), s));
+        STRATA_CUDA_CHECK(cudaMemsetAsync(h->vals_bf.p, 0, total * b * b * sizeof(__nv_bfloat16), s));
+        bsr_unique_kernel<true><<<static_cast<unsigned>(h->mb), 256, 0, s>>>(
+            sorted.p, beg.p, end.p, nullptr, off.p, h->indices.p);
+        bsr_scatter_kernel<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, s>>>(
+            indptr, indices, values, rows, static_cast<int>(b), h->indptr.p, h->indices.p,
+            h->values.p, h->vals_bf.p);
+        STRATA_CUDA_CHECK(cudaGetLastError());
+      }
+      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int strata_bsr_info(const strata_bsr* h, int64_t* mb, int64_t* nb, int64_t* b, int64_t* nblocks,
+                    int64_t* pad_slots) {
+  return guard_bsr([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null bsr handle");
+    if (mb) *mb = h->mb;
+    if (nb) *nb = h->nb;
+    if (b) *b = h->b;
+    if (nblocks) *nblocks = h->nblocks;
+    if (pad_slots) *pad_slots = h->pad_slots;
+  });
+}
+
+int strata_bsr_read(const strata_bsr* h, int32_t* jo_indptr, int32_t* jo_indices, float* values) {
+  return guard_bsr([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null bsr handle");
+    if (jo_indptr)
+      STRATA_CUDA_CHECK(cudaMemcpy(jo_indptr, h->indptr.p, (h->mb + 1) * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost));
+    if (jo_indices && h->nblocks)
+      STRATA_CUDA_CHECK(cudaMemcpy(jo_indices, h->indices.p, h->nblocks * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost));
+    if (values && h->nblocks)
+      STRATA_CUDA_CHECK(cudaMemcpy(values, h->values.p, h->nblocks * h->b * h->b * sizeof(float),
+                                   cudaMemcpyDeviceToHost));
+  });
+}
+
+int strata_bsr_destroy(strata_bsr* h) {
+  delete h;
+  return STRATA_OK;
+}
+
+int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int64_t d,
+                         void* stream) {
+  return guard_bsr([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null bsr handle");
+    if (h->b != kB) throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: tensor-core path needs b == 32");
+    if (h->mb == 0) return;
+    require_device_bsr();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const auto* X = static_cast<const __nv_bfloat16*>(X_bf16);
+    switch (d) {
+      case 64: launch_bsr<64>(*h, X, Y, s); break;
+      case 128: launch_bsr<128>(*h, X, Y, s); break;
+      case 256: launch_bsr<256>(*h, X, Y, s); break;
+      case 512: launch_bsr<512>(*h, X, Y, s); break;
+      default:
+        throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: d must be 64, 128, 256 or 512");
+    }
+  });
+}
+
+}  // extern "C"

@@ -61,6 +61,8 @@ const strata_hyb_impl& hyb_of(const strata_hyb* h) {
 }  // namespace
 
 namespace strata_b200 {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
 int num_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
@@ -107,6 +109,14 @@ int strata_csr_host_info(const strata_csr_host* h, int64_t* rows, int64_t* cols,
 const int32_t* strata_csr_host_indptr(const strata_csr_host* h) { return h ? h->indptr.data() : nullptr; }
 const int32_t* strata_csr_host_indices(const strata_csr_host* h) { return h ? h->indices.data() : nullptr; }
 const float* strata_csr_host_values(const strata_csr_host* h) { return h ? h->values.data() : nullptr; }
+int strata_csr_host_row_order(const strata_csr_host* h, int32_t* out) {
+  return guard([&] {
+    require(h && out, STRATA_ERR_USAGE, "null argument");
+    require(static_cast<int64_t>(h->row_order.size()) == h->rows, STRATA_ERR_USAGE,
+            "row order is only recorded for the powerlaw generator");
+    std::copy(h->row_order.begin(), h->row_order.end(), out);
+  });
+}
 int strata_csr_host_destroy(strata_csr_host* h) {
   delete h;
   return STRATA_OK;
@@ -308,6 +318,17 @@ int strata_sddmm_csr_f32(const int32_t* indptr, const int32_t* indices, const fl
     require(nnz <= INT32_MAX, STRATA_ERR_CAPACITY, "nnz exceeds int32 index range");
     require_device();
     sddmm_csr_launch(indptr, indices, A, X, Y, B, rows, cols, nnz, d, as_stream(stream));
+  });
+}
+
+int strata_ell_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
+                        int64_t rows, int64_t cols, int64_t w, int32_t* J_indices,
+                        float* ell_values, void* stream) {
+  return guard([&] {
+    require(rows >= 0 && cols >= 0, STRATA_ERR_USAGE, "negative dims");
+    if (w >= 1 && w <= cols && rows > 0) require_device();
+    ell_from_csr_launch(indptr, indices, values, rows, cols, w, J_indices, ell_values,
+                        as_stream(stream));
   });
 }
 

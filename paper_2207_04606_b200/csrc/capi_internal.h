@@ -30,6 +30,9 @@ struct CsrHost {
   int64_t rows = 0, cols = 0, nnz = 0;
   std::vector<int32_t> indptr, indices;
   std::vector<float> values;
+  // powerlaw only: rows in the generator's triplet order (driver.cpp:400-411 emits row
+  // rows[i] for i = 0..n-1), needed to replay consumers that walk the COO triplets.
+  std::vector<int32_t> row_order;
 };
 
 void generate_csr(const std::string& kind, int64_t n, int64_t m, double density, int64_t band,
@@ -135,7 +138,13 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
                       const float* X, const float* Y, float* B, int64_t rows, int64_t cols,
                       int64_t nnz, int64_t d, cudaStream_t s);
 
+void ell_from_csr_launch(const int32_t* indptr, const int32_t* indices, const float* values,
+                         int64_t rows, int64_t cols, int64_t w, int32_t* J, float* V,
+                         cudaStream_t s);
+
 int num_sms();
+// Thread-local message returned by strata_last_error() (shared by every translation unit).
+void set_last_error(const std::string& msg);
 
 }  // namespace strata_b200
 

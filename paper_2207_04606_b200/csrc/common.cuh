@@ -6,8 +6,8 @@
 
 namespace strata_b200 {
 
-__host__ __device__ __forceinline__ long long llmin(long long a, long long b) { return a < b ? a : b; }
-__host__ __device__ __forceinline__ long long llmax(long long a, long long b) { return a > b ? a : b; }
+__host__ __device__ __forceinline__ long long min64(long long a, long long b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ long long max64(long long a, long long b) { return a > b ? a : b; }
 
 // Streaming (evict-first) loads for data touched exactly once: index / value arrays.
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }

@@ -72,7 +72,7 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
   const long long e0 = vw * kNnzPerChunk;
   if (e0 >= nnz) return;
-  const long long e1 = llmin(e0 + kNnzPerChunk, nnz);
+  const long long e1 = min64(e0 + kNnzPerChunk, nnz);
 
   // Row of e0: last row r with indptr[r] <= e0 (the reference's LocateSegment, once per chunk).
   long long lo = 0, hi = rows;
@@ -158,7 +158,7 @@ spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ 
     const long long q = g + lane;
     const int32_t col = q < q1 ? ld_stream(indices + q) : 0;
     const float val = q < q1 ? ld_stream(A + q) : 0.f;
-    const int n = static_cast<int>(llmin(L, q1 - g));
+    const int n = static_cast<int>(min64(L, q1 - g));
     for (int u0 = 0; u0 < n; u0 += U) {
       float4 xv[U];
 #pragma unroll
@@ -238,6 +238,68 @@ void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float*
     spmm_csr_kernel<32><<<blocks_for(32), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
   else
     spmm_csr_scalar_kernel<<<static_cast<unsigned>(rows), 128, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  STRATA_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace strata_b200
+
+// ---- csr_to_ell (storage.cpp:190-227) ---------------------------------------------------
+namespace strata_b200 {
+namespace {
+
+__global__ void ell_capacity_kernel(const int32_t* __restrict__ indptr, long long rows,
+                                    long long w, unsigned long long* __restrict__ first_bad) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    if (indptr[i + 1] - indptr[i] > w) atomicMin(first_bad, static_cast<unsigned long long>(i));
+}
+
+__global__ void ell_fill_kernel(const int32_t* __restrict__ indptr,
+                                const int32_t* __restrict__ indices,
+                                const float* __restrict__ values, long long rows, long long w,
+                                int32_t* __restrict__ J, float* __restrict__ V) {
+  const long long total = rows * w;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = t / w, s = t - i * w;
+    const long long q0 = indptr[i], l = indptr[i + 1] - q0;
+    if (s < l) {
+      J[t] = indices[q0 + s];
+      V[t] = values[q0 + s];
+    } else {  // pad with the row's last real column (0 for an empty row), value 0
+      J[t] = l > 0 ? indices[q0 + l - 1] : 0;
+      V[t] = 0.f;
+    }
+  }
+}
+
+}  // namespace
+
+void ell_from_csr_launch(const int32_t* indptr, const int32_t* indices, const float* values,
+                         int64_t rows, int64_t cols, int64_t w, int32_t* J, float* V,
+                         cudaStream_t s) {
+  if (w < 1) throw ApiError(STRATA_ERR_USAGE, "ELL width must be >= 1");
+  if (w > cols) throw ApiError(STRATA_ERR_USAGE, "ELL width exceeds column count");
+  if (rows == 0) return;
+  unsigned long long* bad = nullptr;
+  STRATA_CUDA_CHECK(cudaMallocAsync(&bad, sizeof(unsigned long long), s));
+  STRATA_CUDA_CHECK(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), s));
+  ell_capacity_kernel<<<static_cast<unsigned>(std::min<long long>((rows + 255) / 256, 4096)), 256, 0, s>>>(
+      indptr, rows, w, bad);
+  unsigned long long hbad = 0;
+  STRATA_CUDA_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, s));
+  STRATA_CUDA_CHECK(cudaFreeAsync(bad, s));
+  STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (hbad != ~0ull) {
+    int32_t ip[2];
+    STRATA_CUDA_CHECK(cudaMemcpy(ip, indptr + hbad, sizeof(ip), cudaMemcpyDeviceToHost));
+    throw ApiError(STRATA_ERR_CAPACITY, "row " + std::to_string(hbad) + " has " +
+                                            std::to_string(ip[1] - ip[0]) +
+                                            " non-zeros, exceeds ELL width " + std::to_string(w));
+  }
+  const long long total = rows * w;
+  ell_fill_kernel<<<static_cast<unsigned>(std::min<long long>((total + 255) / 256, 148 * 64)), 256, 0, s>>>(
+      indptr, indices, values, rows, w, J, V);
   STRATA_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -89,6 +89,7 @@ void generate_csr(const std::string& kind, int64_t n, int64_t m, double density,
     std::vector<int64_t> rows(n);
     for (int64_t i = 0; i < n; ++i) rows[i] = i;
     std::shuffle(rows.begin(), rows.end(), rng);  // :402, first RNG consumer
+    out.row_order.assign(rows.begin(), rows.end());
     double total_edges = avg_degree * double(n);
     std::vector<int64_t> deg(n);
     for (int64_t i = 0; i < n; ++i)

@@ -56,7 +56,7 @@ __device__ __forceinline__ RowPart row_part(const int32_t* __restrict__ indptr,
   int64_t a = indptr[i], b = indptr[i + 1];
   if (c == 1) return {a, b - a};
   int64_t lo = static_cast<int64_t>(p) * part_w;
-  int64_t hi = llmin(cols, lo + part_w);
+  int64_t hi = min64(cols, lo + part_w);
   int64_t q0 = lower_bound_i32(indices, a, b, lo);
   int64_t q1 = lower_bound_i32(indices, q0, b, hi);
   return {q0, q1 - q0};
@@ -144,7 +144,7 @@ hyb_scatter_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict
           for (long long s = 0; s < v; ++s) {
             seg_row[base + s] = static_cast<int32_t>(i);
             seg_src[base + s] = rp.q0 + (s << k);
-            seg_len[base + s] = static_cast<int32_t>(llmin(cap, rp.l - (s << k)));
+            seg_len[base + s] = static_cast<int32_t>(min64(cap, rp.l - (s << k)));
           }
         } else {  // long row: hand it to the whole CTA
           int slot = atomicAdd(&qn, 1);
@@ -159,7 +159,7 @@ hyb_scatter_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict
         for (long long s = threadIdx.x; s < ns; s += kTile) {
           seg_row[q.base + s] = q.row;
           seg_src[q.base + s] = q.q0 + (s << k);
-          seg_len[q.base + s] = static_cast<int32_t>(llmin(cap, q.l - (s << k)));
+          seg_len[q.base + s] = static_cast<int32_t>(min64(cap, q.l - (s << k)));
         }
       }
       __syncthreads();
@@ -213,7 +213,7 @@ hyb_fill_kernel(const int32_t* __restrict__ indices, const float* __restrict__ v
 }
 
 // Chunk c of a split part "crosses" into c+1 when the last row of c and the first row of c+1
-// are segments of the same source row.  A crossing run = maximal sequence of crossing
+// are segments of the same source row.  A crossing run = one source row's chain of crossing
 // boundaries; start = its first chunk, end = its last chunk.
 __global__ void cross_flags_kernel(const int32_t* __restrict__ I, long long nrows, int rpc_log2,
                                    long long nchunks, unsigned char* __restrict__ fstart,
@@ -225,9 +225,13 @@ __global__ void cross_flags_kernel(const int32_t* __restrict__ I, long long nrow
     const long long r = (cc + 1) << rpc_log2;
     return r < nrows && I[r - 1] == I[r];
   };
+  // A run passes *through* chunk c only if c holds a single source row (uniform); a chunk that
+  // ends one split row and starts another is the end of one run and the start of the next.
+  const long long r0 = c << rpc_log2, r1 = min64((c + 1) << rpc_log2, nrows);
+  const bool uniform = I[r0] == I[r1 - 1];
   const bool xc = cross(c), xp = cross(c - 1);
-  fstart[c] = xc && !xp;
-  fend[c] = xp && !xc;
+  fstart[c] = xc && !(xp && uniform);
+  fend[c] = xp && !(xc && uniform);
 }
 
 }  // namespace

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kBlock) spmm_hyb_kernel(const __grid_constant_
   const long long wmask = (1ll << b) - 1;
   const long long c = vw - P.chunk_begin;
   const long long r0 = c << P.rpc_log2;
-  const long long r1 = llmin(r0 + (1ll << P.rpc_log2), P.nrows);
+  const long long r1 = min64(r0 + (1ll << P.rpc_log2), P.nrows);
   const int32_t* __restrict__ Ip = a.I + P.row_off;
   const int32_t* __restrict__ Jp = a.J + P.slot_off;
   const float* __restrict__ Vp = a.V + P.slot_off;
@@ -232,7 +232,7 @@ __device__ __forceinline__ void fix_reduce(const float* __restrict__ src, long l
                                            long long d, bool accumulate) {
   __shared__ float4 part[kFixBlock];
   const long long dv = d / V;
-  const int rt = static_cast<int>(llmin(dv, kFixBlock));  // threads per feature row
+  const int rt = static_cast<int>(min64(dv, kFixBlock));  // threads per feature row
   const int G = kFixBlock / rt;
   const int g = threadIdx.x / rt;
   for (long long fb = 0; fb < dv; fb += rt) {

@@ -58,6 +58,7 @@ class CsrMatrix:
     indptr: np.ndarray   # int32 [rows+1]   aux "J_indptr"
     indices: np.ndarray  # int32 [nnz]      aux "J_indices"
     values: np.ndarray   # float32 [nnz]
+    row_order: np.ndarray = None  # powerlaw generator's triplet row order (see split_relations)
 
     @property
     def nnz(self) -> int:
@@ -107,7 +108,11 @@ def generate_matrix(kind: str, n: int, m: int, density: float = 0.0, band: int =
         if nnz:
             C.memmove(indices.ctypes.data, lib.strata_csr_host_indices(h), indices.nbytes)
             C.memmove(values.ctypes.data, lib.strata_csr_host_values(h), values.nbytes)
-        return CsrMatrix(r.value, c.value, indptr, indices, values)
+        order = None
+        if kind == "powerlaw":
+            order = np.empty(r.value, np.int32)
+            check(lib.strata_csr_host_row_order(h, order.ctypes.data))
+        return CsrMatrix(r.value, c.value, indptr, indices, values, order)
     finally:
         lib.strata_csr_host_destroy(h)
 
@@ -276,3 +281,150 @@ def partition_rows(indptr: np.ndarray, parts: int) -> np.ndarray:
     check(lib.strata_partition_rows(indptr.ctypes.data, indptr.shape[0] - 1, parts,
                                     bounds.ctypes.data))
     return bounds
+
+
+# ---- BSR (storage.hpp:117, storage.cpp:138-188) + tensor-core BSR SpMM ---------------------
+
+class BsrMatrix:
+    """Device-resident BSR storage: JO_indptr / JO_indices / values (f32 + bf16 copy)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        v = [C.c_int64() for _ in range(5)]
+        check(lib.strata_bsr_info(handle, *(C.byref(x) for x in v)))
+        self.mb, self.nb, self.b, self.nblocks, self.pad_slots = (x.value for x in v)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def arrays(self, prefix: str = "bsr_") -> dict:
+        jp = np.empty(self.mb + 1, np.int32)
+        ji = np.empty(max(self.nblocks, 1), np.int32)
+        bv = np.empty(max(self.nblocks * self.b * self.b, 1), np.float32)
+        check(lib.strata_bsr_read(self._h, jp.ctypes.data, ji.ctypes.data, bv.ctypes.data))
+        return {prefix + "JO_indptr": jp, prefix + "JO_indices": ji[:self.nblocks],
+                "values": bv[:self.nblocks * self.b * self.b]}
+
+    def close(self):
+        if self._h:
+            lib.strata_bsr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def csr_to_bsr(csr: DeviceCsr, b: int, stream=None) -> BsrMatrix:
+    h = C.c_void_p()
+    check(lib.strata_bsr_from_csr(_ptr(csr.indptr), _ptr(csr.indices), _ptr(csr.values),
+                                  csr.rows, csr.cols, csr.nnz, b, _stream(stream), C.byref(h)))
+    return BsrMatrix(h)
+
+
+def bsr_spmm(bsr: BsrMatrix, X_bf16, Y=None, stream=None):
+    """Y[mb*b][d] (f32) = A_bsr @ X on tcgen05 tensor cores; X is bf16 [nb*b][d]."""
+    import torch
+    d = X_bf16.shape[1]
+    if Y is None:
+        Y = torch.empty((bsr.mb * bsr.b, d), dtype=torch.float32, device=X_bf16.device)
+    check(lib.strata_bsr_spmm_bf16(bsr.handle, _ptr(X_bf16), _ptr(Y), d, _stream(stream)))
+    return Y
+
+
+# ---- ELL (storage.hpp:124, storage.cpp:190-227) --------------------------------------------
+
+def csr_to_ell(csr: DeviceCsr, w: int, stream=None):
+    """Device ELL arrays (J_indices[rows*w], values[rows*w]); StrataError(kind='Capacity')
+    naming the row when a row exceeds w."""
+    import torch
+    dev = csr.indptr.device
+    J = torch.empty(max(csr.rows * w, 1), dtype=torch.int32, device=dev)
+    V = torch.empty(max(csr.rows * w, 1), dtype=torch.float32, device=dev)
+    check(lib.strata_ell_from_csr(_ptr(csr.indptr), _ptr(csr.indices), _ptr(csr.values),
+                                  csr.rows, csr.cols, w, _ptr(J), _ptr(V), _stream(stream)))
+    return J[:csr.rows * w], V[:csr.rows * w]
+
+
+# ---- RGMS / RGCN (kernels.cpp:138-167, driver.cpp:241-314) ---------------------------------
+
+@dataclass
+class RelSparse:
+    """kernels.hpp RelSparse flattened to relation-major edges: rel_ptr[R+1], dst (row i),
+    src (col j), A.  Built from the reference arrays I_indptr/I_indices/J_indptr/J_indices."""
+    relations: int
+    rows: int
+    cols: int
+    rel_ptr: np.ndarray
+    dst: np.ndarray
+    src: np.ndarray
+    A: np.ndarray
+
+    @staticmethod
+    def from_reference_arrays(R, rows, cols, I_indptr, I_indices, J_indptr, J_indices, A):
+        I_indptr = np.asarray(I_indptr, np.int64)
+        J_indptr = np.asarray(J_indptr, np.int64)
+        rel_ptr = J_indptr[I_indptr].astype(np.int32)          # edges of relation r
+        counts = np.diff(J_indptr)
+        dst = np.repeat(np.asarray(I_indices, np.int32), counts)
+        return RelSparse(R, rows, cols, rel_ptr, dst.astype(np.int32),
+                         np.asarray(J_indices, np.int32), np.asarray(A, np.float32))
+
+    @property
+    def nnz(self) -> int:
+        return int(self.src.shape[0])
+
+    def to_device(self, device="cuda"):
+        import torch
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        return RelSparse(self.relations, self.rows, self.cols, t(self.rel_ptr), t(self.dst),
+                         t(self.src), t(self.A))
+
+
+def rgms(rel: RelSparse, X_bf16, W_bf16, Y=None, stream=None):
+    """Y[m][d_out] (f32) = sum_r A_r @ X @ W_r via per-relation gather -> tcgen05 GEMM -> scatter."""
+    import torch
+    d_in, d_out = int(W_bf16.shape[1]), int(W_bf16.shape[2])
+    if Y is None:
+        Y = torch.empty((rel.rows, d_out), dtype=torch.float32, device=X_bf16.device)
+    check(lib.strata_rgms_bf16(_ptr(rel.rel_ptr), _ptr(rel.dst), _ptr(rel.src), _ptr(rel.A),
+                               rel.relations, rel.rows, rel.cols, rel.nnz, _ptr(X_bf16),
+                               _ptr(W_bf16), _ptr(Y), d_in, d_out, _stream(stream)))
+    return Y
+
+
+def split_relations(m: CsrMatrix, relations: int, seed: int):
+    """strata_cli.cpp:70-82: triplet t (in the generator's triplet order == CSR order here)
+    goes to relation mt19937(seed)() % R.  Returns the RelSparse (kernels.cpp:19-62 layout)."""
+    if m.row_order is None:
+        raise StrataError(6, "split_relations needs the generator's triplet order (powerlaw)")
+    draws = np.empty(m.nnz, np.uint32)
+    _mt19937_stream(seed, draws)
+    # CSR position of the t-th reference triplet: rows in generator order, columns ascending.
+    lens = np.diff(m.indptr).astype(np.int64)
+    ro = m.row_order.astype(np.int64)
+    starts = np.repeat(m.indptr[:-1][ro].astype(np.int64) - np.cumsum(lens[ro]) + lens[ro], lens[ro])
+    csr_pos = starts + np.arange(m.nnz, dtype=np.int64)
+    rel = np.empty(m.nnz, np.int64)
+    rel[csr_pos] = draws % relations
+    rows_of = np.repeat(np.arange(m.rows, dtype=np.int64), lens)
+    order = np.lexsort((m.indices, rows_of, rel))  # relation-major, (row, col) inside
+    rel_sorted = rel[order]
+    rel_ptr = np.searchsorted(rel_sorted, np.arange(relations + 1)).astype(np.int32)
+    return RelSparse(relations, m.rows, m.cols, rel_ptr, rows_of[order].astype(np.int32),
+                     m.indices[order].astype(np.int32), m.values[order].astype(np.float32))
+
+
+def _mt19937_stream(seed: int, out: np.ndarray):
+    """Raw 32-bit outputs of std::mt19937(seed): numpy's MT19937 with the legacy
+    init_genrand seeding produces the identical tempered word sequence."""
+    bg = np.random.MT19937(0)
+    bg._legacy_seeding(seed)
+    out[:] = bg.random_raw(out.size).astype(np.uint32)
+
+
+__all__ += ["BsrMatrix", "csr_to_bsr", "bsr_spmm", "csr_to_ell", "RelSparse", "rgms",
+            "split_relations"]
