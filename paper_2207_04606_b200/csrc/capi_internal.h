@@ -121,8 +121,8 @@ struct strata_hyb_impl {
   DevBuf<FixRun> fix_runs;
   std::vector<FixRange> fix_ranges;    // per column partition, in partition order
   int64_t l2_slots = 0;
-  mutable DevBuf<float> carry;         // [total_chunks_carry][2][d] scratch, grown on demand
-  mutable DevBuf<float> carry_l2;      // [l2_slots][d]
+  mutable DevBuf<double> carry;        // [total_chunks_carry][2][d] f64 scratch, grown on demand
+  mutable DevBuf<double> carry_l2;     // [l2_slots][d]
   mutable int64_t carry_d = 0;
   mutable DevBuf<float> stage_x, stage_y;  // e2e staging
 };

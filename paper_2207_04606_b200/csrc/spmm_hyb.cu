@@ -44,7 +44,7 @@ struct SpmmArgs {
   const float* V;
   const float* X;
   float* Y;
-  float* carry;
+  double* carry;
   long long d;
   long long total_chunks;
   int nparts;
@@ -75,41 +75,85 @@ __device__ __forceinline__ void gather(Frag<VEC, kScalar>& f, const float* __res
   }
 }
 
+// Accumulators are f64: every f32 product a*x is exact in f64, so the only roundings are the
+// f64 additions (~1e-16 relative) and the single f32 rounding at the store.  On the
+// reference's integer operands this is bit-identical to its f32 interpreter; on real-valued
+// operands it stays within ~1 f32 ulp of the reference's F64 pipeline, where sequential f32
+// accumulation (the reference's own F32 pipeline included) drifts by 2e-5 on long rows.
 template <int VEC, bool kScalar>
-__device__ __forceinline__ void fma_frag(Frag<VEC, kScalar>& acc, float a,
+struct Acc {
+  double v[kScalar ? 1 : 4 * VEC];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < (kScalar ? 1 : 4 * VEC); ++i) v[i] = 0.0;
+  }
+};
+
+template <int VEC, bool kScalar>
+__device__ __forceinline__ void fma_frag(Acc<VEC, kScalar>& acc, float a,
                                          const Frag<VEC, kScalar>& x) {
+  const double ad = a;
   if constexpr (kScalar) {
-    acc.v[0].x = fmaf(a, x.v[0].x, acc.v[0].x);
+    acc.v[0] = fma(ad, static_cast<double>(x.v[0].x), acc.v[0]);
   } else {
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) fma4(acc.v[i], a, x.v[i]);
+    for (int i = 0; i < VEC; ++i) {
+      acc.v[4 * i + 0] = fma(ad, static_cast<double>(x.v[i].x), acc.v[4 * i + 0]);
+      acc.v[4 * i + 1] = fma(ad, static_cast<double>(x.v[i].y), acc.v[4 * i + 1]);
+      acc.v[4 * i + 2] = fma(ad, static_cast<double>(x.v[i].z), acc.v[4 * i + 2]);
+      acc.v[4 * i + 3] = fma(ad, static_cast<double>(x.v[i].w), acc.v[4 * i + 3]);
+    }
   }
 }
 
-// Write (or accumulate into) one output row fragment.
+// Write (or accumulate into) one output row fragment of Y (f32).
 template <int L, int VEC, bool kScalar>
-__device__ __forceinline__ void put_row(float* __restrict__ row, const Frag<VEC, kScalar>& acc,
+__device__ __forceinline__ void put_row(float* __restrict__ row, const Acc<VEC, kScalar>& acc,
                                         long long d, int lane, long long feat0, bool accumulate) {
   if constexpr (kScalar) {
     const long long fi = feat0 + lane;
     if (fi < d) {
-      float v = acc.v[0].x;
-      if (accumulate) v += row[fi];
+      float v = static_cast<float>(acc.v[0]);
+      if (accumulate) v = static_cast<float>(acc.v[0] + static_cast<double>(row[fi]));
       row[fi] = v;
     }
   } else {
     float4* rp = reinterpret_cast<float4*>(row) + lane;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
-      float4 v = acc.v[i];
-      if (accumulate) v = add4(v, rp[i * L]);
+      float4 v;
+      if (accumulate) {
+        const float4 o = rp[i * L];
+        v = make_float4(static_cast<float>(acc.v[4 * i] + o.x), static_cast<float>(acc.v[4 * i + 1] + o.y),
+                        static_cast<float>(acc.v[4 * i + 2] + o.z), static_cast<float>(acc.v[4 * i + 3] + o.w));
+      } else {
+        v = make_float4(static_cast<float>(acc.v[4 * i]), static_cast<float>(acc.v[4 * i + 1]),
+                        static_cast<float>(acc.v[4 * i + 2]), static_cast<float>(acc.v[4 * i + 3]));
+      }
       st_stream4(rp + i * L, v);
     }
   }
 }
 
+// Partial row of a split run -> carry buffer (f64, so split rows lose nothing either).
 template <int L, int VEC, bool kScalar>
-__global__ void __launch_bounds__(kBlock) spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
+__device__ __forceinline__ void put_carry(double* __restrict__ row, const Acc<VEC, kScalar>& acc,
+                                          long long d, int lane, long long feat0) {
+  if constexpr (kScalar) {
+    const long long fi = feat0 + lane;
+    if (fi < d) row[fi] = acc.v[0];
+  } else {
+    double2* rp = reinterpret_cast<double2*>(row) + 2 * lane;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      rp[2 * i * L] = make_double2(acc.v[4 * i], acc.v[4 * i + 1]);
+      rp[2 * i * L + 1] = make_double2(acc.v[4 * i + 2], acc.v[4 * i + 3]);
+    }
+  }
+}
+
+template <int L, int VEC, bool kScalar>
+__global__ void __launch_bounds__(kBlock, 3) spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int U = kScalar ? 8 : (VEC == 1 ? 8 : (VEC == 2 ? 4 : 2));
   const int wl = threadIdx.x & 31;
   const int lane = threadIdx.x & (L - 1);
@@ -138,26 +182,22 @@ __global__ void __launch_bounds__(kBlock) spmm_hyb_kernel(const __grid_constant_
     tail_cont = c + 1 < P.nchunks && __ldg(Ip + r1 - 1) == __ldg(Ip + r1);
   }
 
-  Frag<VEC, kScalar> acc;
+  Acc<VEC, kScalar> acc;
   acc.zero();
   long long cur_row = -1;
   int32_t cur_dest = -1;
   bool first_group = true;
 
   auto flush = [&](bool is_final) {
-    float* out;
-    bool accum = a.accumulate != 0;
     if (split && first_group && head_cont) {
-      out = a.carry + ((P.carry_off + c) * 2 + 0) * d;
-      accum = false;
+      put_carry<L, VEC, kScalar>(a.carry + ((P.carry_off + c) * 2 + 0) * d, acc, d, lane, feat0);
     } else if (split && is_final && tail_cont) {
-      out = a.carry + ((P.carry_off + c) * 2 + 1) * d;
-      accum = false;
+      put_carry<L, VEC, kScalar>(a.carry + ((P.carry_off + c) * 2 + 1) * d, acc, d, lane, feat0);
     } else {
       const int32_t dest = split ? cur_dest : __ldg(Ip + cur_row);
-      out = a.Y + static_cast<long long>(dest) * d;
+      put_row<L, VEC, kScalar>(a.Y + static_cast<long long>(dest) * d, acc, d, lane, feat0,
+                               a.accumulate != 0);
     }
-    put_row<L, VEC, kScalar>(out, acc, d, lane, feat0, accum);
     acc.zero();
     first_group = false;
   };
@@ -226,11 +266,14 @@ __global__ void __launch_bounds__(kBlock) spmm_hyb_kernel(const __grid_constant_
 //     way.  Fixed shapes and orders => bitwise reproducible; no atomics.
 constexpr int kFixBlock = 128;
 
-template <int V>  // V = 4: float4 lanes (d % 4 == 0); V = 1: scalar
-__device__ __forceinline__ void fix_reduce(const float* __restrict__ src, long long first_row,
-                                           int count, int first_slot, bool two_slot, float* out,
-                                           long long d, bool accumulate) {
-  __shared__ float4 part[kFixBlock];
+// Carries and level-2 partials are f64 (see Acc); only the final store rounds to f32.
+// Output: Y row (f32, optionally accumulated) when yout != nullptr, else an f64 l2 row.
+template <int V>  // V = 2: double2 lanes (d even); V = 1: scalar
+__device__ __forceinline__ void fix_reduce(const double* __restrict__ src, long long first_row,
+                                           int count, int first_slot, bool two_slot,
+                                           float* yout, double* l2out, long long d,
+                                           bool accumulate) {
+  __shared__ double2 part[kFixBlock];
   const long long dv = d / V;
   const int rt = static_cast<int>(min64(dv, kFixBlock));  // threads per feature row
   const int G = kFixBlock / rt;
@@ -238,36 +281,51 @@ __device__ __forceinline__ void fix_reduce(const float* __restrict__ src, long l
   for (long long fb = 0; fb < dv; fb += rt) {
     const long long f = fb + threadIdx.x % rt;
     const bool active = g < G && f < dv;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    double2 acc = make_double2(0.0, 0.0);
     if (active) {
       for (int q0 = g; q0 < count; q0 += 8 * G) {
-        float4 v[8];
+        double2 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int q = q0 + u * G;
-          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u] = make_double2(0.0, 0.0);
           if (q < count) {
             const long long r = two_slot ? (first_row + q) * 2 + (q == 0 ? first_slot : 0)
                                          : first_row + q;
-            if constexpr (V == 4) v[u] = reinterpret_cast<const float4*>(src + r * d)[f];
+            if constexpr (V == 2) v[u] = reinterpret_cast<const double2*>(src + r * d)[f];
             else v[u].x = src[r * d + f];
           }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = add4(acc, v[u]);
+        for (int u = 0; u < 8; ++u) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+        }
       }
     }
     part[threadIdx.x] = acc;
     __syncthreads();
     if (g == 0 && f < dv) {
-      float4 tot = part[threadIdx.x];
-      for (int gg = 1; gg < G; ++gg) tot = add4(tot, part[gg * rt + threadIdx.x]);
-      if constexpr (V == 4) {
-        float4* o = reinterpret_cast<float4*>(out) + f;
-        if (accumulate) tot = add4(tot, *o);
-        *o = tot;
+      double2 tot = part[threadIdx.x];
+      for (int gg = 1; gg < G; ++gg) {
+        tot.x += part[gg * rt + threadIdx.x].x;
+        tot.y += part[gg * rt + threadIdx.x].y;
+      }
+      if (yout) {
+        if constexpr (V == 2) {
+          float2* o = reinterpret_cast<float2*>(yout) + f;
+          if (accumulate) {
+            const float2 old = *o;
+            tot.x += old.x;
+            tot.y += old.y;
+          }
+          *o = make_float2(static_cast<float>(tot.x), static_cast<float>(tot.y));
+        } else {
+          yout[f] = static_cast<float>(accumulate ? tot.x + yout[f] : tot.x);
+        }
       } else {
-        out[f] = accumulate ? out[f] + tot.x : tot.x;
+        if constexpr (V == 2) reinterpret_cast<double2*>(l2out)[f] = tot;
+        else l2out[f] = tot.x;
       }
     }
     __syncthreads();
@@ -276,19 +334,23 @@ __device__ __forceinline__ void fix_reduce(const float* __restrict__ src, long l
 
 template <int V>
 __global__ void __launch_bounds__(kFixBlock)
-spmm_fixup_tiles_kernel(const FixTile* __restrict__ tiles, const float* __restrict__ carry,
-                        float* __restrict__ l2, float* __restrict__ Y, long long d, int accumulate) {
+spmm_fixup_tiles_kernel(const FixTile* __restrict__ tiles, const double* __restrict__ carry,
+                        double* __restrict__ l2, float* __restrict__ Y, long long d, int accumulate) {
   const FixTile t = tiles[blockIdx.x];
-  float* out = t.out >= 0 ? Y + t.out * d : l2 + (-t.out - 1) * d;
-  fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, out, d, t.out >= 0 && accumulate);
+  if (t.out >= 0)
+    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, Y + t.out * d, nullptr, d,
+                  accumulate != 0);
+  else
+    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, nullptr, l2 + (-t.out - 1) * d,
+                  d, false);
 }
 
 template <int V>
 __global__ void __launch_bounds__(kFixBlock)
-spmm_fixup_runs_kernel(const FixRun* __restrict__ runs, const float* __restrict__ l2,
+spmm_fixup_runs_kernel(const FixRun* __restrict__ runs, const double* __restrict__ l2,
                        float* __restrict__ Y, long long d, int accumulate) {
   const FixRun r = runs[blockIdx.x];
-  fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, Y + r.row * d, d, accumulate != 0);
+  fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, Y + r.row * d, nullptr, d, accumulate != 0);
 }
 
 __global__ void zero_rows_kernel(const int32_t* __restrict__ rows, long long n, float* Y,
@@ -343,7 +405,7 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
 
   // One launch (plus the fix-up pair) per column partition, partitions in order.
   size_t pi = 0, fr = 0;
-  const bool vec4 = d % 4 == 0;
+  const bool vec2 = d % 2 == 0;
   while (pi < h.parts.size()) {
     const int part_id = h.parts[pi].partition;
     SpmmArgs args{};
@@ -376,8 +438,8 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
       const FixRange& R = h.fix_ranges[fr];
       const long long nt = R.tile_end - R.tile_begin, nr = R.run_end - R.run_begin;
       if (nt > 0) {
-        if (vec4)
-          spmm_fixup_tiles_kernel<4><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
+        if (vec2)
+          spmm_fixup_tiles_kernel<2><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
               h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, d, h.c > 1);
         else
           spmm_fixup_tiles_kernel<1><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
@@ -385,8 +447,8 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
         STRATA_CUDA_CHECK(cudaGetLastError());
       }
       if (nr > 0) {
-        if (vec4)
-          spmm_fixup_runs_kernel<4><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
+        if (vec2)
+          spmm_fixup_runs_kernel<2><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
               h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, d, h.c > 1);
         else
           spmm_fixup_runs_kernel<1><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
