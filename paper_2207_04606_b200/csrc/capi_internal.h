@@ -123,6 +123,7 @@ struct strata_hyb_impl {
   int64_t l2_slots = 0;
   mutable DevBuf<double> carry;        // [total_chunks_carry][2][d] f64 scratch, grown on demand
   mutable DevBuf<double> carry_l2;     // [l2_slots][d]
+  mutable DevBuf<double> yacc;         // c > 1: f64 [rows][d] accumulator across partitions
   mutable int64_t carry_d = 0;
   mutable DevBuf<float> stage_x, stage_y;  // e2e staging
 };

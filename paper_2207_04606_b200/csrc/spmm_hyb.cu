@@ -45,10 +45,11 @@ struct SpmmArgs {
   const float* X;
   float* Y;
   double* carry;
+  double* yacc;  // c > 1 only: f64 accumulator [rows][d]; else nullptr
   long long d;
   long long total_chunks;
   int nparts;
-  int accumulate;
+  int pad_;
   SpmmPartDev parts[kMaxParts];
 };
 
@@ -106,54 +107,48 @@ __device__ __forceinline__ void fma_frag(Acc<VEC, kScalar>& acc, float a,
   }
 }
 
-// Write (or accumulate into) one output row fragment of Y (f32).
+// Store one output row fragment of Y (f32): the single rounding of the whole sum.
 template <int L, int VEC, bool kScalar>
 __device__ __forceinline__ void put_row(float* __restrict__ row, const Acc<VEC, kScalar>& acc,
-                                        long long d, int lane, long long feat0, bool accumulate) {
+                                        long long d, int lane, long long feat0) {
   if constexpr (kScalar) {
     const long long fi = feat0 + lane;
-    if (fi < d) {
-      float v = static_cast<float>(acc.v[0]);
-      if (accumulate) v = static_cast<float>(acc.v[0] + static_cast<double>(row[fi]));
-      row[fi] = v;
-    }
+    if (fi < d) row[fi] = static_cast<float>(acc.v[0]);
   } else {
     float4* rp = reinterpret_cast<float4*>(row) + lane;
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      float4 v;
-      if (accumulate) {
-        const float4 o = rp[i * L];
-        v = make_float4(static_cast<float>(acc.v[4 * i] + o.x), static_cast<float>(acc.v[4 * i + 1] + o.y),
-                        static_cast<float>(acc.v[4 * i + 2] + o.z), static_cast<float>(acc.v[4 * i + 3] + o.w));
-      } else {
-        v = make_float4(static_cast<float>(acc.v[4 * i]), static_cast<float>(acc.v[4 * i + 1]),
-                        static_cast<float>(acc.v[4 * i + 2]), static_cast<float>(acc.v[4 * i + 3]));
-      }
-      st_stream4(rp + i * L, v);
-    }
+    for (int i = 0; i < VEC; ++i)
+      st_stream4(rp + i * L, make_float4(static_cast<float>(acc.v[4 * i]), static_cast<float>(acc.v[4 * i + 1]),
+                                         static_cast<float>(acc.v[4 * i + 2]), static_cast<float>(acc.v[4 * i + 3])));
   }
 }
 
-// Partial row of a split run -> carry buffer (f64, so split rows lose nothing either).
-template <int L, int VEC, bool kScalar>
-__device__ __forceinline__ void put_carry(double* __restrict__ row, const Acc<VEC, kScalar>& acc,
-                                          long long d, int lane, long long feat0) {
+// Store (carry buffer) or add (c > 1 f64 accumulator) an f64 row fragment.
+template <int L, int VEC, bool kScalar, bool kAdd>
+__device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC, kScalar>& acc,
+                                        long long d, int lane, long long feat0) {
   if constexpr (kScalar) {
     const long long fi = feat0 + lane;
-    if (fi < d) row[fi] = acc.v[0];
+    if (fi < d) row[fi] = kAdd ? row[fi] + acc.v[0] : acc.v[0];
   } else {
     double2* rp = reinterpret_cast<double2*>(row) + 2 * lane;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
-      rp[2 * i * L] = make_double2(acc.v[4 * i], acc.v[4 * i + 1]);
-      rp[2 * i * L + 1] = make_double2(acc.v[4 * i + 2], acc.v[4 * i + 3]);
+      double2 a0 = make_double2(acc.v[4 * i], acc.v[4 * i + 1]);
+      double2 a1 = make_double2(acc.v[4 * i + 2], acc.v[4 * i + 3]);
+      if constexpr (kAdd) {
+        const double2 o0 = rp[2 * i * L], o1 = rp[2 * i * L + 1];
+        a0.x += o0.x; a0.y += o0.y; a1.x += o1.x; a1.y += o1.y;
+      }
+      rp[2 * i * L] = a0;
+      rp[2 * i * L + 1] = a1;
     }
   }
 }
 
 template <int L, int VEC, bool kScalar>
-__global__ void __launch_bounds__(kBlock, 3) spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
+__global__ void __launch_bounds__(kBlock, (L == 32 && VEC == 1) ? 3 : 2)
+spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int U = kScalar ? 8 : (VEC == 1 ? 8 : (VEC == 2 ? 4 : 2));
   const int wl = threadIdx.x & 31;
   const int lane = threadIdx.x & (L - 1);
@@ -190,13 +185,15 @@ __global__ void __launch_bounds__(kBlock, 3) spmm_hyb_kernel(const __grid_consta
 
   auto flush = [&](bool is_final) {
     if (split && first_group && head_cont) {
-      put_carry<L, VEC, kScalar>(a.carry + ((P.carry_off + c) * 2 + 0) * d, acc, d, lane, feat0);
+      put_f64<L, VEC, kScalar, false>(a.carry + ((P.carry_off + c) * 2 + 0) * d, acc, d, lane, feat0);
     } else if (split && is_final && tail_cont) {
-      put_carry<L, VEC, kScalar>(a.carry + ((P.carry_off + c) * 2 + 1) * d, acc, d, lane, feat0);
+      put_f64<L, VEC, kScalar, false>(a.carry + ((P.carry_off + c) * 2 + 1) * d, acc, d, lane, feat0);
     } else {
-      const int32_t dest = split ? cur_dest : __ldg(Ip + cur_row);
-      put_row<L, VEC, kScalar>(a.Y + static_cast<long long>(dest) * d, acc, d, lane, feat0,
-                               a.accumulate != 0);
+      const long long dest = split ? cur_dest : __ldg(Ip + cur_row);
+      if (a.yacc)  // c > 1: partitions accumulate in f64, rounded once at the end
+        put_f64<L, VEC, kScalar, true>(a.yacc + dest * d, acc, d, lane, feat0);
+      else
+        put_row<L, VEC, kScalar>(a.Y + dest * d, acc, d, lane, feat0);
     }
     acc.zero();
     first_group = false;
@@ -267,7 +264,8 @@ __global__ void __launch_bounds__(kBlock, 3) spmm_hyb_kernel(const __grid_consta
 constexpr int kFixBlock = 128;
 
 // Carries and level-2 partials are f64 (see Acc); only the final store rounds to f32.
-// Output: Y row (f32, optionally accumulated) when yout != nullptr, else an f64 l2 row.
+// Output: a Y row (f32 store) when yout != nullptr; else an f64 row, stored (level-2 slot) or
+// added (`accumulate`: the c > 1 f64 accumulator).
 template <int V>  // V = 2: double2 lanes (d even); V = 1: scalar
 __device__ __forceinline__ void fix_reduce(const double* __restrict__ src, long long first_row,
                                            int count, int first_slot, bool two_slot,
@@ -312,34 +310,40 @@ __device__ __forceinline__ void fix_reduce(const double* __restrict__ src, long 
         tot.y += part[gg * rt + threadIdx.x].y;
       }
       if (yout) {
+        if constexpr (V == 2)
+          reinterpret_cast<float2*>(yout)[f] =
+              make_float2(static_cast<float>(tot.x), static_cast<float>(tot.y));
+        else
+          yout[f] = static_cast<float>(tot.x);
+      } else {
         if constexpr (V == 2) {
-          float2* o = reinterpret_cast<float2*>(yout) + f;
+          double2* o = reinterpret_cast<double2*>(l2out) + f;
           if (accumulate) {
-            const float2 old = *o;
+            const double2 old = *o;
             tot.x += old.x;
             tot.y += old.y;
           }
-          *o = make_float2(static_cast<float>(tot.x), static_cast<float>(tot.y));
+          *o = tot;
         } else {
-          yout[f] = static_cast<float>(accumulate ? tot.x + yout[f] : tot.x);
+          l2out[f] = accumulate ? l2out[f] + tot.x : tot.x;
         }
-      } else {
-        if constexpr (V == 2) reinterpret_cast<double2*>(l2out)[f] = tot;
-        else l2out[f] = tot.x;
       }
     }
     __syncthreads();
   }
 }
 
+// yacc != nullptr (c > 1): final rows are added to the f64 accumulator instead of stored to Y.
 template <int V>
 __global__ void __launch_bounds__(kFixBlock)
 spmm_fixup_tiles_kernel(const FixTile* __restrict__ tiles, const double* __restrict__ carry,
-                        double* __restrict__ l2, float* __restrict__ Y, long long d, int accumulate) {
+                        double* __restrict__ l2, float* __restrict__ Y, double* __restrict__ yacc,
+                        long long d) {
   const FixTile t = tiles[blockIdx.x];
-  if (t.out >= 0)
-    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, Y + t.out * d, nullptr, d,
-                  accumulate != 0);
+  if (t.out >= 0 && yacc)
+    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, nullptr, yacc + t.out * d, d, true);
+  else if (t.out >= 0)
+    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, Y + t.out * d, nullptr, d, false);
   else
     fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, nullptr, l2 + (-t.out - 1) * d,
                   d, false);
@@ -348,9 +352,19 @@ spmm_fixup_tiles_kernel(const FixTile* __restrict__ tiles, const double* __restr
 template <int V>
 __global__ void __launch_bounds__(kFixBlock)
 spmm_fixup_runs_kernel(const FixRun* __restrict__ runs, const double* __restrict__ l2,
-                       float* __restrict__ Y, long long d, int accumulate) {
+                       float* __restrict__ Y, double* __restrict__ yacc, long long d) {
   const FixRun r = runs[blockIdx.x];
-  fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, Y + r.row * d, nullptr, d, accumulate != 0);
+  if (yacc)
+    fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, nullptr, yacc + r.row * d, d, true);
+  else
+    fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, Y + r.row * d, nullptr, d, false);
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ in, float* __restrict__ out,
+                                  long long n) {
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[e] = static_cast<float>(in[e]);
 }
 
 __global__ void zero_rows_kernel(const int32_t* __restrict__ rows, long long n, float* Y,
@@ -394,9 +408,13 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
     h.carry_l2.alloc(static_cast<size_t>(h.l2_slots) * d);
     h.carry_d = d;
   }
-  if (h.c > 1 && h.rows > 0)
-    STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * h.rows * d, s));
-  else if (h.n_empty > 0) {
+  // c > 1: partitions accumulate into an f64 [rows][d] workspace, rounded to Y once at the end.
+  double* yacc = nullptr;
+  if (h.c > 1 && h.rows > 0) {
+    if (h.yacc.n < static_cast<size_t>(h.rows * d)) h.yacc.alloc(static_cast<size_t>(h.rows * d));
+    yacc = h.yacc.p;
+    STRATA_CUDA_CHECK(cudaMemsetAsync(yacc, 0, sizeof(double) * h.rows * d, s));
+  } else if (h.n_empty > 0) {
     const long long total = h.n_empty * d;
     const unsigned blocks = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 4096));
     zero_rows_kernel<<<blocks, 256, 0, s>>>(h.empty_rows.p, h.n_empty, Y, d);
@@ -410,7 +428,7 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
     const int part_id = h.parts[pi].partition;
     SpmmArgs args{};
     args.I = h.I.p; args.J = h.J.p; args.V = h.V.p; args.X = X; args.Y = Y;
-    args.carry = h.carry.p; args.d = d; args.accumulate = h.c > 1;
+    args.carry = h.carry.p; args.yacc = yacc; args.d = d;
     long long chunks = 0;
     int np = 0;
     for (; pi < h.parts.size() && h.parts[pi].partition == part_id; ++pi) {
@@ -440,22 +458,28 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t
       if (nt > 0) {
         if (vec2)
           spmm_fixup_tiles_kernel<2><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
-              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, d, h.c > 1);
+              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, yacc, d);
         else
           spmm_fixup_tiles_kernel<1><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
-              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, d, h.c > 1);
+              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, yacc, d);
         STRATA_CUDA_CHECK(cudaGetLastError());
       }
       if (nr > 0) {
         if (vec2)
           spmm_fixup_runs_kernel<2><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
-              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, d, h.c > 1);
+              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, yacc, d);
         else
           spmm_fixup_runs_kernel<1><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
-              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, d, h.c > 1);
+              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, yacc, d);
         STRATA_CUDA_CHECK(cudaGetLastError());
       }
     }
+  }
+  if (yacc) {
+    const long long n = h.rows * d;
+    f64_to_f32_kernel<<<static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148 * 32)), 256, 0, s>>>(
+        yacc, Y, n);
+    STRATA_CUDA_CHECK(cudaGetLastError());
   }
 }
 

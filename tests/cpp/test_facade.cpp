@@ -1,0 +1,401 @@
+// test_facade.cpp — the reference's own storage / kernel known-answer and property tests
+// (proj/tests/test_storage.cpp, test_kernels.cpp, test_exec.cpp), rewritten against the
+// device-backed strata_b200 façade (include/strata_b200.hpp).  Same scenarios, same expected
+// values; every computation runs on the GPU through the C ABI.  Run by
+// tests/test_gpu_cpp.py (needs a B200).
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "strata_b200.hpp"
+
+using namespace strata_b200;
+
+// ---- minimal test harness ----------------------------------------------------------------
+namespace {
+struct Case {
+  const char* name;
+  std::function<void()> fn;
+};
+std::vector<Case>& cases() {
+  static std::vector<Case> c;
+  return c;
+}
+struct Reg {
+  Reg(const char* n, std::function<void()> f) { cases().push_back({n, std::move(f)}); }
+};
+int g_fail = 0, g_checks = 0;
+struct Abort {};
+}  // namespace
+
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST_CASE(name) \
+  static void CAT(tc_, __LINE__)(); static Reg CAT(reg_, __LINE__)(name, CAT(tc_, __LINE__)); \
+  static void CAT(tc_, __LINE__)()
+#define CHECK(...) do { ++g_checks; if (!(__VA_ARGS__)) { ++g_fail; \
+  std::printf("  FAILED %s:%d: %s\n", __FILE__, __LINE__, #__VA_ARGS__); } } while (0)
+#define REQUIRE(...) do { ++g_checks; if (!(__VA_ARGS__)) { ++g_fail; \
+  std::printf("  FAILED %s:%d: %s\n", __FILE__, __LINE__, #__VA_ARGS__); throw Abort{}; } } while (0)
+#define CHECK_THROWS_KIND(expr, k, substr) do { ++g_checks; bool ok_ = false; \
+  try { (void)(expr); } catch (const Error& e_) { ok_ = e_.kind == (k) && \
+    std::string(e_.what()).find(substr) != std::string::npos; } \
+  if (!ok_) { ++g_fail; std::printf("  FAILED %s:%d: throws %s\n", __FILE__, __LINE__, #expr); } } while (0)
+
+namespace {
+
+// test_storage.cpp:18-25
+CooMatrix example_m() {
+  CooMatrix m;
+  m.rows = m.cols = 4;
+  m.triplets = {{0, 0, 1}, {0, 2, 2}, {1, 3, 3}, {2, 0, 4}, {2, 1, 5}, {2, 2, 6}, {2, 3, 7}};
+  return m;
+}
+
+// testutil.cpp:17-33 semantics (values in [-4,4] \ {0}).
+CooMatrix random_coo(std::mt19937& rng, int64_t rows, int64_t cols, double density) {
+  CooMatrix m;
+  m.rows = rows;
+  m.cols = cols;
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  std::uniform_int_distribution<int> val(-4, 4);
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < cols; ++j)
+      if (u(rng) < density) {
+        int v = val(rng);
+        m.triplets.push_back({i, j, double(v ? v : 1)});
+      }
+  return m;
+}
+
+DenseMatrix dense_from_coo(const CooMatrix& m) {
+  DenseMatrix d(m.rows, m.cols);
+  for (const auto& t : m.triplets) d.at(t.row, t.col) += t.value;
+  return d;
+}
+
+DenseMatrix random_dense(std::mt19937& rng, int64_t r, int64_t c) {
+  DenseMatrix d(r, c);
+  std::uniform_int_distribution<int> val(-4, 4);
+  for (auto& v : d.v) v = val(rng);
+  return d;
+}
+
+DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
+  DenseMatrix y(a.rows, b.cols);
+  for (int64_t i = 0; i < a.rows; ++i)
+    for (int64_t j = 0; j < a.cols; ++j)
+      if (a.at(i, j) != 0.0)
+        for (int64_t k = 0; k < b.cols; ++k) y.at(i, k) += a.at(i, j) * b.at(j, k);
+  return y;
+}
+
+// reconstruct_dense of a hyb decomposition (storage.cpp:536-550), padding skipped by the
+// repeated-column rule (storage.cpp:520-531).
+DenseMatrix reconstruct(const HybDecomposition& h) {
+  DenseMatrix d(h.rows, h.cols);
+  for (const auto& p : h.parts) {
+    const std::string pre =
+        "hyb_p" + std::to_string(p.partition) + "_b" + std::to_string(p.bucket) + "_";
+    const IntArray& rmap = p.ell.arr(pre + "I_indices");
+    const IntArray& jx = p.ell.arr(pre + "J_indices");
+    const int64_t w = p.width;
+    for (size_t r = 0; r < rmap.size(); ++r)
+      for (int64_t k = 0; k < w; ++k) {
+        if (k > 0 && jx[r * w + k] == jx[r * w + k - 1]) continue;
+        d.at(rmap[r], jx[r * w + k]) += p.ell.values[r * w + k];
+      }
+  }
+  return d;
+}
+
+DenseMatrix run_spmm(const CooMatrix& m, const DenseMatrix& x, const std::string& fmt) {
+  Pipeline pl = build_matrix_pipeline(KernelOp::SpMM, m, x.cols, FormatRequest::parse(fmt));
+  pl.bindings["X"] = x.v;
+  return pl.run_dense();
+}
+
+}  // namespace
+
+// ---- storage (test_storage.cpp) -------------------------------------------------------------
+TEST_CASE("build_csr matches the hand-derived layout") {  // :30-36
+  TensorStorage s = build_csr(example_m());
+  CHECK(s.arr("J_indptr") == IntArray{0, 2, 3, 7, 7});
+  CHECK(s.arr("J_indices") == IntArray{0, 2, 3, 0, 1, 2, 3});
+}
+
+TEST_CASE("build_csr rejects duplicate coordinates") {  // :56-62
+  CooMatrix m;
+  m.rows = m.cols = 2;
+  m.triplets = {{0, 0, 1}, {0, 0, 2}};
+  CHECK_THROWS_KIND(build_csr(m), ErrKind::Validation, "duplicate");
+}
+
+TEST_CASE("csr_to_bsr tiles the example by hand") {  // :64-77
+  TensorStorage bsr = csr_to_bsr(build_csr(example_m()), 2);
+  CHECK(bsr.arr("JO_indptr") == IntArray{0, 2, 4});
+  CHECK(bsr.arr("JO_indices") == IntArray{0, 1, 0, 1});
+  CHECK(bsr.values[0] == 1 && bsr.values[1] == 0 && bsr.values[2] == 0 && bsr.values[3] == 0);
+  CHECK(bsr.values[4] == 2 && bsr.values[7] == 3);
+}
+
+TEST_CASE("csr_to_bsr of all zeros stores no blocks") {  // :79-84
+  CooMatrix m;
+  m.rows = m.cols = 4;
+  CHECK(csr_to_bsr(build_csr(m), 2).values.empty());
+}
+
+TEST_CASE("csr_to_bsr with b=1 mirrors CSR values") {  // :86-93
+  TensorStorage csr = build_csr(example_m());
+  TensorStorage bsr = csr_to_bsr(csr, 1);
+  REQUIRE(bsr.values.size() == csr.values.size());
+  CHECK(bsr.values == csr.values);
+  CHECK(bsr.arr("JO_indices") == csr.arr("J_indices"));
+}
+
+TEST_CASE("csr_to_ell pads and errors per the capacity rule") {  // :95-113
+  TensorStorage csr = build_csr(example_m());
+  CHECK_THROWS_KIND(csr_to_ell(csr, 2), ErrKind::Capacity, "row 2");
+  TensorStorage ell = csr_to_ell(csr, 4);
+  const IntArray& ix = ell.arr("J_indices");
+  CHECK(ix[0] == 0 && ix[1] == 2 && ix[2] == 2 && ix[3] == 2);
+  CHECK(ix[12] == 0 && ix[15] == 0);
+  CHECK(ell.values[2] == 0);
+  CHECK(std::fabs(padding_ratio(ell) - 9.0 / 16.0) < 1e-12);
+}
+
+TEST_CASE("decompose_hyb buckets the example rows") {  // :122-134
+  HybDecomposition h = decompose_hyb(build_csr(example_m()), 1, 2);
+  REQUIRE(h.parts.size() == 3);
+  CHECK(h.parts[0].bucket == 0);
+  CHECK(h.parts[0].ell.arr("hyb_p0_b0_I_indices") == IntArray{1});
+  CHECK(h.parts[1].ell.arr("hyb_p0_b1_I_indices") == IntArray{0});
+  CHECK(h.parts[2].ell.arr("hyb_p0_b2_I_indices") == IntArray{2});
+  CHECK(h.padding_ratio == 0.0);
+}
+
+TEST_CASE("decompose_hyb splits oversized rows into bucket k segments") {  // :136-146
+  HybDecomposition h = decompose_hyb(build_csr(example_m()), 1, 1);
+  const EllBucketPart* b1 = nullptr;
+  for (const auto& p : h.parts)
+    if (p.bucket == 1) b1 = &p;
+  REQUIRE(b1 != nullptr);
+  CHECK(b1->ell.arr("hyb_p0_b1_I_indices") == IntArray{0, 2, 2});
+  CHECK(reconstruct(h).v == dense_from_coo(example_m()).v);
+}
+
+TEST_CASE("decompose_hyb of a zero matrix is empty") {  // :148-154
+  CooMatrix m;
+  m.rows = m.cols = 4;
+  HybDecomposition h = decompose_hyb(build_csr(m), 2, 2);
+  CHECK(h.parts.empty());
+  CHECK(h.padding_ratio == 0.0);
+}
+
+TEST_CASE("decompose_hyb rejects c < 1 and k < 0") {  // storage.cpp:273
+  CHECK_THROWS_KIND(decompose_hyb(build_csr(example_m()), 0, 1), ErrKind::Usage, "c >= 1");
+  CHECK_THROWS_KIND(decompose_hyb(build_csr(example_m()), 1, -1), ErrKind::Usage, "k >= 0");
+}
+
+TEST_CASE("round trip: hyb and bsr reconstruct random matrices exactly") {  // :217-246
+  std::mt19937 rng(42);
+  for (int trial = 0; trial < 40; ++trial) {
+    int64_t rows = 1 + static_cast<int64_t>(rng() % 64);
+    int64_t cols = 1 + static_cast<int64_t>(rng() % 64);
+    CooMatrix m = random_coo(rng, rows, cols, 0.25);
+    TensorStorage csr = build_csr(m);
+    CHECK(reconstruct(decompose_hyb(csr, 2, 2)).v == dense_from_coo(m).v);
+    TensorStorage bsr = csr_to_bsr(csr, 2);
+    DenseMatrix got(bsr.rows, bsr.cols);
+    const IntArray& ip = bsr.arr("JO_indptr");
+    const IntArray& ix = bsr.arr("JO_indices");
+    for (int64_t br = 0; br < bsr.rows / 2; ++br)
+      for (int32_t p = ip[br]; p < ip[br + 1]; ++p)
+        for (int ii = 0; ii < 2; ++ii)
+          for (int ji = 0; ji < 2; ++ji) got.at(br * 2 + ii, ix[p] * 2 + ji) += bsr.values[p * 4 + ii * 2 + ji];
+    bool ok = true;
+    DenseMatrix want = dense_from_coo(m);
+    for (int64_t i = 0; i < got.rows; ++i)
+      for (int64_t j = 0; j < got.cols; ++j)
+        ok &= got.at(i, j) == ((i < rows && j < cols) ? want.at(i, j) : 0.0);
+    CHECK(ok);
+  }
+}
+
+TEST_CASE("hyb bucket uniformity and entry accounting") {  // :248-263
+  std::mt19937 rng(11);
+  for (int trial = 0; trial < 20; ++trial) {
+    CooMatrix m = random_coo(rng, 32, 32, 0.3);
+    HybDecomposition h = decompose_hyb(build_csr(m), 2, 2);
+    int64_t entries = 0;
+    for (const auto& p : h.parts) {
+      CHECK(p.width == (int64_t{1} << p.bucket));
+      entries += p.ell.nnz;
+    }
+    CHECK(entries == static_cast<int64_t>(m.triplets.size()));
+  }
+}
+
+TEST_CASE("hyb padding ratio is always below one half") {  // :265-287
+  std::mt19937 rng(5);
+  for (int trial = 0; trial < 100; ++trial) {
+    CooMatrix m = random_coo(rng, 24, 24, 0.2 + 0.01 * (trial % 30));
+    HybDecomposition h = decompose_hyb(build_csr(m), 1 + trial % 3, trial % 4);
+    CHECK(h.padding_ratio < 0.5);
+  }
+}
+
+// ---- kernels (test_kernels.cpp, test_exec.cpp) -----------------------------------------------
+TEST_CASE("SpMM with all-ones dense operand yields replicated row sums") {  // :33-41
+  DenseMatrix ones(4, 2);
+  for (auto& v : ones.v) v = 1;
+  for (const char* fmt : {"csr", "hyb:c=1", "hyb:c=2,k=1"}) {
+    DenseMatrix y = run_spmm(example_m(), ones, fmt);
+    double sums[4] = {3, 3, 22, 0};
+    for (int i = 0; i < 4; ++i)
+      for (int k = 0; k < 2; ++k) CHECK(y.at(i, k) == sums[i]);
+  }
+}
+
+TEST_CASE("SpMM identity operand reproduces the matrix") {  // :43-49
+  DenseMatrix eye(4, 4);
+  for (int i = 0; i < 4; ++i) eye.at(i, i) = 1;
+  CHECK(run_spmm(example_m(), eye, "hyb:c=1,k=1").v == dense_from_coo(example_m()).v);
+}
+
+TEST_CASE("SpMM random instances equal the dense oracle in every format") {  // exec :86-102
+  std::mt19937 rng(3);
+  for (int trial = 0; trial < 20; ++trial) {
+    CooMatrix a = random_coo(rng, 1 + rng() % 40, 1 + rng() % 40, 0.3);
+    DenseMatrix x = random_dense(rng, a.cols, 8);
+    DenseMatrix want = matmul(dense_from_coo(a), x);
+    for (const char* fmt : {"csr", "hyb:c=1", "hyb:c=3,k=1", "hyb:c=1,k=0"})
+      CHECK(run_spmm(a, x, fmt).v == want.v);
+  }
+}
+
+TEST_CASE("BSR tensor-core SpMM equals the dense oracle") {
+  std::mt19937 rng(9);
+  for (int trial = 0; trial < 5; ++trial) {
+    CooMatrix a = random_coo(rng, 96, 64, 0.2);
+    DenseMatrix x = random_dense(rng, 64, 64);  // integers: exact in bf16
+    DenseMatrix want = matmul(dense_from_coo(a), x);
+    DenseMatrix got = run_spmm(a, x, "bsr:b=32");
+    CHECK(got.v == want.v);
+  }
+}
+
+TEST_CASE("SpMM is bitwise deterministic") {  // exec :135-157
+  std::mt19937 rng(17);
+  CooMatrix a = generate_matrix("powerlaw", 3000, 3000, 0, 0, 0, 40.0, 3);
+  DenseMatrix x(a.cols, 32);
+  std::normal_distribution<double> nd;
+  for (auto& v : x.v) v = nd(rng);
+  CHECK(run_spmm(a, x, "hyb:c=1,k=2").v == run_spmm(a, x, "hyb:c=1,k=2").v);
+}
+
+TEST_CASE("SDDMM: all-ones mask with identity factors picks the diagonal pattern") {  // :60-79
+  CooMatrix a;
+  a.rows = a.cols = 2;
+  a.triplets = {{0, 0, 1}, {0, 1, 1}, {1, 0, 1}, {1, 1, 1}};
+  Pipeline pl = build_matrix_pipeline(KernelOp::SDDMM, a, 2, FormatRequest{});
+  pl.bindings["X"] = {1, 0, 0, 1};
+  pl.bindings["Y"] = {1, 0, 0, 1};
+  DenseMatrix b = pl.run_dense();
+  CHECK(b.at(0, 0) == 1 && b.at(0, 1) == 0 && b.at(1, 0) == 0 && b.at(1, 1) == 1);
+}
+
+TEST_CASE("SDDMM random instances equal the dense oracle") {  // :81-97
+  std::mt19937 rng(8);
+  for (int trial = 0; trial < 20; ++trial) {
+    CooMatrix a = random_coo(rng, 8, 8, 0.3);
+    Pipeline pl = build_matrix_pipeline(KernelOp::SDDMM, a, 4, FormatRequest{});
+    DenseMatrix x = random_dense(rng, 8, 4), y = random_dense(rng, 4, 8);
+    pl.bindings["X"] = x.v;
+    pl.bindings["Y"] = y.v;
+    DenseMatrix got = pl.run_dense();
+    DenseMatrix xy = matmul(x, y), ad = dense_from_coo(a), want(8, 8);
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) want.at(i, j) = ad.at(i, j) == 0 ? 0 : ad.at(i, j) * xy.at(i, j);
+    REQUIRE(got.v == want.v);
+  }
+}
+
+TEST_CASE("SDDMM of a zero mask is zero") {  // :99-103
+  CooMatrix a;
+  a.rows = a.cols = 4;
+  Pipeline pl = build_matrix_pipeline(KernelOp::SDDMM, a, 2, FormatRequest{});
+  pl.bindings["X"] = std::vector<double>(8, 0.0);
+  pl.bindings["Y"] = std::vector<double>(8, 0.0);
+  for (double v : pl.run_dense().v) CHECK(v == 0.0);
+}
+
+TEST_CASE("RGMS with one relation degenerates to SpMM of X*W") {  // :105-118
+  std::mt19937 rng(12);
+  CooMatrix a = random_coo(rng, 40, 40, 0.3);
+  Pipeline pl = build_rgms_pipeline({a}, 16, 16);
+  DenseMatrix got = pl.run_dense();
+  DenseMatrix x(40, 16), w(16, 16);
+  x.v = pl.bindings["X"];
+  w.v = pl.bindings["W"];
+  CHECK(got.v == matmul(dense_from_coo(a), matmul(x, w)).v);
+}
+
+TEST_CASE("RGMS random instances match the two-stage oracle") {  // :120-156
+  std::mt19937 rng(21);
+  std::uniform_real_distribution<double> u(0, 1);
+  std::uniform_int_distribution<int> val(-3, 3);
+  for (int trial = 0; trial < 25; ++trial) {
+    int R = 1 + trial % 3;
+    std::vector<CooMatrix> rels(R);
+    for (auto& r : rels) {
+      r.rows = r.cols = 48;
+      for (int i = 0; i < 48; ++i)
+        for (int j = 0; j < 48; ++j)
+          if (u(rng) < 0.15) {
+            int v = val(rng);
+            r.triplets.push_back({i, j, double(v ? v : 1)});
+          }
+    }
+    Pipeline pl = build_rgms_pipeline(rels, 16, 32, 100 + trial);
+    DenseMatrix got = pl.run_dense();
+    DenseMatrix x(48, 16), want(48, 32);
+    x.v = pl.bindings["X"];
+    for (int r = 0; r < R; ++r) {  // two_stage_rgms_oracle (kernels.cpp:169-193)
+      DenseMatrix w(16, 32);
+      std::copy(pl.bindings["W"].begin() + r * 512, pl.bindings["W"].begin() + (r + 1) * 512, w.v.begin());
+      DenseMatrix part = matmul(dense_from_coo(rels[r]), matmul(x, w));
+      for (size_t i = 0; i < want.v.size(); ++i) want.v[i] += part.v[i];
+    }
+    REQUIRE(got.v == want.v);
+  }
+}
+
+TEST_CASE("binding size mismatch is an Exec error") {  // interp.cpp:575-578
+  Pipeline pl = build_matrix_pipeline(KernelOp::SpMM, example_m(), 2, FormatRequest::parse("hyb"));
+  pl.bindings["X"] = std::vector<double>(16, 1.0);
+  CHECK_THROWS_KIND(pl.run_dense(), ErrKind::Exec, "binding size mismatch for X");
+}
+
+int main() {
+  int failed_cases = 0;
+  for (auto& c : cases()) {
+    const int before = g_fail;
+    try {
+      c.fn();
+    } catch (const Abort&) {
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  EXCEPTION in '%s': %s\n", c.name, e.what());
+    }
+    if (g_fail != before) {
+      ++failed_cases;
+      std::printf("[FAIL] %s\n", c.name);
+    }
+  }
+  std::printf("cases: %zu  failed: %d  checks: %d\n", cases().size(), failed_cases, g_checks);
+  return failed_cases ? 1 : 0;
+}
