@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstrata_b200.so")
+# STRATA_B200_LIB: development override to A/B two in-tree builds of the same library.
+LIB_PATH = os.environ.get("STRATA_B200_LIB") or os.path.join(_HERE, "libstrata_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

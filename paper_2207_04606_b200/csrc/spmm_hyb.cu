@@ -76,11 +76,12 @@ __device__ __forceinline__ void gather(Frag<VEC, kScalar>& f, const float* __res
   }
 }
 
-// Accumulators are f64: every f32 product a*x is exact in f64, so the only roundings are the
-// f64 additions (~1e-16 relative) and the single f32 rounding at the store.  On the
-// reference's integer operands this is bit-identical to its f32 interpreter; on real-valued
-// operands it stays within ~1 f32 ulp of the reference's F64 pipeline, where sequential f32
-// accumulation (the reference's own F32 pipeline included) drifts by 2e-5 on long rows.
+// Two-level accumulation.  Each batch of <= U gathered slots of one output row is summed with
+// f32 FMAs into a partial, which is then folded into an f64 accumulator; the f64 sum is rounded
+// to f32 once, at the store.  The f32 rounding error is therefore that of an <= U-term sum per
+// batch instead of growing with the row (the reference's sequential f32 accumulation drifts by
+// ~2e-5 from its own F64 pipeline on long rows, golden.npz), and only one F32->F64 conversion
+// per lane-feature per batch is paid.  Integer operands stay exact (all partial sums < 2^24).
 template <int VEC, bool kScalar>
 struct Acc {
   double v[kScalar ? 1 : 4 * VEC];
@@ -91,20 +92,30 @@ struct Acc {
 };
 
 template <int VEC, bool kScalar>
-__device__ __forceinline__ void fma_frag(Acc<VEC, kScalar>& acc, float a,
+__device__ __forceinline__ void fma_part(Frag<VEC, kScalar>& part, float a,
                                          const Frag<VEC, kScalar>& x) {
-  const double ad = a;
   if constexpr (kScalar) {
-    acc.v[0] = fma(ad, static_cast<double>(x.v[0].x), acc.v[0]);
+    part.v[0].x = fmaf(a, x.v[0].x, part.v[0].x);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) fma4(part.v[i], a, x.v[i]);
+  }
+}
+
+template <int VEC, bool kScalar>
+__device__ __forceinline__ void absorb(Acc<VEC, kScalar>& acc, Frag<VEC, kScalar>& part) {
+  if constexpr (kScalar) {
+    acc.v[0] += static_cast<double>(part.v[0].x);
   } else {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
-      acc.v[4 * i + 0] = fma(ad, static_cast<double>(x.v[i].x), acc.v[4 * i + 0]);
-      acc.v[4 * i + 1] = fma(ad, static_cast<double>(x.v[i].y), acc.v[4 * i + 1]);
-      acc.v[4 * i + 2] = fma(ad, static_cast<double>(x.v[i].z), acc.v[4 * i + 2]);
-      acc.v[4 * i + 3] = fma(ad, static_cast<double>(x.v[i].w), acc.v[4 * i + 3]);
+      acc.v[4 * i + 0] += static_cast<double>(part.v[i].x);
+      acc.v[4 * i + 1] += static_cast<double>(part.v[i].y);
+      acc.v[4 * i + 2] += static_cast<double>(part.v[i].z);
+      acc.v[4 * i + 3] += static_cast<double>(part.v[i].w);
     }
   }
+  part.zero();
 }
 
 // Store one output row fragment of Y (f32): the single rounding of the whole sum.
@@ -147,7 +158,10 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 }
 
 template <int L, int VEC, bool kScalar>
-__global__ void __launch_bounds__(kBlock, (L == 32 && VEC == 1) ? 3 : 2)
+#ifndef STRATA_SPMM_MINB32  // CTAs/SM the d=128 variant is register-budgeted for (A/B knob)
+#define STRATA_SPMM_MINB32 3
+#endif
+__global__ void __launch_bounds__(kBlock, (L == 32 && VEC == 1) ? STRATA_SPMM_MINB32 : 2)
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int U = kScalar ? 8 : (VEC == 1 ? 8 : (VEC == 2 ? 4 : 2));
   const int wl = threadIdx.x & 31;
@@ -177,13 +191,16 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
     tail_cont = c + 1 < P.nchunks && __ldg(Ip + r1 - 1) == __ldg(Ip + r1);
   }
 
-  Acc<VEC, kScalar> acc;
+  Acc<VEC, kScalar> acc;    // f64 running sum of the current output row (group)
+  Frag<VEC, kScalar> part;  // f32 partial of the current batch (<= U slots of one row)
   acc.zero();
+  part.zero();
   long long cur_row = -1;
   int32_t cur_dest = -1;
   bool first_group = true;
 
   auto flush = [&](bool is_final) {
+    absorb(acc, part);
     if (split && first_group && head_cont) {
       put_f64<L, VEC, kScalar, false>(a.carry + ((P.carry_off + c) * 2 + 0) * d, acc, d, lane, feat0);
     } else if (split && is_final && tail_cont) {
@@ -247,9 +264,10 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
             }
             cur_row = row;
           }
-          fma_frag(acc, vu, xv[u]);
+          fma_part(part, vu, xv[u]);
         }
       }
+      absorb(acc, part);
     }
   }
   if (cur_row >= 0) flush(true);

@@ -45,7 +45,7 @@ def test_bsr_arrays_golden(cuda, G):
 
 def test_bsr_spmm_golden(cuda, G):
     import torch
-    for key in ("bsr/bs128_b32", "bsr/pl_b32"):
+    for key in ("bsr/bs128_b32", "bsr/pl_b32_b32"):
         rows, cols, prow, pcol, pad = (int(x) for x in G[key + "/shape"])
         m = S.CsrMatrix(rows, cols, G[key + "/csr_indptr"], G[key + "/csr_indices"],
                         G[key + "/csr_values"])

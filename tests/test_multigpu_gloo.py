@@ -1,0 +1,105 @@
+"""CPU suite: the N > 1 path's host logic on a world-size-2 `gloo` group.
+
+Each rank takes its nnz-balanced row shard (RowShardPlan, the code bench.py runs under
+torchrun), decomposes and multiplies it (here with the oracle, since there is no GPU), places
+its rows in slot `rank` of the padded buffer, and the all-gather + unpad must reassemble the
+global result bit for bit.  Also checks SURVEY §7's property that per-shard hyb decompositions
+concatenated per bucket, in shard order, equal the global decomposition."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    import paper_2207_04606_b200 as S
+    from paper_2207_04606_b200.sharding import RowShardPlan
+    from oracle import port as P
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    m = S.generate_matrix("powerlaw", 6000, 5000, 0, 0, 0, 20.0, 3)
+    plan = RowShardPlan(m, world)
+    sh = plan.shard(rank)
+    k = S.hyb_auto_k(m)
+    parts, _ = P.hyb_decompose(sh.rows, sh.cols, sh.indptr, sh.indices, sh.values, 1, k)
+    X = S.dense_int((m.cols, 16), 5)
+    y = P.spmm_hyb_refnum(sh.rows, parts, X)
+    buf = torch.zeros((plan.max_rows, 16), dtype=torch.float32)
+    buf[: sh.rows] = torch.from_numpy(y)
+    gathered = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(gathered, buf)
+    full = plan.unpad(torch.cat(gathered, 0)).numpy()
+    if rank == 0:
+        np.save(out_path, full)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_row_sharded_spmm_allgather_gloo(tmp_path, world):
+    import paper_2207_04606_b200 as S
+    from oracle import port as P
+    out = str(tmp_path / "y.npy")
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    m = S.generate_matrix("powerlaw", 6000, 5000, 0, 0, 0, 20.0, 3)
+    X = S.dense_int((m.cols, 16), 5)
+    want = P.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, X)
+    assert np.array_equal(np.load(out), want)
+
+
+@pytest.mark.parametrize("parts", [2, 3, 5, 8])
+def test_shard_decompositions_concatenate_to_global(parts):
+    import paper_2207_04606_b200 as S
+    from paper_2207_04606_b200.sharding import RowShardPlan
+    from oracle import port as P
+    m = S.generate_matrix("powerlaw", 8000, 8000, 0, 0, 0, 30.0, 1)
+    k = S.hyb_auto_k(m)
+    for c in (1, 3):
+        glob, _ = P.hyb_decompose(m.rows, m.cols, m.indptr, m.indices, m.values, c, k)
+        plan = RowShardPlan(m, parts)
+        cat = {}
+        for r in range(parts):
+            sh = plan.shard(r)
+            r0, _ = plan.rows_of(r)
+            sp, _ = P.hyb_decompose(sh.rows, sh.cols, sh.indptr, sh.indices, sh.values, c, k)
+            for p in sp:
+                key = (p["partition"], p["bucket"])
+                e = cat.setdefault(key, {"I": [], "J": [], "V": []})
+                e["I"].append(p["I_indices"] + r0)
+                e["J"].append(p["J_indices"])
+                e["V"].append(p["values"])
+        assert sorted(cat) == [(p["partition"], p["bucket"]) for p in glob]
+        for p in glob:
+            e = cat[(p["partition"], p["bucket"])]
+            assert np.array_equal(np.concatenate(e["I"]), p["I_indices"])
+            assert np.array_equal(np.concatenate(e["J"]), p["J_indices"])
+            assert np.array_equal(np.concatenate(e["V"]), p["values"])
+
+
+def test_partition_covers_rows_and_balances():
+    import paper_2207_04606_b200 as S
+    from paper_2207_04606_b200.sharding import RowShardPlan
+    m = S.generate_matrix("powerlaw", 50000, 50000, 0, 0, 0, 25.3, 1)
+    for world in (1, 2, 4, 8):
+        plan = RowShardPlan(m, world)
+        assert sum(plan.shard(r).rows for r in range(world)) == m.rows
+        nnz = [plan.shard_nnz(r) for r in range(world)]
+        assert sum(nnz) == m.nnz
+        assert max(nnz) <= m.nnz / world + np.diff(m.indptr).max()
