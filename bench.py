@@ -285,6 +285,51 @@ def extra_reddit(S, torch, dev, stream, peak):
     return out
 
 
+def _time_ms(torch, stream, fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
+    """C3 (BSR sparse attention, bf16, tcgen05) and C4 (RGCN, AM shape, tcgen05)."""
+    out = {}
+    # C3: blocksparse 4096^2, b = 32, density 0.1, seed 1; head dim 64 (and a 12-head batch).
+    m = S.generate_matrix("blocksparse", 4096, 4096, 0.1, 0, 32, 0, 1)
+    bs = S.csr_to_bsr(m.to_device(dev), 32)
+    d = 64
+    X = torch.randint(-3, 4, (4096, d), device=dev).to(torch.bfloat16)
+    Y = torch.empty((4096, d), device=dev)
+    ms = _time_ms(torch, stream, lambda: S.bsr_spmm(bs, X, Y))
+    flops = 2.0 * bs.nblocks * 32 * 32 * d
+    b_alg = bs.nblocks * 32 * 32 * 2 + bs.nblocks * 4 + 129 * 4 + bs.nblocks * 32 * d * 2 + 4096 * d * 4
+    out["c3_bsr_spmm"] = {"ms": round(ms, 5), "gflops": round(flops / (ms * 1e-3) / 1e9, 1),
+                          "blocks": bs.nblocks, "tensor_frac": round(flops / (ms * 1e-3) / 1e12 / bf16_peak, 5),
+                          "hbm_frac": round(b_alg / (ms * 1e-3) / 1e9 / hbm_peak, 4),
+                          "note": "208 MFLOP over 10.8 MB: launch/latency-bound by construction"}
+    # C4: AM-shaped power-law graph split into 133 relations, d_in = d_out = 32.
+    g = S.generate_matrix("powerlaw", 1885136, 1885136, 0, 0, 0, 3.0051, 1)
+    rel = S.split_relations(g, 133, 1).to_device(dev)
+    Xr = torch.randint(-3, 4, (g.cols, 32), device=dev).to(torch.bfloat16)
+    W = torch.randint(-3, 4, (133, 32, 32), device=dev).to(torch.bfloat16)
+    Yr = torch.empty((g.rows, 32), device=dev)
+    ms = _time_ms(torch, stream, lambda: S.rgms(rel, Xr, W, Yr), reps=10)
+    flops = 2.0 * g.nnz * 32 * 32
+    b_onchip = g.nnz * (4 + 4 + 2) + g.nnz * 32 * 2 + 133 * 32 * 32 * 2 + g.rows * 32 * 4
+    out["c4_rgcn"] = {"ms": round(ms, 4), "gflops": round(flops / (ms * 1e-3) / 1e9, 1),
+                      "nnz": g.nnz, "tensor_frac": round(flops / (ms * 1e-3) / 1e12 / bf16_peak, 5),
+                      "hbm_frac_onchip_model": round(b_onchip / (ms * 1e-3) / 1e9 / hbm_peak, 4),
+                      "bytes_model": "nnz*10 + nnz*d_in*2 + R*d_in*d_out*2 + m*d_out*4 (661 MB)"}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -307,10 +352,11 @@ def run_ours(args):
     m = S.generate_matrix(cfg["kind"], cfg["n"], cfg["m"], 0, 0, 0, cfg["avg"], cfg["seed"])
     gen_s = time.time() - t0
     k = S.hyb_auto_k(m)
-    bounds = S.partition_rows(m.indptr, world)
-    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-    shard = m.row_slice(r0, r1)
-    max_rows = int(np.max(np.diff(bounds)))
+    from paper_2207_04606_b200.sharding import RowShardPlan
+    plan = RowShardPlan(m, world)
+    r0, r1 = plan.rows_of(rank)
+    shard = plan.shard(rank)
+    max_rows = plan.max_rows
     stream = torch.cuda.current_stream()
 
     t0 = time.time()
@@ -416,6 +462,10 @@ def run_ours(args):
             extra.update(extra_reddit(S, torch, dev, stream, hbm_peak))
         except Exception as e:  # informational only
             extra["reddit_error"] = str(e)
+        try:
+            extra.update(extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak))
+        except Exception as e:  # informational only
+            extra["tensor_core_error"] = str(e)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline_single(m, d)

@@ -1,0 +1,15 @@
+#!/bin/bash
+# ncu captures (one kernel each) for the workloads in tools/prof_workloads.py.
+# usage: WORKLOADS="reddit_spmm bsr" bash tools/gpu_prof.sh
+mkdir -p gpurun_out
+for w in ${WORKLOADS:-products reddit_spmm reddit_sddmm bsr rgcn}; do
+  case $w in
+    products|reddit_spmm) k=spmm_hyb_kernel ;;
+    reddit_sddmm) k=sddmm_kernel ;;
+    bsr) k=bsr_spmm_tc_kernel ;;
+    rgcn) k=rgms_tc_kernel ;;
+  esac
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
+    -o gpurun_out/prof_$w -f python tools/prof_workloads.py $w 4 > gpurun_out/ncu_$w.log 2>&1
+done
+ls -la gpurun_out
