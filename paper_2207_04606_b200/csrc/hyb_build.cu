@@ -177,7 +177,7 @@ hyb_scatter_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict
 }
 
 struct FillPart {
-  long long slot_off, row_off;
+  long long slot_off, row_off, nslots;
   int b;
 };
 
@@ -198,6 +198,7 @@ hyb_fill_kernel(const int32_t* __restrict__ indices, const float* __restrict__ v
     }
     const FillPart P = sp[lo];
     const long long local = slot - P.slot_off;
+    if (local >= P.nslots) continue;  // alignment gap after a part (never read)
     const long long r = P.row_off + (local >> P.b);
     const int s = static_cast<int>(local & ((1ll << P.b) - 1));
     const long long src = seg_src[r];
@@ -291,8 +292,8 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
     P.col_lo = static_cast<int64_t>(P.partition) * part_w;
     P.col_hi = std::min<int64_t>(cols, (P.partition + 1) * part_w);
     P.row_off = bin_start[bin];
-    P.slot_off = slot_cursor;
-    slot_cursor += P.nrows * P.width;
+    P.slot_off = slot_cursor;  // multiple of 8 slots: the SpMM reads 8-slot tiles as int4 pairs
+    slot_cursor += (P.nrows * P.width + 7) & ~int64_t{7};
     pads += P.pad_slots;
     slots += P.nrows * P.width;
     h.parts.push_back(P);
@@ -313,7 +314,7 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
   }
   if (slot_cursor > 0) {
     std::vector<FillPart> fp;
-    for (const auto& P : h.parts) fp.push_back({P.slot_off, P.row_off, P.bucket});
+    for (const auto& P : h.parts) fp.push_back({P.slot_off, P.row_off, P.nrows * P.width, P.bucket});
     DevBuf<FillPart> dfp(fp.size());
     STRATA_CUDA_CHECK(cudaMemcpyAsync(dfp.p, fp.data(), fp.size() * sizeof(FillPart),
                                       cudaMemcpyHostToDevice, s));

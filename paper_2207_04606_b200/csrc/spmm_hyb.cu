@@ -157,17 +157,21 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
   }
 }
 
-template <int L, int VEC, bool kScalar>
 #ifndef STRATA_SPMM_MINB32  // CTAs/SM the d=128 variant is register-budgeted for (A/B knob)
 #define STRATA_SPMM_MINB32 3
 #endif
-__global__ void __launch_bounds__(kBlock, (L == 32 && VEC == 1) ? STRATA_SPMM_MINB32 : 2)
+
+// Main kernel.  Per virtual warp: one chunk of whole ELL rows, walked in 8-slot tiles.  Each
+// tile's 8 columns and 8 values are fetched with two uniform 128-bit loads each (all lanes of
+// the VW read the same 16 B, one L1 wavefront: no shuffles), so slot positions are
+// compile-time; pad slots (a repeat of the previous column inside a row, the reference's own
+// rule, storage.cpp:528) are skipped by predication; UG gathers are in flight per lane.
+template <int L, int VEC, bool kScalar>
+__global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar) ? STRATA_SPMM_MINB32 : 2))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
-  constexpr int U = kScalar ? 8 : (VEC == 1 ? 8 : (VEC == 2 ? 4 : 2));
-  const int wl = threadIdx.x & 31;
+  constexpr int kT = 8;  // slots per index tile
+  constexpr int UG = kScalar ? 8 : (VEC == 1 ? 8 : (VEC == 2 ? 4 : 2));  // gathers in flight
   const int lane = threadIdx.x & (L - 1);
-  const int vbase = wl & ~(L - 1);
-  const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << vbase);
   const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
   if (vw >= a.total_chunks) return;
   const long long feat0 = kScalar ? static_cast<long long>(blockIdx.y) * 32 : 0;
@@ -181,7 +185,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   const long long r0 = c << P.rpc_log2;
   const long long r1 = min64(r0 + (1ll << P.rpc_log2), P.nrows);
   const int32_t* __restrict__ Ip = a.I + P.row_off;
-  const int32_t* __restrict__ Jp = a.J + P.slot_off;
+  const int32_t* __restrict__ Jp = a.J + P.slot_off;  // slot_off is a multiple of 8 (16 B)
   const float* __restrict__ Vp = a.V + P.slot_off;
   const long long d = a.d;
   const bool split = P.may_split != 0;
@@ -192,7 +196,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   }
 
   Acc<VEC, kScalar> acc;    // f64 running sum of the current output row (group)
-  Frag<VEC, kScalar> part;  // f32 partial of the current batch (<= U slots of one row)
+  Frag<VEC, kScalar> part;  // f32 partial of the current tile
   acc.zero();
   part.zero();
   long long cur_row = -1;
@@ -206,7 +210,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
     } else if (split && is_final && tail_cont) {
       put_f64<L, VEC, kScalar, false>(a.carry + ((P.carry_off + c) * 2 + 1) * d, acc, d, lane, feat0);
     } else {
-      const long long dest = split ? cur_dest : __ldg(Ip + cur_row);
+      const long long dest = cur_dest;
       if (a.yacc)  // c > 1: partitions accumulate in f64, rounded once at the end
         put_f64<L, VEC, kScalar, true>(a.yacc + dest * d, acc, d, lane, feat0);
       else
@@ -216,59 +220,59 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
     first_group = false;
   };
 
-  const long long s_end = r1 << b;
-  int32_t last_col = 0;
-  for (long long g = r0 << b; g < s_end; g += L) {
-    const long long t = g + lane;
-    const bool in = t < s_end;
-    int32_t col = 0;
-    float val = 0.f;
-    if (in) {
-      col = ld_stream(Jp + t);
-      val = ld_stream(Vp + t);
-    }
-    int32_t prev = __shfl_up_sync(vmask, col, 1, L);
-    if (lane == 0) prev = last_col;
-    const bool pad = in && (t & wmask) != 0 && col == prev;
-    unsigned real = __ballot_sync(vmask, in && !pad);
-    if constexpr (L < 32) real = (real >> vbase) & ((1u << L) - 1u);
-    last_col = __shfl_sync(vmask, col, L - 1, L);
+  // A new ELL row starts at slot t: fetch its output row, close the previous group if the
+  // destination changes (split runs keep accumulating across their segments).
+  auto row_start = [&](long long t, int32_t dest) {
+    if (cur_row >= 0 && (!split || dest != cur_dest)) flush(false);
+    cur_dest = dest;
+    cur_row = t >> b;
+  };
 
-    while (real) {
-      int sl[U];
-      bool ok[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        ok[u] = real != 0;
-        sl[u] = ok[u] ? __ffs(real) - 1 : 0;
-        real &= real - 1u;
-      }
-      Frag<VEC, kScalar> xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int32_t cu = __shfl_sync(vmask, col, sl[u], L);
-        if (ok[u]) gather<L, VEC, kScalar>(xv[u], a.X, cu, d, lane, feat0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float vu = __shfl_sync(vmask, val, sl[u], L);
-        if (ok[u]) {
-          const long long row = (g + sl[u]) >> b;
-          if (row != cur_row) {
-            if (split) {
-              const int32_t dest = __ldg(Ip + row);
-              if (cur_row >= 0 && dest != cur_dest) flush(false);
-              cur_dest = dest;
-            } else if (cur_row >= 0) {
-              flush(false);
-            }
-            cur_row = row;
-          }
-          fma_part(part, vu, xv[u]);
-        }
-      }
-      absorb(acc, part);
+  const long long s_end = r1 << b;
+  int32_t last_col = -1;
+  for (long long g = r0 << b; g < s_end; g += kT) {
+    int32_t col[kT];
+    float val[kT];
+    {
+      const int4 c0 = __ldcs(reinterpret_cast<const int4*>(Jp + g));
+      const int4 c1 = __ldcs(reinterpret_cast<const int4*>(Jp + g) + 1);
+      const float4 v0 = __ldcs(reinterpret_cast<const float4*>(Vp + g));
+      const float4 v1 = __ldcs(reinterpret_cast<const float4*>(Vp + g) + 1);
+      col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
+      col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
+      val[0] = v0.x; val[1] = v0.y; val[2] = v0.z; val[3] = v0.w;
+      val[4] = v1.x; val[5] = v1.y; val[6] = v1.z; val[7] = v1.w;
     }
+    // Destination of a row starting at this tile's first slot, fetched before the gathers so
+    // its latency overlaps theirs.
+    const bool start0 = (g & wmask) == 0;
+    const int32_t dest0 = start0 ? __ldg(Ip + (g >> b)) : 0;
+    const int n = static_cast<int>(min64(kT, s_end - g));  // < 8 only in a part's last tile
+    bool live[kT];
+#pragma unroll
+    for (int u = 0; u < kT; ++u) {
+      const bool rs = ((g + u) & wmask) == 0;
+      live[u] = u < n && (rs || col[u] != (u ? col[u - 1] : last_col));
+    }
+    last_col = col[kT - 1];
+#pragma unroll
+    for (int ub = 0; ub < kT; ub += UG) {
+      Frag<VEC, kScalar> xv[UG];
+#pragma unroll
+      for (int u = 0; u < UG; ++u)
+        if (live[ub + u]) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0);
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        const int uu = ub + u;
+        if (uu == 0) {
+          if (start0) row_start(g, dest0);
+        } else if (uu < n && ((g + uu) & wmask) == 0) {  // rows narrower than a tile (W < 8)
+          row_start(g + uu, __ldg(Ip + ((g + uu) >> b)));
+        }
+        if (live[uu]) fma_part(part, val[uu], xv[u]);
+      }
+    }
+    absorb(acc, part);
   }
   if (cur_row >= 0) flush(true);
 }
