@@ -105,8 +105,11 @@ __global__ void bsr_scatter_kernel(const int32_t* __restrict__ indptr,
 
 // ---- tensor-core SpMM ---------------------------------------------------------------------
 constexpr int kB = 32;        // block size served by the tensor-core path
-constexpr int kStages = 4;
+constexpr int kStages = 6;     // smem ring depth
+constexpr int kAhead = kStages - 2;  // blocks in flight: refilling stage j-2's slot leaves the
+                                     // just-issued MMA (j-1) off the critical path
 constexpr int kThreads = 128;
+constexpr int kMaxPre = 256;  // block-column indices of a block row preloaded into smem
 
 template <int D>  // feature count, 64 or a multiple of 128 (<= 512)
 __global__ void __launch_bounds__(kThreads)
@@ -125,10 +128,12 @@ bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restr
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kStages];
   __shared__ uint32_t tmem_slot;
+  __shared__ int32_t s_cols[kMaxPre];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long br = blockIdx.x;
   const int q0 = jo_indptr[br], nblk = jo_indptr[br + 1] - q0;
+  for (int j = tid; j < nblk && j < kMaxPre; j += kThreads) s_cols[j] = jo_indices[q0 + j];
 
   if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
   if (tid == 0) {
@@ -150,7 +155,7 @@ bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restr
       const int ii = c >> 2, kg = c & 3;
       tc::cp_async16(sa + (ii >> 3) * 512 + kg * 128 + (ii & 7) * 16, gb + ii * kB + kg * 8);
     }
-    const long long row0 = static_cast<long long>(jo_indices[q]) * kB;
+    const long long row0 = static_cast<long long>(j < kMaxPre ? s_cols[j] : jo_indices[q]) * kB;
     for (int c = tid; c < kB * D / 8; c += kThreads) {  // chunk c: X row ji, feature group fg
       const int ji = c / (D / 8), fg = c % (D / 8);
       tc::cp_async16(sx + fg * 512 + (ji >> 3) * 128 + (ji & 7) * 16,
@@ -158,19 +163,19 @@ bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restr
     }
   };
 
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < kAhead; ++s) {
     if (s < nblk) load_stage(s, s);
     tc::cp_async_commit();
   }
   for (int j = 0; j < nblk; ++j) {
     const int s = j % kStages;
-    const int jn = j + kStages - 1;
+    const int jn = j + kAhead;  // refills the slot of block j-2 (jn % kStages == (j-2) % kStages)
     if (jn < nblk) {
-      if (j >= 1) tc::mbar_wait(&mbar[(j - 1) % kStages], ((j - 1) / kStages) & 1);
+      if (j >= 2) tc::mbar_wait(&mbar[(j - 2) % kStages], ((j - 2) / kStages) & 1);
       load_stage(jn, jn % kStages);
     }
     tc::cp_async_commit();
-    tc::cp_async_wait<kStages - 1>();
+    tc::cp_async_wait<kAhead>();  // block j's group has landed
     tc::fence_proxy_async();
     __syncthreads();
     if (tid == 0) {

@@ -25,6 +25,9 @@
 
 #include "capi_internal.h"
 #include "common.cuh"
+#include "tc_common.cuh"
+
+#define tc_cp_async16 ::strata_b200::tc::cp_async16
 
 namespace strata_b200 {
 
@@ -32,6 +35,7 @@ namespace {
 
 constexpr int kMaxParts = 32;
 constexpr int kBlock = 256;
+constexpr int kPiece = 256;  // ELL slots staged in shared memory per virtual warp at a time
 
 struct SpmmPartDev {
   long long slot_off, row_off, nrows, chunk_begin, nchunks, carry_off;
@@ -170,7 +174,10 @@ template <int L, int VEC, bool kScalar>
 __global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar) ? STRATA_SPMM_MINB32 : 2))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int kT = 8;  // slots per index tile
-  constexpr int UG = kScalar ? 8 : (VEC == 1 ? 8 : (VEC == 2 ? 4 : 2));  // gathers in flight
+#ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
+#define STRATA_SPMM_UG 8
+#endif
+  constexpr int UG = kScalar ? 8 : (VEC == 1 ? STRATA_SPMM_UG : (VEC == 2 ? 4 : 2));
   const int lane = threadIdx.x & (L - 1);
   const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
   if (vw >= a.total_chunks) return;
@@ -228,16 +235,37 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
     cur_row = t >> b;
   };
 
+  // This VW's shared-memory staging buffer: one 256-slot piece of J then of V (2 KB).
+  extern __shared__ int4 spmm_smem[];
+  int32_t* sJ = reinterpret_cast<int32_t*>(spmm_smem) + (threadIdx.x / L) * (2 * kPiece);
+  float* sV = reinterpret_cast<float*>(sJ + kPiece);
+  const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
+
   const long long s_end = r1 << b;
   int32_t last_col = -1;
-  for (long long g = r0 << b; g < s_end; g += kT) {
+  for (long long pbase = r0 << b; pbase < s_end; pbase += kPiece) {
+    // Stage the piece's index and value tiles with one burst of 16-byte cp.async per lane
+    // (a single memory round trip for up to 256 slots; parts are 8-slot aligned and padded, so
+    // rounding the copy up to whole tiles stays in bounds).
+    const int np = static_cast<int>(min64(kPiece, s_end - pbase));
+    const int nq = ((np + kT - 1) / kT) * (kT / 4);  // 16-byte chunks per array
+    __syncwarp(vmask);  // previous piece fully consumed by every lane
+    for (int q = lane; q < nq; q += L) {
+      tc_cp_async16(sJ + 4 * q, Jp + pbase + 4 * q);
+      tc_cp_async16(sV + 4 * q, Vp + pbase + 4 * q);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp(vmask);
+  for (int gi = 0; gi < np; gi += kT) {
+    const long long g = pbase + gi;
     int32_t col[kT];
     float val[kT];
     {
-      const int4 c0 = __ldcs(reinterpret_cast<const int4*>(Jp + g));
-      const int4 c1 = __ldcs(reinterpret_cast<const int4*>(Jp + g) + 1);
-      const float4 v0 = __ldcs(reinterpret_cast<const float4*>(Vp + g));
-      const float4 v1 = __ldcs(reinterpret_cast<const float4*>(Vp + g) + 1);
+      const int4 c0 = reinterpret_cast<const int4*>(sJ + gi)[0];  // broadcast LDS.128
+      const int4 c1 = reinterpret_cast<const int4*>(sJ + gi)[1];
+      const float4 v0 = reinterpret_cast<const float4*>(sV + gi)[0];
+      const float4 v1 = reinterpret_cast<const float4*>(sV + gi)[1];
       col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
       col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
       val[0] = v0.x; val[1] = v0.y; val[2] = v0.z; val[3] = v0.w;
@@ -273,6 +301,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
       }
     }
     absorb(acc, part);
+  }
   }
   if (cur_row >= 0) flush(true);
 }
@@ -404,7 +433,14 @@ void launch_variant(const SpmmArgs& args, long long total_chunks, long long d, c
   const long long threads = total_chunks * L;
   const unsigned blocks = static_cast<unsigned>((threads + kBlock - 1) / kBlock);
   dim3 grid(blocks, kScalar ? static_cast<unsigned>((d + 31) / 32) : 1u);
-  spmm_hyb_kernel<L, VEC, kScalar><<<grid, kBlock, 0, s>>>(args);
+  constexpr int smem = (kBlock / L) * 2 * kPiece * 4;  // 2 KB staging per virtual warp
+  static bool configured = false;  // host-side, once per instantiation
+  if (!configured) {
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(spmm_hyb_kernel<L, VEC, kScalar>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  spmm_hyb_kernel<L, VEC, kScalar><<<grid, kBlock, smem, s>>>(args);
 }
 
 }  // namespace
