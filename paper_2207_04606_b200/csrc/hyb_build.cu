@@ -292,6 +292,8 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
     P.col_lo = static_cast<int64_t>(P.partition) * part_w;
     P.col_hi = std::min<int64_t>(cols, (P.partition + 1) * part_w);
     P.row_off = bin_start[bin];
+    if (P.nrows * P.width > INT32_MAX - 256)  // the SpMM keeps part-local slot indices in 32 bits
+      throw ApiError(STRATA_ERR_CAPACITY, "hyb part exceeds 2^31 ELL slots");
     P.slot_off = slot_cursor;  // multiple of 8 slots: the SpMM reads 8-slot tiles as int4 pairs
     slot_cursor += (P.nrows * P.width + 7) & ~int64_t{7};
     pads += P.pad_slots;

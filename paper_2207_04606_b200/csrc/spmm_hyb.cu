@@ -187,10 +187,11 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   while (pi + 1 < a.nparts && vw >= a.parts[pi + 1].chunk_begin) ++pi;
   const SpmmPartDev& P = a.parts[pi];
   const int b = P.b;
-  const long long wmask = (1ll << b) - 1;
-  const long long c = vw - P.chunk_begin;
-  const long long r0 = c << P.rpc_log2;
-  const long long r1 = min64(r0 + (1ll << P.rpc_log2), P.nrows);
+  // Part-local row / slot indices are 32-bit (the planner guarantees < 2^31 slots per part).
+  const int wmask = (1 << b) - 1;
+  const int c = static_cast<int>(vw - P.chunk_begin);
+  const int r0 = c << P.rpc_log2;
+  const int r1 = static_cast<int>(min64(static_cast<long long>(r0) + (1ll << P.rpc_log2), P.nrows));
   const int32_t* __restrict__ Ip = a.I + P.row_off;
   const int32_t* __restrict__ Jp = a.J + P.slot_off;  // slot_off is a multiple of 8 (16 B)
   const float* __restrict__ Vp = a.V + P.slot_off;
@@ -206,7 +207,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   Frag<VEC, kScalar> part;  // f32 partial of the current tile
   acc.zero();
   part.zero();
-  long long cur_row = -1;
+  bool started = false;
   int32_t cur_dest = -1;
   bool first_group = true;
 
@@ -227,12 +228,12 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
     first_group = false;
   };
 
-  // A new ELL row starts at slot t: fetch its output row, close the previous group if the
-  // destination changes (split runs keep accumulating across their segments).
-  auto row_start = [&](long long t, int32_t dest) {
-    if (cur_row >= 0 && (!split || dest != cur_dest)) flush(false);
+  // A new ELL row starts with output row `dest`: close the previous group if the destination
+  // changes (split runs keep accumulating across their segments).
+  auto row_start = [&](int32_t dest) {
+    if (started && (!split || dest != cur_dest)) flush(false);
     cur_dest = dest;
-    cur_row = t >> b;
+    started = true;
   };
 
   // This VW's shared-memory staging buffer: one 256-slot piece of J then of V (2 KB).
@@ -241,13 +242,13 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   float* sV = reinterpret_cast<float*>(sJ + kPiece);
   const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
 
-  const long long s_end = r1 << b;
+  const int s_end = r1 << b;
   int32_t last_col = -1;
-  for (long long pbase = r0 << b; pbase < s_end; pbase += kPiece) {
+  for (int pbase = r0 << b; pbase < s_end; pbase += kPiece) {
     // Stage the piece's index and value tiles with one burst of 16-byte cp.async per lane
     // (a single memory round trip for up to 256 slots; parts are 8-slot aligned and padded, so
     // rounding the copy up to whole tiles stays in bounds).
-    const int np = static_cast<int>(min64(kPiece, s_end - pbase));
+    const int np = min(kPiece, s_end - pbase);
     const int nq = ((np + kT - 1) / kT) * (kT / 4);  // 16-byte chunks per array
     __syncwarp(vmask);  // previous piece fully consumed by every lane
     for (int q = lane; q < nq; q += L) {
@@ -257,53 +258,53 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncwarp(vmask);
-  for (int gi = 0; gi < np; gi += kT) {
-    const long long g = pbase + gi;
-    int32_t col[kT];
-    float val[kT];
-    {
-      const int4 c0 = reinterpret_cast<const int4*>(sJ + gi)[0];  // broadcast LDS.128
-      const int4 c1 = reinterpret_cast<const int4*>(sJ + gi)[1];
-      const float4 v0 = reinterpret_cast<const float4*>(sV + gi)[0];
-      const float4 v1 = reinterpret_cast<const float4*>(sV + gi)[1];
-      col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
-      col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
-      val[0] = v0.x; val[1] = v0.y; val[2] = v0.z; val[3] = v0.w;
-      val[4] = v1.x; val[5] = v1.y; val[6] = v1.z; val[7] = v1.w;
-    }
-    // Destination of a row starting at this tile's first slot, fetched before the gathers so
-    // its latency overlaps theirs.
-    const bool start0 = (g & wmask) == 0;
-    const int32_t dest0 = start0 ? __ldg(Ip + (g >> b)) : 0;
-    const int n = static_cast<int>(min64(kT, s_end - g));  // < 8 only in a part's last tile
-    bool live[kT];
-#pragma unroll
-    for (int u = 0; u < kT; ++u) {
-      const bool rs = ((g + u) & wmask) == 0;
-      live[u] = u < n && (rs || col[u] != (u ? col[u - 1] : last_col));
-    }
-    last_col = col[kT - 1];
-#pragma unroll
-    for (int ub = 0; ub < kT; ub += UG) {
-      Frag<VEC, kScalar> xv[UG];
-#pragma unroll
-      for (int u = 0; u < UG; ++u)
-        if (live[ub + u]) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0);
-#pragma unroll
-      for (int u = 0; u < UG; ++u) {
-        const int uu = ub + u;
-        if (uu == 0) {
-          if (start0) row_start(g, dest0);
-        } else if (uu < n && ((g + uu) & wmask) == 0) {  // rows narrower than a tile (W < 8)
-          row_start(g + uu, __ldg(Ip + ((g + uu) >> b)));
-        }
-        if (live[uu]) fma_part(part, val[uu], xv[u]);
+    for (int gi = 0; gi < np; gi += kT) {
+      const int g = pbase + gi;
+      int32_t col[kT];
+      float val[kT];
+      {
+        const int4 c0 = reinterpret_cast<const int4*>(sJ + gi)[0];  // broadcast LDS.128
+        const int4 c1 = reinterpret_cast<const int4*>(sJ + gi)[1];
+        const float4 v0 = reinterpret_cast<const float4*>(sV + gi)[0];
+        const float4 v1 = reinterpret_cast<const float4*>(sV + gi)[1];
+        col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
+        col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
+        val[0] = v0.x; val[1] = v0.y; val[2] = v0.z; val[3] = v0.w;
+        val[4] = v1.x; val[5] = v1.y; val[6] = v1.z; val[7] = v1.w;
       }
+      // Destination of a row starting at this tile's first slot, fetched before the gathers so
+      // its latency overlaps theirs.
+      const bool start0 = (g & wmask) == 0;
+      const int32_t dest0 = start0 ? __ldg(Ip + (g >> b)) : 0;
+      const int n = min(kT, s_end - g);  // < 8 only in a part's last tile
+      bool live[kT];
+#pragma unroll
+      for (int u = 0; u < kT; ++u) {
+        const bool rs = ((g + u) & wmask) == 0;
+        live[u] = u < n && (rs || col[u] != (u ? col[u - 1] : last_col));
+      }
+      last_col = col[kT - 1];
+#pragma unroll
+      for (int ub = 0; ub < kT; ub += UG) {
+        Frag<VEC, kScalar> xv[UG];
+#pragma unroll
+        for (int u = 0; u < UG; ++u)
+          if (live[ub + u]) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0);
+#pragma unroll
+        for (int u = 0; u < UG; ++u) {
+          const int uu = ub + u;
+          if (uu == 0) {
+            if (start0) row_start(dest0);
+          } else if (uu < n && ((g + uu) & wmask) == 0) {  // rows narrower than a tile (W < 8)
+            row_start(__ldg(Ip + ((g + uu) >> b)));
+          }
+          if (live[uu]) fma_part(part, val[uu], xv[u]);
+        }
+      }
+      absorb(acc, part);
     }
-    absorb(acc, part);
   }
-  }
-  if (cur_row >= 0) flush(true);
+  if (started) flush(true);
 }
 
 // Fix-up of split runs that cross chunk boundaries: a deterministic two-level tree.

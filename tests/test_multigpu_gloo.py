@@ -35,17 +35,21 @@ def _worker(rank, world, port, out_path):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     m = S.generate_matrix("powerlaw", 6000, 5000, 0, 0, 0, 20.0, 3)
-    plan = RowShardPlan(m, world)
-    sh = plan.shard(rank)
+    plan = RowShardPlan(m, world, chunks=3)  # bench.py's overlapped layout
     k = S.hyb_auto_k(m)
-    parts, _ = P.hyb_decompose(sh.rows, sh.cols, sh.indptr, sh.indices, sh.values, 1, k)
     X = S.dense_int((m.cols, 16), 5)
-    y = P.spmm_hyb_refnum(sh.rows, parts, X)
-    buf = torch.zeros((plan.max_rows, 16), dtype=torch.float32)
-    buf[: sh.rows] = torch.from_numpy(y)
-    gathered = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(gathered, buf)
-    full = plan.unpad(torch.cat(gathered, 0)).numpy()
+    full_buf = torch.zeros((plan.padded_rows, 16), dtype=torch.float32)
+    for c in range(plan.chunks):  # chunk c computed, then its all-gather (async on a GPU)
+        sh = plan.chunk(rank, c)
+        parts, _ = P.hyb_decompose(sh.rows, sh.cols, sh.indptr, sh.indices, sh.values, 1, k)
+        y = P.spmm_hyb_refnum(sh.rows, parts, X)
+        buf = torch.zeros((plan.max_rows, 16), dtype=torch.float32)
+        buf[: sh.rows] = torch.from_numpy(y)
+        gathered = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(gathered, buf)
+        s0 = plan.slot(c, 0)
+        full_buf[s0: s0 + world * plan.max_rows] = torch.cat(gathered, 0)
+    full = plan.unpad(full_buf).numpy()
     if rank == 0:
         np.save(out_path, full)
     dist.barrier()
