@@ -165,19 +165,25 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 #define STRATA_SPMM_MINB32 3
 #endif
 
-// Main kernel.  Per virtual warp: one chunk of whole ELL rows, walked in 8-slot tiles.  Each
-// tile's 8 columns and 8 values are fetched with two uniform 128-bit loads each (all lanes of
-// the VW read the same 16 B, one L1 wavefront: no shuffles), so slot positions are
-// compile-time; pad slots (a repeat of the previous column inside a row, the reference's own
-// rule, storage.cpp:528) are skipped by predication; UG gathers are in flight per lane.
+// Main kernel.  Per virtual warp (VW): one chunk of whole ELL rows, processed in pieces of
+// <= 256 slots:
+//   1. stage: the piece's J / V tiles and the output rows of its ELL rows are copied to the
+//      VW's shared-memory buffer with one burst of cp.async per lane (one memory round trip);
+//   2. compact (in place): pad slots — a repeat of the previous column inside a row, the
+//      reference's own rule (storage.cpp:528) — are dropped with a VW-wide scan, and the first
+//      slot of every ELL row is flagged in bit 31 of its column;
+//   3. consume: batches of 8 real slots are read with broadcast 128-bit shared loads (no
+//      shuffles), their X rows gathered UG at a time (128-bit per lane), and accumulated.
 template <int L, int VEC, bool kScalar>
 __global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar) ? STRATA_SPMM_MINB32 : 2))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
-  constexpr int kT = 8;  // slots per index tile
+  constexpr int kT = 8;  // real slots per consume batch / slots per lane per compaction round
 #ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
 #define STRATA_SPMM_UG 8
 #endif
   constexpr int UG = kScalar ? 8 : (VEC == 1 ? STRATA_SPMM_UG : (VEC == 2 ? 4 : 2));
+  constexpr int kRound = kT * L;  // slots examined per compaction round
+  constexpr int32_t kRowFlag = static_cast<int32_t>(0x80000000u);
   const int lane = threadIdx.x & (L - 1);
   const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
   if (vw >= a.total_chunks) return;
@@ -204,7 +210,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   }
 
   Acc<VEC, kScalar> acc;    // f64 running sum of the current output row (group)
-  Frag<VEC, kScalar> part;  // f32 partial of the current tile
+  Frag<VEC, kScalar> part;  // f32 partial of the current batch
   acc.zero();
   part.zero();
   bool started = false;
@@ -236,69 +242,108 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
     started = true;
   };
 
-  // This VW's shared-memory staging buffer: one 256-slot piece of J then of V (2 KB).
+  // This VW's staging buffer: J, V and the output rows of one piece (3 KB).
   extern __shared__ int4 spmm_smem[];
-  int32_t* sJ = reinterpret_cast<int32_t*>(spmm_smem) + (threadIdx.x / L) * (2 * kPiece);
+  int32_t* sJ = reinterpret_cast<int32_t*>(spmm_smem) + (threadIdx.x / L) * (3 * kPiece);
   float* sV = reinterpret_cast<float*>(sJ + kPiece);
+  int32_t* sD = sJ + 2 * kPiece;
   const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
 
   const int s_end = r1 << b;
-  int32_t last_col = -1;
+  int32_t carry_col = -1;  // column of the slot before the current compaction round
+  int row = r0 - 1;        // ELL row of the latest row start consumed
   for (int pbase = r0 << b; pbase < s_end; pbase += kPiece) {
-    // Stage the piece's index and value tiles with one burst of 16-byte cp.async per lane
-    // (a single memory round trip for up to 256 slots; parts are 8-slot aligned and padded, so
-    // rounding the copy up to whole tiles stays in bounds).
     const int np = min(kPiece, s_end - pbase);
-    const int nq = ((np + kT - 1) / kT) * (kT / 4);  // 16-byte chunks per array
-    __syncwarp(vmask);  // previous piece fully consumed by every lane
+    const int nq = ((np + kT - 1) / kT) * (kT / 4);  // 16-byte chunks per array (whole tiles:
+                                                     // parts are 8-slot aligned and padded)
+    const int row_lo = pbase >> b;
+    const int nrow = ((pbase + np - 1) >> b) - row_lo + 1;
+    __syncwarp(vmask);  // previous piece fully consumed
     for (int q = lane; q < nq; q += L) {
       tc_cp_async16(sJ + 4 * q, Jp + pbase + 4 * q);
       tc_cp_async16(sV + 4 * q, Vp + pbase + 4 * q);
     }
+    for (int q = lane; q < nrow; q += L) ::strata_b200::tc::cp_async4(sD + q, Ip + row_lo + q);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncwarp(vmask);
-    for (int gi = 0; gi < np; gi += kT) {
-      const int g = pbase + gi;
-      int32_t col[kT];
-      float val[kT];
+
+    // Compaction, in place (an entry only ever moves to a lower index; every lane reads its
+    // 8 slots before any lane writes).
+    int nreal = 0;
+    for (int rb = 0; rb < np; rb += kRound) {
+      const int s0 = rb + lane * kT;
+      int32_t cc[kT];
+      float vv[kT];
       {
-        const int4 c0 = reinterpret_cast<const int4*>(sJ + gi)[0];  // broadcast LDS.128
-        const int4 c1 = reinterpret_cast<const int4*>(sJ + gi)[1];
-        const float4 v0 = reinterpret_cast<const float4*>(sV + gi)[0];
-        const float4 v1 = reinterpret_cast<const float4*>(sV + gi)[1];
-        col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
-        col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
-        val[0] = v0.x; val[1] = v0.y; val[2] = v0.z; val[3] = v0.w;
-        val[4] = v1.x; val[5] = v1.y; val[6] = v1.z; val[7] = v1.w;
+        const int4 c0 = reinterpret_cast<const int4*>(sJ + s0)[0];
+        const int4 c1 = reinterpret_cast<const int4*>(sJ + s0)[1];
+        const float4 v0 = reinterpret_cast<const float4*>(sV + s0)[0];
+        const float4 v1 = reinterpret_cast<const float4*>(sV + s0)[1];
+        cc[0] = c0.x; cc[1] = c0.y; cc[2] = c0.z; cc[3] = c0.w;
+        cc[4] = c1.x; cc[5] = c1.y; cc[6] = c1.z; cc[7] = c1.w;
+        vv[0] = v0.x; vv[1] = v0.y; vv[2] = v0.z; vv[3] = v0.w;
+        vv[4] = v1.x; vv[5] = v1.y; vv[6] = v1.z; vv[7] = v1.w;
       }
-      // Destination of a row starting at this tile's first slot, fetched before the gathers so
-      // its latency overlaps theirs.
-      const bool start0 = (g & wmask) == 0;
-      const int32_t dest0 = start0 ? __ldg(Ip + (g >> b)) : 0;
-      const int n = min(kT, s_end - g);  // < 8 only in a part's last tile
-      bool live[kT];
+      int32_t prev = __shfl_up_sync(vmask, cc[kT - 1], 1, L);
+      if (lane == 0) prev = carry_col;
+      unsigned real = 0, rstart = 0;
 #pragma unroll
       for (int u = 0; u < kT; ++u) {
-        const bool rs = ((g + u) & wmask) == 0;
-        live[u] = u < n && (rs || col[u] != (u ? col[u - 1] : last_col));
+        const int g = pbase + s0 + u;
+        const bool rs = (g & wmask) == 0;
+        const bool in = s0 + u < np;
+        if (in && (rs || cc[u] != (u ? cc[u - 1] : prev))) real |= 1u << u;
+        if (rs) rstart |= 1u << u;
       }
-      last_col = col[kT - 1];
+      const int cnt = __popc(real);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < L; o <<= 1) {
+        const int t = __shfl_up_sync(vmask, incl, o, L);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(vmask, incl, L - 1, L);
+      carry_col = __shfl_sync(vmask, cc[kT - 1], L - 1, L);
+      int pos = nreal + incl - cnt;
+      __syncwarp(vmask);
+#pragma unroll
+      for (int u = 0; u < kT; ++u)
+        if (real & (1u << u)) {
+          sJ[pos] = cc[u] | ((rstart >> u) & 1u ? kRowFlag : 0);
+          sV[pos] = vv[u];
+          ++pos;
+        }
+      nreal += total;
+    }
+    __syncwarp(vmask);
+
+    // Consume the real slots, 8 per batch.
+    for (int e0 = 0; e0 < nreal; e0 += kT) {
+      int32_t col[kT];
+      {
+        const int4 c0 = reinterpret_cast<const int4*>(sJ + e0)[0];  // broadcast LDS.128
+        const int4 c1 = reinterpret_cast<const int4*>(sJ + e0)[1];
+        col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
+        col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
+      }
+      const int n = min(kT, nreal - e0);
+      unsigned starts = 0;  // row-start flags; the columns die once the gathers are issued
+#pragma unroll
+      for (int u = 0; u < kT; ++u) starts |= (col[u] < 0 ? 1u : 0u) << u;
 #pragma unroll
       for (int ub = 0; ub < kT; ub += UG) {
         Frag<VEC, kScalar> xv[UG];
 #pragma unroll
         for (int u = 0; u < UG; ++u)
-          if (live[ub + u]) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0);
+          if (ub + u < n) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u] & 0x7fffffff, d, lane, feat0);
 #pragma unroll
         for (int u = 0; u < UG; ++u) {
           const int uu = ub + u;
-          if (uu == 0) {
-            if (start0) row_start(dest0);
-          } else if (uu < n && ((g + uu) & wmask) == 0) {  // rows narrower than a tile (W < 8)
-            row_start(__ldg(Ip + ((g + uu) >> b)));
+          if (uu < n) {
+            if ((starts >> uu) & 1u) row_start(sD[++row - row_lo]);
+            fma_part(part, sV[e0 + uu], xv[u]);  // broadcast LDS
           }
-          if (live[uu]) fma_part(part, val[uu], xv[u]);
         }
       }
       absorb(acc, part);
@@ -434,7 +479,7 @@ void launch_variant(const SpmmArgs& args, long long total_chunks, long long d, c
   const long long threads = total_chunks * L;
   const unsigned blocks = static_cast<unsigned>((threads + kBlock - 1) / kBlock);
   dim3 grid(blocks, kScalar ? static_cast<unsigned>((d + 31) / 32) : 1u);
-  constexpr int smem = (kBlock / L) * 2 * kPiece * 4;  // 2 KB staging per virtual warp
+  constexpr int smem = (kBlock / L) * 3 * kPiece * 4;  // 3 KB staging per virtual warp
   static bool configured = false;  // host-side, once per instantiation
   if (!configured) {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(spmm_hyb_kernel<L, VEC, kScalar>,
