@@ -63,6 +63,25 @@ const strata_hyb_impl& hyb_of(const strata_hyb* h) {
 namespace strata_b200 {
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+// Stream-ordered workspaces (cudaMallocAsync) come from the device's default pool; keep freed
+// blocks cached there instead of returning them to the driver at every synchronisation, so
+// per-call temporaries cost a pool hit, not a re-map.
+void* workspace_alloc(size_t bytes, cudaStream_t s) {
+  static bool configured[64] = {};
+  int dev = 0;
+  STRATA_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 64 && !configured[dev]) {
+    cudaMemPool_t pool;
+    STRATA_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    STRATA_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured[dev] = true;
+  }
+  void* p = nullptr;
+  STRATA_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(bytes, 1), s));
+  return p;
+}
+
 int num_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)

@@ -144,6 +144,8 @@ void ell_from_csr_launch(const int32_t* indptr, const int32_t* indices, const fl
                          cudaStream_t s);
 
 int num_sms();
+// Stream-ordered scratch from the device pool (kept cached across calls); free with cudaFreeAsync.
+void* workspace_alloc(size_t bytes, cudaStream_t s);
 // Thread-local message returned by strata_last_error() (shared by every translation unit).
 void set_last_error(const std::string& msg);
 

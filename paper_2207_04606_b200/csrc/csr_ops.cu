@@ -198,7 +198,7 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
   if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "sddmm: d must be >= 1");
   if (nnz == 0) return;
   float* Yt = nullptr;
-  STRATA_CUDA_CHECK(cudaMallocAsync(&Yt, sizeof(float) * cols * d, s));
+  Yt = static_cast<float*>(workspace_alloc(sizeof(float) * cols * d, s));
   {
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((d + 31) / 32));
     transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(Y, Yt, d, cols);
@@ -282,7 +282,7 @@ void ell_from_csr_launch(const int32_t* indptr, const int32_t* indices, const fl
   if (w > cols) throw ApiError(STRATA_ERR_USAGE, "ELL width exceeds column count");
   if (rows == 0) return;
   unsigned long long* bad = nullptr;
-  STRATA_CUDA_CHECK(cudaMallocAsync(&bad, sizeof(unsigned long long), s));
+  bad = static_cast<unsigned long long*>(workspace_alloc(sizeof(unsigned long long), s));
   STRATA_CUDA_CHECK(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), s));
   ell_capacity_kernel<<<static_cast<unsigned>(std::min<long long>((rows + 255) / 256, 4096)), 256, 0, s>>>(
       indptr, rows, w, bad);

@@ -216,14 +216,14 @@ extern "C" int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, cons
     const long long max_tiles = (nnz + kEdges - 1) / kEdges + R;  // upper bound on tiles
     long long *ntiles = nullptr, *tile_start = nullptr;
     int32_t* tile_rel = nullptr;
-    STRATA_CUDA_CHECK(cudaMallocAsync(&ntiles, sizeof(long long) * (R + 1), s));
-    STRATA_CUDA_CHECK(cudaMallocAsync(&tile_start, sizeof(long long) * (R + 1), s));
-    STRATA_CUDA_CHECK(cudaMallocAsync(&tile_rel, sizeof(int32_t) * max_tiles, s));
+    ntiles = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
+    tile_start = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
+    tile_rel = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * max_tiles, s));
     rel_tiles_kernel<<<static_cast<unsigned>((R + 1 + 255) / 256), 256, 0, s>>>(rel_ptr, R, ntiles);
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, ntiles, tile_start, R + 1, s);
     void* tmp = nullptr;
-    STRATA_CUDA_CHECK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
+    tmp = workspace_alloc(tb, s);
     cub::DeviceScan::ExclusiveSum(tmp, tb, ntiles, tile_start, R + 1, s);
     tile_rel_kernel<<<static_cast<unsigned>(R), 256, 0, s>>>(tile_start, R, tile_rel);
     STRATA_CUDA_CHECK(cudaGetLastError());
