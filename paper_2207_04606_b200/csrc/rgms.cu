@@ -114,7 +114,9 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
     for (int q = 0; q < kPer; ++q) {
       const int c = tid + q * kThreads;
       const int e = c / (DIN / 8), kc = c % (DIN / 8);
+#ifndef STRATA_RGMS_KO_GATHER
       tc::cp_async16(sA + (e >> 3) * kSboA + kc * 128 + (e & 7) * 16, X + jj[q] * DIN + kc * 8);
+#endif
     }
     const __nv_bfloat16* Wr = W + r * DIN * DOUT;
     for (int c = tid; c < DIN * (DOUT / 8); c += kThreads) {
@@ -136,6 +138,7 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
     __syncthreads();
     const long long e0 = s_e0[s];
     const int ne = s_ne[s];
+#ifndef STRATA_RGMS_KO_MMA
     if (tid == 0) {
       tc::fence_after_sync();
       const uint32_t a0 = tc::smem_u32(smem + s * SM::kStage);
@@ -146,12 +149,15 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
                      tc::make_desc(w0 + kk * 256, 128, kSboW), kIdesc, kk > 0);
       tc::mma_commit(&mbar);
     }
+#endif
     // Epilogue operands, fetched while the MMA runs.
     const int e = warp * 32 + lane;
     const bool valid = e < ne;
     const float a = valid ? __ldg(A + e0 + e) : 0.f;
     const long long drow = valid ? __ldg(dst + e0 + e) : 0;
+#ifndef STRATA_RGMS_KO_MMA
     tc::mbar_wait(&mbar, it & 1);
+#endif
     tc::fence_after_sync();
     float* y = Y + drow * DOUT;
 #pragma unroll
@@ -163,9 +169,14 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
         const int n = DOUT - c0 < 32 ? DOUT - c0 : 32;
 #pragma unroll
         for (int q = 0; q < 32; q += 4)
-          if (q < n)
+          if (q < n) {
+#ifndef STRATA_RGMS_KO_RED
             tc::red_add_v4(y + c0 + q, a * __uint_as_float(v[q]), a * __uint_as_float(v[q + 1]),
                            a * __uint_as_float(v[q + 2]), a * __uint_as_float(v[q + 3]));
+#else
+            reinterpret_cast<float4*>(y + c0 + q)[0] = make_float4(a * __uint_as_float(v[q]), 0.f, 0.f, 0.f);
+#endif
+          }
       }
     }
     tc::fence_before_sync();
