@@ -13,9 +13,12 @@
 // i.e. M = d (feature tile of 64 or 128), N = b = 32, K = b = 32 (two K=16 bf16 steps), with the
 // X tile as the MN-major A operand (X rows are feature-contiguous, so no transpose is needed)
 // and the block as the K-major B operand.  Accumulation over the block row stays in TMEM
-// (f32); a 4-stage cp.async ring streams block/X tiles while the MMAs of earlier blocks run,
-// and tcgen05.commit -> mbarrier recycles stages.  Epilogue: tcgen05.ld -> registers -> Y.
+// (f32).  A TMA producer thread streams blocks (bulk copy of a pre-arranged bf16 block) and
+// X tiles (TMA tensor tiles) through a 6-stage full/empty mbarrier ring to a single MMA-issuer
+// thread; tcgen05.commit recycles stages.  Epilogue: tcgen05.ld -> registers -> Y.
 #include <cub/cub.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cuda_bf16.h>
@@ -99,22 +102,35 @@ __global__ void bsr_scatter_kernel(const int32_t* __restrict__ indptr,
     }
     const long long pos = static_cast<long long>(lo) * b * b + (i % b) * b + (j % b);
     bv[pos] = values[q];
-    bvh[pos] = __float2bfloat16_rn(values[q]);
+    // The bf16 operand copy of a 32x32 block is stored pre-arranged in the UMMA K-major
+    // core-matrix layout (8x8 bf16 core matrices, K groups adjacent), so the SpMM moves each
+    // block into shared memory with a single 2 KB bulk copy.  Other block sizes: row-major.
+    const int ii = static_cast<int>(i % b), ji = static_cast<int>(j % b);
+    const long long hpos = b == 32 ? static_cast<long long>(lo) * 1024 + (ii >> 3) * 256 +
+                                         (ji >> 3) * 64 + (ii & 7) * 8 + (ji & 7)
+                                   : pos;
+    bvh[hpos] = __float2bfloat16_rn(values[q]);
   }
 }
 
 // ---- tensor-core SpMM ---------------------------------------------------------------------
 constexpr int kB = 32;        // block size served by the tensor-core path
-constexpr int kStages = 6;     // smem ring depth
-constexpr int kAhead = kStages - 2;  // blocks in flight: refilling stage j-2's slot leaves the
-                                     // just-issued MMA (j-1) off the critical path
+constexpr int kStages = 6;    // smem ring depth
 constexpr int kThreads = 128;
 constexpr int kMaxPre = 256;  // block-column indices of a block row preloaded into smem
 
+// Warp-specialised, mbarrier-pipelined block-row SpMM:
+//   warp 0 / lane 0  TMA producer: per block, one 2 KB bulk copy of the pre-arranged bf16 block
+//                    (K-major B operand) + d/8 TMA tiles {8 features x 32 rows} of X that land
+//                    exactly in the MN-major A-operand core-matrix layout; completion is
+//                    counted in bytes on full[s]; the slot is reused once empty[s] fires.
+//   warp 1 / lane 0  MMA issuer: waits full[s], issues tcgen05.mma (M = feature tile, N = 32
+//                    block rows, K = 2 x 16), tcgen05.commit -> empty[s]; final commit -> done.
+//   all 4 warps      epilogue: tcgen05.ld of the TMEM accumulator -> Y rows.
 template <int D>  // feature count, 64 or a multiple of 128 (<= 512)
-__global__ void __launch_bounds__(kThreads)
-bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restrict__ jo_indices,
-                   const __nv_bfloat16* __restrict__ bvals, const __nv_bfloat16* __restrict__ X,
+__global__ void __launch_bounds__(kThreads, 1)
+bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ jo_indptr,
+                   const int32_t* __restrict__ jo_indices, const __nv_bfloat16* __restrict__ bvals,
                    float* __restrict__ Y) {
   constexpr int kM = D == 64 ? 64 : 128;         // UMMA M (feature tile)
   constexpr int kTiles = D / kM;                  // feature tiles
@@ -126,7 +142,7 @@ bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restr
   static_assert(D == 64 || (D % 128 == 0 && D <= 512), "unsupported feature size");
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mbar[kStages];
+  __shared__ uint64_t full[kStages], empty[kStages], done;
   __shared__ uint32_t tmem_slot;
   __shared__ int32_t s_cols[kMaxPre];
 
@@ -134,10 +150,13 @@ bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restr
   const long long br = blockIdx.x;
   const int q0 = jo_indptr[br], nblk = jo_indptr[br + 1] - q0;
   for (int j = tid; j < nblk && j < kMaxPre; j += kThreads) s_cols[j] = jo_indices[q0 + j];
-
   if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) tc::mbar_init(&mbar[s], 1);
+  if (tid == 32) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&done, 1);
     tc::mbar_fence_init();
   }
   tc::fence_before_sync();
@@ -145,61 +164,50 @@ bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restr
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
 
-  // Stage loader: block (K-major B operand) and X tile (MN-major A operand), 16 B chunks.
-  auto load_stage = [&](int j, int s) {
-    uint8_t* sa = smem + s * kStageB;  // block
-    uint8_t* sx = sa + kAB;            // X tile
-    const int q = q0 + j;
-    const __nv_bfloat16* gb = bvals + static_cast<long long>(q) * kB * kB;
-    for (int c = tid; c < kB * kB / 8; c += kThreads) {  // chunk c: row ii = c/4, k-group c%4
-      const int ii = c >> 2, kg = c & 3;
-      tc::cp_async16(sa + (ii >> 3) * 512 + kg * 128 + (ii & 7) * 16, gb + ii * kB + kg * 8);
-    }
-    const long long row0 = static_cast<long long>(j < kMaxPre ? s_cols[j] : jo_indices[q]) * kB;
-    for (int c = tid; c < kB * D / 8; c += kThreads) {  // chunk c: X row ji, feature group fg
-      const int ji = c / (D / 8), fg = c % (D / 8);
-      tc::cp_async16(sx + fg * 512 + (ji >> 3) * 128 + (ji & 7) * 16,
-                     X + (row0 + ji) * D + fg * 8);
-    }
-  };
-
-  for (int s = 0; s < kAhead; ++s) {
-    if (s < nblk) load_stage(s, s);
-    tc::cp_async_commit();
-  }
-  for (int j = 0; j < nblk; ++j) {
-    const int s = j % kStages;
-    const int jn = j + kAhead;  // refills the slot of block j-2 (jn % kStages == (j-2) % kStages)
-    if (jn < nblk) {
-      if (j >= 2) tc::mbar_wait(&mbar[(j - 2) % kStages], ((j - 2) / kStages) & 1);
-      load_stage(jn, jn % kStages);
-    }
-    tc::cp_async_commit();
-    tc::cp_async_wait<kAhead>();  // block j's group has landed
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after_sync();
-      const uint32_t sa = tc::smem_u32(smem + s * kStageB);
-      const uint32_t sx = sa + kAB;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      tc::prefetch_tensormap(&xmap);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kStages;
+        if (j >= kStages) tc::mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
+        uint8_t* sa = smem + s * kStageB;
+        tc::mbar_arrive_expect_tx(&full[s], kStageB);
+        tc::bulk_copy_g2s(sa, bvals + static_cast<long long>(q0 + j) * kB * kB, kAB, &full[s]);
+        const int col = j < kMaxPre ? s_cols[j] : jo_indices[q0 + j];
 #pragma unroll
-      for (int t = 0; t < kTiles; ++t) {
-#pragma unroll
-        for (int kk = 0; kk < kB / 16; ++kk) {
-          // A = X tile (MN-major): feature tile t starts kM/8 feature groups * 512 B later.
-          const uint64_t adesc = tc::make_desc(sx + t * (kM / 8) * 512 + kk * 256, 128, 512);
-          const uint64_t bdesc = tc::make_desc(sa + kk * 256, 128, 512);
-          tc::mma_bf16(tmem + t * kB, adesc, bdesc, kIdesc, j > 0 || kk > 0);
-        }
+        for (int fg = 0; fg < D / 8; ++fg)
+          tc::tma_load_2d(sa + kAB + fg * 512, &xmap, fg * 8, col * kB, &full[s]);
       }
-      tc::mma_commit(&mbar[s]);
     }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % kStages;
+        tc::mbar_wait(&full[s], (j / kStages) & 1);
+        tc::fence_after_sync();
+        const uint32_t sa = tc::smem_u32(smem + s * kStageB);
+        const uint32_t sx = sa + kAB;
+#pragma unroll
+        for (int t = 0; t < kTiles; ++t) {
+#pragma unroll
+          for (int kk = 0; kk < kB / 16; ++kk) {
+            // A = X tile (MN-major): feature tile t starts kM/8 feature groups * 512 B later.
+            const uint64_t adesc = tc::make_desc(sx + t * (kM / 8) * 512 + kk * 256, 128, 512);
+            const uint64_t bdesc = tc::make_desc(sa + kk * 256, 128, 512);
+            tc::mma_bf16(tmem + t * kB, adesc, bdesc, kIdesc, j > 0 || kk > 0);
+          }
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      if (nblk > 0) tc::mma_commit(&done);
+    }
+    __syncwarp();
   }
 
   float* yrow = Y + br * kB * D;
   if (nblk > 0) {
-    const int jl = nblk - 1;
-    tc::mbar_wait(&mbar[jl % kStages], (jl / kStages) & 1);
+    tc::mbar_wait(&done, 0);
     tc::fence_after_sync();
 #pragma unroll
     for (int t = 0; t < kTiles; ++t) {
@@ -221,13 +229,43 @@ bsr_spmm_tc_kernel(const int32_t* __restrict__ jo_indptr, const int32_t* __restr
   if (warp == 0) tc::tmem_dealloc<kCols>(tmem);
 }
 
+// TMA descriptor of X viewed as [rows][D] bf16, box {8 features, 32 rows} (16 B x 32 = one
+// 512 B MN-major core-matrix column of the A operand).
+CUtensorMap make_x_map(const __nv_bfloat16* X, long long rows, int D) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    STRATA_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(D) * 2};
+  const cuuint32_t box[2] = {8, kB};
+  const cuuint32_t estride[2] = {1, 1};
+  const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(X),
+                            gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return map;
+}
+
 template <int D>
 void launch_bsr(const strata_bsr& h, const __nv_bfloat16* X, float* Y, cudaStream_t s) {
   constexpr int smem = kStages * (kB * kB * 2 + kB * D * 2);
-  STRATA_CUDA_CHECK(cudaFuncSetAttribute(bsr_spmm_tc_kernel<D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  static bool configured = false;
+  if (!configured) {
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(bsr_spmm_tc_kernel<D>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  const CUtensorMap xmap = make_x_map(X, h.nb * kB, D);
   bsr_spmm_tc_kernel<D><<<static_cast<unsigned>(h.mb), kThreads, smem, s>>>(
-      h.indptr.p, h.indices.p, h.vals_bf.p, X, Y);
+      xmap, h.indptr.p, h.indices.p, h.vals_bf.p, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
 }
 

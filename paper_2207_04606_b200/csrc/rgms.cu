@@ -41,13 +41,26 @@ __global__ void rel_tiles_kernel(const int32_t* __restrict__ rel_ptr, long long 
   if (r == R) ntiles[R] = 0;
 }
 
-// tile_rel[t] = relation of tile t (one CTA per relation).
-__global__ void tile_rel_kernel(const long long* __restrict__ tile_start, long long R,
-                                int32_t* __restrict__ tile_rel) {
+// tile_rel[t] = relation of tile t; key[t] = first destination row of tile t (one CTA per
+// relation).  Unused tail entries of key (t >= tile_start[R]) are set to INT32_MAX.
+__global__ void tile_rel_kernel(const int32_t* __restrict__ rel_ptr,
+                                const long long* __restrict__ tile_start, long long R,
+                                const int32_t* __restrict__ dst, long long max_tiles,
+                                int32_t* __restrict__ tile_rel, int32_t* __restrict__ key,
+                                int32_t* __restrict__ ids) {
   const long long r = blockIdx.x;
-  if (r >= R) return;
-  for (long long t = tile_start[r] + threadIdx.x; t < tile_start[r + 1]; t += blockDim.x)
-    tile_rel[t] = static_cast<int32_t>(r);
+  if (r < R) {
+    for (long long t = tile_start[r] + threadIdx.x; t < tile_start[r + 1]; t += blockDim.x) {
+      tile_rel[t] = static_cast<int32_t>(r);
+      key[t] = dst[rel_ptr[r] + (t - tile_start[r]) * kEdges];
+      ids[t] = static_cast<int32_t>(t);
+    }
+  } else {  // block R: the padding tail
+    for (long long t = tile_start[R] + threadIdx.x; t < max_tiles; t += blockDim.x) {
+      key[t] = INT32_MAX;
+      ids[t] = static_cast<int32_t>(t);
+    }
+  }
 }
 
 template <int DIN, int DOUT>
@@ -61,7 +74,7 @@ struct RgmsSmem {
 template <int DIN, int DOUT>
 __global__ void __launch_bounds__(kThreads)
 rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict__ tile_start,
-               const int32_t* __restrict__ tile_rel, long long R,
+               const int32_t* __restrict__ tile_rel, const int32_t* __restrict__ order, long long R,
                const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
                const float* __restrict__ A, const __nv_bfloat16* __restrict__ X,
                const __nv_bfloat16* __restrict__ W, float* __restrict__ Y) {
@@ -92,8 +105,12 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
 
-  // Issue the gathers of tile t into stage s (no wait).
-  auto load_tile = [&](long long t, int s) {
+  // Issue the gathers of the p-th tile of the schedule into stage s (no wait).  Tiles run in
+  // order of their first destination row, so the CTAs in flight scatter into a narrow window
+  // of Y that stays in L2 (atomics into L2-missing rows were the bottleneck: 3.6 ms -> see
+  // DESIGN.md §4.5).
+  auto load_tile = [&](long long p, int s) {
+    const long long t = order[p];
     const long long r = tile_rel[t];
     const long long e0 = rel_ptr[r] + (t - tile_start[r]) * kEdges;
     const int ne = static_cast<int>(min64(kEdges, rel_ptr[r + 1] - e0));
@@ -187,7 +204,7 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
 
 template <int DIN, int DOUT>
 void launch_rgms(const int32_t* rel_ptr, const long long* tile_start, const int32_t* tile_rel,
-                 long long R, long long max_tiles, const int32_t* dst, const int32_t* src,
+                 const int32_t* order, long long R, long long max_tiles, const int32_t* dst, const int32_t* src,
                  const float* A, const __nv_bfloat16* X, const __nv_bfloat16* W, float* Y,
                  cudaStream_t s) {
   constexpr int smem = RgmsSmem<DIN, DOUT>::kBytes;
@@ -195,7 +212,7 @@ void launch_rgms(const int32_t* rel_ptr, const long long* tile_start, const int3
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const long long grid = std::min<long long>(max_tiles, static_cast<long long>(num_sms()) * kCtasPerSm);
   rgms_tc_kernel<DIN, DOUT><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(
-      rel_ptr, tile_start, tile_rel, R, dst, src, A, X, W, Y);
+      rel_ptr, tile_start, tile_rel, order, R, dst, src, A, X, W, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -213,8 +230,8 @@ extern "C" int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, cons
     STRATA_CUDA_CHECK(cudaGetDevice(&dev));
     STRATA_CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
     if (major != 10) throw ApiError(STRATA_ERR_CUDA, "strata_b200 kernels are built for sm_100a");
-    const int key = static_cast<int>(d_in * 1000 + d_out);
-    switch (key) {
+    const int dims = static_cast<int>(d_in * 1000 + d_out);
+    switch (dims) {
       case 16016: case 16032: case 32016: case 32032: case 32064: case 64032: case 64064:
       case 32128: case 64128: break;
       default:
@@ -236,21 +253,34 @@ extern "C" int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, cons
     void* tmp = nullptr;
     tmp = workspace_alloc(tb, s);
     cub::DeviceScan::ExclusiveSum(tmp, tb, ntiles, tile_start, R + 1, s);
-    tile_rel_kernel<<<static_cast<unsigned>(R), 256, 0, s>>>(tile_start, R, tile_rel);
+    int32_t* key = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * max_tiles * 2, s));
+    int32_t* ids = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * max_tiles * 2, s));
+    tile_rel_kernel<<<static_cast<unsigned>(R + 1), 256, 0, s>>>(rel_ptr, tile_start, R, dst,
+                                                                 max_tiles, tile_rel, key, ids);
+    size_t sb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sb, key, key + max_tiles, ids, ids + max_tiles,
+                                    max_tiles, 0, 32, s);
+    void* stmp = workspace_alloc(sb, s);
+    cub::DeviceRadixSort::SortPairs(stmp, sb, key, key + max_tiles, ids, ids + max_tiles,
+                                    max_tiles, 0, 32, s);
+    const int32_t* order = ids + max_tiles;
     STRATA_CUDA_CHECK(cudaGetLastError());
     const auto* X = static_cast<const __nv_bfloat16*>(X_bf16);
     const auto* W = static_cast<const __nv_bfloat16*>(W_bf16);
 #define STRATA_RGMS_CASE(I, O)                                                                \
   case I * 1000 + O:                                                                          \
-    launch_rgms<I, O>(rel_ptr, tile_start, tile_rel, R, max_tiles, dst, src, A, X, W, Y, s); \
+    launch_rgms<I, O>(rel_ptr, tile_start, tile_rel, order, R, max_tiles, dst, src, A, X, W, Y, s); \
     break;
-    switch (key) {
+    switch (dims) {
       STRATA_RGMS_CASE(16, 16) STRATA_RGMS_CASE(16, 32) STRATA_RGMS_CASE(32, 16)
       STRATA_RGMS_CASE(32, 32) STRATA_RGMS_CASE(32, 64) STRATA_RGMS_CASE(64, 32)
       STRATA_RGMS_CASE(64, 64) STRATA_RGMS_CASE(32, 128) STRATA_RGMS_CASE(64, 128)
     }
 #undef STRATA_RGMS_CASE
     STRATA_CUDA_CHECK(cudaFreeAsync(tmp, s));
+    STRATA_CUDA_CHECK(cudaFreeAsync(stmp, s));
+    STRATA_CUDA_CHECK(cudaFreeAsync(key, s));
+    STRATA_CUDA_CHECK(cudaFreeAsync(ids, s));
     STRATA_CUDA_CHECK(cudaFreeAsync(tile_rel, s));
     STRATA_CUDA_CHECK(cudaFreeAsync(ntiles, s));
     STRATA_CUDA_CHECK(cudaFreeAsync(tile_start, s));

@@ -133,6 +133,30 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory");
 }
 
+// ---- TMA / bulk async copies completing on an mbarrier (byte-counted) -----------------
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+               :: "r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+// 1D bulk copy global -> shared (size multiple of 16, both 16-byte aligned).
+__device__ __forceinline__ void bulk_copy_g2s(void* smem, const void* gmem, uint32_t bytes,
+                                              uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(mbar)) : "memory");
+}
+// 2D TMA tile load (tensor map in param / const / global space), coordinates innermost first.
+__device__ __forceinline__ void tma_load_2d(void* smem, const void* tmap, int c0, int c1,
+                                            uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n"
+      :: "r"(smem_u32(smem)), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(mbar)) : "memory");
+}
+__device__ __forceinline__ void prefetch_tensormap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];\n" :: "l"(tmap) : "memory");
+}
+
 // Vector reduction into global memory (sm_90+): 4 consecutive f32 added atomically.
 __device__ __forceinline__ void red_add_v4(float* gaddr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n"
