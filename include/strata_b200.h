@@ -171,11 +171,29 @@ int strata_ell_from_csr(const int32_t* indptr, const int32_t* indices, const flo
  * rel_ptr[R+1] (edges of relation r are [rel_ptr[r], rel_ptr[r+1])), dst[nnz] (row i),
  * src[nnz] (col j), A[nnz] f32.  X[n][d_in] bf16, W[R][d_in][d_out] bf16, Y[m][d_out] f32
  * (overwritten).  Per-relation gather -> tcgen05 GEMM (W_r in smem) -> scatter.
- * Requires d_in % 16 == 0, d_in <= 64, d_out % 16 == 0, d_out <= 256. */
+ * Requires (d_in, d_out) in {16,32,64} x {16,32,64,128}.  One-shot form of
+ * strata_rgms_plan + strata_rgms_run_bf16 + strata_rgms_destroy (synchronises `stream`). */
 int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, const int32_t* src,
                      const float* A, int64_t R, int64_t m, int64_t n, int64_t nnz,
                      const void* X_bf16, const void* W_bf16, float* Y, int64_t d_in,
                      int64_t d_out, void* stream);
+
+/* Plan / run split of the same operator — the build_rgms_pipeline (decomposition, once) /
+ * interpret (per run) split of driver.cpp:241-314.  The plan copies what it needs (src, A,
+ * rel_ptr) and adds each edge's position in the destination-sorted order (stable: a row's
+ * edges stay in relation order) and the row pointer dptr[m+1].  A run is two kernels:
+ * per-relation 128-edge tcgen05 tiles write message rows T[pos e] = A_e * (X[src e] W_r),
+ * then Y[i] = sum of T rows [dptr i, dptr i+1) — deterministic, no atomics.  The plan keeps
+ * a T workspace of nnz * d_out f32, grown on demand. */
+typedef struct strata_rgms strata_rgms;
+int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, const int32_t* src,
+                     const float* A, int64_t R, int64_t m, int64_t n, int64_t nnz,
+                     strata_rgms** out, void* stream);
+int strata_rgms_run_bf16(const strata_rgms* h, const void* X_bf16, const void* W_bf16, float* Y,
+                         int64_t d_in, int64_t d_out, void* stream);
+/* tiles_bound: upper bound on 128-edge tiles; t_bytes_per_dout: T bytes per output column. */
+int strata_rgms_info(const strata_rgms* h, int64_t* tiles_bound, int64_t* t_bytes_per_dout);
+int strata_rgms_destroy(strata_rgms* h);
 
 /* ---- multi-GPU helpers (host logic, no device work) -----------------------------------
  * Row-partition into `parts` contiguous row ranges balanced by nnz: cut p is the first row

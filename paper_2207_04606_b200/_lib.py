@@ -88,6 +88,10 @@ _sig("strata_bsr_destroy", C.c_int, vp)
 _sig("strata_bsr_spmm_bf16", C.c_int, vp, vp, vp, i64, vp)
 _sig("strata_ell_from_csr", C.c_int, vp, vp, vp, i64, i64, i64, vp, vp, vp)
 _sig("strata_rgms_bf16", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp, vp, i64, i64, vp)
+_sig("strata_rgms_plan", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, C.POINTER(vp), vp)
+_sig("strata_rgms_run_bf16", C.c_int, vp, vp, vp, vp, i64, i64, vp)
+_sig("strata_rgms_info", C.c_int, vp, i64p, i64p)
+_sig("strata_rgms_destroy", C.c_int, vp)
 _sig("strata_partition_rows", C.c_int, vp, i64, C.c_int, vp)
 
 # Every symbol include/strata_b200.h declares (checked by tests/test_abi.py).
@@ -101,5 +105,6 @@ EXPORTED = [
     "strata_hyb_dims", "strata_hyb_destroy", "strata_hyb_schedule_info", "strata_spmm_hyb_f32", "strata_spmm_hyb_f32_host",
     "strata_spmm_csr_f32", "strata_sddmm_csr_f32", "strata_bsr_from_csr", "strata_bsr_info",
     "strata_bsr_read", "strata_bsr_destroy", "strata_bsr_spmm_bf16", "strata_ell_from_csr",
-    "strata_rgms_bf16", "strata_partition_rows",
+    "strata_rgms_bf16", "strata_rgms_plan", "strata_rgms_run_bf16", "strata_rgms_info",
+    "strata_rgms_destroy", "strata_partition_rows",
 ]

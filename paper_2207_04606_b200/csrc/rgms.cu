@@ -1,25 +1,31 @@
-// rgms.cu — RGMS / RGCN aggregation on tcgen05 tensor cores: per-relation gather -> GEMM ->
-// scatter.
+// rgms.cu — RGMS / RGCN aggregation on tcgen05 tensor cores.
 //
 // Reference op (kernels.cpp:138-167, driver.cpp:241-314):
 //   Y[i, l] = sum_r sum_j A[r, i, j] * sum_k X[j, k] * W[r, k, l]
 // over the RelSparse layout (kernels.cpp:19-62): relation-major edges, rows ascending inside a
 // relation.  Flattened here to rel_ptr[R+1] / dst / src / A.
 //
-// Work unit: a tile of 128 edges of one relation r (tiles never straddle relations).
-//   gather   X[src[e]] rows (d_in bf16) into a K-major smem tile       (cp.async, 16 B chunks)
-//   stage    W_r [d_in][d_out] as the MN-major B operand                (cp.async)
-//   MMA      D[e][l] = sum_k X[src e][k] * W_r[k][l]   M = 128 edges, N = d_out, K = d_in,
-//            f32 accumulators in TMEM (d_in / 16 tcgen05.mma steps, one issuing thread)
-//   scatter  thread e: tcgen05.ld its row, scale by A[e], red.global.add.v4.f32 into Y[dst e]
-// Persistent CTAs (TMEM allocated once) walk tiles t = blockIdx.x, +gridDim.x, ... through a
-// two-stage smem ring: the next tile's index loads and row gathers are in flight while the
-// current tile's MMA and scatter run.  A precomputed tile -> relation map replaces any search.
-// The atomic scatter makes the summation order run-dependent; with the reference's integer
-// operands every partial sum is exact in f32, so results are still bitwise equal to it.
+// Two passes, no atomics, deterministic:
+//   plan   (once, like build_rgms_pipeline's decomposition): per-relation 128-edge tiles, and
+//          for every edge its position in the destination-sorted edge order (a stable radix
+//          sort on dst, so a row's edges stay in relation order) plus the row pointer dptr.
+//   pass 1 rgms_edge_gemm_kernel — per tile of 128 edges of one relation r:
+//            gather X[src e] (d_in bf16, K-major A operand) and W_r (MN-major B) via cp.async,
+//            tcgen05.mma M = 128 edges, N = d_out, K = d_in into TMEM (f32),
+//            epilogue: tcgen05.ld, scale by A[e], transpose through a per-warp smem tile and
+//            write the message row T[pos e] with coalesced 128-byte row stores.
+//   pass 2 rgms_row_sum_kernel — Y[i] = sum_{q in [dptr i, dptr i+1)} T[q] (contiguous rows,
+//          streamed once; empty rows write 0 as the reference's zero-initialised Y); rows with
+//          more than kLong edges go through fixed-shape chunk partials (long_chunk / finish).
+// Why not scatter with atomics: the 5.7M x d_out red.global.add into a Y larger than L2 was
+// the bottleneck of the first version (3.7 ms at C4); T costs 2 * nnz * d_out * 4 bytes of
+// streaming traffic instead.
+// Numerics: f32 products / tensor-core f32 accumulation over k, one f32 multiply by A, f32
+// row sums in relation order — exact on the reference's integer operands.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <memory>
 #include <cuda_bf16.h>
 
 #include "capi_internal.h"
@@ -28,11 +34,23 @@
 
 using namespace strata_b200;
 
+struct strata_rgms {
+  int device = 0;
+  int64_t R = 0, m = 0, n = 0, nnz = 0;
+  int64_t ntiles = 0;            // 128-edge tiles (tiles never straddle relations)
+  DevBuf<int32_t> edges;         // [ntiles][kTileWords] per-tile edge blocks (see below)
+  DevBuf<int32_t> dptr;          // [m+1] row pointer into the destination-sorted order
+  int nlong = 0, nchunks = 0;     // rows with > kLong edges and their kChunk-edge chunks
+  DevBuf<int32_t> long_rows;     // [nlong] ascending
+  DevBuf<int32_t> chunk_off;     // [nlong+1] first chunk of long row li
+  mutable DevBuf<float> T;       // [nnz][d_out] message rows, grown on demand
+  mutable DevBuf<float> partial; // [nchunks][d_out] long-row chunk sums
+};
+
 namespace {
 
 constexpr int kEdges = 128;  // UMMA M
 constexpr int kThreads = 128;
-constexpr int kCtasPerSm = 4;
 
 __global__ void rel_tiles_kernel(const int32_t* __restrict__ rel_ptr, long long R,
                                  long long* __restrict__ ntiles) {
@@ -41,59 +59,113 @@ __global__ void rel_tiles_kernel(const int32_t* __restrict__ rel_ptr, long long 
   if (r == R) ntiles[R] = 0;
 }
 
-// tile_rel[t] = relation of tile t; key[t] = first destination row of tile t (one CTA per
-// relation).  Unused tail entries of key (t >= tile_start[R]) are set to INT32_MAX.
-__global__ void tile_rel_kernel(const int32_t* __restrict__ rel_ptr,
-                                const long long* __restrict__ tile_start, long long R,
-                                const int32_t* __restrict__ dst, long long max_tiles,
-                                int32_t* __restrict__ tile_rel, int32_t* __restrict__ key,
-                                int32_t* __restrict__ ids) {
+__global__ void tile_rel_kernel(const long long* __restrict__ tile_start, long long R,
+                                int32_t* __restrict__ tile_rel) {
   const long long r = blockIdx.x;
-  if (r < R) {
-    for (long long t = tile_start[r] + threadIdx.x; t < tile_start[r + 1]; t += blockDim.x) {
-      tile_rel[t] = static_cast<int32_t>(r);
-      key[t] = dst[rel_ptr[r] + (t - tile_start[r]) * kEdges];
-      ids[t] = static_cast<int32_t>(t);
+  for (long long t = tile_start[r] + threadIdx.x; t < tile_start[r + 1]; t += blockDim.x)
+    tile_rel[t] = static_cast<int32_t>(r);
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ v, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    v[i] = static_cast<int32_t>(i);
+}
+
+// pos[order[q]] = q: edge e's slot in the destination-sorted order.
+__global__ void invert_kernel(const int32_t* __restrict__ order, long long n,
+                              int32_t* __restrict__ pos) {
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<long long>(gridDim.x) * blockDim.x)
+    pos[order[q]] = static_cast<int32_t>(q);
+}
+
+// dptr[i] = first q with sorted_dst[q] >= i (i = 0..m).
+__global__ void row_ptr_kernel(const int32_t* __restrict__ sorted_dst, long long nnz, long long m,
+                               int32_t* __restrict__ dptr) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i <= m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long lo = 0, hi = nnz;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (sorted_dst[mid] < i) lo = mid + 1; else hi = mid;
     }
-  } else {  // block R: the padding tail
-    for (long long t = tile_start[R] + threadIdx.x; t < max_tiles; t += blockDim.x) {
-      key[t] = INT32_MAX;
-      ids[t] = static_cast<int32_t>(t);
-    }
+    dptr[i] = static_cast<int32_t>(lo);
+  }
+}
+
+// Per-tile edge block in HBM (built by the plan; tile-padded so every block is 16-byte aligned
+// and one tile's indices are 97 contiguous 16-byte chunks):
+//   [0..3] header {relation r, edges ne, 0, 0}; [4..131] src; [132..259] pos (-1 = pad);
+//   [260..387] A (f32 bits).
+constexpr int kTileWords = 4 + 3 * kEdges;
+constexpr int kTileChunks = kTileWords / 4;  // 97
+
+__global__ void tile_edges_kernel(const int32_t* __restrict__ rel_ptr,
+                                  const long long* __restrict__ tile_start,
+                                  const int32_t* __restrict__ tile_rel, long long ntiles,
+                                  const int32_t* __restrict__ src, const int32_t* __restrict__ pos,
+                                  const float* __restrict__ A, int32_t* __restrict__ ed) {
+  for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+       s < ntiles * kEdges; s += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = s / kEdges;
+    const int i = static_cast<int>(s % kEdges);
+    const int r = tile_rel[t];
+    const long long base = rel_ptr[r] + (t - tile_start[r]) * kEdges;
+    const long long e = base + i;
+    const bool valid = e < rel_ptr[r + 1];
+    int32_t* blk = ed + t * kTileWords;
+    blk[4 + i] = valid ? src[e] : 0;
+    blk[4 + kEdges + i] = valid ? pos[e] : -1;
+    blk[4 + 2 * kEdges + i] = valid ? __float_as_int(A[e]) : 0;
+    if (i < 4)
+      blk[i] = i == 0 ? r : (i == 1 ? static_cast<int>(min64(kEdges, rel_ptr[r + 1] - base)) : 0);
   }
 }
 
 template <int DIN, int DOUT>
 struct RgmsSmem {
+  static constexpr int kStages = 3;  // X / W ring: tile j computes while j+1, j+2 land
+  static constexpr int kIdxSlots = 4;  // index ring: j (epilogue) .. j+3 (landing)
   static constexpr int kABytes = kEdges * DIN * 2;
   static constexpr int kWBytes = DIN * DOUT * 2;
   static constexpr int kStage = kABytes + kWBytes;
-  static constexpr int kBytes = 2 * kStage;
+  static constexpr int kIdxBytes = kTileWords * 4;
+  static constexpr int kNC = DOUT < 32 ? DOUT : 32;          // epilogue column chunk
+  static constexpr int kEpiBytes = (kThreads / 32) * 32 * kNC * 4;  // per-warp transpose tiles
+  static constexpr int kIdxOff = kStages * kStage;
+  static constexpr int kEpiOff = kIdxOff + kIdxSlots * kIdxBytes;
+  static constexpr int kBytes = kEpiOff + kEpiBytes;
 };
 
+// Pass 1.  CTA b processes tiles b, b + G, b + 2G, ... (G = gridDim.x).  cp.async groups are
+// committed in the order I0 I1 I2 X0 X1 | I3 X2 | I4 X3 | ...: before tile j, "all but the
+// newest group" guarantees X(j) and I(j+2) have landed, so the index block of tile j+3 and the
+// row gathers of tile j+2 are issued before tile j's MMA — two tiles of gathers in flight, no
+// dependent global load on the issue path.
 template <int DIN, int DOUT>
-__global__ void __launch_bounds__(kThreads)
-rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict__ tile_start,
-               const int32_t* __restrict__ tile_rel, const int32_t* __restrict__ order, long long R,
-               const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
-               const float* __restrict__ A, const __nv_bfloat16* __restrict__ X,
-               const __nv_bfloat16* __restrict__ W, float* __restrict__ Y) {
+__global__ void __launch_bounds__(kThreads, 4)
+rgms_edge_gemm_kernel(const int32_t* __restrict__ ed, long long ntiles,
+                      const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ W,
+                      float* __restrict__ T) {
   using SM = RgmsSmem<DIN, DOUT>;
   constexpr int kCols = DOUT <= 32 ? 32 : (DOUT <= 64 ? 64 : (DOUT <= 128 ? 128 : 256));
   constexpr int kSboA = (DIN / 8) * 128;  // K-major A: 8-edge group stride
   constexpr int kSboW = (DIN / 8) * 128;  // MN-major B: 8-column group stride
   constexpr uint32_t kIdesc = tc::make_idesc_bf16(kEdges, DOUT, /*A K-major*/ false, /*B MN-major*/ true);
+  constexpr int kNC = SM::kNC;
+  constexpr int kSPR = kNC / 4;       // float4 slots per row of a chunk
+  constexpr int kRPI = 32 / kSPR;     // rows per warp store instruction
   static_assert(DIN % 16 == 0 && DIN <= 64 && DOUT % 16 == 0 && DOUT <= 256, "unsupported dims");
 
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tmem_slot;
-  __shared__ long long s_e0[2];
-  __shared__ int s_ne[2];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long ntiles = tile_start[R];
+  const long long G = gridDim.x;
   if (static_cast<long long>(blockIdx.x) >= ntiles) return;
+  const long long nt = (ntiles - blockIdx.x + G - 1) / G;  // tiles of this CTA
 
   if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
   if (tid == 0) {
@@ -104,58 +176,54 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
+  float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + warp * (32 * kSPR);
+  auto idx_slot = [&](long long j) {
+    return reinterpret_cast<int32_t*>(smem + SM::kIdxOff + (j % SM::kIdxSlots) * SM::kIdxBytes);
+  };
 
-  // Issue the gathers of the p-th tile of the schedule into stage s (no wait).  Tiles run in
-  // order of their first destination row, so the CTAs in flight scatter into a narrow window
-  // of Y that stays in L2 (atomics into L2-missing rows were the bottleneck: 3.6 ms -> see
-  // DESIGN.md §4.5).
-  auto load_tile = [&](long long p, int s) {
-    const long long t = order[p];
-    const long long r = tile_rel[t];
-    const long long e0 = rel_ptr[r] + (t - tile_start[r]) * kEdges;
-    const int ne = static_cast<int>(min64(kEdges, rel_ptr[r + 1] - e0));
-    if (tid == 0) {
-      s_e0[s] = e0;
-      s_ne[s] = ne;
-    }
-    uint8_t* sA = smem + s * SM::kStage;
+  auto issue_idx = [&](long long j) {
+    if (j < nt && tid < kTileChunks)
+      tc::cp_async16(reinterpret_cast<uint8_t*>(idx_slot(j)) + tid * 16,
+                     ed + (blockIdx.x + j * G) * kTileWords + tid * 4);
+  };
+  auto issue_x = [&](long long j) {
+    if (j >= nt) return;
+    const int32_t* si = idx_slot(j);
+    uint8_t* sA = smem + (j % SM::kStages) * SM::kStage;
     uint8_t* sW = sA + SM::kABytes;
-    constexpr int kPer = kEdges * (DIN / 8) / kThreads;  // chunks of the A tile per thread
-    long long jj[kPer];
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {  // all index loads first, then the dependent copies
-      const int e = (tid + q * kThreads) / (DIN / 8);
-      jj[q] = e < ne ? __ldg(src + e0 + e) : 0;
-    }
+    constexpr int kPer = kEdges * (DIN / 8) / kThreads;  // 16-byte chunks of the A tile per thread
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const int c = tid + q * kThreads;
       const int e = c / (DIN / 8), kc = c % (DIN / 8);
-#ifndef STRATA_RGMS_KO_GATHER
-      tc::cp_async16(sA + (e >> 3) * kSboA + kc * 128 + (e & 7) * 16, X + jj[q] * DIN + kc * 8);
-#endif
+      const long long jj = si[4 + e];
+      tc::cp_async16(sA + (e >> 3) * kSboA + kc * 128 + (e & 7) * 16, X + jj * DIN + kc * 8);
     }
-    const __nv_bfloat16* Wr = W + r * DIN * DOUT;
+    const __nv_bfloat16* Wr = W + static_cast<long long>(si[0]) * DIN * DOUT;
     for (int c = tid; c < DIN * (DOUT / 8); c += kThreads) {
       const int k = c / (DOUT / 8), lc = c % (DOUT / 8);
       tc::cp_async16(sW + lc * kSboW + (k >> 3) * 128 + (k & 7) * 16, Wr + k * DOUT + lc * 8);
     }
   };
 
-  long long t = blockIdx.x;
-  load_tile(t, 0);
-  tc::cp_async_commit();
-  for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
-    const int s = it & 1;
-    const long long tn = t + gridDim.x;
-    if (tn < ntiles) load_tile(tn, s ^ 1);
-    tc::cp_async_commit();
-    tc::cp_async_wait<1>();  // this tile's group has landed (the next tile's may still fly)
+  // prologue: I0 I1 I2 X0 X1
+  issue_idx(0); tc::cp_async_commit();
+  issue_idx(1); tc::cp_async_commit();
+  issue_idx(2); tc::cp_async_commit();
+  tc::cp_async_wait<2>();
+  __syncthreads();
+  issue_x(0); tc::cp_async_commit();
+  tc::cp_async_wait<2>();
+  __syncthreads();
+  issue_x(1); tc::cp_async_commit();
+
+  for (long long j = 0; j < nt; ++j) {
+    tc::cp_async_wait<1>();  // X(j) and I(j+2) landed
     tc::fence_proxy_async();
-    __syncthreads();
-    const long long e0 = s_e0[s];
-    const int ne = s_ne[s];
-#ifndef STRATA_RGMS_KO_MMA
+    __syncthreads();         // ... for every thread; stage (j+2)%3 and idx slot (j+3)%4 are free
+    issue_idx(j + 3); tc::cp_async_commit();
+    issue_x(j + 2); tc::cp_async_commit();
+    const int s = static_cast<int>(j % SM::kStages);
     if (tid == 0) {
       tc::fence_after_sync();
       const uint32_t a0 = tc::smem_u32(smem + s * SM::kStage);
@@ -166,124 +234,296 @@ rgms_tc_kernel(const int32_t* __restrict__ rel_ptr, const long long* __restrict_
                      tc::make_desc(w0 + kk * 256, 128, kSboW), kIdesc, kk > 0);
       tc::mma_commit(&mbar);
     }
-#endif
-    // Epilogue operands, fetched while the MMA runs.
-    const int e = warp * 32 + lane;
-    const bool valid = e < ne;
-    const float a = valid ? __ldg(A + e0 + e) : 0.f;
-    const long long drow = valid ? __ldg(dst + e0 + e) : 0;
-#ifndef STRATA_RGMS_KO_MMA
-    tc::mbar_wait(&mbar, it & 1);
-#endif
+    const int32_t* si = idx_slot(j);
+    const float a = __int_as_float(si[4 + 2 * kEdges + warp * 32 + lane]);
+    const int32_t* spos = si + 4 + kEdges + warp * 32;
+    tc::mbar_wait(&mbar, static_cast<uint32_t>(j & 1));
     tc::fence_after_sync();
-    float* y = Y + drow * DOUT;
 #pragma unroll
-    for (int c0 = 0; c0 < DOUT; c0 += 32) {
+    for (int c0 = 0; c0 < DOUT; c0 += kNC) {
       uint32_t v[32];
       tc::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
       tc::tmem_ld_wait();
-      if (valid) {
-        const int n = DOUT - c0 < 32 ? DOUT - c0 : 32;
+      // row `lane` -> smem, float4 slot j stored at j ^ (lane % kSPR) (conflict-free phases)
 #pragma unroll
-        for (int q = 0; q < 32; q += 4)
-          if (q < n) {
-#ifndef STRATA_RGMS_KO_RED
-            tc::red_add_v4(y + c0 + q, a * __uint_as_float(v[q]), a * __uint_as_float(v[q + 1]),
-                           a * __uint_as_float(v[q + 2]), a * __uint_as_float(v[q + 3]));
-#else
-            reinterpret_cast<float4*>(y + c0 + q)[0] = make_float4(a * __uint_as_float(v[q]), 0.f, 0.f, 0.f);
-#endif
-          }
+      for (int q = 0; q < kSPR; ++q)
+        epi[lane * kSPR + (q ^ (lane & (kSPR - 1)))] =
+            make_float4(a * __uint_as_float(v[4 * q]), a * __uint_as_float(v[4 * q + 1]),
+                        a * __uint_as_float(v[4 * q + 2]), a * __uint_as_float(v[4 * q + 3]));
+      __syncwarp();
+      // each instruction writes kRPI whole rows of the chunk (kSPR lanes per row)
+#pragma unroll
+      for (int q = 0; q < kSPR; ++q) {
+        const int row = q * kRPI + lane / kSPR, sl = lane & (kSPR - 1);
+        const int p = spos[row];
+        const float4 val = epi[row * kSPR + (sl ^ (row & (kSPR - 1)))];
+        if (p >= 0) __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(p) * DOUT + c0) + sl, val);
       }
+      __syncwarp();
     }
     tc::fence_before_sync();
-    __syncthreads();  // TMEM drained and stage s free before the next MMA / reload
   }
+  tc::cp_async_wait<0>();
+  __syncthreads();
   if (warp == 0) tc::tmem_dealloc<kCols>(tmem);
 }
 
+// ---- pass 2: Y[i] = sum of T rows [dptr[i], dptr[i+1]) in order --------------------------
+// A T row is read by kL lanes (float4 each, kF float4s per lane when DOUT > 128); kGrp = 32/kL
+// lane groups per warp.  Rows longer than kLong edges (power-law hubs: at C4 2,973 rows hold
+// 39 % of the edges, the longest 171,738) would serialise one lane group, so they are cut into
+// kChunk-edge chunks summed by a whole warp (fixed strided split + fixed shuffle tree) into
+// partials, and a finishing pass adds a row's partials in chunk order — deterministic.
+constexpr int kLong = 64;
+constexpr int kChunk = 1024;
+
+template <int DOUT>
+struct RowSumShape {
+  static constexpr int kF4 = DOUT / 4;
+  static constexpr int kL = kF4 < 32 ? kF4 : 32;
+  static constexpr int kF = kF4 / kL;
+  static constexpr int kGrp = 32 / kL;
+};
+
+// Short rows: a warp takes a block of 32 consecutive rows (bounds: one coalesced load, kept in
+// smem); lane group g owns rows g*kRPV .. g*kRPV + kRPV - 1, whose T rows are contiguous, and
+// walks that range in batches of 8 T rows issued together, flushing a row's sum when the walk
+// crosses its end.  Long rows are stepped over (at most one wasted batch each).
+template <int DOUT>
+__global__ void __launch_bounds__(256)
+rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ T, long long m,
+                    float* __restrict__ Y) {
+  using RS = RowSumShape<DOUT>;
+  constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
+  constexpr int kRPV = 32 / kGrp;  // rows per lane group per block
+  constexpr int kB = 8;            // T rows in flight per lane group
+  __shared__ int sbnd[8][33];
+  const int lane = threadIdx.x & 31, l = lane % kL, g = lane / kL, w = threadIdx.x >> 5;
+  int* bnd = sbnd[w];
+  const long long nwarps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const float4* T4 = reinterpret_cast<const float4*>(T) + l;
+  for (long long b = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + w; b * 32 < m;
+       b += nwarps) {
+    const long long i0 = b * 32;
+    __syncwarp();
+    bnd[lane] = __ldg(dptr + min64(i0 + lane, m));
+    if (lane == 0) bnd[32] = __ldg(dptr + min64(i0 + 32, m));
+    __syncwarp();
+    int r = g * kRPV;
+    const int rend = static_cast<int>(min64(r + kRPV, m - i0));
+    if (r >= rend) continue;
+    int q = bnd[r], nb = bnd[r + 1];
+    const int qend = bnd[rend];
+    bool skip = nb - q > kLong;
+    float4 acc[kF];
+#pragma unroll
+    for (int f = 0; f < kF; ++f) acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto flush = [&] {
+      if (!skip) {
+#pragma unroll
+        for (int f = 0; f < kF; ++f) {
+          st_stream4(reinterpret_cast<float4*>(Y + (i0 + r) * DOUT) + f * kL + l, acc[f]);
+          acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      ++r;
+      nb = r < rend ? bnd[r + 1] : qend;
+      skip = r < rend && nb - bnd[r] > kLong;
+    };
+    while (q < qend) {
+      if (skip) {  // long row: its T rows are summed by rgms_long_chunk_kernel
+        q = nb;
+        flush();
+        continue;
+      }
+      float4 u[kB][kF];
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+#pragma unroll
+        for (int f = 0; f < kF; ++f)
+          u[j][f] = q + j < qend ? __ldcs(T4 + static_cast<long long>(q + j) * kF4 + f * kL)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      int used = kB;
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (used == kB) {
+          const int qq = q + j;
+          if (qq >= qend) {
+            used = j;
+          } else {
+            while (qq >= nb) flush();
+            if (skip) {
+              used = j;  // qq starts a long row: the next round steps over it
+            } else {
+#pragma unroll
+              for (int f = 0; f < kF; ++f) acc[f] = add4(acc[f], u[j][f]);
+            }
+          }
+        }
+      }
+      q += used;
+    }
+    while (r < rend) flush();  // trailing rows (their sums, or zeros for empty rows)
+  }
+}
+
+// Warp-wide fixed-order reduction of the kGrp lane groups' float4s (lane group 0 ends with it).
+template <int kL>
+__device__ __forceinline__ float4 reduce_groups(float4 v) {
+#pragma unroll
+  for (int off = 16; off >= kL; off >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, off);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, off);
+    v.z += __shfl_down_sync(0xffffffffu, v.z, off);
+    v.w += __shfl_down_sync(0xffffffffu, v.w, off);
+  }
+  return v;
+}
+
+// One warp per chunk of a long row: partial[c] = sum of T rows [q0, q1).  Lane group g sums
+// rows q0 + g, q0 + g + kGrp, ... (4 in flight), then the groups are combined.
+template <int DOUT>
+__global__ void __launch_bounds__(256)
+rgms_long_chunk_kernel(const int32_t* __restrict__ dptr, const int32_t* __restrict__ long_rows,
+                       const int32_t* __restrict__ chunk_off, int nlong, int nchunks,
+                       const float* __restrict__ T, float* __restrict__ partial) {
+  using RS = RowSumShape<DOUT>;
+  constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
+  const int lane = threadIdx.x & 31, l = lane % kL, grp = lane / kL;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nchunks; c += nwarps) {
+    int lo = 0, hi = nlong;  // long row owning chunk c: last li with chunk_off[li] <= c
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(chunk_off + mid) <= c) lo = mid; else hi = mid;
+    }
+    const int row = __ldg(long_rows + lo);
+    const int q0 = __ldg(dptr + row) + (c - __ldg(chunk_off + lo)) * kChunk;
+    const int q1 = min(q0 + kChunk, __ldg(dptr + row + 1));
+    float4 acc[kF];
+#pragma unroll
+    for (int g = 0; g < kF; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int q = q0 + grp;
+    for (; q + 3 * kGrp < q1; q += 4 * kGrp) {
+      float4 u[4][kF];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int g = 0; g < kF; ++g)
+          u[j][g] = __ldcs(reinterpret_cast<const float4*>(T) +
+                           static_cast<long long>(q + j * kGrp) * kF4 + g * kL + l);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int g = 0; g < kF; ++g) acc[g] = add4(acc[g], u[j][g]);
+    }
+    for (; q < q1; q += kGrp) {
+#pragma unroll
+      for (int g = 0; g < kF; ++g)
+        acc[g] = add4(acc[g], __ldcs(reinterpret_cast<const float4*>(T) +
+                                     static_cast<long long>(q) * kF4 + g * kL + l));
+    }
+#pragma unroll
+    for (int g = 0; g < kF; ++g) {
+      const float4 v = reduce_groups<kL>(acc[g]);
+      if (grp == 0) reinterpret_cast<float4*>(partial + static_cast<long long>(c) * DOUT)[g * kL + l] = v;
+    }
+  }
+}
+
+// One warp per long row: Y[row] = sum of its chunks' partials (same fixed split as above).
+template <int DOUT>
+__global__ void __launch_bounds__(256)
+rgms_long_finish_kernel(const int32_t* __restrict__ long_rows, const int32_t* __restrict__ chunk_off,
+                        int nlong, const float* __restrict__ partial, float* __restrict__ Y) {
+  using RS = RowSumShape<DOUT>;
+  constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
+  const int lane = threadIdx.x & 31, l = lane % kL, grp = lane / kL;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); li < nlong; li += nwarps) {
+    const int c0 = __ldg(chunk_off + li), c1 = __ldg(chunk_off + li + 1);
+    float4 acc[kF];
+#pragma unroll
+    for (int g = 0; g < kF; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = c0 + grp; c < c1; c += kGrp) {
+#pragma unroll
+      for (int g = 0; g < kF; ++g)
+        acc[g] = add4(acc[g], reinterpret_cast<const float4*>(partial + static_cast<long long>(c) * DOUT)[g * kL + l]);
+    }
+    const long long row = __ldg(long_rows + li);
+#pragma unroll
+    for (int g = 0; g < kF; ++g) {
+      const float4 v = reduce_groups<kL>(acc[g]);
+      if (grp == 0) st_stream4(reinterpret_cast<float4*>(Y + row * DOUT) + g * kL + l, v);
+    }
+  }
+}
+
+// Plan helpers for the long rows.
+__global__ void long_flags_kernel(const int32_t* __restrict__ dptr, long long m,
+                                  uint8_t* __restrict__ flag, int32_t* __restrict__ nch) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int deg = dptr[i + 1] - dptr[i];
+    flag[i] = deg > kLong;
+    nch[i] = deg > kLong ? (deg + kChunk - 1) / kChunk : 0;
+  }
+}
+
+__global__ void gather_i32_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ v,
+                                  int n, int32_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = v[idx[i]];
+}
+
 template <int DIN, int DOUT>
-void launch_rgms(const int32_t* rel_ptr, const long long* tile_start, const int32_t* tile_rel,
-                 const int32_t* order, long long R, long long max_tiles, const int32_t* dst, const int32_t* src,
-                 const float* A, const __nv_bfloat16* X, const __nv_bfloat16* W, float* Y,
+void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat16* W, float* Y,
                  cudaStream_t s) {
   constexpr int smem = RgmsSmem<DIN, DOUT>::kBytes;
-  STRATA_CUDA_CHECK(cudaFuncSetAttribute(rgms_tc_kernel<DIN, DOUT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const long long grid = std::min<long long>(max_tiles, static_cast<long long>(num_sms()) * kCtasPerSm);
-  rgms_tc_kernel<DIN, DOUT><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(
-      rel_ptr, tile_start, tile_rel, order, R, dst, src, A, X, W, Y);
+  auto* k1 = rgms_edge_gemm_kernel<DIN, DOUT>;
+  STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  // Resident CTAs per SM: shared memory (~227 KB usable) and TMEM (512 columns) bound it.
+  constexpr int kTmemCols = DOUT <= 32 ? 32 : (DOUT <= 64 ? 64 : (DOUT <= 128 ? 128 : 256));
+  const int per_sm = std::max(1, std::min({4, (227 * 1024) / (smem + 1024), 512 / kTmemCols}));
+  const long long grid = std::min<long long>(h.ntiles, static_cast<long long>(num_sms()) * per_sm);
+  k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kThreads, smem, s>>>(h.edges.p, h.ntiles, X, W, h.T.p);
+  STRATA_CUDA_CHECK(cudaGetLastError());
+  const long long lanes = h.m * RowSumShape<DOUT>::kL;
+  const long long blocks = std::min<long long>((lanes + 255) / 256, static_cast<long long>(num_sms()) * 8);
+  rgms_row_sum_kernel<DOUT><<<static_cast<unsigned>(std::max<long long>(blocks, 1)), 256, 0, s>>>(
+      h.dptr.p, h.T.p, h.m, Y);
+  if (h.nlong > 0) {
+    const int wpb = 8;
+    rgms_long_chunk_kernel<DOUT><<<static_cast<unsigned>((h.nchunks + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
+        h.dptr.p, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks, h.T.p, h.partial.p);
+    rgms_long_finish_kernel<DOUT><<<static_cast<unsigned>((h.nlong + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
+        h.long_rows.p, h.chunk_off.p, h.nlong, h.partial.p, Y);
+  }
   STRATA_CUDA_CHECK(cudaGetLastError());
 }
 
-}  // namespace
+void require_sm100() {
+  int dev = 0, major = 0;
+  STRATA_CUDA_CHECK(cudaGetDevice(&dev));
+  STRATA_CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) throw ApiError(STRATA_ERR_CUDA, "strata_b200 kernels are built for sm_100a");
+}
 
-extern "C" int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, const int32_t* src,
-                                const float* A, int64_t R, int64_t m, int64_t n, int64_t nnz,
-                                const void* X_bf16, const void* W_bf16, float* Y, int64_t d_in,
-                                int64_t d_out, void* stream) {
+void check_dims(int64_t d_in, int64_t d_out) {
+  switch (d_in * 1000 + d_out) {
+    case 16016: case 16032: case 32016: case 32032: case 32064: case 64032: case 64064:
+    case 32128: case 64128: return;
+    default:
+      throw ApiError(STRATA_ERR_USAGE,
+                     "rgms_bf16: (d_in, d_out) must be in {16,32,64} x {16,32,64,128}");
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
   try {
-    (void)n;
-    if (R < 1) throw ApiError(STRATA_ERR_USAGE, "RGMS requires at least one relation");  // kernels.cpp:139
-    if (nnz > INT32_MAX) throw ApiError(STRATA_ERR_CAPACITY, "nnz exceeds int32");
-    int dev = 0, major = 0;
-    STRATA_CUDA_CHECK(cudaGetDevice(&dev));
-    STRATA_CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
-    if (major != 10) throw ApiError(STRATA_ERR_CUDA, "strata_b200 kernels are built for sm_100a");
-    const int dims = static_cast<int>(d_in * 1000 + d_out);
-    switch (dims) {
-      case 16016: case 16032: case 32016: case 32032: case 32064: case 64032: case 64064:
-      case 32128: case 64128: break;
-      default:
-        throw ApiError(STRATA_ERR_USAGE,
-                       "rgms_bf16: (d_in, d_out) must be in {16,32,64} x {16,32,64,128}");
-    }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (m > 0) STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * m * d_out, s));
-    if (nnz == 0) return STRATA_OK;
-    const long long max_tiles = (nnz + kEdges - 1) / kEdges + R;  // upper bound on tiles
-    long long *ntiles = nullptr, *tile_start = nullptr;
-    int32_t* tile_rel = nullptr;
-    ntiles = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
-    tile_start = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
-    tile_rel = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * max_tiles, s));
-    rel_tiles_kernel<<<static_cast<unsigned>((R + 1 + 255) / 256), 256, 0, s>>>(rel_ptr, R, ntiles);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, ntiles, tile_start, R + 1, s);
-    void* tmp = nullptr;
-    tmp = workspace_alloc(tb, s);
-    cub::DeviceScan::ExclusiveSum(tmp, tb, ntiles, tile_start, R + 1, s);
-    int32_t* key = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * max_tiles * 2, s));
-    int32_t* ids = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * max_tiles * 2, s));
-    tile_rel_kernel<<<static_cast<unsigned>(R + 1), 256, 0, s>>>(rel_ptr, tile_start, R, dst,
-                                                                 max_tiles, tile_rel, key, ids);
-    size_t sb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, sb, key, key + max_tiles, ids, ids + max_tiles,
-                                    max_tiles, 0, 32, s);
-    void* stmp = workspace_alloc(sb, s);
-    cub::DeviceRadixSort::SortPairs(stmp, sb, key, key + max_tiles, ids, ids + max_tiles,
-                                    max_tiles, 0, 32, s);
-    const int32_t* order = ids + max_tiles;
-    STRATA_CUDA_CHECK(cudaGetLastError());
-    const auto* X = static_cast<const __nv_bfloat16*>(X_bf16);
-    const auto* W = static_cast<const __nv_bfloat16*>(W_bf16);
-#define STRATA_RGMS_CASE(I, O)                                                                \
-  case I * 1000 + O:                                                                          \
-    launch_rgms<I, O>(rel_ptr, tile_start, tile_rel, order, R, max_tiles, dst, src, A, X, W, Y, s); \
-    break;
-    switch (dims) {
-      STRATA_RGMS_CASE(16, 16) STRATA_RGMS_CASE(16, 32) STRATA_RGMS_CASE(32, 16)
-      STRATA_RGMS_CASE(32, 32) STRATA_RGMS_CASE(32, 64) STRATA_RGMS_CASE(64, 32)
-      STRATA_RGMS_CASE(64, 64) STRATA_RGMS_CASE(32, 128) STRATA_RGMS_CASE(64, 128)
-    }
-#undef STRATA_RGMS_CASE
-    STRATA_CUDA_CHECK(cudaFreeAsync(tmp, s));
-    STRATA_CUDA_CHECK(cudaFreeAsync(stmp, s));
-    STRATA_CUDA_CHECK(cudaFreeAsync(key, s));
-    STRATA_CUDA_CHECK(cudaFreeAsync(ids, s));
-    STRATA_CUDA_CHECK(cudaFreeAsync(tile_rel, s));
-    STRATA_CUDA_CHECK(cudaFreeAsync(ntiles, s));
-    STRATA_CUDA_CHECK(cudaFreeAsync(tile_start, s));
+    f();
     return STRATA_OK;
   } catch (const ApiError& e) {
     set_last_error(e.what());
@@ -292,4 +532,179 @@ extern "C" int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, cons
     set_last_error(e.what());
     return STRATA_ERR_INTERNAL;
   }
+}
+
+}  // namespace
+
+extern "C" int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, const int32_t* src,
+                                const float* A, int64_t R, int64_t m, int64_t n, int64_t nnz,
+                                strata_rgms** out, void* stream) {
+  return guarded([&] {
+    if (!out) throw ApiError(STRATA_ERR_USAGE, "null output handle");
+    *out = nullptr;
+    if (R < 1) throw ApiError(STRATA_ERR_USAGE, "RGMS requires at least one relation");  // kernels.cpp:139
+    if (nnz > INT32_MAX || m >= INT32_MAX) throw ApiError(STRATA_ERR_CAPACITY, "nnz exceeds int32");
+    require_sm100();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto h = std::make_unique<strata_rgms>();
+    STRATA_CUDA_CHECK(cudaGetDevice(&h->device));
+    h->R = R; h->m = m; h->n = n; h->nnz = nnz;
+    h->dptr.alloc(m + 1);
+    const long long max_tiles = (nnz + kEdges - 1) / kEdges + R;  // upper bound on tiles
+    long long* ntiles = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
+    long long* tile_start = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
+    int32_t* tile_rel = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * max_tiles, s));
+    rel_tiles_kernel<<<static_cast<unsigned>((R + 1 + 255) / 256), 256, 0, s>>>(rel_ptr, R, ntiles);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, ntiles, tile_start, R + 1, s);
+    void* tmp = workspace_alloc(tb, s);
+    cub::DeviceScan::ExclusiveSum(tmp, tb, ntiles, tile_start, R + 1, s);
+    tile_rel_kernel<<<static_cast<unsigned>(R), 256, 0, s>>>(tile_start, R, tile_rel);
+    long long hnt = 0;
+    STRATA_CUDA_CHECK(cudaMemcpyAsync(&hnt, tile_start + R, sizeof(hnt), cudaMemcpyDeviceToHost, s));
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+    h->ntiles = hnt;
+    if (nnz > 0) {
+      // Stable sort of edge ids by destination: a row's edges keep relation order.
+      int32_t* ids = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * nnz * 4, s));
+      int32_t* order = ids + nnz;
+      int32_t* keys = ids + 2 * nnz;
+      int32_t* pos = ids + 3 * nnz;
+      const unsigned g = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, num_sms() * 16LL));
+      iota_kernel<<<g, 256, 0, s>>>(ids, nnz);
+      int bits = 1;
+      while (bits < 31 && (1LL << bits) <= m) ++bits;
+      size_t sb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, sb, dst, keys, ids, order, nnz, 0, bits, s);
+      void* stmp = workspace_alloc(sb, s);
+      cub::DeviceRadixSort::SortPairs(stmp, sb, dst, keys, ids, order, nnz, 0, bits, s);
+      invert_kernel<<<g, 256, 0, s>>>(order, nnz, pos);
+      const unsigned gr = static_cast<unsigned>(std::min<long long>((m + 1 + 255) / 256, num_sms() * 16LL));
+      row_ptr_kernel<<<gr, 256, 0, s>>>(keys, nnz, m, h->dptr.p);
+      h->edges.alloc(static_cast<size_t>(h->ntiles) * kTileWords);
+      const unsigned ge = static_cast<unsigned>(std::min<long long>((h->ntiles * kEdges + 255) / 256, num_sms() * 16LL));
+      tile_edges_kernel<<<ge, 256, 0, s>>>(rel_ptr, tile_start, tile_rel, h->ntiles, src, pos, A,
+                                           h->edges.p);
+      STRATA_CUDA_CHECK(cudaFreeAsync(stmp, s));
+      STRATA_CUDA_CHECK(cudaFreeAsync(ids, s));
+      // Long rows (> kLong edges) and their chunk offsets; one host sync sizes the partials.
+      if (m > 0) {
+        uint8_t* flag = static_cast<uint8_t*>(workspace_alloc(m, s));
+        int32_t* nch = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * (m + 1), s));
+        int32_t* sel = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * (m + 1), s));
+        int32_t* cnt = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * 2, s));
+        const unsigned gm = static_cast<unsigned>(std::min<long long>((m + 255) / 256, num_sms() * 16LL));
+        long_flags_kernel<<<gm, 256, 0, s>>>(h->dptr.p, m, flag, nch);
+        cub::CountingInputIterator<int32_t> it(0);
+        size_t fb = 0, rb = 0;
+        cub::DeviceSelect::Flagged(nullptr, fb, it, flag, sel, cnt, m, s);
+        cub::DeviceReduce::Sum(nullptr, rb, nch, cnt + 1, m, s);
+        void* ftmp = workspace_alloc(std::max(fb, rb), s);
+        cub::DeviceSelect::Flagged(ftmp, fb, it, flag, sel, cnt, m, s);
+        cub::DeviceReduce::Sum(ftmp, rb, nch, cnt + 1, m, s);
+        int32_t hc[2] = {0, 0};
+        STRATA_CUDA_CHECK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+        STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+        h->nlong = hc[0];
+        h->nchunks = hc[1];
+        if (h->nlong > 0) {
+          h->long_rows.alloc(h->nlong);
+          h->chunk_off.alloc(h->nlong + 1);
+          STRATA_CUDA_CHECK(cudaMemcpyAsync(h->long_rows.p, sel, sizeof(int32_t) * h->nlong,
+                                            cudaMemcpyDeviceToDevice, s));
+          // chunk counts of the long rows, then their exclusive scan (+ total at [nlong])
+          int32_t* lc = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * (h->nlong + 1), s));
+          gather_i32_kernel<<<static_cast<unsigned>((h->nlong + 255) / 256), 256, 0, s>>>(
+              sel, nch, h->nlong, lc);
+          STRATA_CUDA_CHECK(cudaMemsetAsync(lc + h->nlong, 0, sizeof(int32_t), s));
+          size_t eb = 0;
+          cub::DeviceScan::ExclusiveSum(nullptr, eb, lc, h->chunk_off.p, h->nlong + 1, s);
+          void* etmp = workspace_alloc(eb, s);
+          cub::DeviceScan::ExclusiveSum(etmp, eb, lc, h->chunk_off.p, h->nlong + 1, s);
+          STRATA_CUDA_CHECK(cudaFreeAsync(etmp, s));
+          STRATA_CUDA_CHECK(cudaFreeAsync(lc, s));
+        }
+        STRATA_CUDA_CHECK(cudaFreeAsync(ftmp, s));
+        STRATA_CUDA_CHECK(cudaFreeAsync(cnt, s));
+        STRATA_CUDA_CHECK(cudaFreeAsync(sel, s));
+        STRATA_CUDA_CHECK(cudaFreeAsync(nch, s));
+        STRATA_CUDA_CHECK(cudaFreeAsync(flag, s));
+      }
+    } else if (m >= 0) {
+      STRATA_CUDA_CHECK(cudaMemsetAsync(h->dptr.p, 0, sizeof(int32_t) * (m + 1), s));
+    }
+    STRATA_CUDA_CHECK(cudaFreeAsync(tmp, s));
+    STRATA_CUDA_CHECK(cudaFreeAsync(tile_rel, s));
+    STRATA_CUDA_CHECK(cudaFreeAsync(tile_start, s));
+    STRATA_CUDA_CHECK(cudaFreeAsync(ntiles, s));
+    STRATA_CUDA_CHECK(cudaGetLastError());
+    *out = h.release();
+  });
+}
+
+extern "C" int strata_rgms_run_bf16(const strata_rgms* h, const void* X_bf16, const void* W_bf16,
+                                    float* Y, int64_t d_in, int64_t d_out, void* stream) {
+  return guarded([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null rgms plan");
+    check_dims(d_in, d_out);
+    require_sm100();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (h->nnz == 0) {
+      if (h->m > 0) STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * h->m * d_out, s));
+      return;
+    }
+    const size_t need = static_cast<size_t>(h->nnz) * d_out;
+    const size_t pneed = static_cast<size_t>(h->nchunks) * d_out;
+    if (h->T.n < need || h->partial.n < pneed) {
+      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));  // earlier runs may still read the old T
+      if (h->T.n < need) h->T.alloc(need);
+      if (h->partial.n < pneed) h->partial.alloc(pneed);
+    }
+    const auto* X = static_cast<const __nv_bfloat16*>(X_bf16);
+    const auto* W = static_cast<const __nv_bfloat16*>(W_bf16);
+#define STRATA_RGMS_CASE(I, O) \
+  case I * 1000 + O: launch_rgms<I, O>(*h, X, W, Y, s); break;
+    switch (d_in * 1000 + d_out) {
+      STRATA_RGMS_CASE(16, 16) STRATA_RGMS_CASE(16, 32) STRATA_RGMS_CASE(32, 16)
+      STRATA_RGMS_CASE(32, 32) STRATA_RGMS_CASE(32, 64) STRATA_RGMS_CASE(64, 32)
+      STRATA_RGMS_CASE(64, 64) STRATA_RGMS_CASE(32, 128) STRATA_RGMS_CASE(64, 128)
+    }
+#undef STRATA_RGMS_CASE
+  });
+}
+
+extern "C" int strata_rgms_info(const strata_rgms* h, int64_t* tiles_bound, int64_t* t_bytes_per_dout) {
+  return guarded([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null rgms plan");
+    if (tiles_bound) *tiles_bound = h->ntiles;
+    if (t_bytes_per_dout) *t_bytes_per_dout = h->nnz * 4;
+  });
+}
+
+extern "C" int strata_rgms_destroy(strata_rgms* h) {
+  return guarded([&] {
+    if (h) {
+      cudaSetDevice(h->device);
+      delete h;
+    }
+  });
+}
+
+extern "C" int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, const int32_t* src,
+                                const float* A, int64_t R, int64_t m, int64_t n, int64_t nnz,
+                                const void* X_bf16, const void* W_bf16, float* Y, int64_t d_in,
+                                int64_t d_out, void* stream) {
+  if (R >= 1) {  // dimension errors before any device work, like the reference's binding checks
+    const int rc = guarded([&] { check_dims(d_in, d_out); });
+    if (rc != STRATA_OK) return rc;
+  }
+  strata_rgms* h = nullptr;
+  int rc = strata_rgms_plan(rel_ptr, dst, src, A, R, m, n, nnz, &h, stream);
+  if (rc != STRATA_OK) return rc;
+  rc = strata_rgms_run_bf16(h, X_bf16, W_bf16, Y, d_in, d_out, stream);
+  if (rc == STRATA_OK) {  // the plan's buffers are freed synchronously: finish its work first
+    rc = guarded([&] { STRATA_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });
+  }
+  strata_rgms_destroy(h);
+  return rc;
 }

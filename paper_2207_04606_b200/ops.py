@@ -384,9 +384,42 @@ class RelSparse:
                          t(self.src), t(self.A))
 
 
-def rgms(rel: RelSparse, X_bf16, W_bf16, Y=None, stream=None):
-    """Y[m][d_out] (f32) = sum_r A_r @ X @ W_r via per-relation gather -> tcgen05 GEMM -> scatter."""
+class RgmsPlan:
+    """Device plan of one RelSparse (strata_rgms_plan): the build step of build_rgms_pipeline
+    (driver.cpp:241-314).  ``run`` is the interpret step: Y = sum_r A_r @ X @ W_r."""
+
+    def __init__(self, rel: RelSparse, stream=None):
+        self.rows, self.cols, self.relations, self.nnz = rel.rows, rel.cols, rel.relations, rel.nnz
+        h = C.c_void_p()
+        check(lib.strata_rgms_plan(_ptr(rel.rel_ptr), _ptr(rel.dst), _ptr(rel.src), _ptr(rel.A),
+                                   rel.relations, rel.rows, rel.cols, rel.nnz, C.byref(h),
+                                   _stream(stream)))
+        self._h = h
+
+    def run(self, X_bf16, W_bf16, Y=None, stream=None):
+        import torch
+        d_in, d_out = int(W_bf16.shape[1]), int(W_bf16.shape[2])
+        if Y is None:
+            Y = torch.empty((self.rows, d_out), dtype=torch.float32, device=X_bf16.device)
+        check(lib.strata_rgms_run_bf16(self._h, _ptr(X_bf16), _ptr(W_bf16), _ptr(Y), d_in, d_out,
+                                       _stream(stream)))
+        return Y
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            import torch
+            torch.cuda.synchronize()
+            lib.strata_rgms_destroy(h)
+            self._h = None
+
+
+def rgms(rel, X_bf16, W_bf16, Y=None, stream=None):
+    """Y[m][d_out] (f32) = sum_r A_r @ X @ W_r.  ``rel`` is a device RelSparse (one-shot
+    strata_rgms_bf16: plan + run) or an RgmsPlan (run only)."""
     import torch
+    if isinstance(rel, RgmsPlan):
+        return rel.run(X_bf16, W_bf16, Y, stream)
     d_in, d_out = int(W_bf16.shape[1]), int(W_bf16.shape[2])
     if Y is None:
         Y = torch.empty((rel.rows, d_out), dtype=torch.float32, device=X_bf16.device)
@@ -426,5 +459,5 @@ def _mt19937_stream(seed: int, out: np.ndarray):
     out[:] = bg.random_raw(out.size).astype(np.uint32)
 
 
-__all__ += ["BsrMatrix", "csr_to_bsr", "bsr_spmm", "csr_to_ell", "RelSparse", "rgms",
+__all__ += ["BsrMatrix", "csr_to_bsr", "bsr_spmm", "csr_to_ell", "RelSparse", "RgmsPlan", "rgms",
             "split_relations"]

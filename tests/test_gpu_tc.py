@@ -153,3 +153,63 @@ def test_rgms_am_shape_relation_split(cuda):
     rel = S.split_relations(m, 133, 1)
     per = np.diff(rel.rel_ptr)
     assert per.sum() == m.nnz and per.min() >= 42033 and per.max() <= 43251
+
+
+def _rgms_dense_f64(rel, X, W):
+    """Per-relation f64 restatement of the RGMS nest (kernels.cpp:138-167) for large checks:
+    exact on integer operands, so it equals the reference's F32 pipeline bitwise."""
+    Y = np.zeros((rel.rows, W.shape[2]), np.float64)
+    Xd = X.astype(np.float64)
+    for r in range(rel.relations):
+        e0, e1 = int(rel.rel_ptr[r]), int(rel.rel_ptr[r + 1])
+        if e1 == e0:
+            continue
+        msg = (Xd[rel.src[e0:e1]] @ W[r].astype(np.float64)) * rel.A[e0:e1, None]
+        np.add.at(Y, rel.dst[e0:e1], msg)
+    return Y
+
+
+def test_rgms_c4_full_size(cuda):
+    """C4 at full size (1.9M nodes, 5.67M edges, 133 relations, d 32 -> 32) through the plan /
+    run split, bitwise vs the f64 restatement on integer operands; a second run on the same
+    plan with new X and W (plan reuse) and a run with d_out = 64 (T workspace growth)."""
+    import torch
+    m = S.generate_matrix("powerlaw", 1885136, 1885136, 0, 0, 0, 3.0051, 1)
+    rel = S.split_relations(m, 133, 1)
+    plan = S.RgmsPlan(rel.to_device(cuda))
+    for seed, dout in ((2, 32), (4, 32), (6, 64)):
+        X = S.dense_int((m.cols, 32), seed)
+        W = S.dense_int((133, 32, dout), seed + 1)
+        Y = plan.run(bf16(torch.from_numpy(X).to(cuda)), bf16(torch.from_numpy(W).to(cuda)))
+        want = _rgms_dense_f64(rel, X, W)
+        assert np.array_equal(Y.cpu().numpy(), want.astype(np.float32)), (seed, dout)
+
+
+def test_rgms_empty_relations_and_rows(cuda):
+    """Relations without edges, rows without edges (Y row = 0, interp.cpp:584-587) and an
+    edgeless RelSparse; dimension errors are Usage errors naming the supported set."""
+    import torch
+    R, rows, cols = 5, 300, 200
+    rng = np.random.default_rng(3)
+    dst = np.sort(rng.integers(0, rows // 2, 700)).astype(np.int32)  # rows >= 150 stay empty
+    counts = np.array([0, 400, 0, 300, 0])
+    rel_ptr = np.r_[0, np.cumsum(counts)].astype(np.int32)
+    dsts = np.concatenate([np.sort(dst[:400]), np.sort(dst[400:])]).astype(np.int32)
+    rel = S.RelSparse(R, rows, cols, rel_ptr, dsts, rng.integers(0, cols, 700).astype(np.int32),
+                      rng.integers(1, 10, 700).astype(np.float32))
+    X = S.dense_int((cols, 16), 5)
+    W = S.dense_int((R, 16, 16), 6)
+    Y = S.rgms(rel.to_device(cuda), bf16(torch.from_numpy(X).to(cuda)),
+               bf16(torch.from_numpy(W).to(cuda))).cpu().numpy()
+    assert np.array_equal(Y, _rgms_dense_f64(rel, X, W).astype(np.float32))
+    assert not Y[150:].any()
+    empty = S.RelSparse(2, 10, 10, np.zeros(3, np.int32), np.zeros(0, np.int32),
+                        np.zeros(0, np.int32), np.zeros(0, np.float32))
+    Xe = bf16(torch.ones((10, 16), device=cuda))
+    We = bf16(torch.ones((2, 16, 16), device=cuda))
+    Ye = S.rgms(S.RgmsPlan(empty.to_device(cuda)), Xe, We)
+    assert Ye.shape == (10, 16) and not Ye.any()
+    with pytest.raises(S.StrataError) as e:
+        S.rgms(rel.to_device(cuda), bf16(torch.ones((cols, 48), device=cuda)),
+               bf16(torch.ones((R, 48, 16), device=cuda)))
+    assert e.value.kind == "Usage"

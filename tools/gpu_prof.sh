@@ -7,7 +7,8 @@ for w in ${WORKLOADS:-products reddit_spmm reddit_sddmm bsr rgcn}; do
     products|reddit_spmm) k=spmm_hyb_kernel ;;
     reddit_sddmm) k=sddmm_kernel ;;
     bsr) k=bsr_spmm_tc_kernel ;;
-    rgcn) k=rgms_tc_kernel ;;
+    rgcn) k=rgms_edge_gemm_kernel ;;
+    rgcn_sum) k=rgms_row_sum_kernel; w=rgcn ;;
   esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
     -o gpurun_out/prof_$w -f python tools/prof_workloads.py $w 4 > gpurun_out/ncu_$w.log 2>&1

@@ -36,10 +36,10 @@ def main():
         fn = lambda: S.bsr_spmm(bs, X)
     elif which == "rgcn":
         m = S.generate_matrix("powerlaw", 1885136, 1885136, 0, 0, 0, 3.0051, 1)
-        rel = S.split_relations(m, 133, 1).to_device(dev)
+        plan = S.RgmsPlan(S.split_relations(m, 133, 1).to_device(dev))
         X = torch.randint(-3, 4, (m.cols, 32), device=dev).to(torch.bfloat16)
         W = torch.randint(-3, 4, (133, 32, 32), device=dev).to(torch.bfloat16)
-        fn = lambda: S.rgms(rel, X, W)
+        fn = lambda: plan.run(X, W)
     else:
         raise SystemExit(f"unknown workload {which}")
     for _ in range(reps):
