@@ -119,6 +119,12 @@ int strata_spmm_hyb_f32(const strata_hyb* h, const float* X, float* Y, int64_t d
  * are inside the call, which returns after Y is on the host. */
 int strata_spmm_hyb_f32_host(const strata_hyb* h, const float* X_host, float* Y_host, int64_t d,
                              void* stream);
+/* Batched end-to-end form: nbatch independent feature matrices X_host[b] -> Y_host[b] (host,
+ * pinned) through one plan.  Copy-in of matrix b+1 and copy-out of matrix b-1 overlap the SpMM
+ * of matrix b (separate copy streams, two device staging slots); returns when every Y_host[b]
+ * is written.  Results are identical to nbatch calls of strata_spmm_hyb_f32_host. */
+int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_host,
+                                   float* const* Y_host, int64_t nbatch, int64_t d, void* stream);
 
 /* ---- CSR SpMM (device, row-split baseline form of the same op) ---------------------
  * Replaces: build_matrix_pipeline(SpMM, ..., "csr") + interpret. */

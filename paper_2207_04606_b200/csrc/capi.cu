@@ -303,18 +303,67 @@ int strata_spmm_hyb_f32(const strata_hyb* h, const float* X, float* Y, int64_t d
 
 int strata_spmm_hyb_f32_host(const strata_hyb* h, const float* X_host, float* Y_host, int64_t d,
                              void* stream) {
+  return strata_spmm_hyb_f32_host_batch(h, &X_host, &Y_host, 1, d, stream);
+}
+
+// Batched end-to-end form.  Three streams and two staging slots: the copy-in of matrix b+1
+// (H2D engine) and the copy-out of matrix b-1 (D2H engine) overlap the SpMM of matrix b, so on
+// a full-duplex link a batch costs max(H2D, D2H) per matrix instead of H2D + SpMM + D2H.
+int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_host,
+                                   float* const* Y_host, int64_t nbatch, int64_t d, void* stream) {
   return guard([&] {
     const auto& H = hyb_of(h);
     require(d >= 1, STRATA_ERR_USAGE, "spmm: d must be >= 1");
+    require(nbatch >= 0 && (nbatch == 0 || (X_host && Y_host)), STRATA_ERR_USAGE,
+            "spmm_host_batch: bad batch arguments");
     require_device();
+    if (nbatch == 0) return;
     cudaStream_t s = as_stream(stream);
     const size_t xn = static_cast<size_t>(H.cols) * d, yn = static_cast<size_t>(H.rows) * d;
-    if (H.stage_x.n < xn) H.stage_x.alloc(xn);
-    if (H.stage_y.n < yn) H.stage_y.alloc(yn);
-    if (xn) STRATA_CUDA_CHECK(cudaMemcpyAsync(H.stage_x.p, X_host, xn * 4, cudaMemcpyHostToDevice, s));
-    spmm_hyb_launch(H, H.stage_x.p, H.stage_y.p, d, s);
-    if (yn) STRATA_CUDA_CHECK(cudaMemcpyAsync(Y_host, H.stage_y.p, yn * 4, cudaMemcpyDeviceToHost, s));
-    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+    const int nslots = nbatch > 1 ? 2 : 1;
+    for (int k = 0; k < nslots; ++k) {
+      if (H.stage_x[k].n < xn) H.stage_x[k].alloc(xn);
+      if (H.stage_y[k].n < yn) H.stage_y[k].alloc(yn);
+    }
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t ev[9] = {};  // entry, x_ready[2], x_free[2], y_ready[2], y_free[2]
+    auto cleanup = [&] {
+      for (auto& e : ev) if (e) cudaEventDestroy(e);
+      if (cin) cudaStreamDestroy(cin);
+      if (cout) cudaStreamDestroy(cout);
+    };
+    try {
+      STRATA_CUDA_CHECK(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+      STRATA_CUDA_CHECK(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+      for (auto& e : ev) STRATA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      cudaEvent_t entry = ev[0], *x_ready = ev + 1, *x_free = ev + 3, *y_ready = ev + 5,
+                  *y_free = ev + 7;
+      STRATA_CUDA_CHECK(cudaEventRecord(entry, s));  // everything follows prior work on `s`
+      STRATA_CUDA_CHECK(cudaStreamWaitEvent(cin, entry, 0));
+      STRATA_CUDA_CHECK(cudaStreamWaitEvent(cout, entry, 0));
+      for (int64_t b = 0; b < nbatch; ++b) {
+        const int k = static_cast<int>(b % nslots);
+        float* sx = H.stage_x[k].p;
+        float* sy = H.stage_y[k].p;
+        if (b >= nslots) STRATA_CUDA_CHECK(cudaStreamWaitEvent(cin, x_free[k], 0));
+        if (xn) STRATA_CUDA_CHECK(cudaMemcpyAsync(sx, X_host[b], xn * 4, cudaMemcpyHostToDevice, cin));
+        STRATA_CUDA_CHECK(cudaEventRecord(x_ready[k], cin));
+        STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, x_ready[k], 0));
+        if (b >= nslots) STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, y_free[k], 0));
+        spmm_hyb_launch(H, sx, sy, d, s);
+        STRATA_CUDA_CHECK(cudaEventRecord(x_free[k], s));
+        STRATA_CUDA_CHECK(cudaEventRecord(y_ready[k], s));
+        STRATA_CUDA_CHECK(cudaStreamWaitEvent(cout, y_ready[k], 0));
+        if (yn) STRATA_CUDA_CHECK(cudaMemcpyAsync(Y_host[b], sy, yn * 4, cudaMemcpyDeviceToHost, cout));
+        STRATA_CUDA_CHECK(cudaEventRecord(y_free[k], cout));
+      }
+      STRATA_CUDA_CHECK(cudaStreamSynchronize(cout));
+      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
   });
 }
 

@@ -125,7 +125,7 @@ struct strata_hyb_impl {
   mutable DevBuf<double> carry_l2;     // [l2_slots][d]
   mutable DevBuf<double> yacc;         // c > 1: f64 [rows][d] accumulator across partitions
   mutable int64_t carry_d = 0;
-  mutable DevBuf<float> stage_x, stage_y;  // e2e staging
+  mutable DevBuf<float> stage_x[2], stage_y[2];  // e2e staging (double-buffered)
 };
 
 // Kernel launchers (defined in .cu files).

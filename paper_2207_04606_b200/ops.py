@@ -26,7 +26,8 @@ from ._lib import StrataError, check, lib
 
 __all__ = [
     "StrataError", "CsrMatrix", "generate_matrix", "dense_int", "hyb_auto_k", "EllBucketPart",
-    "HybDecomposition", "decompose_hyb", "hyb_rules", "spmm", "spmm_host", "spmm_csr", "sddmm",
+    "HybDecomposition", "decompose_hyb", "hyb_rules", "spmm", "spmm_host", "spmm_host_batch",
+    "spmm_csr", "sddmm",
     "partition_rows", "device_ok",
 ]
 
@@ -250,6 +251,22 @@ def spmm_host(hyb: HybDecomposition, X_host, Y_host, stream=None):
     check(lib.strata_spmm_hyb_f32_host(hyb.handle, _ptr(X_host), _ptr(Y_host), d,
                                        _stream(stream)))
     return Y_host
+
+
+def spmm_host_batch(hyb: HybDecomposition, X_hosts, Y_hosts, stream=None):
+    """Batched end-to-end form: host (pinned) X_hosts[b] -> Y_hosts[b]; copy-in of the next
+    matrix and copy-out of the previous one overlap each SpMM."""
+    if len(X_hosts) != len(Y_hosts):
+        raise StrataError(6, "spmm_host_batch: X and Y lists differ in length")
+    n = len(X_hosts)
+    if n == 0:
+        return Y_hosts
+    d = X_hosts[0].shape[1]
+    xs = (C.c_void_p * n)(*[_ptr(x) for x in X_hosts])
+    ys = (C.c_void_p * n)(*[_ptr(y) for y in Y_hosts])
+    check(lib.strata_spmm_hyb_f32_host_batch(hyb.handle, C.cast(xs, C.c_void_p),
+                                             C.cast(ys, C.c_void_p), n, d, _stream(stream)))
+    return Y_hosts
 
 
 def spmm_csr(csr: DeviceCsr, X, Y=None, stream=None):

@@ -191,6 +191,23 @@ def test_spmm_host_e2e(cuda):
     assert np.array_equal(Y.numpy(), want)
 
 
+def test_spmm_host_batch_pipelined(cuda):
+    """Batched e2e form: 5 different feature matrices through two staging slots (slot reuse
+    ordering across the copy-in / compute / copy-out streams), each equal to the oracle; a
+    pageable (non-pinned) output and an empty batch are accepted."""
+    import torch
+    m = S.generate_matrix("powerlaw", 8000, 8000, 0, 0, 0, 16.0, 1)
+    h = S.decompose_hyb(m.to_device(cuda), 1, S.hyb_auto_k(m))
+    Xs = [torch.from_numpy(S.dense_int((m.cols, 64), 10 + b)).pin_memory() for b in range(5)]
+    Ys = [torch.empty((m.rows, 64), dtype=torch.float32).pin_memory() for _ in range(4)]
+    Ys.append(torch.empty((m.rows, 64), dtype=torch.float32))
+    S.spmm_host_batch(h, Xs, Ys)
+    for X, Y in zip(Xs, Ys):
+        want = port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, X.numpy())
+        assert np.array_equal(Y.numpy(), want)
+    S.spmm_host_batch(h, [], [])
+
+
 def test_spmm_c1_full_vs_oracle(cuda):
     """BASELINE config C1 (power-law n=65,536, avg 16, seed 1, d=32, hyb:c=1) at full size."""
     import torch
