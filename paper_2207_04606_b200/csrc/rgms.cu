@@ -38,6 +38,7 @@ struct strata_rgms {
   int device = 0;
   int64_t R = 0, m = 0, n = 0, nnz = 0;
   int64_t ntiles = 0;            // 128-edge tiles (tiles never straddle relations)
+  int64_t nruns = 0;             // message runs = T rows (see run_heads_kernel)
   DevBuf<int32_t> edges;         // [ntiles][kTileWords] per-tile edge blocks (see below)
   DevBuf<int32_t> dptr;          // [m+1] row pointer into the destination-sorted order
   int nlong = 0, nchunks = 0;     // rows with > kLong edges and their kChunk-edge chunks
@@ -101,10 +102,39 @@ __global__ void row_ptr_kernel(const int32_t* __restrict__ sorted_dst, long long
 constexpr int kTileWords = 4 + 3 * kEdges;
 constexpr int kTileChunks = kTileWords / 4;  // 97
 
-__global__ void tile_edges_kernel(const int32_t* __restrict__ rel_ptr,
+// Message runs: consecutive edges of one relation with the same destination inside one 32-edge
+// warp group of a tile are summed in pass 1's epilogue and leave one T row (a "run").  head[e]
+// marks the first edge of a run.
+__global__ void run_heads_kernel(const int32_t* __restrict__ rel_ptr,
+                                 const long long* __restrict__ tile_start,
+                                 const int32_t* __restrict__ tile_rel, long long ntiles,
+                                 const int32_t* __restrict__ dst, int32_t* __restrict__ head) {
+  for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+       s < ntiles * kEdges; s += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = s / kEdges;
+    const int i = static_cast<int>(s % kEdges);
+    const int r = tile_rel[t];
+    const long long e = rel_ptr[r] + (t - tile_start[r]) * kEdges + i;
+    if (e < rel_ptr[r + 1]) head[e] = (i % 32 == 0 || dst[e] != dst[e - 1]) ? 1 : 0;
+  }
+}
+
+// run_dst[run of e] = dst[e] for run heads (run = inclusive-scan(head)[e] - 1).
+__global__ void run_dst_kernel(const int32_t* __restrict__ head, const int32_t* __restrict__ incl,
+                               const int32_t* __restrict__ dst, long long nnz,
+                               int32_t* __restrict__ run_dst) {
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    if (head[e]) run_dst[incl[e] - 1] = dst[e];
+}
+
+// Per-tile edge blocks; the pos word of an edge is its run's T row for a run head, -2 for a
+// run continuation and -1 for padding.
+__global__ void tile_edges_kernel(const int32_t* __restrict__ rel_ptr, long long R,
                                   const long long* __restrict__ tile_start,
                                   const int32_t* __restrict__ tile_rel, long long ntiles,
-                                  const int32_t* __restrict__ src, const int32_t* __restrict__ pos,
+                                  const int32_t* __restrict__ src, const int32_t* __restrict__ head,
+                                  const int32_t* __restrict__ incl, const int32_t* __restrict__ run_pos,
                                   const float* __restrict__ A, int32_t* __restrict__ ed) {
   for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
        s < ntiles * kEdges; s += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -116,26 +146,41 @@ __global__ void tile_edges_kernel(const int32_t* __restrict__ rel_ptr,
     const bool valid = e < rel_ptr[r + 1];
     int32_t* blk = ed + t * kTileWords;
     blk[4 + i] = valid ? src[e] : 0;
-    blk[4 + kEdges + i] = valid ? pos[e] : -1;
+    blk[4 + kEdges + i] = valid ? (head[e] ? run_pos[incl[e] - 1] : -2) : -1;
     blk[4 + 2 * kEdges + i] = valid ? __float_as_int(A[e]) : 0;
     if (i < 4)
-      blk[i] = i == 0 ? r : (i == 1 ? static_cast<int>(min64(kEdges, rel_ptr[r + 1] - base)) : 0);
+      blk[i] = i == 0 ? static_cast<int>(r % R)
+                      : (i == 1 ? static_cast<int>(min64(kEdges, rel_ptr[r + 1] - base)) : 0);
   }
 }
 
+#ifndef STRATA_RGMS_STAGES
+#define STRATA_RGMS_STAGES 3
+#endif
+#ifndef STRATA_RGMS_IDXAHEAD
+#define STRATA_RGMS_IDXAHEAD 6
+#endif
+
 template <int DIN, int DOUT>
 struct RgmsSmem {
-  static constexpr int kStages = 3;  // X / W ring: tile j computes while j+1, j+2 land
-  static constexpr int kIdxSlots = 4;  // index ring: j (epilogue) .. j+3 (landing)
+  // X / W ring: tile j computes while tiles j+1 .. j+kStages-1 land.
+  static constexpr int kStages = STRATA_RGMS_STAGES;
+  // Index blocks run kIdxAhead tiles ahead (>= 2 * kStages - 2, so the block a gather needs
+  // is always older than the oldest gather group still allowed in flight).
+  static constexpr int kIdxAhead = STRATA_RGMS_IDXAHEAD;
+  static constexpr int kIdxSlots = kIdxAhead + 1;  // j (epilogue) .. j + kIdxAhead (landing)
+  static_assert(kStages >= 2 && kIdxAhead >= 2 * kStages - 2, "pipeline depths");
   static constexpr int kABytes = kEdges * DIN * 2;
   static constexpr int kWBytes = DIN * DOUT * 2;
   static constexpr int kStage = kABytes + kWBytes;
   static constexpr int kIdxBytes = kTileWords * 4;
-  static constexpr int kNC = DOUT < 32 ? DOUT : 32;          // epilogue column chunk
-  static constexpr int kEpiBytes = (kThreads / 32) * 32 * kNC * 4;  // per-warp transpose tiles
+  // Epilogue column chunk: the per-warp transpose tiles (4 warps x 32 rows x kNC f32) live in
+  // the A region of the tile being finished (its MMA has completed), so kNC <= kABytes / 512.
+  static constexpr int kNCcap = kABytes / 512;
+  static constexpr int kNC = (DOUT < 32 ? DOUT : 32) < kNCcap ? (DOUT < 32 ? DOUT : 32) : kNCcap;
   static constexpr int kIdxOff = kStages * kStage;
-  static constexpr int kEpiOff = kIdxOff + kIdxSlots * kIdxBytes;
-  static constexpr int kBytes = kEpiOff + kEpiBytes;
+  static constexpr int kBytes = kIdxOff + kIdxSlots * kIdxBytes;
+  static_assert(kNC >= 8 && DOUT % kNC == 0, "epilogue chunk");
 };
 
 // Pass 1.  CTA b processes tiles b, b + G, b + 2G, ... (G = gridDim.x).  cp.async groups are
@@ -144,7 +189,7 @@ struct RgmsSmem {
 // row gathers of tile j+2 are issued before tile j's MMA — two tiles of gathers in flight, no
 // dependent global load on the issue path.
 template <int DIN, int DOUT>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, 6)
 rgms_edge_gemm_kernel(const int32_t* __restrict__ ed, long long ntiles,
                       const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ W,
                       float* __restrict__ T) {
@@ -176,7 +221,6 @@ rgms_edge_gemm_kernel(const int32_t* __restrict__ ed, long long ntiles,
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
-  float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + warp * (32 * kSPR);
   auto idx_slot = [&](long long j) {
     return reinterpret_cast<int32_t*>(smem + SM::kIdxOff + (j % SM::kIdxSlots) * SM::kIdxBytes);
   };
@@ -206,23 +250,27 @@ rgms_edge_gemm_kernel(const int32_t* __restrict__ ed, long long ntiles,
     }
   };
 
-  // prologue: I0 I1 I2 X0 X1
-  issue_idx(0); tc::cp_async_commit();
-  issue_idx(1); tc::cp_async_commit();
-  issue_idx(2); tc::cp_async_commit();
-  tc::cp_async_wait<2>();
+  // Prologue: index blocks 0 .. kIdxAhead-1 as one group, then gathers 0 .. kStages-2, each
+  // preceded by an empty group so the steady-state pairing [I(j+kIdxAhead), X(j+kStages-1)]
+  // holds from the first iteration: "all but the newest 2(kStages-2) groups" is then exactly
+  // "X(j) has landed" (and every index block older than it, incl. I(j+kStages-1)).
+  constexpr int kS = SM::kStages, kL = SM::kIdxAhead;
+  for (int k = 0; k < kL; ++k) issue_idx(k);
+  tc::cp_async_commit();
+  tc::cp_async_wait<0>();
   __syncthreads();
-  issue_x(0); tc::cp_async_commit();
-  tc::cp_async_wait<2>();
-  __syncthreads();
-  issue_x(1); tc::cp_async_commit();
+  for (int k = 0; k < kS - 1; ++k) {
+    tc::cp_async_commit();
+    issue_x(k);
+    tc::cp_async_commit();
+  }
 
   for (long long j = 0; j < nt; ++j) {
-    tc::cp_async_wait<1>();  // X(j) and I(j+2) landed
+    tc::cp_async_wait<2 * (kS - 2)>();  // X(j) (and I(j + kS - 1)) landed
     tc::fence_proxy_async();
-    __syncthreads();         // ... for every thread; stage (j+2)%3 and idx slot (j+3)%4 are free
-    issue_idx(j + 3); tc::cp_async_commit();
-    issue_x(j + 2); tc::cp_async_commit();
+    __syncthreads();  // ... for every thread; stage (j-1)%kS and idx slot (j-1)%(kL+1) are free
+    issue_idx(j + kL); tc::cp_async_commit();
+    issue_x(j + kS - 1); tc::cp_async_commit();
     const int s = static_cast<int>(j % SM::kStages);
     if (tid == 0) {
       tc::fence_after_sync();
@@ -237,27 +285,42 @@ rgms_edge_gemm_kernel(const int32_t* __restrict__ ed, long long ntiles,
     const int32_t* si = idx_slot(j);
     const float a = __int_as_float(si[4 + 2 * kEdges + warp * 32 + lane]);
     const int32_t* spos = si + 4 + kEdges + warp * 32;
+    const int myword = spos[lane];
+    const unsigned heads = __ballot_sync(0xffffffffu, myword >= 0);
+    const unsigned pads = __ballot_sync(0xffffffffu, myword == -1);
+    const int first_pad = pads ? __ffs(pads) - 1 : 32;
     tc::mbar_wait(&mbar, static_cast<uint32_t>(j & 1));
     tc::fence_after_sync();
+    float4* epi = reinterpret_cast<float4*>(smem + s * SM::kStage) + warp * (32 * kSPR);
+    const int gi = lane / kSPR, sl = lane & (kSPR - 1);
+    unsigned mine = heads;  // runs gi, gi + kRPI, ... belong to lane group gi
+    for (int i = 0; i < gi; ++i) mine &= mine - 1;
 #pragma unroll
     for (int c0 = 0; c0 < DOUT; c0 += kNC) {
-      uint32_t v[32];
-      tc::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+      uint32_t v[kNC];
+      tc::tmem_ld_32x32b<kNC>(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
       tc::tmem_ld_wait();
-      // row `lane` -> smem, float4 slot j stored at j ^ (lane % kSPR) (conflict-free phases)
+      // row `lane` -> smem, float4 slot q stored at q ^ (lane % kSPR) (conflict-free phases)
 #pragma unroll
       for (int q = 0; q < kSPR; ++q)
         epi[lane * kSPR + (q ^ (lane & (kSPR - 1)))] =
             make_float4(a * __uint_as_float(v[4 * q]), a * __uint_as_float(v[4 * q + 1]),
                         a * __uint_as_float(v[4 * q + 2]), a * __uint_as_float(v[4 * q + 3]));
       __syncwarp();
-      // each instruction writes kRPI whole rows of the chunk (kSPR lanes per row)
+      // Runs of this warp's 32 rows (heads: pos word >= 0; continuation -2; padding -1): each
+      // lane group (kSPR lanes, one float4 column slot each) sums its runs and writes each as
+      // one T row.
+      unsigned m = mine;
+      while (m) {
+        const int r0 = __ffs(m) - 1;
+        const unsigned later = heads & ~((2u << r0) - 1u);
+        const int r1 = min(later ? __ffs(later) - 1 : 32, first_pad);
+        float4 acc = epi[r0 * kSPR + (sl ^ (r0 & (kSPR - 1)))];
+        for (int row = r0 + 1; row < r1; ++row)
+          acc = add4(acc, epi[row * kSPR + (sl ^ (row & (kSPR - 1)))]);
+        __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(spos[r0]) * DOUT + c0) + sl, acc);
 #pragma unroll
-      for (int q = 0; q < kSPR; ++q) {
-        const int row = q * kRPI + lane / kSPR, sl = lane & (kSPR - 1);
-        const int p = spos[row];
-        const float4 val = epi[row * kSPR + (sl ^ (row & (kSPR - 1)))];
-        if (p >= 0) __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(p) * DOUT + c0) + sl, val);
+        for (int i = 0; i < kRPI; ++i) m &= m - 1;
       }
       __syncwarp();
     }
@@ -485,7 +548,7 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
   STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   // Resident CTAs per SM: shared memory (~227 KB usable) and TMEM (512 columns) bound it.
   constexpr int kTmemCols = DOUT <= 32 ? 32 : (DOUT <= 64 ? 64 : (DOUT <= 128 ? 128 : 256));
-  const int per_sm = std::max(1, std::min({4, (227 * 1024) / (smem + 1024), 512 / kTmemCols}));
+  const int per_sm = std::max(1, std::min({8, (227 * 1024) / (smem + 1024), 512 / kTmemCols}));
   const long long grid = std::min<long long>(h.ntiles, static_cast<long long>(num_sms()) * per_sm);
   k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kThreads, smem, s>>>(h.edges.p, h.ntiles, X, W, h.T.p);
   STRATA_CUDA_CHECK(cudaGetLastError());
@@ -550,6 +613,7 @@ extern "C" int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, cons
     STRATA_CUDA_CHECK(cudaGetDevice(&h->device));
     h->R = R; h->m = m; h->n = n; h->nnz = nnz;
     h->dptr.alloc(m + 1);
+    const long long RR = R;
     const long long max_tiles = (nnz + kEdges - 1) / kEdges + R;  // upper bound on tiles
     long long* ntiles = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
     long long* tile_start = static_cast<long long*>(workspace_alloc(sizeof(long long) * (R + 1), s));
@@ -565,28 +629,46 @@ extern "C" int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, cons
     STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
     h->ntiles = hnt;
     if (nnz > 0) {
-      // Stable sort of edge ids by destination: a row's edges keep relation order.
-      int32_t* ids = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * nnz * 4, s));
-      int32_t* order = ids + nnz;
-      int32_t* keys = ids + 2 * nnz;
-      int32_t* pos = ids + 3 * nnz;
+      // Runs: heads -> inclusive scan -> run ids; a stable radix sort of the runs by
+      // destination gives each run its T row (a row's runs keep relation order) and dptr.
+      int32_t* head = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * nnz * 2, s));
+      int32_t* incl = head + nnz;
       const unsigned g = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, num_sms() * 16LL));
-      iota_kernel<<<g, 256, 0, s>>>(ids, nnz);
+      const unsigned ge = static_cast<unsigned>(std::min<long long>((h->ntiles * kEdges + 255) / 256, num_sms() * 16LL));
+      run_heads_kernel<<<ge, 256, 0, s>>>(rel_ptr, tile_start, tile_rel, h->ntiles, dst, head);
+      size_t ib = 0;
+      cub::DeviceScan::InclusiveSum(nullptr, ib, head, incl, nnz, s);
+      void* itmp = workspace_alloc(ib, s);
+      cub::DeviceScan::InclusiveSum(itmp, ib, head, incl, nnz, s);
+      int32_t hr = 0;
+      STRATA_CUDA_CHECK(cudaMemcpyAsync(&hr, incl + nnz - 1, sizeof(hr), cudaMemcpyDeviceToHost, s));
+      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+      const long long nr = hr;
+      h->nruns = nr;
+      int32_t* ids = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * nr * 5, s));
+      int32_t* order = ids + nr;
+      int32_t* keys = ids + 2 * nr;
+      int32_t* run_pos = ids + 3 * nr;
+      int32_t* run_dst = ids + 4 * nr;
+      const unsigned gn = static_cast<unsigned>(std::min<long long>((nr + 255) / 256, num_sms() * 16LL));
+      run_dst_kernel<<<g, 256, 0, s>>>(head, incl, dst, nnz, run_dst);
+      iota_kernel<<<gn, 256, 0, s>>>(ids, nr);
       int bits = 1;
       while (bits < 31 && (1LL << bits) <= m) ++bits;
       size_t sb = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, sb, dst, keys, ids, order, nnz, 0, bits, s);
+      cub::DeviceRadixSort::SortPairs(nullptr, sb, run_dst, keys, ids, order, nr, 0, bits, s);
       void* stmp = workspace_alloc(sb, s);
-      cub::DeviceRadixSort::SortPairs(stmp, sb, dst, keys, ids, order, nnz, 0, bits, s);
-      invert_kernel<<<g, 256, 0, s>>>(order, nnz, pos);
+      cub::DeviceRadixSort::SortPairs(stmp, sb, run_dst, keys, ids, order, nr, 0, bits, s);
+      invert_kernel<<<gn, 256, 0, s>>>(order, nr, run_pos);
       const unsigned gr = static_cast<unsigned>(std::min<long long>((m + 1 + 255) / 256, num_sms() * 16LL));
-      row_ptr_kernel<<<gr, 256, 0, s>>>(keys, nnz, m, h->dptr.p);
+      row_ptr_kernel<<<gr, 256, 0, s>>>(keys, nr, m, h->dptr.p);
       h->edges.alloc(static_cast<size_t>(h->ntiles) * kTileWords);
-      const unsigned ge = static_cast<unsigned>(std::min<long long>((h->ntiles * kEdges + 255) / 256, num_sms() * 16LL));
-      tile_edges_kernel<<<ge, 256, 0, s>>>(rel_ptr, tile_start, tile_rel, h->ntiles, src, pos, A,
-                                           h->edges.p);
+      tile_edges_kernel<<<ge, 256, 0, s>>>(rel_ptr, RR, tile_start, tile_rel, h->ntiles, src, head,
+                                           incl, run_pos, A, h->edges.p);
       STRATA_CUDA_CHECK(cudaFreeAsync(stmp, s));
       STRATA_CUDA_CHECK(cudaFreeAsync(ids, s));
+      STRATA_CUDA_CHECK(cudaFreeAsync(itmp, s));
+      STRATA_CUDA_CHECK(cudaFreeAsync(head, s));
       // Long rows (> kLong edges) and their chunk offsets; one host sync sizes the partials.
       if (m > 0) {
         uint8_t* flag = static_cast<uint8_t*>(workspace_alloc(m, s));
@@ -653,7 +735,7 @@ extern "C" int strata_rgms_run_bf16(const strata_rgms* h, const void* X_bf16, co
       if (h->m > 0) STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * h->m * d_out, s));
       return;
     }
-    const size_t need = static_cast<size_t>(h->nnz) * d_out;
+    const size_t need = static_cast<size_t>(h->nruns) * d_out;
     const size_t pneed = static_cast<size_t>(h->nchunks) * d_out;
     if (h->T.n < need || h->partial.n < pneed) {
       STRATA_CUDA_CHECK(cudaStreamSynchronize(s));  // earlier runs may still read the old T
@@ -677,7 +759,7 @@ extern "C" int strata_rgms_info(const strata_rgms* h, int64_t* tiles_bound, int6
   return guarded([&] {
     if (!h) throw ApiError(STRATA_ERR_USAGE, "null rgms plan");
     if (tiles_bound) *tiles_bound = h->ntiles;
-    if (t_bytes_per_dout) *t_bytes_per_dout = h->nnz * 4;
+    if (t_bytes_per_dout) *t_bytes_per_dout = h->nruns * 4;
   });
 }
 

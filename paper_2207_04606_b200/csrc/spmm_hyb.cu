@@ -161,6 +161,9 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
   }
 }
 
+#ifndef STRATA_SPMM_MINB16  // CTAs/SM the d=64 variant is register-budgeted for (A/B knob)
+#define STRATA_SPMM_MINB16 2
+#endif
 #ifndef STRATA_SPMM_MINB32  // CTAs/SM the d=128 variant is register-budgeted for (A/B knob)
 #define STRATA_SPMM_MINB32 3
 #endif
@@ -175,7 +178,7 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 //   3. consume: batches of 8 real slots are read with broadcast 128-bit shared loads (no
 //      shuffles), their X rows gathered UG at a time (128-bit per lane), and accumulated.
 template <int L, int VEC, bool kScalar>
-__global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar) ? STRATA_SPMM_MINB32 : 2))
+__global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2)))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int kT = 8;  // real slots per consume batch / slots per lane per compaction round
 #ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
@@ -484,6 +487,10 @@ void launch_variant(const SpmmArgs& args, long long total_chunks, long long d, c
   if (!configured) {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(spmm_hyb_kernel<L, VEC, kScalar>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+#ifdef STRATA_SPMM_CARVEOUT  // A/B knob: prefer the largest shared-memory carveout
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(spmm_hyb_kernel<L, VEC, kScalar>,
+                                           cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+#endif
     configured = true;
   }
   spmm_hyb_kernel<L, VEC, kScalar><<<grid, kBlock, smem, s>>>(args);
