@@ -298,6 +298,29 @@ def _time_ms(torch, stream, fn, reps=20):
     return e0.elapsed_time(e1) / reps
 
 
+def _time_graph_ms(torch, fn, calls=20, reps=10):
+    """Per-call device time of a launch-bound op replayed from a CUDA graph of `calls`
+    back-to-back calls (captured on a side stream; CUDA events around `reps` replays)."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(calls):
+                fn()
+        g.replay()
+        s.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+        s.synchronize()
+    return e0.elapsed_time(e1) / (reps * calls)
+
+
 def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     """C3 (BSR sparse attention, bf16, tcgen05) and C4 (RGCN, AM shape, tcgen05)."""
     out = {}
@@ -307,13 +330,29 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     d = 64
     X = torch.randint(-3, 4, (4096, d), device=dev).to(torch.bfloat16)
     Y = torch.empty((4096, d), device=dev)
-    ms = _time_ms(torch, stream, lambda: S.bsr_spmm(bs, X, Y))
+    ms_loop = _time_ms(torch, stream, lambda: S.bsr_spmm(bs, X, Y))
+    ms = _time_graph_ms(torch, lambda: S.bsr_spmm(bs, X, Y))
     flops = 2.0 * bs.nblocks * 32 * 32 * d
     b_alg = bs.nblocks * 32 * 32 * 2 + bs.nblocks * 4 + 129 * 4 + bs.nblocks * 32 * d * 2 + 4096 * d * 4
     out["c3_bsr_spmm"] = {"ms": round(ms, 5), "gflops": round(flops / (ms * 1e-3) / 1e9, 1),
                           "blocks": bs.nblocks, "tensor_frac": round(flops / (ms * 1e-3) / 1e12 / bf16_peak, 5),
                           "hbm_frac": round(b_alg / (ms * 1e-3) / 1e9 / hbm_peak, 4),
+                          "python_loop_ms": round(ms_loop, 5),
+                          "timing": "CUDA graph of 20 back-to-back calls (launch-bound op); "
+                                    "python_loop_ms = ctypes call per launch",
                           "note": "208 MFLOP over 10.8 MB: launch/latency-bound by construction"}
+    # 12-head batched variant: heads share the mask, own values and features.
+    H = 12
+    Vh = torch.randint(1, 10, (H, bs.nblocks, 32, 32), device=dev).to(torch.bfloat16)
+    Xh = torch.randint(-3, 4, (H, 4096, d), device=dev).to(torch.bfloat16)
+    Yh = torch.empty((H, 4096, d), device=dev)
+    msh = _time_graph_ms(torch, lambda: S.bsr_spmm_batched(bs, Vh, Xh, Yh))
+    flops_h = H * flops
+    b_alg_h = H * (bs.nblocks * 32 * 32 * 2 + bs.nblocks * 32 * d * 2 + 4096 * d * 4) + bs.nblocks * 4 + 129 * 4
+    out["c3_bsr_spmm_12head"] = {"ms": round(msh, 5), "gflops": round(flops_h / (msh * 1e-3) / 1e9, 1),
+                                 "tensor_frac": round(flops_h / (msh * 1e-3) / 1e12 / bf16_peak, 5),
+                                 "hbm_frac": round(b_alg_h / (msh * 1e-3) / 1e9 / hbm_peak, 4),
+                                 "bytes_model": "heads*(blocks*2KB + blocks*32*d*2 + 4096*d*4)"}
     # C4: AM-shaped power-law graph split into 133 relations, d_in = d_out = 32.
     g = S.generate_matrix("powerlaw", 1885136, 1885136, 0, 0, 0, 3.0051, 1)
     rel = S.split_relations(g, 133, 1).to_device(dev)
@@ -327,15 +366,19 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     ms = _time_ms(torch, stream, lambda: plan.run(Xr, W, Yr), reps=10)
     flops = 2.0 * g.nnz * 32 * 32
     b_onchip = g.nnz * (4 + 4 + 2) + g.nnz * 32 * 2 + 133 * 32 * 32 * 2 + g.rows * 32 * 4
-    # two-pass model actually executed: (src, pos, A) + X row gather + T write, T read + dptr + Y
-    b_2pass = g.nnz * 12 + g.nnz * 32 * 2 + g.nnz * 32 * 4 * 2 + (g.rows + 1) * 4 + g.rows * 32 * 4
+    # two-pass model actually executed: (src, pos, A) + X row gather + message-row write, then
+    # message-row read + dptr + Y; message rows = the plan's (relation, destination) runs
+    runs = plan.message_rows
+    b_2pass = g.nnz * 12 + g.nnz * 32 * 2 + runs * 32 * 4 * 2 + (g.rows + 1) * 4 + g.rows * 32 * 4
     out["c4_rgcn"] = {"ms": round(ms, 4), "gflops": round(flops / (ms * 1e-3) / 1e9, 1),
                       "nnz": g.nnz, "plan_ms": round(plan_ms, 1),
                       "tensor_frac": round(flops / (ms * 1e-3) / 1e12 / bf16_peak, 5),
                       "hbm_frac_onchip_model": round(b_onchip / (ms * 1e-3) / 1e9 / hbm_peak, 4),
                       "hbm_frac_two_pass_model": round(b_2pass / (ms * 1e-3) / 1e9 / hbm_peak, 4),
+                      "message_rows": runs,
                       "bytes_model": "on-chip: nnz*10 + nnz*d_in*2 + R*d_in*d_out*2 + m*d_out*4 "
-                                     "(661 MB); two-pass: + 2*nnz*d_out*4 message rows (2.1 GB)"}
+                                     "(661 MB); two-pass: nnz*12 + nnz*d_in*2 + 2*runs*d_out*4 "
+                                     "+ (m+1)*4 + m*d_out*4"}
     return out
 
 

@@ -157,9 +157,15 @@ int strata_bsr_info(const strata_bsr* h, int64_t* mb, int64_t* nb, int64_t* b, i
 int strata_bsr_read(const strata_bsr* h, int32_t* jo_indptr, int32_t* jo_indices, float* values);
 int strata_bsr_destroy(strata_bsr* h);
 /* BSR SpMM on tcgen05 tensor cores: Y[mb*b][d] (f32, overwritten) = A_bsr(bf16) * X
- * (X[nb*b][d] bf16 row-major).  Requires b == 32 and d % 16 == 0 (16 <= d <= 256). */
+ * (X[nb*b][d] bf16 row-major).  Requires b == 32 and d in {64, 128, 256, 512}. */
 int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int64_t d,
                          void* stream);
+/* Multi-head form (batched SpMM of sparse attention): `heads` problems share the
+ * block structure of h; values_bf16 [heads][nblocks][b][b] (row-major blocks, the reference's
+ * A_bsr layout) or NULL (heads == 1: h's own values), X [heads][nb*b][d] bf16,
+ * Y [heads][mb*b][d] f32.  Grid = block rows x heads. */
+int strata_bsr_spmm_bf16_batched(const strata_bsr* h, const void* values_bf16, const void* X_bf16,
+                                 float* Y, int64_t heads, int64_t d, void* stream);
 
 /* ---- ELL (device) ---------------------------------------------------------------------
  * Replaces: csr_to_ell(csr, w, prefix) (storage.hpp:124, storage.cpp:190-227).

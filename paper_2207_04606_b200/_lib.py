@@ -87,6 +87,7 @@ _sig("strata_bsr_info", C.c_int, vp, i64p, i64p, i64p, i64p, i64p)
 _sig("strata_bsr_read", C.c_int, vp, vp, vp, vp)
 _sig("strata_bsr_destroy", C.c_int, vp)
 _sig("strata_bsr_spmm_bf16", C.c_int, vp, vp, vp, i64, vp)
+_sig("strata_bsr_spmm_bf16_batched", C.c_int, vp, vp, vp, vp, i64, i64, vp)
 _sig("strata_ell_from_csr", C.c_int, vp, vp, vp, i64, i64, i64, vp, vp, vp)
 _sig("strata_rgms_bf16", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp, vp, i64, i64, vp)
 _sig("strata_rgms_plan", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, C.POINTER(vp), vp)
@@ -106,7 +107,8 @@ EXPORTED = [
     "strata_hyb_dims", "strata_hyb_destroy", "strata_hyb_schedule_info", "strata_spmm_hyb_f32", "strata_spmm_hyb_f32_host",
     "strata_spmm_hyb_f32_host_batch",
     "strata_spmm_csr_f32", "strata_sddmm_csr_f32", "strata_bsr_from_csr", "strata_bsr_info",
-    "strata_bsr_read", "strata_bsr_destroy", "strata_bsr_spmm_bf16", "strata_ell_from_csr",
+    "strata_bsr_read", "strata_bsr_destroy", "strata_bsr_spmm_bf16",
+    "strata_bsr_spmm_bf16_batched", "strata_ell_from_csr",
     "strata_rgms_bf16", "strata_rgms_plan", "strata_rgms_run_bf16", "strata_rgms_info",
     "strata_rgms_destroy", "strata_partition_rows",
 ]

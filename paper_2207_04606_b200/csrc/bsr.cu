@@ -102,52 +102,67 @@ __global__ void bsr_scatter_kernel(const int32_t* __restrict__ indptr,
     }
     const long long pos = static_cast<long long>(lo) * b * b + (i % b) * b + (j % b);
     bv[pos] = values[q];
-    // The bf16 operand copy of a 32x32 block is stored pre-arranged in the UMMA K-major
-    // core-matrix layout (8x8 bf16 core matrices, K groups adjacent), so the SpMM moves each
-    // block into shared memory with a single 2 KB bulk copy.  Other block sizes: row-major.
-    const int ii = static_cast<int>(i % b), ji = static_cast<int>(j % b);
-    const long long hpos = b == 32 ? static_cast<long long>(lo) * 1024 + (ii >> 3) * 256 +
-                                         (ji >> 3) * 64 + (ii & 7) * 8 + (ji & 7)
-                                   : pos;
-    bvh[hpos] = __float2bfloat16_rn(values[q]);
+    bvh[pos] = __float2bfloat16_rn(values[q]);  // tensor-core operand copy, same layout
   }
 }
 
 // ---- tensor-core SpMM ---------------------------------------------------------------------
+#ifdef STRATA_BSR_TRACE  // development: per-CTA %globaltimer stamps (tools/ab_rgcn.py prints them)
+__device__ unsigned long long g_bsr_trace[1024][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define BSR_TRACE(k) \
+  do { if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) g_bsr_trace[blockIdx.x][k] = gtimer(); } while (0)
+#else
+#define BSR_TRACE(k) do {} while (0)
+#endif
 constexpr int kB = 32;        // block size served by the tensor-core path
-constexpr int kStages = 6;    // smem ring depth
+// smem ring depth: 8 stages (48 KB at d = 64: 4 CTAs per SM for the multi-head grid; a
+// 16-deep ring measured no faster on C3), bounded by ~200 KB of stages.
+template <int D>
+constexpr int bsr_stages() {
+  constexpr int stage = 32 * 32 * 2 + 32 * D * 2;
+  return (200 * 1024) / stage < 8 ? (200 * 1024) / stage : 8;
+}
 constexpr int kThreads = 128;
 constexpr int kMaxPre = 256;  // block-column indices of a block row preloaded into smem
 
 // Warp-specialised, mbarrier-pipelined block-row SpMM:
 //   warp 0 / lane 0  TMA producer: per block, one 2 KB bulk copy of the pre-arranged bf16 block
-//                    (K-major B operand) + d/8 TMA tiles {8 features x 32 rows} of X that land
-//                    exactly in the MN-major A-operand core-matrix layout; completion is
+//                    (K-major B operand) + d/64 TMA tiles {64 features x 32 rows} of X with
+//                    the 128-byte swizzle (MN-major SW128 A operand); completion is
 //                    counted in bytes on full[s]; the slot is reused once empty[s] fires.
 //   warp 1 / lane 0  MMA issuer: waits full[s], issues tcgen05.mma (M = feature tile, N = 32
 //                    block rows, K = 2 x 16), tcgen05.commit -> empty[s]; final commit -> done.
 //   all 4 warps      epilogue: tcgen05.ld of the TMEM accumulator -> Y rows.
 template <int D>  // feature count, 64 or a multiple of 128 (<= 512)
 __global__ void __launch_bounds__(kThreads, 1)
-bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ jo_indptr,
-                   const int32_t* __restrict__ jo_indices, const __nv_bfloat16* __restrict__ bvals,
-                   float* __restrict__ Y) {
+bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap xmap,
+                   const int32_t* __restrict__ jo_indptr, const int32_t* __restrict__ jo_indices,
+                   long long nblocks, long long x_rows, long long y_rows, float* __restrict__ Y) {
   constexpr int kM = D == 64 ? 64 : 128;         // UMMA M (feature tile)
   constexpr int kTiles = D / kM;                  // feature tiles
   constexpr int kCols = kTiles * kB < 32 ? 32 : kTiles * kB;  // TMEM columns (pow2 >= 32)
   constexpr int kAB = kB * kB * 2;                // block bytes (B operand)
   constexpr int kXB = kB * D * 2;                 // X tile bytes (A operand)
   constexpr int kStageB = kAB + kXB;
+  constexpr int kStages = bsr_stages<D>();
   constexpr uint32_t kIdesc = tc::make_idesc_bf16(kM, kB, /*A MN-major*/ true, /*B K-major*/ false);
   static_assert(D == 64 || (D % 128 == 0 && D <= 512), "unsupported feature size");
 
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SWIZZLE_128B atoms need 1024-byte alignment: round the dynamic base up (1 KB is reserved).
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   __shared__ uint64_t full[kStages], empty[kStages], done;
   __shared__ uint32_t tmem_slot;
   __shared__ int32_t s_cols[kMaxPre];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long br = blockIdx.x;
+  const long long br = blockIdx.x, head = blockIdx.y;  // block row, batch entry (head)
+  BSR_TRACE(0);
   const int q0 = jo_indptr[br], nblk = jo_indptr[br + 1] - q0;
   for (int j = tid; j < nblk && j < kMaxPre; j += kThreads) s_cols[j] = jo_indices[q0 + j];
   if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
@@ -163,20 +178,24 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __re
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
+  BSR_TRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
+      tc::prefetch_tensormap(&amap);
       tc::prefetch_tensormap(&xmap);
       for (int j = 0; j < nblk; ++j) {
         const int s = j % kStages;
         if (j >= kStages) tc::mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
         uint8_t* sa = smem + s * kStageB;
         tc::mbar_arrive_expect_tx(&full[s], kStageB);
-        tc::bulk_copy_g2s(sa, bvals + static_cast<long long>(q0 + j) * kB * kB, kAB, &full[s]);
+        // block (head, q0 + j): rows of the [heads * nblocks * 32][32] value view, SW64
+        tc::tma_load_2d(sa, &amap, 0, static_cast<int>((head * nblocks + q0 + j) * kB), &full[s]);
         const int col = j < kMaxPre ? s_cols[j] : jo_indices[q0 + j];
 #pragma unroll
-        for (int fg = 0; fg < D / 8; ++fg)
-          tc::tma_load_2d(sa + kAB + fg * 512, &xmap, fg * 8, col * kB, &full[s]);
+        for (int fa = 0; fa < D / 64; ++fa)  // one {64 features x 32 rows} box per 128-B atom
+          tc::tma_load_2d(sa + kAB + fa * 4096, &xmap, fa * 64,
+                          static_cast<int>(head * x_rows + col * kB), &full[s]);
       }
     }
     __syncwarp();
@@ -185,6 +204,8 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __re
       for (int j = 0; j < nblk; ++j) {
         const int s = j % kStages;
         tc::mbar_wait(&full[s], (j / kStages) & 1);
+        if (j == 0) BSR_TRACE(2);
+        if (j == nblk - 1) BSR_TRACE(3);
         tc::fence_after_sync();
         const uint32_t sa = tc::smem_u32(smem + s * kStageB);
         const uint32_t sx = sa + kAB;
@@ -192,9 +213,12 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __re
         for (int t = 0; t < kTiles; ++t) {
 #pragma unroll
           for (int kk = 0; kk < kB / 16; ++kk) {
-            // A = X tile (MN-major): feature tile t starts kM/8 feature groups * 512 B later.
-            const uint64_t adesc = tc::make_desc(sx + t * (kM / 8) * 512 + kk * 256, 128, 512);
-            const uint64_t bdesc = tc::make_desc(sa + kk * 256, 128, 512);
+            // A = X tile, MN-major SWIZZLE_128B: 64-feature atoms 4 KB apart (LBO), 8-row K
+            // groups 1 KB apart (SBO); K step kk starts 16 rows = 2 KB later.
+            const uint64_t adesc = tc::make_desc_sw128(sx + t * (kM / 64) * 4096 + kk * 2048, 4096, 1024);
+            // B = block, K-major SWIZZLE_64B (rows ii of 64 B, 8-row groups 512 B apart);
+            // K step kk = 16 elements = 32 B inside the swizzled row.
+            const uint64_t bdesc = tc::make_desc_sw64(sa + kk * 32, 0, 512);
             tc::mma_bf16(tmem + t * kB, adesc, bdesc, kIdesc, j > 0 || kk > 0);
           }
         }
@@ -205,9 +229,10 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __re
     __syncwarp();
   }
 
-  float* yrow = Y + br * kB * D;
+  float* yrow = Y + (head * y_rows + br * kB) * D;
   if (nblk > 0) {
     tc::mbar_wait(&done, 0);
+    if (tid == 0) BSR_TRACE(4);
     tc::fence_after_sync();
 #pragma unroll
     for (int t = 0; t < kTiles; ++t) {
@@ -226,12 +251,11 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __re
   }
   tc::fence_before_sync();
   __syncthreads();
+  BSR_TRACE(5);
   if (warp == 0) tc::tmem_dealloc<kCols>(tmem);
 }
 
-// TMA descriptor of X viewed as [rows][D] bf16, box {8 features, 32 rows} (16 B x 32 = one
-// 512 B MN-major core-matrix column of the A operand).
-CUtensorMap make_x_map(const __nv_bfloat16* X, long long rows, int D) {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -241,31 +265,47 @@ CUtensorMap make_x_map(const __nv_bfloat16* X, long long rows, int D) {
       throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  return encode;
+}
+
+// 2D bf16 tensor map over a row-major [rows][cols] array with a {box_cols, 32} box.
+CUtensorMap make_map_2d(const __nv_bfloat16* base, long long rows, int cols, int box_cols,
+                        CUtensorMapSwizzle swz) {
   CUtensorMap map;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(D) * 2};
-  const cuuint32_t box[2] = {8, kB};
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(cols) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), kB};
   const cuuint32_t estride[2] = {1, 1};
-  const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(X),
-                            gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                          const_cast<__nv_bfloat16*>(base), gdim, gstride, box,
+                                          estride, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return map;
 }
 
+// X viewed as [heads * x_rows][D] bf16, box {64 features, 32 rows}, 128-byte swizzle: one box
+// = one 4 KB column of MN-major SW128 atoms of the A operand.  Block values viewed as
+// [heads * nblocks * 32][32] bf16 (row-major blocks), box {32, 32}, 64-byte swizzle: one box =
+// the K-major SW64 B operand.
 template <int D>
-void launch_bsr(const strata_bsr& h, const __nv_bfloat16* X, float* Y, cudaStream_t s) {
-  constexpr int smem = kStages * (kB * kB * 2 + kB * D * 2);
+void launch_bsr(const strata_bsr& h, const __nv_bfloat16* vals, long long heads,
+                const __nv_bfloat16* X, float* Y, cudaStream_t s) {
+  constexpr int smem = bsr_stages<D>() * (kB * kB * 2 + kB * D * 2) + 1024;
   static bool configured = false;
   if (!configured) {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(bsr_spmm_tc_kernel<D>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  const CUtensorMap xmap = make_x_map(X, h.nb * kB, D);
-  bsr_spmm_tc_kernel<D><<<static_cast<unsigned>(h.mb), kThreads, smem, s>>>(
-      xmap, h.indptr.p, h.indices.p, h.vals_bf.p, Y);
+  const long long x_rows = h.nb * kB, y_rows = h.mb * kB;
+  const CUtensorMap xmap = make_map_2d(X, heads * x_rows, D, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap amap =
+      make_map_2d(vals, heads * std::max<long long>(h.nblocks, 1) * kB, kB, kB, CU_TENSOR_MAP_SWIZZLE_64B);
+  const dim3 grid(static_cast<unsigned>(h.mb), static_cast<unsigned>(heads));
+  bsr_spmm_tc_kernel<D><<<grid, kThreads, smem, s>>>(amap, xmap, h.indptr.p, h.indices.p,
+                                                     h.nblocks, x_rows, y_rows, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -293,6 +333,12 @@ int guard_bsr(F&& f) {
 }  // namespace
 
 extern "C" {
+
+#ifdef STRATA_BSR_TRACE
+int strata_debug_bsr_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_bsr_trace, sizeof(g_bsr_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 int strata_bsr_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
                         int64_t rows, int64_t cols, int64_t nnz, int64_t b, void* stream,
@@ -404,24 +450,37 @@ int strata_bsr_destroy(strata_bsr* h) {
   return STRATA_OK;
 }
 
-int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int64_t d,
-                         void* stream) {
+int strata_bsr_spmm_bf16_batched(const strata_bsr* h, const void* values_bf16, const void* X_bf16,
+                                 float* Y, int64_t heads, int64_t d, void* stream) {
   return guard_bsr([&] {
     if (!h) throw ApiError(STRATA_ERR_USAGE, "null bsr handle");
     if (h->b != kB) throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: tensor-core path needs b == 32");
+    if (heads < 1 || heads > 65535) throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: heads must be in [1, 65535]");
+    if (d != 64 && d != 128 && d != 256 && d != 512)
+      throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: d must be 64, 128, 256 or 512");
+    if (!values_bf16 && heads > 1)
+      throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: per-head values are required when heads > 1");
     if (h->mb == 0) return;
     require_device_bsr();
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const auto* X = static_cast<const __nv_bfloat16*>(X_bf16);
+    const auto* V = values_bf16 ? static_cast<const __nv_bfloat16*>(values_bf16) : h->vals_bf.p;
+    if (h->nblocks == 0) {  // no stored block: Y = 0 (interp.cpp:584-587)
+      STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * heads * h->mb * kB * d, s));
+      return;
+    }
     switch (d) {
-      case 64: launch_bsr<64>(*h, X, Y, s); break;
-      case 128: launch_bsr<128>(*h, X, Y, s); break;
-      case 256: launch_bsr<256>(*h, X, Y, s); break;
-      case 512: launch_bsr<512>(*h, X, Y, s); break;
-      default:
-        throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: d must be 64, 128, 256 or 512");
+      case 64: launch_bsr<64>(*h, V, heads, X, Y, s); break;
+      case 128: launch_bsr<128>(*h, V, heads, X, Y, s); break;
+      case 256: launch_bsr<256>(*h, V, heads, X, Y, s); break;
+      case 512: launch_bsr<512>(*h, V, heads, X, Y, s); break;
     }
   });
+}
+
+int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int64_t d,
+                         void* stream) {
+  return strata_bsr_spmm_bf16_batched(h, nullptr, X_bf16, Y, 1, d, stream);
 }
 
 }  // extern "C"

@@ -30,6 +30,20 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;                             // base_offset 0, lbo_mode 0, layout_type 0 (none)
 }
 
+// Same with the 128-byte swizzle layout (what a TMA tensor map with CU_TENSOR_MAP_SWIZZLE_128B
+// writes; atoms of 8 rows x 128 B, 16-byte chunk c of row r stored at c ^ (r % 8); the
+// atom's base must be 1024-byte aligned).  MN-major: LBO = stride between 128-byte MN atoms,
+// SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return make_desc(saddr, lbo, sbo) | (static_cast<uint64_t>(2) << 61);
+}
+
+// 64-byte swizzle (CU_TENSOR_MAP_SWIZZLE_64B): atoms of 8 rows x 64 B (512 B, 512-aligned).
+// K-major with K <= 32 bf16: SBO = stride between 8-row groups, LBO unused.
+__device__ __forceinline__ uint64_t make_desc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return make_desc(saddr, lbo, sbo) | (static_cast<uint64_t>(4) << 61);
+}
+
 // Instruction descriptor, kind::f16 with bf16 inputs and f32 accumulation.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_major,
                                                        bool b_mn_major) {

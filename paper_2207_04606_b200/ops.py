@@ -352,6 +352,22 @@ def bsr_spmm(bsr: BsrMatrix, X_bf16, Y=None, stream=None):
     return Y
 
 
+def bsr_spmm_batched(bsr: BsrMatrix, values_bf16, X_bf16, Y=None, stream=None):
+    """Multi-head block-sparse SpMM (batched SpMM of sparse attention): the heads
+    share the block structure of ``bsr`` and bring their own block values.
+    values_bf16 [H][nblocks][b][b] (row-major blocks, the reference's A_bsr layout per head),
+    X_bf16 [H][nb*b][d] -> Y [H][mb*b][d] f32, Y[h] = A_h @ X[h]."""
+    import torch
+    H, _, d = X_bf16.shape
+    if tuple(values_bf16.shape) != (H, bsr.nblocks, bsr.b, bsr.b):
+        raise StrataError(6, "bsr_spmm_batched: values must be [heads][nblocks][b][b]")
+    if Y is None:
+        Y = torch.empty((H, bsr.mb * bsr.b, d), dtype=torch.float32, device=X_bf16.device)
+    check(lib.strata_bsr_spmm_bf16_batched(bsr.handle, _ptr(values_bf16), _ptr(X_bf16), _ptr(Y),
+                                           H, d, _stream(stream)))
+    return Y
+
+
 # ---- ELL (storage.hpp:124, storage.cpp:190-227) --------------------------------------------
 
 def csr_to_ell(csr: DeviceCsr, w: int, stream=None):
@@ -412,6 +428,13 @@ class RgmsPlan:
                                    rel.relations, rel.rows, rel.cols, rel.nnz, C.byref(h),
                                    _stream(stream)))
         self._h = h
+
+    @property
+    def message_rows(self) -> int:
+        """T rows a run writes and reads back: (relation, destination) runs of the plan."""
+        t, b = C.c_int64(), C.c_int64()
+        check(lib.strata_rgms_info(self._h, C.byref(t), C.byref(b)))
+        return b.value // 4
 
     def run(self, X_bf16, W_bf16, Y=None, stream=None):
         import torch
@@ -476,5 +499,5 @@ def _mt19937_stream(seed: int, out: np.ndarray):
     out[:] = bg.random_raw(out.size).astype(np.uint32)
 
 
-__all__ += ["BsrMatrix", "csr_to_bsr", "bsr_spmm", "csr_to_ell", "RelSparse", "RgmsPlan", "rgms",
+__all__ += ["BsrMatrix", "csr_to_bsr", "bsr_spmm", "bsr_spmm_batched", "csr_to_ell", "RelSparse", "RgmsPlan", "rgms",
             "split_relations"]

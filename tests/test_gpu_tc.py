@@ -81,6 +81,30 @@ def test_bsr_spmm_c3_shape(cuda, d):
     assert close_ref_metric(Yr, dense @ Xr64, 1e-2)
 
 
+@pytest.mark.parametrize("heads,d", [(12, 64), (3, 128), (2, 512)])
+def test_bsr_spmm_batched_heads(cuda, heads, d):
+    """Multi-head batched SpMM: 12 heads on the C3 mask, per-head block values
+    and features; each head bitwise equal to the oracle on integer operands, and the
+    single-head call through the batched entry equal to strata_bsr_spmm_bf16."""
+    import torch
+    m = S.generate_matrix("blocksparse", 4096, 4096, 0.1, 0, 32, 0, 1)
+    bs = S.csr_to_bsr(m.to_device(cuda), 32)
+    jp, ji, _ = port.csr_to_bsr(m.rows, m.cols, m.indptr, m.indices, m.values, 32)
+    rng = np.random.default_rng(heads * 1000 + d)
+    vals = rng.integers(1, 10, (heads, bs.nblocks, 32, 32)).astype(np.float32)
+    X = rng.integers(-3, 4, (heads, 4096, d)).astype(np.float32)
+    Y = S.bsr_spmm_batched(bs, bf16(torch.from_numpy(vals).to(cuda)),
+                           bf16(torch.from_numpy(X).to(cuda))).cpu().numpy()
+    for h in range(heads):
+        want = port.bsr_spmm_refnum(128, 32, jp, ji, vals[h].reshape(-1), X[h])
+        assert np.array_equal(Y[h], want), h
+    one = S.bsr_spmm(bs, bf16(torch.from_numpy(X[0]).to(cuda))).cpu().numpy()
+    own = bs.arrays()["values"].reshape(1, bs.nblocks, 32, 32)
+    Y1 = S.bsr_spmm_batched(bs, bf16(torch.from_numpy(own).to(cuda)),
+                            bf16(torch.from_numpy(X[:1]).to(cuda))).cpu().numpy()
+    assert np.array_equal(Y1[0], one)
+
+
 def test_bsr_empty_block_rows(cuda):
     import torch
     m = S.generate_matrix("blocksparse", 512, 256, 0.05, 0, 32, 0, 4)
