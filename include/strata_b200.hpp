@@ -263,6 +263,159 @@ inline double padding_ratio(const TensorStorage& s) {
   return s.values.empty() ? 0.0 : static_cast<double>(s.pad_slots) / static_cast<double>(s.values.size());
 }
 
+// ---- invariants / accounting (storage.cpp:455-630), host-side on read-back storage ---------
+namespace detail {
+// aux array whose name ends with `suffix` (storages carry caller prefixes, e.g. hyb_p0_b1_)
+inline const IntArray* find_suffix(const TensorStorage& s, const std::string& suffix) {
+  for (const auto& kv : s.aux)
+    if (kv.first.size() >= suffix.size() &&
+        kv.first.compare(kv.first.size() - suffix.size(), suffix.size(), suffix) == 0)
+      return &kv.second;
+  return nullptr;
+}
+inline const IntArray& need_suffix(const TensorStorage& s, const std::string& suffix) {
+  const IntArray* a = find_suffix(s, suffix);
+  if (!a) fail(ErrKind::Lookup, "storage has no aux array: *" + suffix);
+  return *a;
+}
+}  // namespace detail
+
+// for_each_stored_cell (storage.cpp:455-534): every stored (row, col, value), ELL padding
+// (a repeat of the previous column inside a row) skipped.
+template <class F>
+void for_each_stored_cell(const TensorStorage& s, F&& fn) {
+  switch (s.kind) {
+    case FormatKind::Csr: {
+      const IntArray& ip = detail::need_suffix(s, "J_indptr");
+      const IntArray& ix = detail::need_suffix(s, "J_indices");
+      for (int64_t i = 0; i < s.rows; ++i)
+        for (int32_t p = ip[i]; p < ip[i + 1]; ++p) fn(i, int64_t{ix[p]}, double{s.values[p]});
+      break;
+    }
+    case FormatKind::Bsr: {
+      const int64_t b = s.block;
+      const IntArray& ip = detail::need_suffix(s, "JO_indptr");
+      const IntArray& ix = detail::need_suffix(s, "JO_indices");
+      for (int64_t br = 0; br < s.rows / b; ++br)
+        for (int32_t p = ip[br]; p < ip[br + 1]; ++p)
+          for (int64_t ii = 0; ii < b; ++ii)
+            for (int64_t ji = 0; ji < b; ++ji)
+              fn(br * b + ii, ix[p] * b + ji, double{s.values[(p * b + ii) * b + ji]});
+      break;
+    }
+    case FormatKind::Ell:
+    case FormatKind::EllBucket: {
+      const IntArray& jx = detail::need_suffix(s, "J_indices");
+      const IntArray* rmap = s.kind == FormatKind::EllBucket ? &detail::need_suffix(s, "I_indices") : nullptr;
+      const int64_t w = s.width;
+      const int64_t nrows = rmap ? static_cast<int64_t>(rmap->size()) : s.rows;
+      for (int64_t r = 0; r < nrows; ++r)
+        for (int64_t k = 0; k < w; ++k) {
+          if (k > 0 && jx[r * w + k] == jx[r * w + k - 1]) continue;  // padding
+          fn(rmap ? int64_t{(*rmap)[r]} : r, int64_t{jx[r * w + k]}, double{s.values[r * w + k]});
+        }
+      break;
+    }
+  }
+}
+
+// reconstruct_dense (storage.cpp:536-550): O(rows * cols) — toy sizes only, as in the reference.
+inline DenseMatrix reconstruct_dense(const TensorStorage& s) {
+  DenseMatrix d(s.rows, s.cols);
+  for_each_stored_cell(s, [&](int64_t i, int64_t j, double v) { d.at(i, j) += v; });
+  return d;
+}
+inline DenseMatrix reconstruct_dense(const HybDecomposition& h) {
+  DenseMatrix d(h.rows, h.cols);
+  for (const auto& part : h.parts)
+    for_each_stored_cell(part.ell, [&](int64_t i, int64_t j, double v) { d.at(i, j) += v; });
+  return d;
+}
+
+// validate_storage (storage.cpp:567-630): the index invariants of the stored format, as a list
+// of messages (empty = valid).  Per compressed axis: indptr starts at 0, is non-decreasing and
+// ends at the entry count; indices are in range and sorted inside a segment, and a repeated
+// index may only start the trailing padding run of an ELL segment.
+inline std::vector<std::string> validate_storage(const TensorStorage& s) {
+  std::vector<std::string> out;
+  auto check_indptr = [&](const std::string& axis, const IntArray& p, int64_t count) {
+    if (p.empty() || p.front() != 0) out.push_back(axis + ": indptr must start at 0");
+    for (size_t i = 1; i < p.size(); ++i)
+      if (p[i] < p[i - 1]) {
+        out.push_back(axis + ": indptr not non-decreasing");
+        break;
+      }
+    if (!p.empty() && count >= 0 && p.back() != count) out.push_back(axis + ": indptr tail != nnz");
+  };
+  auto check_segments = [&](const std::string& axis, const IntArray& ix, int64_t length,
+                            const std::vector<std::pair<int64_t, int64_t>>& segs, bool pad_ok) {
+    for (auto [lo, hi] : segs) {
+      bool in_pad_run = false;
+      for (int64_t i = lo; i < hi; ++i) {
+        if (ix[i] < 0 || ix[i] >= length) {
+          out.push_back(axis + ": index out of range");
+          break;
+        }
+        if (i == lo) continue;
+        if (ix[i] < ix[i - 1]) {
+          out.push_back(axis + ": indices not sorted within segment");
+          break;
+        }
+        if (ix[i] == ix[i - 1]) {
+          if (pad_ok) in_pad_run = true; else { out.push_back(axis + ": duplicate index inside segment"); break; }
+        } else if (in_pad_run) {
+          out.push_back(axis + ": duplicate index inside segment");
+          break;
+        }
+      }
+    }
+  };
+  std::vector<std::pair<int64_t, int64_t>> segs;
+  switch (s.kind) {
+    case FormatKind::Csr: {
+      const IntArray& ip = detail::need_suffix(s, "J_indptr");
+      const IntArray& ix = detail::need_suffix(s, "J_indices");
+      check_indptr("J", ip, static_cast<int64_t>(ix.size()));
+      if (static_cast<int64_t>(ip.size()) != s.rows + 1) out.push_back("J: indptr length != rows + 1");
+      for (size_t i = 0; i + 1 < ip.size(); ++i) segs.emplace_back(ip[i], std::min<int64_t>(ip[i + 1], ix.size()));
+      check_segments("J", ix, s.cols, segs, false);
+      break;
+    }
+    case FormatKind::Bsr: {
+      const IntArray& ip = detail::need_suffix(s, "JO_indptr");
+      const IntArray& ix = detail::need_suffix(s, "JO_indices");
+      check_indptr("JO", ip, static_cast<int64_t>(ix.size()));
+      for (size_t i = 0; i + 1 < ip.size(); ++i) segs.emplace_back(ip[i], std::min<int64_t>(ip[i + 1], ix.size()));
+      check_segments("JO", ix, s.block > 0 ? s.cols / s.block : 0, segs, false);
+      if (static_cast<int64_t>(s.values.size()) != static_cast<int64_t>(ix.size()) * s.block * s.block)
+        out.push_back("JO: values size != blocks * b * b");
+      break;
+    }
+    case FormatKind::Ell:
+    case FormatKind::EllBucket: {
+      const IntArray& jx = detail::need_suffix(s, "J_indices");
+      int64_t nrows = s.rows;
+      if (s.kind == FormatKind::EllBucket) {
+        const IntArray& rmap = detail::need_suffix(s, "I_indices");
+        if (const IntArray* ip = detail::find_suffix(s, "I_indptr"))
+          check_indptr("I", *ip, static_cast<int64_t>(rmap.size()));
+        nrows = static_cast<int64_t>(rmap.size());
+        for (int64_t r = 0; r < nrows; ++r)
+          if (rmap[r] < 0 || rmap[r] >= s.rows) {
+            out.push_back("I: index out of range");
+            break;
+          }
+      }
+      if (static_cast<int64_t>(jx.size()) != nrows * s.width) out.push_back("J: indices size != rows * width");
+      for (int64_t r = 0; r < nrows && (r + 1) * s.width <= static_cast<int64_t>(jx.size()); ++r)
+        segs.emplace_back(r * s.width, (r + 1) * s.width);
+      check_segments("J", jx, s.cols, segs, true);
+      break;
+    }
+  }
+  return out;
+}
+
 // Device-resident BSR (tensor-core SpMM input).
 class DeviceBsr {
  public:

@@ -107,6 +107,16 @@ __device__ __forceinline__ void fma_part(Frag<VEC, kScalar>& part, float a,
 }
 
 template <int VEC, bool kScalar>
+__device__ __forceinline__ void add_part(Frag<VEC, kScalar>& part, const Frag<VEC, kScalar>& p1) {
+  if constexpr (kScalar) {
+    part.v[0].x += p1.v[0].x;
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) part.v[i] = add4(part.v[i], p1.v[i]);
+  }
+}
+
+template <int VEC, bool kScalar>
 __device__ __forceinline__ void absorb(Acc<VEC, kScalar>& acc, Frag<VEC, kScalar>& part) {
   if constexpr (kScalar) {
     acc.v[0] += static_cast<double>(part.v[0].x);
@@ -334,6 +344,31 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
       unsigned starts = 0;  // row-start flags; the columns die once the gathers are issued
 #pragma unroll
       for (int u = 0; u < kT; ++u) starts |= (col[u] < 0 ? 1u : 0u) << u;
+#ifndef STRATA_SPMM_FAST32  // A/B knob: fast path for the d = 128 (L = 32) variant too
+#define STRATA_SPMM_FAST32 0
+#endif
+      // (the L = 32 variant is register-budgeted at 80 for 3 CTAs/SM and DRAM-bound at C5: the
+      // fast path's second chain spills there and costs 26 %, so it is L < 32 only)
+      if ((L < 32 || STRATA_SPMM_FAST32) && n == kT && starts == 0) {
+        // Full batch inside one output row (most batches once rows are longer than a batch):
+        // no per-slot predication or row-start branches; two independent FMA chains (even /
+        // odd slots) halve the dependent-FMA latency.  part is zero here (absorbed after
+        // every batch), and the batch sum (even + odd) is folded into f64 as before.
+        Frag<VEC, kScalar> p1;
+        p1.zero();
+#pragma unroll
+        for (int ub = 0; ub < kT; ub += UG) {
+          Frag<VEC, kScalar> xv[UG];
+#pragma unroll
+          for (int u = 0; u < UG; ++u)
+            gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0);
+#pragma unroll
+          for (int u = 0; u < UG; ++u) fma_part((ub + u) & 1 ? p1 : part, sV[e0 + ub + u], xv[u]);
+        }
+        add_part(part, p1);
+        absorb(acc, part);
+        continue;
+      }
 #pragma unroll
       for (int ub = 0; ub < kT; ub += UG) {
         Frag<VEC, kScalar> xv[UG];

@@ -93,24 +93,8 @@ DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
   return y;
 }
 
-// reconstruct_dense of a hyb decomposition (storage.cpp:536-550), padding skipped by the
-// repeated-column rule (storage.cpp:520-531).
-DenseMatrix reconstruct(const HybDecomposition& h) {
-  DenseMatrix d(h.rows, h.cols);
-  for (const auto& p : h.parts) {
-    const std::string pre =
-        "hyb_p" + std::to_string(p.partition) + "_b" + std::to_string(p.bucket) + "_";
-    const IntArray& rmap = p.ell.arr(pre + "I_indices");
-    const IntArray& jx = p.ell.arr(pre + "J_indices");
-    const int64_t w = p.width;
-    for (size_t r = 0; r < rmap.size(); ++r)
-      for (int64_t k = 0; k < w; ++k) {
-        if (k > 0 && jx[r * w + k] == jx[r * w + k - 1]) continue;
-        d.at(rmap[r], jx[r * w + k]) += p.ell.values[r * w + k];
-      }
-  }
-  return d;
-}
+// reconstruct_dense of a hyb decomposition (storage.cpp:536-550), via the façade.
+DenseMatrix reconstruct(const HybDecomposition& h) { return reconstruct_dense(h); }
 
 DenseMatrix run_spmm(const CooMatrix& m, const DenseMatrix& x, const std::string& fmt) {
   Pipeline pl = build_matrix_pipeline(KernelOp::SpMM, m, x.cols, FormatRequest::parse(fmt));
@@ -223,6 +207,26 @@ TEST_CASE("round trip: hyb and bsr reconstruct random matrices exactly") {  // :
         ok &= got.at(i, j) == ((i < rows && j < cols) ? want.at(i, j) : 0.0);
     CHECK(ok);
   }
+}
+
+TEST_CASE("indptr arrays are monotone and indices sorted per segment") {  // :319-331
+  std::mt19937 rng(3);
+  for (int trial = 0; trial < 10; ++trial) {
+    CooMatrix m = random_coo(rng, 20, 20, 0.3);
+    TensorStorage csr = build_csr(m);
+    CHECK(validate_storage(csr).empty());
+    CHECK(validate_storage(csr_to_bsr(csr, 2)).empty());
+    for (const auto& p : decompose_hyb(csr, 2, 2).parts) CHECK(validate_storage(p.ell).empty());
+    CHECK(reconstruct_dense(csr).v == dense_from_coo(m).v);
+  }
+  // corrupted storages are reported, not thrown
+  TensorStorage bad = build_csr(example_m());
+  bad.aux["J_indices"][1] = 0;  // row 0 holds columns {0, 2} -> {0, 0}
+  auto msgs = validate_storage(bad);
+  CHECK(!msgs.empty() && msgs[0] == "J: duplicate index inside segment");
+  TensorStorage bad2 = build_csr(example_m());
+  bad2.aux["J_indptr"][0] = 1;
+  CHECK(!validate_storage(bad2).empty() && validate_storage(bad2)[0] == "J: indptr must start at 0");
 }
 
 TEST_CASE("hyb bucket uniformity and entry accounting") {  // :248-263
