@@ -8,9 +8,11 @@
 //    per call into a row-major Yt[n][d] workspace (d*n*8 bytes of traffic, tiny next to the
 //    nnz*d gathers) so every gather is one coalesced 128-bit access per lane;
 //  * work is split by non-zeros, not rows (power-law rows range over 4+ orders of magnitude):
-//    each virtual warp (L = d/4 lanes) takes a fixed 256-non-zero chunk, finds its first row
-//    with one binary search on indptr (the reference does one per non-zero, lower.cpp:375-402),
-//    and walks rows forward;
+//    each virtual warp (L = d/4 lanes) takes a fixed 256-non-zero chunk, stages its column
+//    indices and A values in shared memory (cp.async; read back as broadcasts, no per-non-zero
+//    shuffles), finds its first row with one binary search on indptr (the reference does one
+//    per non-zero, lower.cpp:375-402) and walks rows forward holding the X row fragment in
+//    registers; groups of L non-zeros without a row boundary skip the per-non-zero row test;
 //  * per group of L non-zeros each lane forms partial dot products over its 4 features, then
 //    a butterfly reduce-scatter (L-1 shuffles for L results, PAPER.md:442's two-stage
 //    reduction) leaves non-zero t's full dot product in lane t, which scales by A and stores
@@ -19,6 +21,7 @@
 
 #include "capi_internal.h"
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace strata_b200 {
 
@@ -72,49 +75,77 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
   const long long e0 = vw * kNnzPerChunk;
   if (e0 >= nnz) return;
-  const long long e1 = min64(e0 + kNnzPerChunk, nnz);
+  const int ne = static_cast<int>(min64(kNnzPerChunk, nnz - e0));
 
-  // Row of e0: last row r with indptr[r] <= e0 (the reference's LocateSegment, once per chunk).
+  // Stage the chunk's column indices and A values in this VW's shared-memory slice (one
+  // memory round trip; read back as broadcasts, no per-non-zero shuffles).
+  extern __shared__ int4 sddmm_smem[];
+  int32_t* sJ = reinterpret_cast<int32_t*>(sddmm_smem) + (threadIdx.x / L) * (2 * kNnzPerChunk);
+  float* sA = reinterpret_cast<float*>(sJ + kNnzPerChunk);
+  if (ne == kNnzPerChunk) {
+    for (int q = lane; q < kNnzPerChunk / 4; q += L) {
+      ::strata_b200::tc::cp_async16(sJ + 4 * q, indices + e0 + 4 * q);
+      ::strata_b200::tc::cp_async16(sA + 4 * q, A + e0 + 4 * q);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  } else {
+    for (int q = lane; q < ne; q += L) {
+      sJ[q] = ld_stream(indices + e0 + q);
+      sA[q] = ld_stream(A + e0 + q);
+    }
+  }
+
+  // Row of e0: last row r with indptr[r] <= e0 (the reference's LocateSegment, once per chunk),
+  // then rows advance with the chunk; the VW keeps the current X row fragment in registers.
   long long lo = 0, hi = rows;
   while (lo < hi) {
     const long long mid = (lo + hi + 1) >> 1;
     if (__ldg(indptr + mid) <= e0) lo = mid; else hi = mid - 1;
   }
-  long long row = lo;  // walks forward with the group
-  long long xrow = -1;
-  float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+  int row = static_cast<int>(lo);
+  long long row_end = __ldg(indptr + row + 1);
+  float4 x = ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncwarp(vmask);
 
-  for (long long g = e0; g < e1; g += L) {
-    const long long e = g + lane;
-    const bool in = e < e1;
-    const int32_t col = in ? ld_stream(indices + e) : 0;
-    const float av = in ? ld_stream(A + e) : 0.f;
-    // Row of each lane's non-zero (skips empty rows).
-    long long my_row = row;
-    if (in) while (__ldg(indptr + my_row + 1) <= e) ++my_row;
+  const float4* Y4 = reinterpret_cast<const float4*>(Yt) + lane;
+  const int d4 = static_cast<int>(d / 4);
+  for (int g = 0; g < ne; g += L) {
+    const int n = min(L, ne - g);
+    const bool one_row = e0 + g + n <= row_end;  // VW-uniform: no row boundary in this group
     float part[L];
 #pragma unroll
     for (int u0 = 0; u0 < L; u0 += U) {
       float4 yv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int32_t cu = __shfl_sync(vmask, col, u0 + u, L);
-        yv[u] = (g + u0 + u < e1) ? ld_gather4(reinterpret_cast<const float4*>(Yt + static_cast<long long>(cu) * d) + lane)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      for (int u = 0; u < U; u += 4) {
+        const int4 c = *reinterpret_cast<const int4*>(sJ + g + u0 + u);  // broadcast LDS.128
+        const int cc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long ru = __shfl_sync(vmask, my_row, u0 + u, L);
-        if (g + u0 + u < e1 && ru != xrow) {
-          x = ld_gather4(reinterpret_cast<const float4*>(X + ru * d) + lane);
-          xrow = ru;
+        for (int v = 0; v < 4; ++v)
+          yv[u + v] = (u0 + u + v < n) ? ld_gather4(Y4 + static_cast<long long>(cc[v]) * d4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (one_row) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          part[u0 + u] = x.x * yv[u].x + x.y * yv[u].y + x.z * yv[u].z + x.w * yv[u].w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u0 + u < n) {
+            const long long e = e0 + g + u0 + u;
+            if (e >= row_end) {  // next non-empty row containing e
+              do { ++row; row_end = __ldg(indptr + row + 1); } while (e >= row_end);
+              x = ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane);
+            }
+          }
+          part[u0 + u] = x.x * yv[u].x + x.y * yv[u].y + x.z * yv[u].z + x.w * yv[u].w;
         }
-        part[u0 + u] = x.x * yv[u].x + x.y * yv[u].y + x.z * yv[u].z + x.w * yv[u].w;
       }
     }
-    row = __shfl_sync(vmask, my_row, L - 1, L);
     const float dot = reduce_scatter<L>(part, lane, vmask);
-    if (in) st_stream(B + e, av * dot);
+    if (lane < n) st_stream(B + e0 + g + lane, sA[g + lane] * dot);
   }
 }
 
@@ -209,12 +240,21 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
   auto blocks_for = [&](int L) {
     return static_cast<unsigned>((chunks * L + kBlock - 1) / kBlock);
   };
-  if (aligned && d == 32)
-    sddmm_kernel<8><<<blocks_for(8), kBlock, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
-  else if (aligned && d == 64)
-    sddmm_kernel<16><<<blocks_for(16), kBlock, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
-  else if (aligned && d == 128)
-    sddmm_kernel<32><<<blocks_for(32), kBlock, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  // per virtual warp: column indices + A values of one chunk (2 KB)
+  auto smem_for = [&](int L) { return (kBlock / L) * 2 * kNnzPerChunk * 4; };
+  const bool staged = aligned && reinterpret_cast<uintptr_t>(indices) % 16 == 0 &&
+                      reinterpret_cast<uintptr_t>(A) % 16 == 0;
+  static bool configured = false;
+  if (!configured) {  // d = 32: 64 KB per block
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8)));
+    configured = true;
+  }
+  if (staged && d == 32)
+    sddmm_kernel<8><<<blocks_for(8), kBlock, smem_for(8), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  else if (staged && d == 64)
+    sddmm_kernel<16><<<blocks_for(16), kBlock, smem_for(16), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  else if (staged && d == 128)
+    sddmm_kernel<32><<<blocks_for(32), kBlock, smem_for(32), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   else {
     const unsigned blocks = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, 148 * 32));
     sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
