@@ -2,15 +2,18 @@
 # ncu captures (one kernel each) for the workloads in tools/prof_workloads.py.
 # usage: WORKLOADS="reddit_spmm bsr" bash tools/gpu_prof.sh
 mkdir -p gpurun_out
-for w in ${WORKLOADS:-products reddit_spmm reddit_sddmm bsr rgcn}; do
+for w in ${WORKLOADS:-products reddit_spmm reddit_sddmm bsr bsr12 rgcn rgcn_sum}; do
+  run=$w
   case $w in
     products|reddit_spmm) k=spmm_hyb_kernel ;;
     reddit_sddmm) k=sddmm_kernel ;;
-    bsr) k=bsr_spmm_tc_kernel ;;
+    bsr|bsr12) k=bsr_spmm_tc_kernel ;;
     rgcn) k=rgms_edge_gemm_kernel ;;
-    rgcn_sum) k=rgms_row_sum_kernel; w=rgcn ;;
+    rgcn_sum) k=rgms_row_sum_kernel; run=rgcn ;;
   esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
-    -o gpurun_out/prof_$w -f python tools/prof_workloads.py $w 4 > gpurun_out/ncu_$w.log 2>&1
+    -o gpurun_out/prof_$w -f python tools/prof_workloads.py $run 4 > gpurun_out/ncu_$w.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_$w.csv python tools/prof_workloads.py $run 3 > /dev/null 2>&1
 done
 ls -la gpurun_out

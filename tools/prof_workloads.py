@@ -1,5 +1,5 @@
 """Run one BASELINE workload a few times (for ncu captures): python tools/prof_workloads.py
-{products|reddit_spmm|reddit_sddmm|bsr|rgcn} [reps]"""
+{products|reddit_spmm|reddit_sddmm|bsr|bsr12|rgcn} [reps]"""
 import os
 import sys
 
@@ -34,6 +34,12 @@ def main():
         bs = S.csr_to_bsr(m.to_device(dev), 32)
         X = torch.randint(-3, 4, (4096, 64), device=dev).to(torch.bfloat16)
         fn = lambda: S.bsr_spmm(bs, X)
+    elif which == "bsr12":  # 12-head batched variant
+        m = S.generate_matrix("blocksparse", 4096, 4096, 0.1, 0, 32, 0, 1)
+        bs = S.csr_to_bsr(m.to_device(dev), 32)
+        V = torch.randint(1, 10, (12, bs.nblocks, 32, 32), device=dev).to(torch.bfloat16)
+        X = torch.randint(-3, 4, (12, 4096, 64), device=dev).to(torch.bfloat16)
+        fn = lambda: S.bsr_spmm_batched(bs, V, X)
     elif which == "rgcn":
         m = S.generate_matrix("powerlaw", 1885136, 1885136, 0, 0, 0, 3.0051, 1)
         plan = S.RgmsPlan(S.split_relations(m, 133, 1).to_device(dev))
