@@ -255,36 +255,6 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
   if (warp == 0) tc::tmem_dealloc<kCols>(tmem);
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    STRATA_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess)
-      throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  return encode;
-}
-
-// 2D bf16 tensor map over a row-major [rows][cols] array with a {box_cols, 32} box.
-CUtensorMap make_map_2d(const __nv_bfloat16* base, long long rows, int cols, int box_cols,
-                        CUtensorMapSwizzle swz) {
-  CUtensorMap map;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(cols) * 2};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), kB};
-  const cuuint32_t estride[2] = {1, 1};
-  const CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                          const_cast<__nv_bfloat16*>(base), gdim, gstride, box,
-                                          estride, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  return map;
-}
-
 // X viewed as [heads * x_rows][D] bf16, box {64 features, 32 rows}, 128-byte swizzle: one box
 // = one 4 KB column of MN-major SW128 atoms of the A operand.  Block values viewed as
 // [heads * nblocks * 32][32] bf16 (row-major blocks), box {32, 32}, 64-byte swizzle: one box =
@@ -300,9 +270,9 @@ void launch_bsr(const strata_bsr& h, const __nv_bfloat16* vals, long long heads,
     configured = true;
   }
   const long long x_rows = h.nb * kB, y_rows = h.mb * kB;
-  const CUtensorMap xmap = make_map_2d(X, heads * x_rows, D, 64, CU_TENSOR_MAP_SWIZZLE_128B);
-  const CUtensorMap amap =
-      make_map_2d(vals, heads * std::max<long long>(h.nblocks, 1) * kB, kB, kB, CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap xmap = make_tensor_map_bf16_2d(X, heads * x_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap amap = make_tensor_map_bf16_2d(vals, heads * std::max<long long>(h.nblocks, 1) * kB,
+                                                   kB, kB, kB, CU_TENSOR_MAP_SWIZZLE_64B);
   const dim3 grid(static_cast<unsigned>(h.mb), static_cast<unsigned>(heads));
   bsr_spmm_tc_kernel<D><<<grid, kThreads, smem, s>>>(amap, xmap, h.indptr.p, h.indices.p,
                                                      h.nblocks, x_rows, y_rows, Y);

@@ -8,6 +8,8 @@
 #include <exception>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "capi_internal.h"
 
 using namespace strata_b200;
@@ -62,6 +64,29 @@ const strata_hyb_impl& hyb_of(const strata_hyb* h) {
 
 namespace strata_b200 {
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+CUtensorMap make_tensor_map_bf16_2d(const void* base, long long rows, long long cols,
+                                    int box_cols, int box_rows, CUtensorMapSwizzle swizzle) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    STRATA_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(cols) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estride[2] = {1, 1};
+  const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim,
+                            gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ApiError(STRATA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return map;
+}
 
 // Stream-ordered workspaces (cudaMallocAsync) come from the device's default pool; keep freed
 // blocks cached there instead of returning them to the driver at every synchronisation, so

@@ -1,6 +1,7 @@
 // capi_internal.h — host-side internals shared by the C-ABI translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -144,6 +145,10 @@ void ell_from_csr_launch(const int32_t* indptr, const int32_t* indices, const fl
                          cudaStream_t s);
 
 int num_sms();
+// 2D bf16 TMA descriptor over a row-major [rows][cols] array with a {box_cols, box_rows} box
+// (cuTensorMapEncodeTiled through the runtime's driver entry point).
+CUtensorMap make_tensor_map_bf16_2d(const void* base, long long rows, long long cols,
+                                    int box_cols, int box_rows, CUtensorMapSwizzle swizzle);
 // Stream-ordered scratch from the device pool (kept cached across calls); free with cudaFreeAsync.
 void* workspace_alloc(size_t bytes, cudaStream_t s);
 // Thread-local message returned by strata_last_error() (shared by every translation unit).

@@ -6,22 +6,23 @@
 // relation.  Flattened here to rel_ptr[R+1] / dst / src / A.
 //
 // Two passes, no atomics, deterministic:
-//   plan   (once, like build_rgms_pipeline's decomposition): per-relation 128-edge tiles, and
-//          for every edge its position in the destination-sorted edge order (a stable radix
-//          sort on dst, so a row's edges stay in relation order) plus the row pointer dptr.
-//   pass 1 rgms_edge_gemm_kernel — per tile of 128 edges of one relation r:
-//            gather X[src e] (d_in bf16, K-major A operand) and W_r (MN-major B) via cp.async,
-//            tcgen05.mma M = 128 edges, N = d_out, K = d_in into TMEM (f32),
-//            epilogue: tcgen05.ld, scale by A[e], transpose through a per-warp smem tile and
-//            write the message row T[pos e] with coalesced 128-byte row stores.
+//   plan   (once, like build_rgms_pipeline's decomposition): per-relation 128-edge tiles;
+//          message *runs* (consecutive edges of one relation with one destination inside a
+//          32-edge warp group) get rows of T in destination order (stable radix sort, so a row's
+//          runs stay in relation order) and the row pointer dptr.
+//   pass 1 rgms_edge_gemm_kernel — warp-specialised, mbarrier-pipelined: producers gather the
+//          tile's 128 X rows (cp.async into the swizzled K-major A operand) and TMA-load W_r and
+//          the index block; one thread issues tcgen05.mma M = 128 edges, N = d_out, K = d_in
+//          into a double-buffered TMEM accumulator; four epilogue warps scale by A, sum runs and
+//          write one message row per run.
 //   pass 2 rgms_row_sum_kernel — Y[i] = sum_{q in [dptr i, dptr i+1)} T[q] (contiguous rows,
 //          streamed once; empty rows write 0 as the reference's zero-initialised Y); rows with
-//          more than kLong edges go through fixed-shape chunk partials (long_chunk / finish).
+//          more than kLong runs go through fixed-shape chunk partials (long_chunk / finish).
 // Why not scatter with atomics: the 5.7M x d_out red.global.add into a Y larger than L2 was
-// the bottleneck of the first version (3.7 ms at C4); T costs 2 * nnz * d_out * 4 bytes of
+// the bottleneck of the first version (3.7 ms at C4); T costs 2 * runs * d_out * 4 bytes of
 // streaming traffic instead.
 // Numerics: f32 products / tensor-core f32 accumulation over k, one f32 multiply by A, f32
-// row sums in relation order — exact on the reference's integer operands.
+// run and row sums in relation order — exact on the reference's integer operands.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -51,7 +52,6 @@ struct strata_rgms {
 namespace {
 
 constexpr int kEdges = 128;  // UMMA M
-constexpr int kThreads = 128;
 
 __global__ void rel_tiles_kernel(const int32_t* __restrict__ rel_ptr, long long R,
                                  long long* __restrict__ ntiles) {
@@ -154,67 +154,98 @@ __global__ void tile_edges_kernel(const int32_t* __restrict__ rel_ptr, long long
   }
 }
 
-#ifndef STRATA_RGMS_STAGES
-#define STRATA_RGMS_STAGES 3
+// ---- pass 1: warp-specialised, mbarrier-pipelined tcgen05 tiles --------------------------
+// Roles (224 threads):
+//   warps 0-1 producers: index blocks kIdxAhead tiles ahead (1-D TMA bulk copies); per tile,
+//           once its stage is free, W_r by d_out/8 TMA boxes {8 columns x d_in} into the
+//           MN-major (SWIZZLE_NONE) B operand, and the 128 X rows by 16-byte cp.async chunks
+//           written to their swizzled positions of the K-major A operand, completing on the
+//           stage's mbarrier (cp.async.mbarrier.arrive.noinc).  (TMA tile::gather4 of the rows
+//           works too — 4 rows per op — but measured 8 % slower at C4: 288 vs 266 us.)
+//   warp 2  MMA issuer (lane 0): tcgen05.mma M = 128 edges, N = d_out, K = d_in into one of two
+//           TMEM accumulators; tcgen05.commit frees the stage and publishes the accumulator;
+//   warps 3-6 epilogue: tcgen05.ld of their 32 TMEM lanes, scale by A, per-warp swizzled
+//           transpose through shared memory, one message row per run (st.global.cs), then
+//           release the accumulator and the index block.
+// Every hand-off is an mbarrier (TMA byte counts, tcgen05.commit or epilogue-warp arrivals), so
+// the producer runs up to kStages tiles ahead of the MMA and the epilogue of tile j overlaps
+// the MMA of tile j+1 — no CTA-wide barrier in the loop.
+#ifndef STRATA_RGMS_PROD_WARPS  // A/B knob
+#define STRATA_RGMS_PROD_WARPS 2
 #endif
-#ifndef STRATA_RGMS_IDXAHEAD
-#define STRATA_RGMS_IDXAHEAD 6
+constexpr int kProdWarps = STRATA_RGMS_PROD_WARPS;  // warps 0 .. kProdWarps-1: producers
+constexpr int kMmaWarp = kProdWarps;                // then the MMA issuer warp
+constexpr int kWsThreads = (kProdWarps + 1 + 4) * 32;  // then 4 epilogue warps
+#ifndef STRATA_RGMS_WS_STAGES
+#define STRATA_RGMS_WS_STAGES 4
 #endif
+constexpr int kStagesWs = STRATA_RGMS_WS_STAGES;
+constexpr int kIdxAheadWs = 3;
+constexpr int kIdxSlotsWs = kIdxAheadWs + kStagesWs + 2;
 
 template <int DIN, int DOUT>
-struct RgmsSmem {
-  // X / W ring: tile j computes while tiles j+1 .. j+kStages-1 land.
-  static constexpr int kStages = STRATA_RGMS_STAGES;
-  // Index blocks run kIdxAhead tiles ahead (>= 2 * kStages - 2, so the block a gather needs
-  // is always older than the oldest gather group still allowed in flight).
-  static constexpr int kIdxAhead = STRATA_RGMS_IDXAHEAD;
-  static constexpr int kIdxSlots = kIdxAhead + 1;  // j (epilogue) .. j + kIdxAhead (landing)
-  static_assert(kStages >= 2 && kIdxAhead >= 2 * kStages - 2, "pipeline depths");
-  static constexpr int kABytes = kEdges * DIN * 2;
+struct RgmsWsSmem {
+  static constexpr int kRowB = DIN * 2;              // A row bytes = swizzle width
+  static constexpr int kABytes = kEdges * kRowB;
   static constexpr int kWBytes = DIN * DOUT * 2;
-  static constexpr int kStage = kABytes + kWBytes;
-  static constexpr int kIdxBytes = kTileWords * 4;
-  // Epilogue column chunk: the per-warp transpose tiles (4 warps x 32 rows x kNC f32) live in
-  // the A region of the tile being finished (its MMA has completed), so kNC <= kABytes / 512.
-  static constexpr int kNCcap = kABytes / 512;
-  static constexpr int kNC = (DOUT < 32 ? DOUT : 32) < kNCcap ? (DOUT < 32 ? DOUT : 32) : kNCcap;
-  static constexpr int kIdxOff = kStages * kStage;
-  static constexpr int kBytes = kIdxOff + kIdxSlots * kIdxBytes;
-  static_assert(kNC >= 8 && DOUT % kNC == 0, "epilogue chunk");
+  static constexpr int kStage = kABytes + kWBytes;   // keeps every A region swizzle-atom aligned
+  static constexpr int kIdxBytes = kTileWords * 4;   // 1552
+  static constexpr int kNC = DOUT < 16 ? DOUT : 16;  // epilogue column chunk
+  static constexpr int kEpiBytes = 4 * 32 * kNC * 4;
+  static constexpr int kIdxOff = kStagesWs * kStage;
+  static constexpr int kEpiOff = kIdxOff + kIdxSlotsWs * kIdxBytes;
+  static constexpr int kBytes = kEpiOff + kEpiBytes + 1024;  // + alignment slack
+  static constexpr int kAccCols = DOUT < 32 ? 32 : DOUT;
+  static constexpr int kTmemCols = 2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
 };
 
-// Pass 1.  CTA b processes tiles b, b + G, b + 2G, ... (G = gridDim.x).  cp.async groups are
-// committed in the order I0 I1 I2 X0 X1 | I3 X2 | I4 X3 | ...: before tile j, "all but the
-// newest group" guarantees X(j) and I(j+2) have landed, so the index block of tile j+3 and the
-// row gathers of tile j+2 are issued before tile j's MMA — two tiles of gathers in flight, no
-// dependent global load on the issue path.
+template <int DIN>
+__device__ __forceinline__ uint64_t a_desc_kmajor(uint32_t saddr) {
+  // K-major, swizzle width = one row (DIN * 2 bytes): 8-row atoms, SBO = 8 rows.
+  if constexpr (DIN == 16) return tc::make_desc_sw32(saddr, 0, 8 * 32);
+  else if constexpr (DIN == 32) return tc::make_desc_sw64(saddr, 0, 8 * 64);
+  else return tc::make_desc_sw128(saddr, 0, 8 * 128);
+}
+
 template <int DIN, int DOUT>
-__global__ void __launch_bounds__(kThreads, 6)
-rgms_edge_gemm_kernel(const int32_t* __restrict__ ed, long long ntiles,
-                      const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ W,
-                      float* __restrict__ T) {
-  using SM = RgmsSmem<DIN, DOUT>;
-  constexpr int kCols = DOUT <= 32 ? 32 : (DOUT <= 64 ? 64 : (DOUT <= 128 ? 128 : 256));
-  constexpr int kSboA = (DIN / 8) * 128;  // K-major A: 8-edge group stride
-  constexpr int kSboW = (DIN / 8) * 128;  // MN-major B: 8-column group stride
+__global__ void __launch_bounds__(kWsThreads, 1)
+rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloat16* __restrict__ X,
+                      const int32_t* __restrict__ ed, long long ntiles, float* __restrict__ T) {
+  using SM = RgmsWsSmem<DIN, DOUT>;
+  constexpr int kSboW = (DIN / 8) * 128;  // MN-major B (SWIZZLE_NONE): 8-column group stride
   constexpr uint32_t kIdesc = tc::make_idesc_bf16(kEdges, DOUT, /*A K-major*/ false, /*B MN-major*/ true);
   constexpr int kNC = SM::kNC;
-  constexpr int kSPR = kNC / 4;       // float4 slots per row of a chunk
-  constexpr int kRPI = 32 / kSPR;     // rows per warp store instruction
-  static_assert(DIN % 16 == 0 && DIN <= 64 && DOUT % 16 == 0 && DOUT <= 256, "unsupported dims");
+  constexpr int kSPR = kNC / 4;    // float4 slots per row of a chunk
+  constexpr int kRPI = 32 / kSPR;  // lane groups per warp
+  static_assert(DIN == 16 || DIN == 32 || DIN == 64, "d_in");
+  static_assert(DOUT % 16 == 0 && DOUT <= 128, "d_out");
 
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t mbar;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  __shared__ uint64_t full[kStagesWs], empty[kStagesWs];
+  __shared__ uint64_t idx_full[kIdxSlotsWs], idx_free[kIdxSlotsWs];
+  __shared__ uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_slot;
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long G = gridDim.x;
   if (static_cast<long long>(blockIdx.x) >= ntiles) return;
-  const long long nt = (ntiles - blockIdx.x + G - 1) / G;  // tiles of this CTA
+  const long long nt = (ntiles - blockIdx.x + G - 1) / G;  // tiles of this CTA: b, b+G, ...
 
-  if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
-  if (tid == 0) {
-    tc::mbar_init(&mbar, 1);
+  if (warp == 0) tc::tmem_alloc<SM::kTmemCols>(&tmem_slot);
+  if (threadIdx.x == 32 * kMmaWarp) {
+    for (int i = 0; i < kStagesWs; ++i) {
+      tc::mbar_init(&full[i], 32 * kProdWarps + 1);  // producer cp.async arrivals + W expect_tx
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < kIdxSlotsWs; ++i) {
+      tc::mbar_init(&idx_full[i], 1);
+      tc::mbar_init(&idx_free[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&acc_full[i], 1);
+      tc::mbar_init(&acc_empty[i], 4);
+    }
     tc::mbar_fence_init();
   }
   tc::fence_before_sync();
@@ -222,113 +253,129 @@ rgms_edge_gemm_kernel(const int32_t* __restrict__ ed, long long ntiles,
   tc::fence_after_sync();
   const uint32_t tmem = tmem_slot;
   auto idx_slot = [&](long long j) {
-    return reinterpret_cast<int32_t*>(smem + SM::kIdxOff + (j % SM::kIdxSlots) * SM::kIdxBytes);
+    return reinterpret_cast<int32_t*>(smem + SM::kIdxOff + (j % kIdxSlotsWs) * SM::kIdxBytes);
   };
 
-  auto issue_idx = [&](long long j) {
-    if (j < nt && tid < kTileChunks)
-      tc::cp_async16(reinterpret_cast<uint8_t*>(idx_slot(j)) + tid * 16,
-                     ed + (blockIdx.x + j * G) * kTileWords + tid * 4);
-  };
-  auto issue_x = [&](long long j) {
-    if (j >= nt) return;
-    const int32_t* si = idx_slot(j);
-    uint8_t* sA = smem + (j % SM::kStages) * SM::kStage;
-    uint8_t* sW = sA + SM::kABytes;
-    constexpr int kPer = kEdges * (DIN / 8) / kThreads;  // 16-byte chunks of the A tile per thread
+  if (warp < kProdWarps) {
+    // ---------------- producers ----------------
+    const int pt = threadIdx.x;  // 0 .. 32 * kProdWarps - 1
+    if (pt == 0) tc::prefetch_tensormap(&wmap);
+    auto issue_idx = [&](long long j) {  // thread 0
+      const int k = static_cast<int>(j % kIdxSlotsWs);
+      if (j >= kIdxSlotsWs) tc::mbar_wait(&idx_free[k], static_cast<uint32_t>((j / kIdxSlotsWs - 1) & 1));
+      tc::mbar_arrive_expect_tx(&idx_full[k], SM::kIdxBytes);
+      tc::bulk_copy_g2s(idx_slot(j), ed + (blockIdx.x + j * G) * kTileWords, SM::kIdxBytes, &idx_full[k]);
+    };
+    if (pt == 0)
+      for (long long j = 0; j < kIdxAheadWs && j < nt; ++j) issue_idx(j);
+    constexpr int kCpr = DIN / 8;                        // 16-byte chunks per X row
+    constexpr int kPer = kEdges * kCpr / (32 * kProdWarps);
+    constexpr int kSwzMask = SM::kRowB / 16 - 1;         // address bits [4:6] ^= bits [7:9]
+    for (long long j = 0; j < nt; ++j) {
+      if (pt == 0 && j + kIdxAheadWs < nt) issue_idx(j + kIdxAheadWs);
+      const int s = static_cast<int>(j % kStagesWs);
+      if (j >= kStagesWs) tc::mbar_wait(&empty[s], static_cast<uint32_t>((j / kStagesWs - 1) & 1));
+      tc::mbar_wait(&idx_full[j % kIdxSlotsWs], static_cast<uint32_t>((j / kIdxSlotsWs) & 1));
+      const int32_t* si = idx_slot(j);
+      uint8_t* sA = smem + s * SM::kStage;
+      uint8_t* sW = sA + SM::kABytes;
+      if (pt == 0) {
+        tc::mbar_arrive_expect_tx(&full[s], SM::kWBytes);
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int c = tid + q * kThreads;
-      const int e = c / (DIN / 8), kc = c % (DIN / 8);
-      const long long jj = si[4 + e];
-      tc::cp_async16(sA + (e >> 3) * kSboA + kc * 128 + (e & 7) * 16, X + jj * DIN + kc * 8);
-    }
-    const __nv_bfloat16* Wr = W + static_cast<long long>(si[0]) * DIN * DOUT;
-    for (int c = tid; c < DIN * (DOUT / 8); c += kThreads) {
-      const int k = c / (DOUT / 8), lc = c % (DOUT / 8);
-      tc::cp_async16(sW + lc * kSboW + (k >> 3) * 128 + (k & 7) * 16, Wr + k * DOUT + lc * 8);
-    }
-  };
-
-  // Prologue: index blocks 0 .. kIdxAhead-1 as one group, then gathers 0 .. kStages-2, each
-  // preceded by an empty group so the steady-state pairing [I(j+kIdxAhead), X(j+kStages-1)]
-  // holds from the first iteration: "all but the newest 2(kStages-2) groups" is then exactly
-  // "X(j) has landed" (and every index block older than it, incl. I(j+kStages-1)).
-  constexpr int kS = SM::kStages, kL = SM::kIdxAhead;
-  for (int k = 0; k < kL; ++k) issue_idx(k);
-  tc::cp_async_commit();
-  tc::cp_async_wait<0>();
-  __syncthreads();
-  for (int k = 0; k < kS - 1; ++k) {
-    tc::cp_async_commit();
-    issue_x(k);
-    tc::cp_async_commit();
-  }
-
-  for (long long j = 0; j < nt; ++j) {
-    tc::cp_async_wait<2 * (kS - 2)>();  // X(j) (and I(j + kS - 1)) landed
-    tc::fence_proxy_async();
-    __syncthreads();  // ... for every thread; stage (j-1)%kS and idx slot (j-1)%(kL+1) are free
-    issue_idx(j + kL); tc::cp_async_commit();
-    issue_x(j + kS - 1); tc::cp_async_commit();
-    const int s = static_cast<int>(j % SM::kStages);
-    if (tid == 0) {
-      tc::fence_after_sync();
-      const uint32_t a0 = tc::smem_u32(smem + s * SM::kStage);
-      const uint32_t w0 = a0 + SM::kABytes;
-#pragma unroll
-      for (int kk = 0; kk < DIN / 16; ++kk)
-        tc::mma_bf16(tmem, tc::make_desc(a0 + kk * 256, 128, kSboA),
-                     tc::make_desc(w0 + kk * 256, 128, kSboW), kIdesc, kk > 0);
-      tc::mma_commit(&mbar);
-    }
-    const int32_t* si = idx_slot(j);
-    const float a = __int_as_float(si[4 + 2 * kEdges + warp * 32 + lane]);
-    const int32_t* spos = si + 4 + kEdges + warp * 32;
-    const int myword = spos[lane];
-    const unsigned heads = __ballot_sync(0xffffffffu, myword >= 0);
-    const unsigned pads = __ballot_sync(0xffffffffu, myword == -1);
-    const int first_pad = pads ? __ffs(pads) - 1 : 32;
-    tc::mbar_wait(&mbar, static_cast<uint32_t>(j & 1));
-    tc::fence_after_sync();
-    float4* epi = reinterpret_cast<float4*>(smem + s * SM::kStage) + warp * (32 * kSPR);
-    const int gi = lane / kSPR, sl = lane & (kSPR - 1);
-    unsigned mine = heads;  // runs gi, gi + kRPI, ... belong to lane group gi
-    for (int i = 0; i < gi; ++i) mine &= mine - 1;
-#pragma unroll
-    for (int c0 = 0; c0 < DOUT; c0 += kNC) {
-      uint32_t v[kNC];
-      tc::tmem_ld_32x32b<kNC>(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-      tc::tmem_ld_wait();
-      // row `lane` -> smem, float4 slot q stored at q ^ (lane % kSPR) (conflict-free phases)
-#pragma unroll
-      for (int q = 0; q < kSPR; ++q)
-        epi[lane * kSPR + (q ^ (lane & (kSPR - 1)))] =
-            make_float4(a * __uint_as_float(v[4 * q]), a * __uint_as_float(v[4 * q + 1]),
-                        a * __uint_as_float(v[4 * q + 2]), a * __uint_as_float(v[4 * q + 3]));
-      __syncwarp();
-      // Runs of this warp's 32 rows (heads: pos word >= 0; continuation -2; padding -1): each
-      // lane group (kSPR lanes, one float4 column slot each) sums its runs and writes each as
-      // one T row.
-      unsigned m = mine;
-      while (m) {
-        const int r0 = __ffs(m) - 1;
-        const unsigned later = heads & ~((2u << r0) - 1u);
-        const int r1 = min(later ? __ffs(later) - 1 : 32, first_pad);
-        float4 acc = epi[r0 * kSPR + (sl ^ (r0 & (kSPR - 1)))];
-        for (int row = r0 + 1; row < r1; ++row)
-          acc = add4(acc, epi[row * kSPR + (sl ^ (row & (kSPR - 1)))]);
-        __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(spos[r0]) * DOUT + c0) + sl, acc);
-#pragma unroll
-        for (int i = 0; i < kRPI; ++i) m &= m - 1;
+        for (int g = 0; g < DOUT / 8; ++g)  // W_r: one {8 columns x d_in rows} box per group
+          tc::tma_load_2d(sW + g * kSboW, &wmap, g * 8, si[0] * DIN, &full[s]);
       }
-      __syncwarp();
+      // X rows: 16-byte cp.async chunks written to their swizzled positions of the K-major
+      // A operand; completion arrives on full[s] (cp.async.mbarrier.arrive.noinc).
+      int32_t src[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) src[u] = si[4 + (pt + u * 32 * kProdWarps) / kCpr];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int c = pt + u * 32 * kProdWarps;
+        const int e = c / kCpr, kc = c % kCpr;
+        const uint32_t o = e * SM::kRowB + kc * 16;
+        tc::cp_async16(sA + (o ^ (((o >> 7) & kSwzMask) << 4)),
+                       X + static_cast<long long>(src[u]) * DIN + kc * 8);
+      }
+      tc::cp_async_mbar_arrive_noinc(&full[s]);
     }
-    tc::fence_before_sync();
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      for (long long j = 0; j < nt; ++j) {
+        const int s = static_cast<int>(j % kStagesWs);
+        const int b = static_cast<int>(j & 1);
+        tc::mbar_wait(&full[s], static_cast<uint32_t>((j / kStagesWs) & 1));
+        if (j >= 2) tc::mbar_wait(&acc_empty[b], static_cast<uint32_t>((j / 2 - 1) & 1));
+        tc::fence_proxy_async();  // cp.async (generic-proxy) writes -> tensor-core reads
+        tc::fence_after_sync();
+        const uint32_t a0 = tc::smem_u32(smem + s * SM::kStage);
+        const uint32_t w0 = a0 + SM::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < DIN / 16; ++kk)
+          tc::mma_bf16(tmem + b * SM::kAccCols, a_desc_kmajor<DIN>(a0 + kk * 32),
+                       tc::make_desc(w0 + kk * 256, 128, kSboW), kIdesc, kk > 0);
+        tc::mma_commit(&empty[s]);
+        tc::mma_commit(&acc_full[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (warps 3-6: TMEM lanes 32 * (warp % 4) ..) ----------------
+    const int q = warp & 3;
+    float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + (warp - kMmaWarp - 1) * (32 * kSPR);
+    const int gi = lane / kSPR, sl = lane & (kSPR - 1);
+    for (long long j = 0; j < nt; ++j) {
+      const int b = static_cast<int>(j & 1);
+      // The accumulator being published implies the producer saw this tile's index block land
+      // (idx_full -> gathers -> full -> MMA -> commit), so the block is read only after it.
+      tc::mbar_wait(&acc_full[b], static_cast<uint32_t>((j / 2) & 1));
+      tc::fence_after_sync();
+      const int32_t* si = idx_slot(j);
+      const float a = __int_as_float(si[4 + 2 * kEdges + q * 32 + lane]);
+      const int32_t* spos = si + 4 + kEdges + q * 32;
+      const int myword = spos[lane];
+      const unsigned heads = __ballot_sync(0xffffffffu, myword >= 0);
+      const unsigned pads = __ballot_sync(0xffffffffu, myword == -1);
+      const int first_pad = pads ? __ffs(pads) - 1 : 32;
+      unsigned mine = heads;  // runs gi, gi + kRPI, ... belong to lane group gi
+      for (int i = 0; i < gi; ++i) mine &= mine - 1;
+#pragma unroll
+      for (int c0 = 0; c0 < DOUT; c0 += kNC) {
+        uint32_t v[kNC];
+        tc::tmem_ld_32x32b<kNC>(tmem + b * SM::kAccCols + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < kSPR; ++u)
+          epi[lane * kSPR + (u ^ (lane & (kSPR - 1)))] =
+              make_float4(a * __uint_as_float(v[4 * u]), a * __uint_as_float(v[4 * u + 1]),
+                          a * __uint_as_float(v[4 * u + 2]), a * __uint_as_float(v[4 * u + 3]));
+        __syncwarp();
+        unsigned m = mine;
+        while (m) {
+          const int r0 = __ffs(m) - 1;
+          const unsigned later = heads & ~((2u << r0) - 1u);
+          const int r1 = min(later ? __ffs(later) - 1 : 32, first_pad);
+          float4 acc = epi[r0 * kSPR + (sl ^ (r0 & (kSPR - 1)))];
+          for (int row = r0 + 1; row < r1; ++row)
+            acc = add4(acc, epi[row * kSPR + (sl ^ (row & (kSPR - 1)))]);
+          __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(spos[r0]) * DOUT + c0) + sl, acc);
+#pragma unroll
+          for (int i = 0; i < kRPI; ++i) m &= m - 1;
+        }
+        __syncwarp();
+      }
+      tc::fence_before_sync();
+      if (lane == 0) {
+        tc::mbar_arrive(&acc_empty[b]);
+        tc::mbar_arrive(&idx_free[j % kIdxSlotsWs]);
+      }
+    }
   }
-  tc::cp_async_wait<0>();
+  tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<kCols>(tmem);
+  if (warp == 0) tc::tmem_dealloc<SM::kTmemCols>(tmem);
 }
 
 // ---- pass 2: Y[i] = sum of T rows [dptr[i], dptr[i+1]) in order --------------------------
@@ -542,15 +589,20 @@ __global__ void gather_i32_kernel(const int32_t* __restrict__ idx, const int32_t
 template <int DIN, int DOUT>
 void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat16* W, float* Y,
                  cudaStream_t s) {
-  constexpr int smem = RgmsSmem<DIN, DOUT>::kBytes;
+  using SM = RgmsWsSmem<DIN, DOUT>;
+  constexpr int smem = SM::kBytes;
   auto* k1 = rgms_edge_gemm_kernel<DIN, DOUT>;
-  STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  static bool configured = false;
+  if (!configured) {
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
   // Resident CTAs per SM: shared memory (~227 KB usable) and TMEM (512 columns) bound it.
-  constexpr int kTmemCols = DOUT <= 32 ? 32 : (DOUT <= 64 ? 64 : (DOUT <= 128 ? 128 : 256));
-  const int per_sm = std::max(1, std::min({8, (227 * 1024) / (smem + 1024), 512 / kTmemCols}));
+  const int per_sm = std::max(1, std::min({3, (227 * 1024) / (smem + 2048), 512 / SM::kTmemCols}));
   const long long grid = std::min<long long>(h.ntiles, static_cast<long long>(num_sms()) * per_sm);
-  k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kThreads, smem, s>>>(h.edges.p, h.ntiles, X, W, h.T.p);
+  const CUtensorMap wmap = make_tensor_map_bf16_2d(W, h.R * DIN, DOUT, 8, DIN, CU_TENSOR_MAP_SWIZZLE_NONE);
+  k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kWsThreads, smem, s>>>(wmap, X, h.edges.p,
+                                                                                   h.ntiles, h.T.p);
   STRATA_CUDA_CHECK(cudaGetLastError());
   const long long lanes = h.m * RowSumShape<DOUT>::kL;
   const long long blocks = std::min<long long>((lanes + 255) / 256, static_cast<long long>(num_sms()) * 8);

@@ -44,6 +44,11 @@ __device__ __forceinline__ uint64_t make_desc_sw64(uint32_t saddr, uint32_t lbo,
   return make_desc(saddr, lbo, sbo) | (static_cast<uint64_t>(4) << 61);
 }
 
+// 32-byte swizzle (CU_TENSOR_MAP_SWIZZLE_32B): atoms of 8 rows x 32 B (256 B, 256-aligned).
+__device__ __forceinline__ uint64_t make_desc_sw32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return make_desc(saddr, lbo, sbo) | (static_cast<uint64_t>(6) << 61);
+}
+
 // Instruction descriptor, kind::f16 with bf16 inputs and f32 accumulation.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_major,
                                                        bool b_mn_major) {
@@ -194,6 +199,24 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const void* tmap, int c0
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3}], [%4];\n"
       :: "r"(smem_u32(smem)), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(mbar)) : "memory");
+}
+// TMA tile::gather4: rows r0..r3 (each one box of the 2D map, box height 1) of column c0 land
+// consecutively at smem (swizzled by address like a 4-row box).
+__device__ __forceinline__ void tma_gather4(void* smem, const void* tmap, int c0, int r0, int r1,
+                                            int r2, int r3, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+      :: "r"(smem_u32(smem)), "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+         "r"(smem_u32(mbar)) : "memory");
+}
+// Arrive on an mbarrier once all prior cp.async of this thread complete (counts as one of the
+// barrier's expected arrivals: .noinc).
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* mbar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" :: "r"(smem_u32(mbar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" :: "r"(smem_u32(mbar)) : "memory");
 }
 __device__ __forceinline__ void prefetch_tensormap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];\n" :: "l"(tmap) : "memory");
