@@ -282,6 +282,14 @@ def extra_reddit(S, torch, dev, stream, peak):
                      "b_alg_gbs": round(gbs, 1), "frac_of_hbm": round(gbs / peak, 3),
                      "note": "X is L2-resident (59.6 MB < 126 MB L2): frac is L2-assisted"}
     out["reddit_nnz"] = m.nnz
+    # The reference tuner's c-grid (tune.cpp:19-36) on the device: hyb(c in 1..16) timed, gated
+    # bitwise against the CSR format on integer operands (CSR itself is left out: its
+    # row-per-warp schedule is the load-imbalanced baseline, 51 ms here).
+    from paper_2207_04606_b200 import tune as T
+    rep = T.run_trials("spmm", m, d, T.SearchSpace.hyb_c_grid(include_csr=False), repeats=5, warmup=2)
+    out["reddit_tuner"] = {"best": rep.trials[rep.best].point.format,
+                           "ms": {t.point.format: round(t.median_ns / 1e6, 4) for t in rep.trials},
+                           "all_correct": all(t.correct for t in rep.trials)}
     return out
 
 

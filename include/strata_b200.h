@@ -104,6 +104,10 @@ int strata_hyb_destroy(strata_hyb* h);
  * launches (used by bench.py to report gpu_launches). */
 int strata_hyb_schedule_info(const strata_hyb* h, int64_t* slots, int64_t* chunks,
                              int64_t* crossing_runs, int64_t* empty_rows, int* launches_per_spmm);
+/* Row-work balance of the decomposition — tune.cpp:46-76 (hyb_balance): per part, the max over
+ * its ELL rows of the real (non-padding) slots divided by their mean; the worst part (>= 1).
+ * Computed on the device; synchronises `stream`. */
+int strata_hyb_row_work_balance(const strata_hyb* h, double* balance, void* stream);
 
 /* ---- hyb SpMM (device) ---------------------------------------------------------------
  * Replaces: Pipeline::run_dense() / interpret(stage3, bindings) for

@@ -310,6 +310,15 @@ int strata_hyb_schedule_info(const strata_hyb* h, int64_t* slots, int64_t* chunk
   });
 }
 
+int strata_hyb_row_work_balance(const strata_hyb* h, double* balance, void* stream) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    require(balance != nullptr, STRATA_ERR_USAGE, "null output");
+    require_device();
+    *balance = hyb_row_work_balance(H, as_stream(stream));
+  });
+}
+
 int strata_hyb_destroy(strata_hyb* h) {
   delete h;
   return STRATA_OK;

@@ -132,6 +132,8 @@ struct strata_hyb_impl {
 // Kernel launchers (defined in .cu files).
 void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32_t* indices,
                           const float* values, cudaStream_t s);
+// max / mean real (non-padding) slots per ELL row, worst over the parts (tune.cpp hyb_balance).
+double hyb_row_work_balance(const strata_hyb_impl& h, cudaStream_t s);
 void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t d,
                      cudaStream_t s);
 void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,

@@ -408,4 +408,53 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
                                  cudaMemcpyHostToDevice));
 }
 
+
+// ---- row-work balance (tune.cpp:46-76 hyb_balance) ---------------------------------------
+namespace {
+// Per ELL row of one part: real (non-padding) slots; per part the max and the sum.
+__global__ void row_work_kernel(const int32_t* __restrict__ J, long long nrows, int w,
+                                unsigned long long* __restrict__ out /* [max, sum] */) {
+  unsigned long long mx = 0, sum = 0;
+  for (long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int32_t* row = J + r * w;
+    unsigned long long real = 1;
+    for (int k = 1; k < w; ++k) real += row[k] != row[k - 1];
+    mx = max(mx, real);
+    sum += real;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, mx);
+    atomicAdd(out + 1, sum);
+  }
+}
+}  // namespace
+
+double hyb_row_work_balance(const strata_hyb_impl& h, cudaStream_t s) {
+  double worst = 1.0;
+  if (h.parts.empty()) return worst;
+  DevBuf<unsigned long long> acc(2 * h.parts.size());
+  STRATA_CUDA_CHECK(cudaMemsetAsync(acc.p, 0, acc.n * sizeof(unsigned long long), s));
+  for (size_t i = 0; i < h.parts.size(); ++i) {
+    const HybPart& P = h.parts[i];
+    if (P.nrows == 0) continue;
+    const unsigned g = static_cast<unsigned>(std::min<long long>((P.nrows + 255) / 256, num_sms() * 8LL));
+    row_work_kernel<<<g, 256, 0, s>>>(h.J.p + P.slot_off, P.nrows, static_cast<int>(P.width), acc.p + 2 * i);
+  }
+  STRATA_CUDA_CHECK(cudaGetLastError());
+  std::vector<unsigned long long> hv(acc.n);
+  STRATA_CUDA_CHECK(cudaMemcpyAsync(hv.data(), acc.p, acc.n * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, s));
+  STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < h.parts.size(); ++i) {
+    if (h.parts[i].nrows == 0 || hv[2 * i + 1] == 0) continue;
+    const double mean = static_cast<double>(hv[2 * i + 1]) / static_cast<double>(h.parts[i].nrows);
+    worst = std::max(worst, static_cast<double>(hv[2 * i]) / mean);
+  }
+  return worst;
+}
 }  // namespace strata_b200
