@@ -130,6 +130,23 @@ int strata_spmm_hyb_f32_host(const strata_hyb* h, const float* X_host, float* Y_
 int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_host,
                                    float* const* Y_host, int64_t nbatch, int64_t d, void* stream);
 
+/* Multi-destination form — the fused SpMM + all-gather of a row-sharded multi-GPU run: every
+ * output row of h (local row i) is stored to Y_dsts[0 .. ndst-1][i][0 .. d-1] (ndst <= 8).  The
+ * pointers may be peers' Y replicas mapped over NVLink (strata_ipc_open_handle), pre-offset by
+ * the caller to this shard's first global row, so the all-gather's traffic leaves the SMs as the
+ * rows are produced instead of in a separate collective.  Stream-ordered; the caller fences the
+ * ranks (e.g. a one-element NCCL all-reduce on the same stream) before reading peers' rows. */
+int strata_spmm_hyb_f32_multi(const strata_hyb* h, const float* X, float* const* Y_dsts, int ndst,
+                              int64_t d, void* stream);
+
+/* CUDA IPC plumbing for the peer mapping above (one process per GPU): a 64-byte handle of the
+ * device allocation holding dev_ptr plus dev_ptr's offset in it; the other process opens the
+ * handle (allocation base, peer-accessible) and adds the offset. */
+#define STRATA_IPC_HANDLE_BYTES 64
+int strata_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset);
+int strata_ipc_open_handle(const void* handle, void** dev_ptr);
+int strata_ipc_close(void* dev_ptr);
+
 /* ---- CSR SpMM (device, row-split baseline form of the same op) ---------------------
  * Replaces: build_matrix_pipeline(SpMM, ..., "csr") + interpret. */
 int strata_spmm_csr_f32(const int32_t* indptr, const int32_t* indices, const float* A,

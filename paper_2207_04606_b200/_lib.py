@@ -47,6 +47,8 @@ i64 = C.c_int64
 
 
 def _sig(name, restype, *args):
+    if os.environ.get("STRATA_B200_LIB") and not hasattr(lib, name):
+        return None  # A/B against an older build: symbols it predates stay unbound
     fn = getattr(lib, name)
     fn.restype = restype
     fn.argtypes = list(args)
@@ -81,6 +83,10 @@ _sig("strata_hyb_row_work_balance", C.c_int, vp, C.POINTER(C.c_double), vp)
 _sig("strata_spmm_hyb_f32", C.c_int, vp, vp, vp, i64, vp)
 _sig("strata_spmm_hyb_f32_host", C.c_int, vp, vp, vp, i64, vp)
 _sig("strata_spmm_hyb_f32_host_batch", C.c_int, vp, vp, vp, i64, i64, vp)
+_sig("strata_spmm_hyb_f32_multi", C.c_int, vp, vp, vp, C.c_int, i64, vp)
+_sig("strata_ipc_get_handle", C.c_int, vp, vp, i64p)
+_sig("strata_ipc_open_handle", C.c_int, vp, C.POINTER(vp))
+_sig("strata_ipc_close", C.c_int, vp)
 _sig("strata_spmm_csr_f32", C.c_int, vp, vp, vp, vp, vp, i64, i64, i64, vp)
 _sig("strata_sddmm_csr_f32", C.c_int, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, vp)
 _sig("strata_bsr_from_csr", C.c_int, vp, vp, vp, i64, i64, i64, i64, vp, C.POINTER(vp))
@@ -107,7 +113,8 @@ EXPORTED = [
     "strata_hyb_part_read", "strata_hyb_part_device", "strata_hyb_padding_ratio",
     "strata_hyb_dims", "strata_hyb_destroy", "strata_hyb_schedule_info",
     "strata_hyb_row_work_balance", "strata_spmm_hyb_f32", "strata_spmm_hyb_f32_host",
-    "strata_spmm_hyb_f32_host_batch",
+    "strata_spmm_hyb_f32_host_batch", "strata_spmm_hyb_f32_multi", "strata_ipc_get_handle",
+    "strata_ipc_open_handle", "strata_ipc_close",
     "strata_spmm_csr_f32", "strata_sddmm_csr_f32", "strata_bsr_from_csr", "strata_bsr_info",
     "strata_bsr_read", "strata_bsr_destroy", "strata_bsr_spmm_bf16",
     "strata_bsr_spmm_bf16_batched", "strata_ell_from_csr",

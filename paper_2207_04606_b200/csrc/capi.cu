@@ -331,7 +331,7 @@ int strata_spmm_hyb_f32(const strata_hyb* h, const float* X, float* Y, int64_t d
     require(d >= 1, STRATA_ERR_USAGE, "spmm: d must be >= 1");
     require((H.cols == 0 || X) && (H.rows == 0 || Y), STRATA_ERR_USAGE, "null operand");
     require_device();
-    spmm_hyb_launch(H, X, Y, d, as_stream(stream));
+    spmm_hyb_launch(H, X, &Y, 1, d, as_stream(stream));
   });
 }
 
@@ -384,7 +384,7 @@ int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_ho
         STRATA_CUDA_CHECK(cudaEventRecord(x_ready[k], cin));
         STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, x_ready[k], 0));
         if (b >= nslots) STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, y_free[k], 0));
-        spmm_hyb_launch(H, sx, sy, d, s);
+        spmm_hyb_launch(H, sx, &sy, 1, d, s);
         STRATA_CUDA_CHECK(cudaEventRecord(x_free[k], s));
         STRATA_CUDA_CHECK(cudaEventRecord(y_ready[k], s));
         STRATA_CUDA_CHECK(cudaStreamWaitEvent(cout, y_ready[k], 0));
@@ -398,6 +398,61 @@ int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_ho
       throw;
     }
     cleanup();
+  });
+}
+
+int strata_spmm_hyb_f32_multi(const strata_hyb* h, const float* X, float* const* Y_dsts, int ndst,
+                              int64_t d, void* stream) {
+  return guard([&] {
+    const auto& H = hyb_of(h);
+    require(d >= 1, STRATA_ERR_USAGE, "spmm: d must be >= 1");
+    require(Y_dsts != nullptr && ndst >= 1 && ndst <= STRATA_MAX_Y_DESTS, STRATA_ERR_USAGE,
+            "spmm_multi: 1 to " + std::to_string(STRATA_MAX_Y_DESTS) + " output buffers");
+    for (int i = 0; i < ndst; ++i) require(Y_dsts[i] != nullptr, STRATA_ERR_USAGE, "spmm_multi: null output");
+    require_device();
+    spmm_hyb_launch(H, X, Y_dsts, ndst, d, as_stream(stream));
+  });
+}
+
+int strata_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset) {
+  return guard([&] {
+    require(dev_ptr && handle_out && offset, STRATA_ERR_USAGE, "ipc: null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == STRATA_IPC_HANDLE_BYTES, "IPC handle size");
+    // The handle names the whole allocation; pooled allocators hand out interior pointers, so
+    // the pointer's offset from the allocation base travels with it.
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      STRATA_CUDA_CHECK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+      require(fn && q == cudaDriverEntryPointSuccess, STRATA_ERR_CUDA, "cuMemGetAddressRange unavailable");
+      get_range = reinterpret_cast<GetRange>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    require(get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) == CUDA_SUCCESS,
+            STRATA_ERR_CUDA, "ipc: not a device allocation");
+    cudaIpcMemHandle_t hd;
+    STRATA_CUDA_CHECK(cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base)));
+    std::memcpy(handle_out, &hd, sizeof(hd));
+    *offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  });
+}
+
+int strata_ipc_open_handle(const void* handle, void** dev_ptr) {
+  return guard([&] {
+    require(handle && dev_ptr, STRATA_ERR_USAGE, "ipc: null pointer");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    STRATA_CUDA_CHECK(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int strata_ipc_close(void* dev_ptr) {
+  return guard([&] {
+    require(dev_ptr != nullptr, STRATA_ERR_USAGE, "ipc: null pointer");
+    STRATA_CUDA_CHECK(cudaIpcCloseMemHandle(dev_ptr));
   });
 }
 

@@ -134,8 +134,10 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
                           const float* values, cudaStream_t s);
 // max / mean real (non-padding) slots per ELL row, worst over the parts (tune.cpp hyb_balance).
 double hyb_row_work_balance(const strata_hyb_impl& h, cudaStream_t s);
-void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t d,
-                     cudaStream_t s);
+// Every finished Y row is stored to each of Ydst[0 .. ndst-1] (ndst <= STRATA_MAX_Y_DESTS).
+#define STRATA_MAX_Y_DESTS 8
+void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Ydst, int ndst,
+                     int64_t d, cudaStream_t s);
 void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,
                      const float* X, float* Y, int64_t rows, int64_t d, cudaStream_t s);
 void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,

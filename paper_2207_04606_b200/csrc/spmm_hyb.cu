@@ -22,6 +22,7 @@
 //  * c > 1: partitions are launched in order and accumulate (Y zeroed first), which keeps
 //    the reference's per-row accumulation order across partitions (ascending columns).
 #include <algorithm>
+#include <string>
 
 #include "capi_internal.h"
 #include "common.cuh"
@@ -36,10 +37,18 @@ namespace {
 constexpr int kMaxParts = 32;
 constexpr int kBlock = 256;
 constexpr int kPiece = 256;  // ELL slots staged in shared memory per virtual warp at a time
+constexpr int kMaxYDests = STRATA_MAX_Y_DESTS;
 
 struct SpmmPartDev {
   long long slot_off, row_off, nrows, chunk_begin, nchunks, carry_off;
   int b, rpc_log2, may_split, pad_;
+};
+
+// Output row destinations: every finished Y row is stored to each of the n buffers (the
+// caller's Y, plus — for the fused multi-GPU all-gather — peers' Y replicas mapped over NVLink).
+struct YDests {
+  float* p[kMaxYDests];
+  int n;
 };
 
 struct SpmmArgs {
@@ -47,7 +56,7 @@ struct SpmmArgs {
   const int32_t* J;
   const float* V;
   const float* X;
-  float* Y;
+  YDests Y;
   double* carry;
   double* yacc;  // c > 1 only: f64 accumulator [rows][d]; else nullptr
   long long d;
@@ -187,7 +196,7 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 //      slot of every ELL row is flagged in bit 31 of its column;
 //   3. consume: batches of 8 real slots are read with broadcast 128-bit shared loads (no
 //      shuffles), their X rows gathered UG at a time (128-bit per lane), and accumulated.
-template <int L, int VEC, bool kScalar>
+template <int L, int VEC, bool kScalar, bool kMulti>
 __global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2)))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int kT = 8;  // real slots per consume batch / slots per lane per compaction round
@@ -241,7 +250,10 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
       if (a.yacc)  // c > 1: partitions accumulate in f64, rounded once at the end
         put_f64<L, VEC, kScalar, true>(a.yacc + dest * d, acc, d, lane, feat0);
       else
-        put_row<L, VEC, kScalar>(a.Y + dest * d, acc, d, lane, feat0);
+        put_row<L, VEC, kScalar>(a.Y.p[0] + dest * d, acc, d, lane, feat0);
+        if constexpr (kMulti)  // replicas of the fused all-gather (separate instantiation:
+          for (int i = 1; i < a.Y.n; ++i)  // the single-output kernels keep their registers)
+            put_row<L, VEC, kScalar>(a.Y.p[i] + dest * d, acc, d, lane, feat0);
     }
     acc.zero();
     first_group = false;
@@ -404,8 +416,8 @@ constexpr int kFixBlock = 128;
 template <int V>  // V = 2: double2 lanes (d even); V = 1: scalar
 __device__ __forceinline__ void fix_reduce(const double* __restrict__ src, long long first_row,
                                            int count, int first_slot, bool two_slot,
-                                           float* yout, double* l2out, long long d,
-                                           bool accumulate) {
+                                           const YDests* ydst, long long yrow, double* l2out,
+                                           long long d, bool accumulate) {
   __shared__ double2 part[kFixBlock];
   const long long dv = d / V;
   const int rt = static_cast<int>(min64(dv, kFixBlock));  // threads per feature row
@@ -444,12 +456,15 @@ __device__ __forceinline__ void fix_reduce(const double* __restrict__ src, long 
         tot.x += part[gg * rt + threadIdx.x].x;
         tot.y += part[gg * rt + threadIdx.x].y;
       }
-      if (yout) {
-        if constexpr (V == 2)
-          reinterpret_cast<float2*>(yout)[f] =
-              make_float2(static_cast<float>(tot.x), static_cast<float>(tot.y));
-        else
-          yout[f] = static_cast<float>(tot.x);
+      if (ydst) {
+        for (int i = 0; i < ydst->n; ++i) {
+          float* yout = ydst->p[i] + yrow * d;
+          if constexpr (V == 2)
+            reinterpret_cast<float2*>(yout)[f] =
+                make_float2(static_cast<float>(tot.x), static_cast<float>(tot.y));
+          else
+            yout[f] = static_cast<float>(tot.x);
+        }
       } else {
         if constexpr (V == 2) {
           double2* o = reinterpret_cast<double2*>(l2out) + f;
@@ -472,72 +487,86 @@ __device__ __forceinline__ void fix_reduce(const double* __restrict__ src, long 
 template <int V>
 __global__ void __launch_bounds__(kFixBlock)
 spmm_fixup_tiles_kernel(const FixTile* __restrict__ tiles, const double* __restrict__ carry,
-                        double* __restrict__ l2, float* __restrict__ Y, double* __restrict__ yacc,
-                        long long d) {
+                        double* __restrict__ l2, const __grid_constant__ YDests Y,
+                        double* __restrict__ yacc, long long d) {
   const FixTile t = tiles[blockIdx.x];
   if (t.out >= 0 && yacc)
-    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, nullptr, yacc + t.out * d, d, true);
+    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, nullptr, 0, yacc + t.out * d, d, true);
   else if (t.out >= 0)
-    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, Y + t.out * d, nullptr, d, false);
+    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, &Y, t.out, nullptr, d, false);
   else
-    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, nullptr, l2 + (-t.out - 1) * d,
+    fix_reduce<V>(carry, t.carry0, t.count, t.first_slot, true, nullptr, 0, l2 + (-t.out - 1) * d,
                   d, false);
 }
 
 template <int V>
 __global__ void __launch_bounds__(kFixBlock)
 spmm_fixup_runs_kernel(const FixRun* __restrict__ runs, const double* __restrict__ l2,
-                       float* __restrict__ Y, double* __restrict__ yacc, long long d) {
+                       const __grid_constant__ YDests Y, double* __restrict__ yacc, long long d) {
   const FixRun r = runs[blockIdx.x];
   if (yacc)
-    fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, nullptr, yacc + r.row * d, d, true);
+    fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, nullptr, 0, yacc + r.row * d, d, true);
   else
-    fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, Y + r.row * d, nullptr, d, false);
+    fix_reduce<V>(l2, r.l2_first, r.ntiles, 0, false, &Y, r.row, nullptr, d, false);
 }
 
-__global__ void f64_to_f32_kernel(const double* __restrict__ in, float* __restrict__ out,
+__global__ void f64_to_f32_kernel(const double* __restrict__ in, const __grid_constant__ YDests Y,
                                   long long n) {
   for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-       e += static_cast<long long>(gridDim.x) * blockDim.x)
-    out[e] = static_cast<float>(in[e]);
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float v = static_cast<float>(in[e]);
+    for (int i = 0; i < Y.n; ++i) Y.p[i][e] = v;
+  }
 }
 
-__global__ void zero_rows_kernel(const int32_t* __restrict__ rows, long long n, float* Y,
-                                 long long d) {
+__global__ void zero_rows_kernel(const int32_t* __restrict__ rows, long long n,
+                                 const __grid_constant__ YDests Y, long long d) {
   const long long total = n * d;
   for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = e / d, f = e - r * d;
-    Y[static_cast<long long>(rows[r]) * d + f] = 0.f;
+    for (int i = 0; i < Y.n; ++i) Y.p[i][static_cast<long long>(rows[r]) * d + f] = 0.f;
   }
 }
 
-template <int L, int VEC, bool kScalar>
-void launch_variant(const SpmmArgs& args, long long total_chunks, long long d, cudaStream_t s) {
+template <int L, int VEC, bool kScalar, bool kMulti>
+void launch_variant_m(const SpmmArgs& args, long long total_chunks, long long d, cudaStream_t s) {
   const long long threads = total_chunks * L;
   const unsigned blocks = static_cast<unsigned>((threads + kBlock - 1) / kBlock);
   dim3 grid(blocks, kScalar ? static_cast<unsigned>((d + 31) / 32) : 1u);
   constexpr int smem = (kBlock / L) * 3 * kPiece * 4;  // 3 KB staging per virtual warp
+  auto* kern = spmm_hyb_kernel<L, VEC, kScalar, kMulti>;
   static bool configured = false;  // host-side, once per instantiation
   if (!configured) {
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(spmm_hyb_kernel<L, VEC, kScalar>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 #ifdef STRATA_SPMM_CARVEOUT  // A/B knob: prefer the largest shared-memory carveout
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(spmm_hyb_kernel<L, VEC, kScalar>,
-                                           cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 #endif
     configured = true;
   }
-  spmm_hyb_kernel<L, VEC, kScalar><<<grid, kBlock, smem, s>>>(args);
+  kern<<<grid, kBlock, smem, s>>>(args);
+}
+
+template <int L, int VEC, bool kScalar>
+void launch_variant(const SpmmArgs& args, long long total_chunks, long long d, cudaStream_t s) {
+  if (args.Y.n > 1) launch_variant_m<L, VEC, kScalar, true>(args, total_chunks, d, s);
+  else launch_variant_m<L, VEC, kScalar, false>(args, total_chunks, d, s);
 }
 
 }  // namespace
 
-void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* Y, int64_t d,
-                     cudaStream_t s) {
+void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Ydst, int ndst,
+                     int64_t d, cudaStream_t s) {
   if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "spmm: d must be >= 1");
-  const bool aligned = (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
-                       (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+  if (ndst < 1 || ndst > kMaxYDests)
+    throw ApiError(STRATA_ERR_USAGE, "spmm: 1 to " + std::to_string(kMaxYDests) + " output buffers");
+  YDests Y{};
+  Y.n = ndst;
+  bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0;
+  for (int i = 0; i < ndst; ++i) {
+    Y.p[i] = Ydst[i];
+    aligned = aligned && reinterpret_cast<uintptr_t>(Ydst[i]) % 16 == 0;
+  }
   // Variant: lanes per VW (L) and float4s per lane (VEC).
   int L = 32, VEC = 1;
   bool scalar = true;

@@ -27,6 +27,7 @@ from ._lib import StrataError, check, lib
 __all__ = [
     "StrataError", "CsrMatrix", "generate_matrix", "dense_int", "hyb_auto_k", "EllBucketPart",
     "HybDecomposition", "decompose_hyb", "hyb_rules", "spmm", "spmm_host", "spmm_host_batch",
+    "spmm_multi", "ipc_handle", "ipc_open", "ipc_close",
     "spmm_csr", "sddmm",
     "partition_rows", "device_ok",
 ]
@@ -251,6 +252,35 @@ def spmm_host(hyb: HybDecomposition, X_host, Y_host, stream=None):
     check(lib.strata_spmm_hyb_f32_host(hyb.handle, _ptr(X_host), _ptr(Y_host), d,
                                        _stream(stream)))
     return Y_host
+
+
+def spmm_multi(hyb: HybDecomposition, X, dst_ptrs, stream=None):
+    """Y rows of ``hyb`` stored to every device address in ``dst_ptrs`` (ints: row-major
+    [rows][d] f32 buffers, possibly peer-mapped; see sharding.PeerAllGather)."""
+    d = X.shape[1]
+    n = len(dst_ptrs)
+    arr = (C.c_void_p * n)(*dst_ptrs)
+    check(lib.strata_spmm_hyb_f32_multi(hyb.handle, _ptr(X), C.cast(arr, C.c_void_p), n, d,
+                                        _stream(stream)))
+
+
+def ipc_handle(t) -> tuple:
+    """(64-byte CUDA IPC handle of the allocation holding device tensor t, offset of t in it)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_int64()
+    check(lib.strata_ipc_get_handle(_ptr(t), buf, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation (handle from ipc_handle); returns its base address."""
+    p = C.c_void_p()
+    check(lib.strata_ipc_open_handle(C.c_char_p(handle), C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    check(lib.strata_ipc_close(C.c_void_p(ptr)))
 
 
 def spmm_host_batch(hyb: HybDecomposition, X_hosts, Y_hosts, stream=None):

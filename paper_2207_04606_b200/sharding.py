@@ -69,3 +69,50 @@ class RowShardPlan:
             return np.concatenate(parts, axis=0)
         import torch
         return torch.cat(parts, dim=0)
+
+
+class PeerAllGather:
+    """Fused SpMM + all-gather over peer memory (one process per GPU).
+
+    Every rank owns a full [rows][d] f32 replica of Y.  The replicas' CUDA IPC handles are
+    exchanged once through the process group; each rank then runs its shard's SpMM with
+    ``ops.spmm_multi`` storing every finished row into all replicas (its own plus the peers',
+    written over NVLink), so the reassembly traffic leaves the SMs as rows are produced — no
+    separate collective, no padded buffer, global row order directly.  ``fence()`` (a
+    one-element all-reduce on the stream) orders the next layer's reads after every rank's
+    stores.
+    """
+
+    def __init__(self, y_full, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        from .ops import ipc_handle, ipc_open
+        self.y = y_full
+        self.rank, self.world, self.group = rank, world, group
+        self.d = int(y_full.shape[1])
+        mine = ipc_handle(y_full)
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        self.ptrs, self._opened = [], []
+        for r, (hd, off) in enumerate(handles):
+            if r == rank:
+                self.ptrs.append(y_full.data_ptr())
+            else:
+                base = ipc_open(hd)
+                self._opened.append(base)
+                self.ptrs.append(base + off)
+        import torch
+        self._flag = torch.zeros(1, dtype=torch.int32, device=y_full.device)
+
+    def dsts(self, row0: int):
+        """Destination addresses of global row ``row0`` in every replica."""
+        return [p + row0 * self.d * 4 for p in self.ptrs]
+
+    def fence(self):
+        import torch.distributed as dist
+        dist.all_reduce(self._flag, group=self.group)
+
+    def close(self):
+        from .ops import ipc_close
+        for p in self._opened:
+            ipc_close(p)
+        self._opened = []
