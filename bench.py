@@ -399,10 +399,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         args.gpus = world
+    # STRATA_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 with a gloo group, so the
+    # N > 1 code path (sharding, IPC peer stores, fallbacks) runs on a one-GPU box.
+    share = os.environ.get("STRATA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2207_04606_b200 as S
 
     hbm_peak, bf16_peak, peak_kind = load_peaks()
@@ -413,9 +421,13 @@ def run_ours(args):
     gen_s = time.time() - t0
     k = S.hyb_auto_k(m)
     from paper_2207_04606_b200.sharding import RowShardPlan
-    # N > 1: each rank's rows are cut into sub-chunks so chunk c's NCCL all-gather overlaps the
-    # SpMM of chunk c+1 (sharding.py); N = 1 runs the whole graph as one chunk.
-    chunks = 4 if world > 1 else 1
+    # N > 1, --allgather p2p (default): the fused SpMM + all-gather — every rank's SpMM stores
+    # its rows straight into all ranks' full Y replicas over NVLink (strata_spmm_hyb_f32_multi,
+    # CUDA IPC mappings), verified once against the NCCL path below, which it falls back to.
+    # --allgather nccl: each rank's rows are cut into sub-chunks so chunk c's NCCL all-gather
+    # overlaps the SpMM of chunk c+1 (sharding.py).  N = 1 runs the whole graph as one chunk.
+    p2p = world > 1 and args.allgather == "p2p"
+    chunks = 4 if (world > 1 and not p2p) else 1
     plan = RowShardPlan(m, world, chunks)
     r0, r1 = plan.rows_of(rank)
     shard = plan.shard(rank)
@@ -448,7 +460,37 @@ def run_ours(args):
             ys.append(Yloc[c, :n_c])
     gviews = [Yfull[plan.slot(c, 0): plan.slot(c, 0) + world * plan.max_rows] for c in range(chunks)]
 
+    pag, p2p_note = None, None
+    if p2p:
+        from paper_2207_04606_b200.sharding import PeerAllGather
+        Yrep = torch.empty((m.rows, d), device=dev, dtype=torch.float32)
+        try:
+            pag = PeerAllGather(Yrep, rank, world)
+            # one-time check against the NCCL path: local rows + all_gather + unpad
+            S.spmm(hs[0], X, ys[0], stream=stream)
+            dist.all_gather_into_tensor(gviews[0], Yloc[0])
+            S.spmm_multi(hs[0], X, pag.dsts(r0), stream=stream)
+            pag.fence()
+            torch.cuda.synchronize()
+            same = torch.equal(Yrep, plan.unpad(Yfull))
+            ok = torch.tensor([1 if same else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok[0]) != 1:
+                raise RuntimeError("peer all-gather differs from the NCCL all-gather")
+        except Exception as e:  # noqa: BLE001 — fall back to the NCCL collective
+            p2p_note = f"p2p unavailable ({e}); NCCL all-gather used"
+            pag = None
+            p2p = False
+
     def step(evs=None):
+        if pag is not None:
+            if evs is not None:
+                evs[0][0].record(stream)
+            S.spmm_multi(hs[0], X, pag.dsts(r0), stream=stream)
+            if evs is not None:
+                evs[0][1].record(stream)
+            pag.fence()
+            return
         works = []
         for c in range(chunks):
             if evs is not None:
@@ -549,6 +591,8 @@ def run_ours(args):
              "schedule": sched, "spmm_ms_max_over_ranks": round(spmm_ms_max, 4),
              "allgather_exposed_ms": round(ms_per_step - spmm_ms_max, 4) if world > 1 else 0.0,
              "chunks_per_rank": chunks,
+             "allgather": ("none" if world == 1 else ("p2p" if pag is not None else "nccl")),
+             "allgather_note": p2p_note,
              "compute_only_gflops": round(flops / (spmm_ms_max * 1e-3) / 1e9, 2),
              "frac_of_8tbs_nameplate": round(achieved / 8000.0, 4)}
     if rank == 0 and world == 1 and not args.no_extra:
@@ -576,8 +620,10 @@ def run_ours(args):
             "config": {"workload": "hyb SpMM fp32, ogbn-products shape (n=2,449,029, "
                                    "nnz=61,943,588, d=128), hyb:c=1,k=5",
                        "format": f"hyb:c=1,k={k}", "nnz": m.nnz, "rows": m.rows, "d": d,
-                       "parallelism": f"row-sharded x{world} (nnz-balanced) + NCCL all-gather"
-                                      if world > 1 else "single GPU",
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"row-sharded x{world} (nnz-balanced) + " +
+                                       ("fused peer-store all-gather (NVLink, CUDA IPC)" if pag is not None
+                                        else "NCCL all-gather (4 chunks overlapped)")),
                        "l2": "no flush: inputs larger than L2 (X 1.25 GB, ELL 0.57 GB)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
@@ -597,6 +643,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--allgather", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 reassembly of Y: fused peer stores (p2p) or NCCL all-gather")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
