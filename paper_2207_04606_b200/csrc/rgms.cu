@@ -384,7 +384,16 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
 // 39 % of the edges, the longest 171,738) would serialise one lane group, so they are cut into
 // kChunk-edge chunks summed by a whole warp (fixed strided split + fixed shuffle tree) into
 // partials, and a finishing pass adds a row's partials in chunk order — deterministic.
-constexpr int kLong = 64;
+#ifndef STRATA_RGMS_SUM_MINB  // A/B knobs of the row-sum pass
+#define STRATA_RGMS_SUM_MINB 1
+#endif
+#ifndef STRATA_RGMS_SUM_KB
+#define STRATA_RGMS_SUM_KB 8
+#endif
+#ifndef STRATA_RGMS_LONG
+#define STRATA_RGMS_LONG 64
+#endif
+constexpr int kLong = STRATA_RGMS_LONG;
 constexpr int kChunk = 1024;
 
 template <int DOUT>
@@ -400,13 +409,13 @@ struct RowSumShape {
 // walks that range in batches of 8 T rows issued together, flushing a row's sum when the walk
 // crosses its end.  Long rows are stepped over (at most one wasted batch each).
 template <int DOUT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, STRATA_RGMS_SUM_MINB)
 rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ T, long long m,
                     float* __restrict__ Y) {
   using RS = RowSumShape<DOUT>;
   constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
   constexpr int kRPV = 32 / kGrp;  // rows per lane group per block
-  constexpr int kB = 8;            // T rows in flight per lane group
+  constexpr int kB = STRATA_RGMS_SUM_KB;  // T rows in flight per lane group
   __shared__ int sbnd[8][33];
   const int lane = threadIdx.x & 31, l = lane % kL, g = lane / kL, w = threadIdx.x >> 5;
   int* bnd = sbnd[w];
