@@ -83,7 +83,11 @@ __device__ __forceinline__ void gather(Frag<VEC, kScalar>& f, const float* __res
     const long long fi = feat0 + lane;
     f.v[0].x = fi < d ? ld_gather(X + col * d + fi) : 0.f;
   } else {
-    const float4* xp = reinterpret_cast<const float4*>(X + col * d) + lane;
+    // Vector variants are launched only for d == 4 * L * VEC, so the row stride is a
+    // compile-time power of two: one shift instead of a 64-bit multiply per gathered slot.
+    (void)d;
+    const float4* xp = reinterpret_cast<const float4*>(X) +
+                       (static_cast<unsigned long long>(static_cast<uint32_t>(col)) * (L * VEC)) + lane;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) f.v[i] = ld_gather4(xp + i * L);
   }
