@@ -188,6 +188,16 @@ int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int6
 int strata_bsr_spmm_bf16_batched(const strata_bsr* h, const void* values_bf16, const void* X_bf16,
                                  float* Y, int64_t heads, int64_t d, void* stream);
 
+/* ---- COO ingest (device) -------------------------------------------------------------
+ * Replaces: build_csr(coo, prefix) (storage.hpp:111, storage.cpp:89-124) for COO triplets
+ * already in HBM: row[nnz], col[nnz] (int32), val[nnz] (f32) -> indptr[rows+1], indices[nnz],
+ * values[nnz] sorted by (row, col).  STRATA_ERR_VALIDATION "coordinate out of range" or
+ * "duplicate coordinate (r, c)" (the first duplicate in sorted order) exactly like the
+ * reference.  Radix sort of 64-bit keys; one host sync (the validation verdict). */
+int strata_csr_from_coo(const int32_t* row, const int32_t* col, const float* val, int64_t nnz,
+                        int64_t rows, int64_t cols, int32_t* indptr, int32_t* indices,
+                        float* values, void* stream);
+
 /* ---- ELL (device) ---------------------------------------------------------------------
  * Replaces: csr_to_ell(csr, w, prefix) (storage.hpp:124, storage.cpp:190-227).
  * Output device arrays J_indices[rows*w], values[rows*w] (caller-allocated).  Fails with

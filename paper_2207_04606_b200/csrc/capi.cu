@@ -478,6 +478,17 @@ int strata_sddmm_csr_f32(const int32_t* indptr, const int32_t* indices, const fl
   });
 }
 
+int strata_csr_from_coo(const int32_t* row, const int32_t* col, const float* val, int64_t nnz,
+                        int64_t rows, int64_t cols, int32_t* indptr, int32_t* indices,
+                        float* values, void* stream) {
+  return guard([&] {
+    require(nnz == 0 || (row && col && val && indices && values), STRATA_ERR_USAGE, "null array");
+    require(indptr != nullptr, STRATA_ERR_USAGE, "null indptr");
+    require_device();
+    csr_from_coo_device(row, col, val, nnz, rows, cols, indptr, indices, values, as_stream(stream));
+  });
+}
+
 int strata_ell_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
                         int64_t rows, int64_t cols, int64_t w, int32_t* J_indices,
                         float* ell_values, void* stream) {

@@ -144,6 +144,9 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
                       const float* X, const float* Y, float* B, int64_t rows, int64_t cols,
                       int64_t nnz, int64_t d, cudaStream_t s);
 
+void csr_from_coo_device(const int32_t* r, const int32_t* c, const float* v, int64_t nnz,
+                         int64_t rows, int64_t cols, int32_t* indptr, int32_t* indices,
+                         float* values, cudaStream_t s);
 void ell_from_csr_launch(const int32_t* indptr, const int32_t* indices, const float* values,
                          int64_t rows, int64_t cols, int64_t w, int32_t* J, float* V,
                          cudaStream_t s);

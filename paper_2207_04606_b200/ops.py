@@ -25,7 +25,7 @@ import numpy as np
 from ._lib import StrataError, check, lib
 
 __all__ = [
-    "StrataError", "CsrMatrix", "generate_matrix", "dense_int", "hyb_auto_k", "EllBucketPart",
+    "StrataError", "CsrMatrix", "build_csr_device", "generate_matrix", "dense_int", "hyb_auto_k", "EllBucketPart",
     "HybDecomposition", "decompose_hyb", "hyb_rules", "spmm", "spmm_host", "spmm_host_batch",
     "spmm_multi", "ipc_handle", "ipc_open", "ipc_close",
     "spmm_csr", "sddmm",
@@ -91,6 +91,21 @@ class DeviceCsr:
     @property
     def nnz(self) -> int:
         return int(self.indices.shape[0])
+
+
+def build_csr_device(rows: int, cols: int, row, col, val, stream=None) -> "DeviceCsr":
+    """build_csr (storage.cpp:89-124) on the device: COO triplets (device int32 row / col, f32
+    val) -> DeviceCsr sorted by (row, col); StrataError(kind='Validation') on out-of-range or
+    duplicate coordinates with the reference's messages."""
+    import torch
+    dev = row.device
+    nnz = int(row.shape[0])
+    indptr = torch.empty(rows + 1, dtype=torch.int32, device=dev)
+    indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    values = torch.empty(max(nnz, 1), dtype=torch.float32, device=dev)
+    check(lib.strata_csr_from_coo(_ptr(row), _ptr(col), _ptr(val), nnz, rows, cols, _ptr(indptr),
+                                  _ptr(indices), _ptr(values), _stream(stream)))
+    return DeviceCsr(rows, cols, indptr, indices[:nnz], values[:nnz])
 
 
 def generate_matrix(kind: str, n: int, m: int, density: float = 0.0, band: int = 0,

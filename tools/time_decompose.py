@@ -40,3 +40,14 @@ _, t1 = wall(lambda: S.RgmsPlan(rel))
 _, t2 = wall(lambda: S.RgmsPlan(rel))
 out["C4_rgms_plan_ms"] = [round(t1, 1), round(t2, 1)]
 print(json.dumps(out))
+
+# device build_csr (COO -> CSR) at the C5 shape, triplets shuffled
+import numpy as np  # noqa: E402
+m = S.generate_matrix("powerlaw", 2449029, 2449029, 0, 0, 0, 25.3, 1)
+rows = np.repeat(np.arange(m.rows, dtype=np.int32), np.diff(m.indptr))
+perm = np.random.default_rng(0).permutation(m.nnz)
+t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+r, c, v = t(rows[perm]), t(m.indices[perm]), t(m.values[perm])
+_, t1 = wall(lambda: S.build_csr_device(m.rows, m.cols, r, c, v))
+_, t2 = wall(lambda: S.build_csr_device(m.rows, m.cols, r, c, v))
+print(json.dumps({"C5_build_csr_device_ms": [round(t1, 1), round(t2, 1)]}))
