@@ -198,6 +198,43 @@ int strata_csr_from_coo(const int32_t* row, const int32_t* col, const float* val
                         int64_t rows, int64_t cols, int32_t* indptr, int32_t* indices,
                         float* values, void* stream);
 
+/* ---- DBSR (device) -------------------------------------------------------------------
+ * Replaces: csr_to_dbsr(csr, b, prefix) (storage.hpp, storage.cpp:336-370): the BSR of the
+ * matrix plus its stored block rows.  Readback: IO_indices[nstored] (stored block rows),
+ * JO_indptr[nstored+1], JO_indices[nblocks], values[nblocks*b*b] (f32; the BSR's block order).
+ * SpMM: tcgen05 BSR kernel over the stored rows only (row map), unstored rows zero. */
+typedef struct strata_dbsr strata_dbsr;
+int strata_dbsr_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
+                         int64_t rows, int64_t cols, int64_t nnz, int64_t b, void* stream,
+                         strata_dbsr** out);
+int strata_dbsr_info(const strata_dbsr* h, int64_t* mb, int64_t* nb, int64_t* b, int64_t* nstored,
+                     int64_t* nblocks, int64_t* pad_slots);
+int strata_dbsr_read(const strata_dbsr* h, int32_t* io_indices, int32_t* jo_indptr,
+                     int32_t* jo_indices, float* values);
+int strata_dbsr_destroy(strata_dbsr* h);
+/* Y[mb*b][d] (f32, overwritten) = A_dbsr(bf16) * X (X[nb*b][d] bf16).  b == 32, d in
+ * {64, 128, 256, 512}. */
+int strata_dbsr_spmm_bf16(const strata_dbsr* h, const void* X_bf16, float* Y, int64_t d,
+                          void* stream);
+
+/* ---- SR-BCRS (device) ------------------------------------------------------------------
+ * Replaces: csr_to_srbcrs(csr, t, g, prefix) (storage.cpp:372-440): tile rows of t rows, their
+ * distinct columns in groups of g (last group padded with the last column), values slot-major
+ * [groups*g][t].  Readback: G_indptr[mb+1], JT_indices[groups*g], values[groups*g*t] (f32),
+ * bit-exact.  SpMM (t == 8, g == 32): tcgen05, the 32 X rows of a group gathered by TMA
+ * tile::gather4 into the A operand, the group's values as the B operand. */
+typedef struct strata_srbcrs strata_srbcrs;
+int strata_srbcrs_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
+                           int64_t rows, int64_t cols, int64_t nnz, int64_t t, int64_t g,
+                           void* stream, strata_srbcrs** out);
+int strata_srbcrs_info(const strata_srbcrs* h, int64_t* mb, int64_t* t, int64_t* g,
+                       int64_t* groups, int64_t* pad_slots);
+int strata_srbcrs_read(const strata_srbcrs* h, int32_t* g_indptr, int32_t* jt_indices, float* values);
+int strata_srbcrs_destroy(strata_srbcrs* h);
+/* Y[mb*t][d] (f32, overwritten) = A_srbcrs(bf16) * X (X[cols][d] bf16). */
+int strata_srbcrs_spmm_bf16(const strata_srbcrs* h, const void* X_bf16, float* Y, int64_t d,
+                            void* stream);
+
 /* ---- ELL (device) ---------------------------------------------------------------------
  * Replaces: csr_to_ell(csr, w, prefix) (storage.hpp:124, storage.cpp:190-227).
  * Output device arrays J_indices[rows*w], values[rows*w] (caller-allocated).  Fails with

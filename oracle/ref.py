@@ -44,6 +44,8 @@ def lib():
         L.sref_dense_int.argtypes = [i64, C.c_uint64, vp]
         L.sref_build_csr.argtypes = [vp, C.c_int, C.POINTER(vp)]
         L.sref_csr_to_bsr.argtypes = [vp, i64, C.POINTER(vp)]
+        L.sref_csr_to_dbsr.argtypes = [vp, i64, C.POINTER(vp)]
+        L.sref_csr_to_srbcrs.argtypes = [vp, i64, i64, C.POINTER(vp)]
         L.sref_csr_to_ell.argtypes = [vp, i64, C.POINTER(vp)]
         L.sref_hyb_auto_k.argtypes = [vp]
         L.sref_storage_info.argtypes = [vp, vp]
@@ -144,6 +146,16 @@ class Storage:
     def to_bsr(self, b):
         h = vp()
         _chk(lib().sref_csr_to_bsr(self.h, b, C.byref(h)))
+        return Storage(h)
+
+    def to_dbsr(self, b):
+        h = vp()
+        _chk(lib().sref_csr_to_dbsr(self.h, b, C.byref(h)))
+        return Storage(h)
+
+    def to_srbcrs(self, t, g):
+        h = vp()
+        _chk(lib().sref_csr_to_srbcrs(self.h, t, g, C.byref(h)))
         return Storage(h)
 
     def to_ell(self, w):

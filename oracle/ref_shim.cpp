@@ -137,6 +137,16 @@ int sref_csr_to_ell(void* csr, int64_t w, void** out) {
   return guard([&] { *out = new TensorStorage(csr_to_ell(*static_cast<TensorStorage*>(csr), w)); });
 }
 
+int sref_csr_to_dbsr(void* csr, int64_t b, void** out) {
+  return guard([&] { *out = new TensorStorage(csr_to_dbsr(*static_cast<TensorStorage*>(csr), b)); });
+}
+
+int sref_csr_to_srbcrs(void* csr, int64_t t, int64_t g, void** out) {
+  return guard([&] {
+    *out = new TensorStorage(csr_to_srbcrs(*static_cast<TensorStorage*>(csr), t, g));
+  });
+}
+
 int sref_hyb_auto_k(void* csr) { return hyb_auto_k(*static_cast<TensorStorage*>(csr)); }
 
 // info: rows, cols, nnz, pad_slots, block, nvalues, orig_rows, orig_cols

@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <memory>
 #include <cuda_bf16.h>
 
 #include "capi_internal.h"
@@ -29,12 +30,22 @@
 
 using namespace strata_b200;
 
+struct strata_dbsr;
 struct strata_bsr {
   int device = 0;
   int64_t rows = 0, cols = 0, nnz = 0, b = 0, mb = 0, nb = 0, nblocks = 0, pad_slots = 0;
   DevBuf<int32_t> indptr, indices;
   DevBuf<float> values;           // f32, bit-exact readback
   DevBuf<__nv_bfloat16> vals_bf;  // tensor-core operand
+};
+
+// DBSR (storage.cpp:336-370): the BSR of the same matrix plus its stored block rows.
+struct strata_dbsr {
+  strata_bsr* bsr = nullptr;
+  int64_t nstored = 0;
+  DevBuf<int32_t> stored;  // IO_indices [nstored]
+  DevBuf<int32_t> jptr;    // JO_indptr [nstored + 1] over stored rows
+  ~strata_dbsr() { delete bsr; }
 };
 
 namespace {
@@ -142,7 +153,8 @@ template <int D>  // feature count, 64 or a multiple of 128 (<= 512)
 __global__ void __launch_bounds__(kThreads, 1)
 bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap xmap,
                    const int32_t* __restrict__ jo_indptr, const int32_t* __restrict__ jo_indices,
-                   long long nblocks, long long x_rows, long long y_rows, float* __restrict__ Y) {
+                   const int32_t* __restrict__ rowmap, long long nblocks, long long x_rows,
+                   long long y_rows, float* __restrict__ Y) {
   constexpr int kM = D == 64 ? 64 : 128;         // UMMA M (feature tile)
   constexpr int kTiles = D / kM;                  // feature tiles
   constexpr int kCols = kTiles * kB < 32 ? 32 : kTiles * kB;  // TMEM columns (pow2 >= 32)
@@ -161,9 +173,11 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
   __shared__ int32_t s_cols[kMaxPre];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long br = blockIdx.x, head = blockIdx.y;  // block row, batch entry (head)
+  // CTA = (stored block row, head); DBSR maps stored row -> block row (IO_indices).
+  const long long sr = blockIdx.x, head = blockIdx.y;
+  const long long br = rowmap ? rowmap[sr] : sr;
   BSR_TRACE(0);
-  const int q0 = jo_indptr[br], nblk = jo_indptr[br + 1] - q0;
+  const int q0 = jo_indptr[sr], nblk = jo_indptr[sr + 1] - q0;
   for (int j = tid; j < nblk && j < kMaxPre; j += kThreads) s_cols[j] = jo_indices[q0 + j];
   if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
   if (tid == 32) {
@@ -261,7 +275,8 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
 // the K-major SW64 B operand.
 template <int D>
 void launch_bsr(const strata_bsr& h, const __nv_bfloat16* vals, long long heads,
-                const __nv_bfloat16* X, float* Y, cudaStream_t s) {
+                const __nv_bfloat16* X, float* Y, cudaStream_t s, const int32_t* jo_indptr,
+                const int32_t* rowmap, long long nrows) {
   constexpr int smem = bsr_stages<D>() * (kB * kB * 2 + kB * D * 2) + 1024;
   static bool configured = false;
   if (!configured) {
@@ -273,10 +288,28 @@ void launch_bsr(const strata_bsr& h, const __nv_bfloat16* vals, long long heads,
   const CUtensorMap xmap = make_tensor_map_bf16_2d(X, heads * x_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap amap = make_tensor_map_bf16_2d(vals, heads * std::max<long long>(h.nblocks, 1) * kB,
                                                    kB, kB, kB, CU_TENSOR_MAP_SWIZZLE_64B);
-  const dim3 grid(static_cast<unsigned>(h.mb), static_cast<unsigned>(heads));
-  bsr_spmm_tc_kernel<D><<<grid, kThreads, smem, s>>>(amap, xmap, h.indptr.p, h.indices.p,
+  const dim3 grid(static_cast<unsigned>(nrows), static_cast<unsigned>(heads));
+  bsr_spmm_tc_kernel<D><<<grid, kThreads, smem, s>>>(amap, xmap, jo_indptr, h.indices.p, rowmap,
                                                      h.nblocks, x_rows, y_rows, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
+}
+
+// rows of a stored-row view: stored[i] = block rows with >= 1 block, jptr = compressed indptr
+__global__ void dbsr_rows_kernel(const int32_t* __restrict__ bp, long long mb,
+                                 const long long* __restrict__ pos, int32_t* __restrict__ stored,
+                                 int32_t* __restrict__ jptr) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < mb && bp[r + 1] > bp[r]) {
+    stored[pos[r]] = static_cast<int32_t>(r);
+    jptr[pos[r] + 1] = bp[r + 1];
+  }
+  if (r == 0) jptr[0] = 0;
+}
+
+__global__ void nonempty_kernel(const int32_t* __restrict__ bp, long long mb, long long* __restrict__ f) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < mb) f[r] = bp[r + 1] > bp[r] ? 1 : 0;
+  if (r == mb) f[r] = 0;
 }
 
 void require_device_bsr() {
@@ -440,10 +473,10 @@ int strata_bsr_spmm_bf16_batched(const strata_bsr* h, const void* values_bf16, c
       return;
     }
     switch (d) {
-      case 64: launch_bsr<64>(*h, V, heads, X, Y, s); break;
-      case 128: launch_bsr<128>(*h, V, heads, X, Y, s); break;
-      case 256: launch_bsr<256>(*h, V, heads, X, Y, s); break;
-      case 512: launch_bsr<512>(*h, V, heads, X, Y, s); break;
+      case 64: launch_bsr<64>(*h, V, heads, X, Y, s, h->indptr.p, nullptr, h->mb); break;
+      case 128: launch_bsr<128>(*h, V, heads, X, Y, s, h->indptr.p, nullptr, h->mb); break;
+      case 256: launch_bsr<256>(*h, V, heads, X, Y, s, h->indptr.p, nullptr, h->mb); break;
+      case 512: launch_bsr<512>(*h, V, heads, X, Y, s, h->indptr.p, nullptr, h->mb); break;
     }
   });
 }
@@ -451,6 +484,93 @@ int strata_bsr_spmm_bf16_batched(const strata_bsr* h, const void* values_bf16, c
 int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int64_t d,
                          void* stream) {
   return strata_bsr_spmm_bf16_batched(h, nullptr, X_bf16, Y, 1, d, stream);
+}
+
+int strata_dbsr_from_csr(const int32_t* indptr, const int32_t* indices, const float* values,
+                         int64_t rows, int64_t cols, int64_t nnz, int64_t b, void* stream,
+                         strata_dbsr** out) {
+  return guard_bsr([&] {
+    if (!out) throw ApiError(STRATA_ERR_USAGE, "null output handle");
+    *out = nullptr;
+    strata_bsr* bsr = nullptr;
+    const int rc = strata_bsr_from_csr(indptr, indices, values, rows, cols, nnz, b, stream, &bsr);
+    if (rc != STRATA_OK) throw ApiError(rc, strata_last_error());
+    auto h = std::make_unique<strata_dbsr>();
+    h->bsr = bsr;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const long long mb = bsr->mb;
+    DevBuf<long long> flag(mb + 1), pos(mb + 1);
+    const unsigned g = static_cast<unsigned>((mb + 1 + 255) / 256);
+    nonempty_kernel<<<g, 256, 0, s>>>(bsr->indptr.p, mb, flag.p);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos.p, mb + 1, s);
+    DevBuf<unsigned char> tmp(tb);
+    cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, pos.p, mb + 1, s);
+    long long ns = 0;
+    STRATA_CUDA_CHECK(cudaMemcpyAsync(&ns, pos.p + mb, sizeof(ns), cudaMemcpyDeviceToHost, s));
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+    h->nstored = ns;
+    h->stored.alloc(std::max<long long>(ns, 1));
+    h->jptr.alloc(ns + 1);
+    dbsr_rows_kernel<<<g, 256, 0, s>>>(bsr->indptr.p, mb, pos.p, h->stored.p, h->jptr.p);
+    STRATA_CUDA_CHECK(cudaGetLastError());
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+    *out = h.release();
+  });
+}
+
+int strata_dbsr_info(const strata_dbsr* h, int64_t* mb, int64_t* nb, int64_t* b, int64_t* nstored,
+                     int64_t* nblocks, int64_t* pad_slots) {
+  return guard_bsr([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null dbsr handle");
+    if (nstored) *nstored = h->nstored;
+    const int rc = strata_bsr_info(h->bsr, mb, nb, b, nblocks, pad_slots);
+    if (rc != STRATA_OK) throw ApiError(rc, strata_last_error());
+  });
+}
+
+int strata_dbsr_read(const strata_dbsr* h, int32_t* io_indices, int32_t* jo_indptr,
+                     int32_t* jo_indices, float* values) {
+  return guard_bsr([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null dbsr handle");
+    if (io_indices && h->nstored)
+      STRATA_CUDA_CHECK(cudaMemcpy(io_indices, h->stored.p, h->nstored * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost));
+    if (jo_indptr)
+      STRATA_CUDA_CHECK(cudaMemcpy(jo_indptr, h->jptr.p, (h->nstored + 1) * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost));
+    const int rc = strata_bsr_read(h->bsr, nullptr, jo_indices, values);  // same block order
+    if (rc != STRATA_OK) throw ApiError(rc, strata_last_error());
+  });
+}
+
+int strata_dbsr_destroy(strata_dbsr* h) {
+  delete h;
+  return STRATA_OK;
+}
+
+int strata_dbsr_spmm_bf16(const strata_dbsr* h, const void* X_bf16, float* Y, int64_t d,
+                          void* stream) {
+  return guard_bsr([&] {
+    if (!h) throw ApiError(STRATA_ERR_USAGE, "null dbsr handle");
+    const strata_bsr* b = h->bsr;
+    if (b->b != kB) throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: tensor-core path needs b == 32");
+    if (d != 64 && d != 128 && d != 256 && d != 512)
+      throw ApiError(STRATA_ERR_USAGE, "bsr_spmm_bf16: d must be 64, 128, 256 or 512");
+    if (b->mb == 0) return;
+    require_device_bsr();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // Block rows that DBSR does not store are zero (interp.cpp:584-587).
+    if (h->nstored < b->mb) STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * b->mb * kB * d, s));
+    if (h->nstored == 0) return;
+    const auto* X = static_cast<const __nv_bfloat16*>(X_bf16);
+    switch (d) {
+      case 64: launch_bsr<64>(*b, b->vals_bf.p, 1, X, Y, s, h->jptr.p, h->stored.p, h->nstored); break;
+      case 128: launch_bsr<128>(*b, b->vals_bf.p, 1, X, Y, s, h->jptr.p, h->stored.p, h->nstored); break;
+      case 256: launch_bsr<256>(*b, b->vals_bf.p, 1, X, Y, s, h->jptr.p, h->stored.p, h->nstored); break;
+      case 512: launch_bsr<512>(*b, b->vals_bf.p, 1, X, Y, s, h->jptr.p, h->stored.p, h->nstored); break;
+    }
+  });
 }
 
 }  // extern "C"

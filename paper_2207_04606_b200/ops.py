@@ -413,6 +413,104 @@ def bsr_spmm_batched(bsr: BsrMatrix, values_bf16, X_bf16, Y=None, stream=None):
     return Y
 
 
+# ---- DBSR / SR-BCRS (storage.cpp:336-440) ---------------------------------------------------
+
+class DbsrMatrix:
+    """Device DBSR: the BSR of the matrix plus its stored block rows (IO_indices)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        v = [C.c_int64() for _ in range(6)]
+        check(lib.strata_dbsr_info(handle, *(C.byref(x) for x in v)))
+        self.mb, self.nb, self.b, self.nstored, self.nblocks, self.pad_slots = (x.value for x in v)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def arrays(self, prefix: str = "dbsr_") -> dict:
+        io = np.empty(max(self.nstored, 1), np.int32)
+        jp = np.empty(self.nstored + 1, np.int32)
+        ji = np.empty(max(self.nblocks, 1), np.int32)
+        bv = np.empty(max(self.nblocks * self.b * self.b, 1), np.float32)
+        check(lib.strata_dbsr_read(self._h, io.ctypes.data, jp.ctypes.data, ji.ctypes.data,
+                                   bv.ctypes.data))
+        return {prefix + "IO_indptr": np.array([0, self.nstored], np.int32),
+                prefix + "IO_indices": io[:self.nstored], prefix + "JO_indptr": jp,
+                prefix + "JO_indices": ji[:self.nblocks],
+                "values": bv[:self.nblocks * self.b * self.b]}
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.strata_dbsr_destroy(self._h)
+            self._h = None
+
+
+def csr_to_dbsr(csr: DeviceCsr, b: int, stream=None) -> DbsrMatrix:
+    h = C.c_void_p()
+    check(lib.strata_dbsr_from_csr(_ptr(csr.indptr), _ptr(csr.indices), _ptr(csr.values), csr.rows,
+                                   csr.cols, csr.nnz, b, _stream(stream), C.byref(h)))
+    return DbsrMatrix(h)
+
+
+def dbsr_spmm(dbsr: DbsrMatrix, X_bf16, Y=None, stream=None):
+    """Y[mb*b][d] (f32) = A_dbsr @ X on tcgen05 (stored block rows only)."""
+    import torch
+    d = X_bf16.shape[1]
+    if Y is None:
+        Y = torch.empty((dbsr.mb * dbsr.b, d), dtype=torch.float32, device=X_bf16.device)
+    check(lib.strata_dbsr_spmm_bf16(dbsr.handle, _ptr(X_bf16), _ptr(Y), d, _stream(stream)))
+    return Y
+
+
+class SrbcrsMatrix:
+    """Device SR-BCRS(t, g): G_indptr / JT_indices / slot-major values."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        v = [C.c_int64() for _ in range(5)]
+        check(lib.strata_srbcrs_info(handle, *(C.byref(x) for x in v)))
+        self.mb, self.t, self.g, self.groups, self.pad_slots = (x.value for x in v)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def arrays(self, prefix: str = "srbcrs_") -> dict:
+        gp = np.empty(self.mb + 1, np.int32)
+        jt = np.empty(max(self.groups * self.g, 1), np.int32)
+        v = np.empty(max(self.groups * self.g * self.t, 1), np.float32)
+        check(lib.strata_srbcrs_read(self._h, gp.ctypes.data, jt.ctypes.data, v.ctypes.data))
+        return {prefix + "G_indptr": gp, prefix + "JT_indices": jt[:self.groups * self.g],
+                "values": v[:self.groups * self.g * self.t]}
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.strata_srbcrs_destroy(self._h)
+            self._h = None
+
+
+def csr_to_srbcrs(csr: DeviceCsr, t: int, g: int, stream=None) -> SrbcrsMatrix:
+    h = C.c_void_p()
+    check(lib.strata_srbcrs_from_csr(_ptr(csr.indptr), _ptr(csr.indices), _ptr(csr.values),
+                                     csr.rows, csr.cols, csr.nnz, t, g, _stream(stream), C.byref(h)))
+    return SrbcrsMatrix(h)
+
+
+def srbcrs_spmm(sr: SrbcrsMatrix, X_bf16, Y=None, stream=None):
+    """Y[mb*t][d] (f32) = A_srbcrs @ X on tcgen05 (t = 8, g = 32)."""
+    import torch
+    d = X_bf16.shape[1]
+    if Y is None:
+        Y = torch.empty((sr.mb * sr.t, d), dtype=torch.float32, device=X_bf16.device)
+    check(lib.strata_srbcrs_spmm_bf16(sr.handle, _ptr(X_bf16), _ptr(Y), d, _stream(stream)))
+    return Y
+
+
+__all__ += ["DbsrMatrix", "csr_to_dbsr", "dbsr_spmm", "SrbcrsMatrix", "csr_to_srbcrs",
+            "srbcrs_spmm"]
+
+
 # ---- ELL (storage.hpp:124, storage.cpp:190-227) --------------------------------------------
 
 def csr_to_ell(csr: DeviceCsr, w: int, stream=None):

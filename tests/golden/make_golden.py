@@ -113,6 +113,40 @@ def main():
         out[key + "/X"] = X.astype(np.float32)
         out[key + "/Y"] = pl.run().astype(np.float32).reshape(-1, d)
 
+    # DBSR (storage.cpp:336-370) and SR-BCRS (storage.cpp:372-440): arrays + the reference's
+    # SpMM pipeline output for the tensor-core shapes (b = 32; t = 8, g = 32)
+    for name, coo in [("example", example_coo()),
+                      ("bs128", ref.Coo.generate("blocksparse", 128, 96, 0.3, 0, 32, 0, 1)),
+                      ("pl", ref.Coo.generate("powerlaw", 300, 250, 0, 0, 0, 6.0, 5))]:
+        csr = ref.Storage.csr(coo)
+        ip, ix, v = csr_arrays(csr)
+        out[f"fmt/{name}/csr"] = np.concatenate([[csr.rows, csr.cols], ip]).astype(np.int64)
+        out[f"fmt/{name}/indices"], out[f"fmt/{name}/values"] = ix, v
+        for b in (2, 32):
+            db = csr.to_dbsr(b)
+            key = f"dbsr/{name}_b{b}"
+            out[key + "/IO_indices"] = db.aux("IO_indices")
+            out[key + "/JO_indptr"] = db.aux("JO_indptr")
+            out[key + "/JO_indices"] = db.aux("JO_indices")
+            out[key + "/values"] = db.values().astype(np.float32)
+            out[key + "/shape"] = np.array([db.rows, db.cols, db.pad_slots], np.int64)
+        for t, g in ((2, 2), (3, 5), (8, 32)):
+            sr = csr.to_srbcrs(t, g)
+            key = f"srbcrs/{name}_t{t}_g{g}"
+            out[key + "/G_indptr"] = sr.aux("G_indptr")
+            out[key + "/JT_indices"] = sr.aux("JT_indices")
+            out[key + "/values"] = sr.values().astype(np.float32)
+            out[key + "/shape"] = np.array([sr.rows, sr.cols, sr.pad_slots], np.int64)
+        d = 64
+        for fmt in ("dbsr:b=32", "srbcrs:t=8,g=32"):
+            pl = ref.Pipeline.matrix("spmm", coo, d, ref.F32, fmt)
+            rows_x = -(-csr.cols // 32) * 32 if fmt.startswith("dbsr") else csr.cols  # pad_for_format
+            X = ref.dense_int(rows_x * d, 11).reshape(rows_x, d)
+            pl.set("X", X)
+            key = f"fmtspmm/{name}/{fmt.split(':')[0]}"
+            out[key + "/X"] = X.astype(np.float32)
+            out[key + "/Y"] = pl.run().astype(np.float32).reshape(-1, d)
+
     # RGMS: power-law graph split into relations (strata_cli.cpp:70-82), csr and hyb formats
     base = ref.Coo.generate("powerlaw", 400, 400, 0, 0, 0, 3.0, 1)
     R = 5
