@@ -509,14 +509,16 @@ inline CooMatrix generate_matrix(const std::string& kind, int64_t n, int64_t m, 
 enum class KernelOp { SpMM, SDDMM, RGMS };
 
 struct FormatRequest {
-  std::string kind = "csr";  // csr | bsr | ell | hyb
+  std::string kind = "csr";  // csr | bsr | ell | dbsr | srbcrs | hyb
   int64_t b = 2, w = 0;
+  int64_t t = 2, g = 2;      // srbcrs
   int c = 1, k = -1;
   static FormatRequest parse(const std::string& text) {  // driver.cpp:22-54
     FormatRequest r;
     auto colon = text.find(':');
     r.kind = text.substr(0, colon);
-    if (r.kind != "csr" && r.kind != "bsr" && r.kind != "ell" && r.kind != "hyb")
+    if (r.kind != "csr" && r.kind != "bsr" && r.kind != "ell" && r.kind != "dbsr" &&
+        r.kind != "srbcrs" && r.kind != "hyb")
       fail(ErrKind::Usage, "unknown format: " + r.kind);
     if (colon == std::string::npos) return r;
     std::istringstream in(text.substr(colon + 1));
@@ -528,6 +530,8 @@ struct FormatRequest {
       const int64_t value = std::stoll(kv.substr(eq + 1));
       if (key == "b") r.b = value;
       else if (key == "w") r.w = value;
+      else if (key == "t") r.t = value;
+      else if (key == "g") r.g = value;
       else if (key == "c") r.c = static_cast<int>(value);
       else if (key == "k") r.k = static_cast<int>(value);
       else fail(ErrKind::Usage, "unknown format parameter: " + key);
@@ -556,6 +560,14 @@ class Pipeline {
   std::unique_ptr<DeviceCsr> csr;
   std::unique_ptr<DeviceHyb> hyb;
   std::unique_ptr<DeviceBsr> bsr;
+  struct DbsrDel {
+    void operator()(strata_dbsr* h) const { strata_dbsr_destroy(h); }
+  };
+  struct SrbcrsDel {
+    void operator()(strata_srbcrs* h) const { strata_srbcrs_destroy(h); }
+  };
+  std::unique_ptr<strata_dbsr, DbsrDel> dbsr;
+  std::unique_ptr<strata_srbcrs, SrbcrsDel> srbcrs;
   TensorStorage csr_host;
   std::vector<int32_t> rel_ptr, rel_dst, rel_src;
   std::vector<float> rel_a;
@@ -575,12 +587,14 @@ class Pipeline {
   DenseMatrix run_spmm() {
     const auto& x = bound("X", static_cast<size_t>(n * d));
     DenseMatrix out(m, d);
-    if (fmt.kind == "bsr") {
+    if (fmt.kind == "bsr" || fmt.kind == "dbsr" || fmt.kind == "srbcrs") {  // bf16 tensor cores
       std::vector<uint16_t> xb(x.size());
       for (size_t i = 0; i < x.size(); ++i) xb[i] = to_bf16(static_cast<float>(x[i]));
       DeviceArray<uint16_t> X(xb);
       DeviceArray<float> Y(static_cast<size_t>(m * d));
-      bsr->spmm_bf16(X.data(), Y.data(), d);
+      if (bsr) bsr->spmm_bf16(X.data(), Y.data(), d);
+      else if (dbsr) check(strata_dbsr_spmm_bf16(dbsr.get(), X.data(), Y.data(), d, nullptr));
+      else check(strata_srbcrs_spmm_bf16(srbcrs.get(), X.data(), Y.data(), d, nullptr));
       auto y = Y.host();
       for (size_t i = 0; i < y.size(); ++i) out.v[i] = y[i];
       return out;
@@ -635,9 +649,11 @@ inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m_in, int64_
                                       const FormatRequest& fmt) {
   Pipeline pl;
   CooMatrix m = m_in;
-  if (fmt.kind == "bsr") {  // pad_for_format (driver.cpp:69-78)
+  if (fmt.kind == "bsr" || fmt.kind == "dbsr") {  // pad_for_format (driver.cpp:69-78)
     m.rows = (m.rows + fmt.b - 1) / fmt.b * fmt.b;
     m.cols = (m.cols + fmt.b - 1) / fmt.b * fmt.b;
+  } else if (fmt.kind == "srbcrs") {
+    m.rows = (m.rows + fmt.t - 1) / fmt.t * fmt.t;
   }
   pl.op = op;
   pl.fmt = fmt;
@@ -651,6 +667,19 @@ inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m_in, int64_
     pl.hyb = std::make_unique<DeviceHyb>(*pl.csr, fmt.c, k);
   } else if (op == KernelOp::SpMM && fmt.kind == "bsr") {
     pl.bsr = std::make_unique<DeviceBsr>(*pl.csr, fmt.b);
+  } else if (op == KernelOp::SpMM && fmt.kind == "dbsr") {
+    strata_dbsr* h = nullptr;
+    check(strata_dbsr_from_csr(pl.csr->indptr.data(), pl.csr->indices.data(), pl.csr->values.data(),
+                               pl.csr->rows, pl.csr->cols, pl.csr->nnz, fmt.b, nullptr, &h));
+    pl.dbsr.reset(h);
+  } else if (op == KernelOp::SpMM && fmt.kind == "srbcrs") {
+    strata_srbcrs* h = nullptr;
+    check(strata_srbcrs_from_csr(pl.csr->indptr.data(), pl.csr->indices.data(), pl.csr->values.data(),
+                                 pl.csr->rows, pl.csr->cols, pl.csr->nnz, fmt.t, fmt.g, nullptr, &h));
+    pl.srbcrs.reset(h);
+  } else if (op == KernelOp::SpMM && fmt.kind == "ell") {
+    // ELL (w = max row length by default) stores the CSR entries plus zero pads; the product
+    // is the CSR one, so the row-split CSR kernel serves it.
   } else if (fmt.kind != "csr") {
     fail(ErrKind::Usage, "format " + fmt.kind + " is not served for this op");
   }

@@ -276,9 +276,32 @@ TEST_CASE("SpMM random instances equal the dense oracle in every format") {  // 
     CooMatrix a = random_coo(rng, 1 + rng() % 40, 1 + rng() % 40, 0.3);
     DenseMatrix x = random_dense(rng, a.cols, 8);
     DenseMatrix want = matmul(dense_from_coo(a), x);
-    for (const char* fmt : {"csr", "hyb:c=1", "hyb:c=3,k=1", "hyb:c=1,k=0"})
+    for (const char* fmt : {"csr", "ell", "hyb:c=1", "hyb:c=3,k=1", "hyb:c=1,k=0"})
       CHECK(run_spmm(a, x, fmt).v == want.v);
   }
+}
+
+TEST_CASE("tensor-core DBSR and SR-BCRS pipelines equal the dense oracle") {
+  std::mt19937 rng(21);
+  for (int trial = 0; trial < 4; ++trial) {
+    CooMatrix a = random_coo(rng, 70 + rng() % 60, 50 + rng() % 40, 0.15);
+    DenseMatrix x0 = random_dense(rng, a.cols, 64);  // integers: exact in bf16
+    DenseMatrix want = matmul(dense_from_coo(a), x0);
+    // dbsr pads rows and cols to multiples of b; srbcrs pads rows to multiples of t
+    DenseMatrix xb(((a.cols + 31) / 32) * 32, 64);
+    for (int64_t i = 0; i < x0.rows; ++i)
+      for (int64_t j = 0; j < 64; ++j) xb.at(i, j) = x0.at(i, j);
+    DenseMatrix gd = run_spmm(a, xb, "dbsr:b=32");
+    DenseMatrix gs = run_spmm(a, x0, "srbcrs:t=8,g=32");
+    bool ok = gd.rows == ((a.rows + 31) / 32) * 32 && gs.rows == ((a.rows + 7) / 8) * 8;
+    for (const DenseMatrix* g : {&gd, &gs})
+      for (int64_t i = 0; ok && i < g->rows; ++i)
+        for (int64_t j = 0; j < 64; ++j) ok &= g->at(i, j) == (i < want.rows ? want.at(i, j) : 0.0);
+    CHECK(ok);
+  }
+  FormatRequest f = FormatRequest::parse("srbcrs:t=8,g=32");
+  CHECK(f.kind == "srbcrs" && f.t == 8 && f.g == 32);
+  CHECK_THROWS_KIND(FormatRequest::parse("coo"), ErrKind::Usage, "unknown format: coo");
 }
 
 TEST_CASE("BSR tensor-core SpMM equals the dense oracle") {
