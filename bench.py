@@ -361,6 +361,27 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
                                  "tensor_frac": round(flops_h / (msh * 1e-3) / 1e12 / bf16_peak, 5),
                                  "hbm_frac": round(b_alg_h / (msh * 1e-3) / 1e9 / hbm_peak, 4),
                                  "bytes_model": "heads*(blocks*2KB + blocks*32*d*2 + 4096*d*4)"}
+    # Pruned-weight formats: a 4096 x 4096 power-law weight (avg 64 per
+    # row) as SR-BCRS(8, 32) and a 2 %-dense block mask as DBSR(32), d = 128, tcgen05.
+    wm = S.generate_matrix("powerlaw", 4096, 4096, 0, 0, 0, 64.0, 3)
+    sr = S.csr_to_srbcrs(wm.to_device(dev), 8, 32)
+    Xw = torch.randint(-3, 4, (4096, 128), device=dev).to(torch.bfloat16)
+    Yw = torch.empty((sr.mb * 8, 128), device=dev)
+    ms_sr = _time_graph_ms(torch, lambda: S.srbcrs_spmm(sr, Xw, Yw))
+    slots = sr.groups * 32 * 8
+    out["srbcrs_8_32_spmm"] = {"ms": round(ms_sr, 5), "nnz": wm.nnz, "stored_slots": slots,
+                               "gflops_useful": round(2.0 * wm.nnz * 128 / (ms_sr * 1e-3) / 1e9, 1),
+                               "tensor_tflops_issued": round(2.0 * sr.groups * 32 * 16 * 128 / (ms_sr * 1e-3) / 1e12, 2),
+                               "timing": "CUDA graph of 20 calls"}
+    bm = S.generate_matrix("blocksparse", 8192, 8192, 0.02, 0, 32, 0, 4)
+    db = S.csr_to_dbsr(bm.to_device(dev), 32)
+    Xd = torch.randint(-3, 4, (8192, 128), device=dev).to(torch.bfloat16)
+    Yd2 = torch.empty((8192, 128), device=dev)
+    ms_db = _time_graph_ms(torch, lambda: S.dbsr_spmm(db, Xd, Yd2))
+    out["dbsr_32_spmm"] = {"ms": round(ms_db, 5), "blocks": db.nblocks, "stored_block_rows": db.nstored,
+                           "block_rows": db.mb,
+                           "gflops": round(2.0 * db.nblocks * 1024 * 128 / (ms_db * 1e-3) / 1e9, 1),
+                           "timing": "CUDA graph of 20 calls"}
     # C4: AM-shaped power-law graph split into 133 relations, d_in = d_out = 32.
     g = S.generate_matrix("powerlaw", 1885136, 1885136, 0, 0, 0, 3.0051, 1)
     rel = S.split_relations(g, 133, 1).to_device(dev)
