@@ -282,6 +282,18 @@ def extra_reddit(S, torch, dev, stream, peak):
                      "b_alg_gbs": round(gbs, 1), "frac_of_hbm": round(gbs / peak, 3),
                      "note": "X is L2-resident (59.6 MB < 126 MB L2): frac is L2-assisted"}
     out["reddit_nnz"] = m.nnz
+    # Fused SDDMM -> edge softmax -> SpMM (GAT-style layer step), d = 64.
+    plan = S.AttentionPlan(dcsr)
+    Qa = torch.randn(m.rows, d, device=dev) * 0.1
+    Ka = torch.randn(m.cols, d, device=dev) * 0.1
+    Va = torch.randn(m.cols, d, device=dev)
+    Za = torch.empty((m.rows, d), device=dev)
+    ms_a = _time_ms(torch, stream, lambda: plan(Qa, Ka, Va, Za), reps=10)
+    b_a = m.nnz * 8 + 2.0 * m.nnz * d * 4 + 2.0 * m.rows * d * 4 + (m.rows + 1) * 4
+    out["reddit_fused_attention"] = {
+        "ms": round(ms_a, 4), "gflops": round(4.0 * m.nnz * d / (ms_a * 1e-3) / 1e9, 1),
+        "b_alg_gbs": round(b_a / (ms_a * 1e-3) / 1e9, 1),
+        "note": "one pass (online softmax); K, V rows gathered per edge, L2-resident at C2"}
     # The reference tuner's c-grid (tune.cpp:19-36) on the device: hyb(c in 1..16) timed, gated
     # bitwise against the CSR format on integer operands (CSR itself is left out: its
     # row-per-warp schedule is the load-imbalanced baseline, 51 ms here).

@@ -275,6 +275,23 @@ int strata_rgms_run_bf16(const strata_rgms* h, const void* X_bf16, const void* W
 int strata_rgms_info(const strata_rgms* h, int64_t* tiles_bound, int64_t* t_bytes_per_dout);
 int strata_rgms_destroy(strata_rgms* h);
 
+/* ---- fused attention layer step (GAT-style) --------------------------
+ * SDDMM -> row softmax -> SpMM in one pass over each row's edges (online softmax):
+ *   s_ij = A_ij <Q_i, K_j>,  a_ij = softmax_j(s_ij) over the stored j of row i,
+ *   Z_i = sum_j a_ij V_j     (Z_i = 0 for an empty row).
+ * Q[m][d], K[n][d], V[n][d], Z[m][d] f32 row-major, d in {32, 64, 128}.  The plan (built once
+ * per sparsity pattern, one host sync) splits rows longer than 256 edges into chunks merged by
+ * a log-sum-exp pass.  Composes the reference's SDDMM (kernels.cpp:110-136) and SpMM
+ * (kernels.cpp:85-108) nests with a softmax between them; neither scores nor weights are
+ * written to HBM. */
+typedef struct strata_attn_plan strata_attn_plan;
+int strata_attn_plan_create(const int32_t* indptr, int64_t m, int64_t nnz, strata_attn_plan** out,
+                            void* stream);
+int strata_attn_plan_destroy(strata_attn_plan* p);
+int strata_attn_csr_f32(const strata_attn_plan* p, const int32_t* indptr, const int32_t* indices,
+                        const float* A, const float* Q, const float* K, const float* V, float* Z,
+                        int64_t d, void* stream);
+
 /* ---- multi-GPU helpers (host logic, no device work) -----------------------------------
  * Row-partition into `parts` contiguous row ranges balanced by nnz: cut p is the first row
  * r with indptr[r] >= nnz*p/parts (binary search on the HOST indptr).  bounds[parts+1]. */

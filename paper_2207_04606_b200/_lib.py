@@ -105,6 +105,9 @@ _sig("strata_srbcrs_info", C.c_int, vp, i64p, i64p, i64p, i64p, i64p)
 _sig("strata_srbcrs_read", C.c_int, vp, vp, vp, vp)
 _sig("strata_srbcrs_destroy", C.c_int, vp)
 _sig("strata_srbcrs_spmm_bf16", C.c_int, vp, vp, vp, i64, vp)
+_sig("strata_attn_plan_create", C.c_int, vp, i64, i64, C.POINTER(vp), vp)
+_sig("strata_attn_plan_destroy", C.c_int, vp)
+_sig("strata_attn_csr_f32", C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp)
 _sig("strata_csr_from_coo", C.c_int, vp, vp, vp, i64, i64, i64, vp, vp, vp, vp)
 _sig("strata_ell_from_csr", C.c_int, vp, vp, vp, i64, i64, i64, vp, vp, vp)
 _sig("strata_rgms_bf16", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp, vp, i64, i64, vp)
@@ -131,7 +134,8 @@ EXPORTED = [
     "strata_bsr_spmm_bf16_batched", "strata_csr_from_coo",
     "strata_dbsr_from_csr", "strata_dbsr_info", "strata_dbsr_read", "strata_dbsr_destroy",
     "strata_dbsr_spmm_bf16", "strata_srbcrs_from_csr", "strata_srbcrs_info", "strata_srbcrs_read",
-    "strata_srbcrs_destroy", "strata_srbcrs_spmm_bf16", "strata_ell_from_csr",
+    "strata_srbcrs_destroy", "strata_srbcrs_spmm_bf16", "strata_attn_plan_create",
+    "strata_attn_plan_destroy", "strata_attn_csr_f32", "strata_ell_from_csr",
     "strata_rgms_bf16", "strata_rgms_plan", "strata_rgms_run_bf16", "strata_rgms_info",
     "strata_rgms_destroy", "strata_partition_rows",
 ]

@@ -511,6 +511,39 @@ __all__ += ["DbsrMatrix", "csr_to_dbsr", "dbsr_spmm", "SrbcrsMatrix", "csr_to_sr
             "srbcrs_spmm"]
 
 
+# ---- fused attention layer step (SDDMM -> edge softmax -> SpMM) ------------------------------
+
+class AttentionPlan:
+    """Row/chunk work plan of a CSR pattern for ``attention`` (strata_attn_plan_create)."""
+
+    def __init__(self, csr: DeviceCsr, stream=None):
+        self.csr = csr
+        h = C.c_void_p()
+        check(lib.strata_attn_plan_create(_ptr(csr.indptr), csr.rows, csr.nnz, C.byref(h),
+                                          _stream(stream)))
+        self._h = h
+
+    def __call__(self, Q, K, V, Z=None, stream=None):
+        """Z[i] = sum_j softmax_j(A_ij <Q_i, K_j>) V_j over the stored j of row i."""
+        import torch
+        d = int(Q.shape[1])
+        if Z is None:
+            Z = torch.empty((self.csr.rows, d), dtype=torch.float32, device=Q.device)
+        check(lib.strata_attn_csr_f32(self._h, _ptr(self.csr.indptr), _ptr(self.csr.indices),
+                                      _ptr(self.csr.values), _ptr(Q), _ptr(K), _ptr(V), _ptr(Z), d,
+                                      _stream(stream)))
+        return Z
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.strata_attn_plan_destroy(h)
+            self._h = None
+
+
+__all__ += ["AttentionPlan"]
+
+
 # ---- ELL (storage.hpp:124, storage.cpp:190-227) --------------------------------------------
 
 def csr_to_ell(csr: DeviceCsr, w: int, stream=None):
