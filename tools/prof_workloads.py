@@ -1,5 +1,5 @@
 """Run one BASELINE workload a few times (for ncu captures): python tools/prof_workloads.py
-{products|reddit_spmm|reddit_sddmm|bsr|bsr12|rgcn} [reps]"""
+{products|reddit_spmm|reddit_sddmm|bsr|bsr12|rgcn|srbcrs|attention} [reps]"""
 import os
 import sys
 
@@ -40,6 +40,18 @@ def main():
         V = torch.randint(1, 10, (12, bs.nblocks, 32, 32), device=dev).to(torch.bfloat16)
         X = torch.randint(-3, 4, (12, 4096, 64), device=dev).to(torch.bfloat16)
         fn = lambda: S.bsr_spmm_batched(bs, V, X)
+    elif which == "srbcrs":  # pruned-weight SR-BCRS(8, 32), d = 128
+        m = S.generate_matrix("powerlaw", 4096, 4096, 0, 0, 0, 64.0, 3)
+        sr = S.csr_to_srbcrs(m.to_device(dev), 8, 32)
+        X = torch.randint(-3, 4, (4096, 128), device=dev).to(torch.bfloat16)
+        fn = lambda: S.srbcrs_spmm(sr, X)
+    elif which == "attention":  # fused SDDMM -> softmax -> SpMM at C2, d = 64
+        m = S.generate_matrix("powerlaw", 232965, 232965, 0, 0, 0, 567.5267, 1)
+        plan = S.AttentionPlan(m.to_device(dev))
+        Q = torch.randn(m.rows, 64, device=dev) * 0.1
+        K = torch.randn(m.cols, 64, device=dev) * 0.1
+        V = torch.randn(m.cols, 64, device=dev)
+        fn = lambda: plan(Q, K, V)
     elif which == "rgcn":
         m = S.generate_matrix("powerlaw", 1885136, 1885136, 0, 0, 0, 3.0051, 1)
         plan = S.RgmsPlan(S.split_relations(m, 133, 1).to_device(dev))
