@@ -423,9 +423,10 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
                                  "tensor_frac": round(flops_h / (msh * 1e-3) / 1e12 / bf16_peak, 5),
                                  "hbm_frac": round(b_alg_h / (msh * 1e-3) / 1e9 / hbm_peak, 4),
                                  "bytes_model": "heads*(blocks*2KB + blocks*32*d*2 + 4096*d*4)"}
-    # Pruned-weight formats: a 4096 x 4096 power-law weight (avg 64 per
-    # row) as SR-BCRS(8, 32) and a 2 %-dense block mask as DBSR(32), d = 128, tcgen05.
-    wm = S.generate_matrix("powerlaw", 4096, 4096, 0, 0, 0, 64.0, 3)
+    # Pruned-weight formats: a 4096 x 4096 weight pruned
+    # to 5 % density (unstructured, "random") as SR-BCRS(8, 32) and a 2 %-dense block mask as
+    # DBSR(32), d = 128, tcgen05.
+    wm = S.generate_matrix("random", 4096, 4096, 0.05, 0, 0, 0, 3)
     sr = S.csr_to_srbcrs(wm.to_device(dev), 8, 32)
     Xw = torch.randint(-3, 4, (4096, 128), device=dev).to(torch.bfloat16)
     Yw = torch.empty((sr.mb * 8, 128), device=dev)

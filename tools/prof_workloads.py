@@ -40,8 +40,8 @@ def main():
         V = torch.randint(1, 10, (12, bs.nblocks, 32, 32), device=dev).to(torch.bfloat16)
         X = torch.randint(-3, 4, (12, 4096, 64), device=dev).to(torch.bfloat16)
         fn = lambda: S.bsr_spmm_batched(bs, V, X)
-    elif which == "srbcrs":  # pruned-weight SR-BCRS(8, 32), d = 128
-        m = S.generate_matrix("powerlaw", 4096, 4096, 0, 0, 0, 64.0, 3)
+    elif which == "srbcrs":  # pruned-weight SR-BCRS(8, 32) (5 % unstructured), d = 128
+        m = S.generate_matrix("random", 4096, 4096, 0.05, 0, 0, 0, 3)
         sr = S.csr_to_srbcrs(m.to_device(dev), 8, 32)
         X = torch.randint(-3, 4, (4096, 128), device=dev).to(torch.bfloat16)
         fn = lambda: S.srbcrs_spmm(sr, X)
