@@ -344,11 +344,10 @@ def extra_reddit(S, torch, dev, stream, peak):
         "ms": round(ms_a, 4), "gflops": round(4.0 * m.nnz * d / (ms_a * 1e-3) / 1e9, 1),
         "b_alg_gbs": round(b_a / (ms_a * 1e-3) / 1e9, 1),
         "note": "one pass (online softmax); K, V rows gathered per edge, L2-resident at C2"}
-    # The reference tuner's c-grid (tune.cpp:19-36) on the device: hyb(c in 1..16) timed, gated
-    # bitwise against the CSR format on integer operands (CSR itself is left out: its
-    # row-per-warp schedule is the load-imbalanced baseline, 51 ms here).
+    # The reference tuner's c-grid (tune.cpp:19-36) on the device: csr + hyb(c in 1..16) timed,
+    # gated bitwise against the CSR format on integer operands.
     from paper_2207_04606_b200 import tune as T
-    rep = T.run_trials("spmm", m, d, T.SearchSpace.hyb_c_grid(include_csr=False), repeats=5, warmup=2)
+    rep = T.run_trials("spmm", m, d, T.SearchSpace.hyb_c_grid(), repeats=5, warmup=2)
     out["reddit_tuner"] = {"best": rep.trials[rep.best].point.format,
                            "ms": {t.point.format: round(t.median_ns / 1e6, 4) for t in rep.trials},
                            "all_correct": all(t.correct for t in rep.trials)}

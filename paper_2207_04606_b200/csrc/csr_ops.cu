@@ -17,6 +17,8 @@
 //    a butterfly reduce-scatter (L-1 shuffles for L results, PAPER.md:442's two-stage
 //    reduction) leaves non-zero t's full dot product in lane t, which scales by A and stores
 //    B coalesced.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 
 #include "capi_internal.h"
@@ -29,6 +31,9 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kNnzPerChunk = 256;
+constexpr long long kCsrLong = 2048;  // row-split CSR SpMM: longer rows are chunked
+constexpr long long kCsrChunk = 256;  // non-zeros per chunk of a long row
+constexpr long long kCsrGroup = 64;   // chunk partials summed per level-1 group
 
 __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out,
                                  long long rows, long long cols) {
@@ -184,6 +189,7 @@ spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ 
   const long long r = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
   if (r >= rows) return;
   const long long q0 = __ldg(indptr + r), q1 = __ldg(indptr + r + 1);
+  if (q1 - q0 > kCsrLong) return;  // long row: spmm_csr_chunk_kernel + the two merge levels
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (long long g = q0; g < q1; g += L) {
     const long long q = g + lane;
@@ -205,6 +211,111 @@ spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ 
     }
   }
   st_stream4(reinterpret_cast<float4*>(Y + r * d) + lane, acc);
+}
+
+// ---- long rows of the row-split CSR SpMM --------------------------------------------------
+// A power-law hub row (C5: 1.8 M non-zeros) would serialise one virtual warp for milliseconds.
+// Rows longer than kCsrLong are cut into kCsrChunk-non-zero chunks (one VW each, f32 partial
+// in non-zero order); level 1 sums up to kCsrGroup consecutive chunk partials of a row, level
+// 2 sums a row's level-1 partials — fixed shapes and orders, so the result is deterministic.
+// All counts stay on the device (grid-stride over an upper bound): no host synchronisation.
+struct CsrLongPlan {
+  long long* coff;   // [rows + 1] exclusive scan of chunks per row (0 for short rows)
+  long long* goff;   // [rows + 1] exclusive scan of level-1 groups per row
+};
+
+__global__ void csr_long_counts_kernel(const int32_t* __restrict__ indptr, long long rows,
+                                       long long* __restrict__ nch, long long* __restrict__ ngr) {
+  for (long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; r <= rows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long len = r < rows ? indptr[r + 1] - indptr[r] : 0;
+    const long long c = len > kCsrLong ? (len + kCsrChunk - 1) / kCsrChunk : 0;
+    nch[r] = c;
+    ngr[r] = (c + kCsrGroup - 1) / kCsrGroup;
+  }
+}
+
+// owner of item c: last r with off[r] <= c (off non-decreasing, off[rows] = total)
+__device__ __forceinline__ long long owner_row(const long long* __restrict__ off, long long rows,
+                                               long long c) {
+  long long lo = 0, hi = rows;
+  while (hi - lo > 1) {
+    const long long mid = (lo + hi) >> 1;
+    if (off[mid] <= c) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int L>
+__global__ void __launch_bounds__(kBlock)
+spmm_csr_chunk_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                      const float* __restrict__ A, const float* __restrict__ X,
+                      const long long* __restrict__ coff, long long rows, float* __restrict__ part) {
+  constexpr int U = 8, D = 4 * L;
+  const int lane = threadIdx.x & (L - 1);
+  const long long nvw = static_cast<long long>(gridDim.x) * kBlock / L;
+  const long long total = coff[rows];
+  for (long long c = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L; c < total;
+       c += nvw) {
+    const long long r = owner_row(coff, rows, c);
+    const long long q0 = indptr[r] + (c - coff[r]) * kCsrChunk;
+    const long long q1 = min64(q0 + kCsrChunk, static_cast<long long>(indptr[r + 1]));
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long g = q0; g < q1; g += U) {
+      float4 xv[U];
+      float vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (g + u < q1) {
+          const int32_t cu = __ldg(indices + g + u);
+          vv[u] = __ldg(A + g + u);
+          xv[u] = ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(cu) * D) + lane);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (g + u < q1) fma4(acc, vv[u], xv[u]);
+    }
+    reinterpret_cast<float4*>(part + c * D)[lane] = acc;
+  }
+}
+
+// level 1: group g of a row sums chunk partials [first, first + kCsrGroup) of that row, in order
+template <int L>
+__global__ void __launch_bounds__(kBlock)
+spmm_csr_group_kernel(const long long* __restrict__ coff, const long long* __restrict__ goff,
+                      long long rows, const float* __restrict__ part, float* __restrict__ l1) {
+  constexpr int D = 4 * L;
+  const int lane = threadIdx.x & (L - 1);
+  const long long nvw = static_cast<long long>(gridDim.x) * kBlock / L;
+  const long long total = goff[rows];
+  for (long long g = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L; g < total;
+       g += nvw) {
+    const long long r = owner_row(goff, rows, g);
+    const long long c0 = coff[r] + (g - goff[r]) * kCsrGroup;
+    const long long c1 = min64(c0 + kCsrGroup, coff[r + 1]);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long c = c0; c < c1; ++c) acc = add4(acc, reinterpret_cast<const float4*>(part + c * D)[lane]);
+    reinterpret_cast<float4*>(l1 + g * D)[lane] = acc;
+  }
+}
+
+// level 2: one VW per long row, its level-1 partials in order -> Y row
+template <int L>
+__global__ void __launch_bounds__(kBlock)
+spmm_csr_rowsum_kernel(const long long* __restrict__ goff, long long rows,
+                       const float* __restrict__ l1, float* __restrict__ Y) {
+  constexpr int D = 4 * L;
+  const int lane = threadIdx.x & (L - 1);
+  const long long nvw = static_cast<long long>(gridDim.x) * kBlock / L;
+  for (long long r = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L; r < rows;
+       r += nvw) {
+    const long long g0 = goff[r], g1 = goff[r + 1];
+    if (g1 == g0) continue;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long g = g0; g < g1; ++g) acc = add4(acc, reinterpret_cast<const float4*>(l1 + g * D)[lane]);
+    st_stream4(reinterpret_cast<float4*>(Y + r * D) + lane, acc);
+  }
 }
 
 __global__ void spmm_csr_scalar_kernel(const int32_t* __restrict__ indptr,
@@ -270,15 +381,58 @@ void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float*
   const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(Y) % 16 == 0;
   auto blocks_for = [&](int L) { return static_cast<unsigned>((rows * L + kBlock - 1) / kBlock); };
-  if (aligned && d == 32)
-    spmm_csr_kernel<8><<<blocks_for(8), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
-  else if (aligned && d == 64)
-    spmm_csr_kernel<16><<<blocks_for(16), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
-  else if (aligned && d == 128)
-    spmm_csr_kernel<32><<<blocks_for(32), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
-  else
+  const int L = !aligned ? 0 : (d == 32 ? 8 : (d == 64 ? 16 : (d == 128 ? 32 : 0)));
+  if (L == 0) {
     spmm_csr_scalar_kernel<<<static_cast<unsigned>(rows), 128, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+    STRATA_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
+  if (L == 8) spmm_csr_kernel<8><<<blocks_for(8), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  else if (L == 16) spmm_csr_kernel<16><<<blocks_for(16), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  else spmm_csr_kernel<32><<<blocks_for(32), kBlock, 0, s>>>(indptr, indices, A, X, Y, rows, d);
+  // Long rows: per-row chunk and group counts, their scans, one host read of the totals (the
+  // only synchronisation of this call; skipped work when no row is long), then three passes.
+  long long* nch = static_cast<long long*>(workspace_alloc(sizeof(long long) * (rows + 1) * 4, s));
+  long long *ngr = nch + (rows + 1), *coff = ngr + (rows + 1), *goff = coff + (rows + 1);
+  const unsigned gr = static_cast<unsigned>(std::min<long long>((rows + 256) / 256, 148LL * 16));
+  csr_long_counts_kernel<<<gr, 256, 0, s>>>(indptr, rows, nch, ngr);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, nch, coff, rows + 1, s);
+  void* tmp = workspace_alloc(tb, s);
+  cub::DeviceScan::ExclusiveSum(tmp, tb, nch, coff, rows + 1, s);
+  cub::DeviceScan::ExclusiveSum(tmp, tb, ngr, goff, rows + 1, s);
+  long long tot[2] = {0, 0};
+  STRATA_CUDA_CHECK(cudaMemcpyAsync(&tot[0], coff + rows, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  STRATA_CUDA_CHECK(cudaMemcpyAsync(&tot[1], goff + rows, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+  const long long max_chunks = tot[0], max_groups = tot[1];
+  if (max_chunks == 0) {
+    STRATA_CUDA_CHECK(cudaFreeAsync(tmp, s));
+    STRATA_CUDA_CHECK(cudaFreeAsync(nch, s));
+    return;
+  }
+  float* part = static_cast<float*>(workspace_alloc(sizeof(float) * (max_chunks + max_groups) * d, s));
+  float* l1 = part + max_chunks * d;
+  const unsigned gc = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((max_chunks * L + kBlock - 1) / kBlock, 148LL * 64)));
+  const unsigned gg = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((max_groups * L + kBlock - 1) / kBlock, 148LL * 64)));
+  const unsigned grr = static_cast<unsigned>(std::min<long long>((rows * L + kBlock - 1) / kBlock, 148LL * 64));
+  if (L == 8) {
+    spmm_csr_chunk_kernel<8><<<gc, kBlock, 0, s>>>(indptr, indices, A, X, coff, rows, part);
+    spmm_csr_group_kernel<8><<<gg, kBlock, 0, s>>>(coff, goff, rows, part, l1);
+    spmm_csr_rowsum_kernel<8><<<grr, kBlock, 0, s>>>(goff, rows, l1, Y);
+  } else if (L == 16) {
+    spmm_csr_chunk_kernel<16><<<gc, kBlock, 0, s>>>(indptr, indices, A, X, coff, rows, part);
+    spmm_csr_group_kernel<16><<<gg, kBlock, 0, s>>>(coff, goff, rows, part, l1);
+    spmm_csr_rowsum_kernel<16><<<grr, kBlock, 0, s>>>(goff, rows, l1, Y);
+  } else {
+    spmm_csr_chunk_kernel<32><<<gc, kBlock, 0, s>>>(indptr, indices, A, X, coff, rows, part);
+    spmm_csr_group_kernel<32><<<gg, kBlock, 0, s>>>(coff, goff, rows, part, l1);
+    spmm_csr_rowsum_kernel<32><<<grr, kBlock, 0, s>>>(goff, rows, l1, Y);
+  }
   STRATA_CUDA_CHECK(cudaGetLastError());
+  STRATA_CUDA_CHECK(cudaFreeAsync(part, s));
+  STRATA_CUDA_CHECK(cudaFreeAsync(tmp, s));
+  STRATA_CUDA_CHECK(cudaFreeAsync(nch, s));
 }
 
 }  // namespace strata_b200

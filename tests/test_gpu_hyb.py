@@ -234,3 +234,23 @@ def test_spmm_products_full_vs_oracle(cuda):
     want = port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, X)
     got = S.spmm(h, torch.from_numpy(X).to(cuda)).cpu().numpy()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_spmm_csr_long_rows(cuda, d):
+    """Row-split CSR SpMM (the reference's default "csr" format) on a power-law graph whose hub
+    rows exceed the 2,048-non-zero threshold: chunked long rows and the two merge levels are
+    bitwise equal to the oracle on integer operands, the rest of the rows too; real-valued data
+    within the F64 bar."""
+    import torch
+    m = S.generate_matrix("powerlaw", 60000, 60000, 0, 0, 0, 20.0, 3)
+    assert np.diff(m.indptr).max() > 2048 * 4
+    dm = m.to_device(cuda)
+    X = S.dense_int((m.cols, d), 5)
+    Y = S.spmm_csr(dm, torch.from_numpy(X).to(cuda)).cpu().numpy()
+    assert np.array_equal(Y, port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, X))
+    xr = np.random.default_rng(d).standard_normal((m.cols, d)).astype(np.float32)
+    Yr = S.spmm_csr(dm, torch.from_numpy(xr).to(cuda)).cpu().numpy()
+    want64 = port.spmm_csr_f64(m.rows, m.indptr, m.indices, m.values, xr)
+    ref32 = port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, xr)
+    assert close_to_f64(Yr, want64, ref32)

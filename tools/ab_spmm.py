@@ -34,6 +34,7 @@ def main():
         X = torch.randint(-3, 4, (m.cols, d), device=dev, dtype=torch.float32)
         Y = torch.empty((m.rows, d), device=dev)
         out[f"{name}_spmm_ms"] = round(timeit(lambda: S.spmm(h, X, Y)), 4)
+        out[f"{name}_csr_ms"] = round(timeit(lambda: S.spmm_csr(dcsr, X, Y), 3), 4)
         if name == "C2":
             Xs = torch.randint(-3, 4, (m.rows, d), device=dev, dtype=torch.float32)
             Yd = torch.randint(-3, 4, (d, m.cols), device=dev, dtype=torch.float32)
