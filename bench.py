@@ -422,6 +422,18 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
                                  "tensor_frac": round(flops_h / (msh * 1e-3) / 1e12 / bf16_peak, 5),
                                  "hbm_frac": round(b_alg_h / (msh * 1e-3) / 1e9 / hbm_peak, 4),
                                  "bytes_model": "heads*(blocks*2KB + blocks*32*d*2 + 4096*d*4)"}
+    # 12-head block-sparse SDDMM (sparse-attention scores) on tcgen05, C3 mask.
+    Qh = torch.randint(-3, 4, (H, 4096, d), device=dev).to(torch.bfloat16)
+    Kh = torch.randint(-3, 4, (H, 4096, d), device=dev).to(torch.bfloat16)
+    Sh = torch.empty((H, bs.nblocks, 32, 32), device=dev)
+    ms_sd = _time_graph_ms(torch, lambda: S.bsr_sddmm(bs, Qh, Kh, Sh))
+    fl_sd = H * bs.nblocks * 2.0 * 32 * 32 * d
+    b_sd = H * (bs.nblocks * 32 * 32 * 4 * 2 + bs.nblocks * 32 * d * 2 + 4096 * d * 2)
+    out["c3_bsr_sddmm_12head"] = {"ms": round(ms_sd, 5), "gflops": round(fl_sd / (ms_sd * 1e-3) / 1e9, 1),
+                                  "tensor_frac": round(fl_sd / (ms_sd * 1e-3) / 1e12 / bf16_peak, 5),
+                                  "hbm_frac": round(b_sd / (ms_sd * 1e-3) / 1e9 / hbm_peak, 4),
+                                  "bytes_model": "heads*(blocks*4KB A in + 4KB S out + blocks*32*d*2 K + 4096*d*2 Q)",
+                                  "timing": "CUDA graph of 20 calls"}
     # Pruned-weight formats: a 4096 x 4096 weight pruned
     # to 5 % density (unstructured, "random") as SR-BCRS(8, 32) and a 2 %-dense block mask as
     # DBSR(32), d = 128, tcgen05.

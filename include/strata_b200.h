@@ -187,6 +187,12 @@ int strata_bsr_spmm_bf16(const strata_bsr* h, const void* X_bf16, float* Y, int6
  * Y [heads][mb*b][d] f32.  Grid = block rows x heads. */
 int strata_bsr_spmm_bf16_batched(const strata_bsr* h, const void* values_bf16, const void* X_bf16,
                                  float* Y, int64_t heads, int64_t d, void* stream);
+/* Block-sparse SDDMM on tcgen05 (the score half of sparse attention): for every
+ * stored block q of h and head hd, S[hd][q][ii][ji] = A_bsr[q][ii][ji] *
+ * sum_f Q[hd][br*b + ii][f] * K[hd][JO[q]*b + ji][f].  Q [heads][mb*b][d], K [heads][nb*b][d]
+ * bf16; S [heads][nblocks][b][b] f32 in the BSR block layout.  b == 32, d in {64, 128}. */
+int strata_bsr_sddmm_bf16(const strata_bsr* h, const void* Q_bf16, const void* K_bf16, float* S,
+                          int64_t heads, int64_t d, void* stream);
 
 /* ---- COO ingest (device) -------------------------------------------------------------
  * Replaces: build_csr(coo, prefix) (storage.hpp:111, storage.cpp:89-124) for COO triplets

@@ -95,6 +95,7 @@ _sig("strata_bsr_read", C.c_int, vp, vp, vp, vp)
 _sig("strata_bsr_destroy", C.c_int, vp)
 _sig("strata_bsr_spmm_bf16", C.c_int, vp, vp, vp, i64, vp)
 _sig("strata_bsr_spmm_bf16_batched", C.c_int, vp, vp, vp, vp, i64, i64, vp)
+_sig("strata_bsr_sddmm_bf16", C.c_int, vp, vp, vp, vp, i64, i64, vp)
 _sig("strata_dbsr_from_csr", C.c_int, vp, vp, vp, i64, i64, i64, i64, vp, C.POINTER(vp))
 _sig("strata_dbsr_info", C.c_int, vp, i64p, i64p, i64p, i64p, i64p, i64p)
 _sig("strata_dbsr_read", C.c_int, vp, vp, vp, vp, vp)
@@ -132,7 +133,7 @@ EXPORTED = [
     "strata_spmm_csr_f32", "strata_sddmm_csr_f32", "strata_bsr_from_csr", "strata_bsr_info",
     "strata_bsr_read", "strata_bsr_destroy", "strata_bsr_spmm_bf16",
     "strata_bsr_spmm_bf16_batched", "strata_csr_from_coo",
-    "strata_dbsr_from_csr", "strata_dbsr_info", "strata_dbsr_read", "strata_dbsr_destroy",
+    "strata_bsr_sddmm_bf16", "strata_dbsr_from_csr", "strata_dbsr_info", "strata_dbsr_read", "strata_dbsr_destroy",
     "strata_dbsr_spmm_bf16", "strata_srbcrs_from_csr", "strata_srbcrs_info", "strata_srbcrs_read",
     "strata_srbcrs_destroy", "strata_srbcrs_spmm_bf16", "strata_attn_plan_create",
     "strata_attn_plan_destroy", "strata_attn_csr_f32", "strata_ell_from_csr",

@@ -30,14 +30,6 @@
 
 using namespace strata_b200;
 
-struct strata_dbsr;
-struct strata_bsr {
-  int device = 0;
-  int64_t rows = 0, cols = 0, nnz = 0, b = 0, mb = 0, nb = 0, nblocks = 0, pad_slots = 0;
-  DevBuf<int32_t> indptr, indices;
-  DevBuf<float> values;           // f32, bit-exact readback
-  DevBuf<__nv_bfloat16> vals_bf;  // tensor-core operand
-};
 
 // DBSR (storage.cpp:336-370): the BSR of the same matrix plus its stored block rows.
 struct strata_dbsr {

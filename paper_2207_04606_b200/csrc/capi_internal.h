@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -164,3 +165,12 @@ void set_last_error(const std::string& msg);
 }  // namespace strata_b200
 
 struct strata_hyb : strata_b200::strata_hyb_impl {};
+
+// Device BSR (bsr.cu; the SDDMM of bsr_sddmm.cu reads it too).
+struct strata_bsr {
+  int device = 0;
+  int64_t rows = 0, cols = 0, nnz = 0, b = 0, mb = 0, nb = 0, nblocks = 0, pad_slots = 0;
+  strata_b200::DevBuf<int32_t> indptr, indices;
+  strata_b200::DevBuf<float> values;           // f32, bit-exact readback
+  strata_b200::DevBuf<__nv_bfloat16> vals_bf;  // tensor-core operand
+};

@@ -544,6 +544,22 @@ class AttentionPlan:
 __all__ += ["AttentionPlan"]
 
 
+def bsr_sddmm(bsr: BsrMatrix, Q_bf16, K_bf16, S=None, stream=None):
+    """Block-sparse SDDMM (sparse-attention scores) on tcgen05: Q [H][mb*b][d], K [H][nb*b][d]
+    bf16 -> S [H][nblocks][b][b] f32 = A_bsr (.) Q K^T on the stored blocks (2-D Q/K: H = 1)."""
+    import torch
+    Q3 = Q_bf16 if Q_bf16.dim() == 3 else Q_bf16.unsqueeze(0)
+    K3 = K_bf16 if K_bf16.dim() == 3 else K_bf16.unsqueeze(0)
+    H, _, d = Q3.shape
+    if S is None:
+        S = torch.empty((H, bsr.nblocks, bsr.b, bsr.b), dtype=torch.float32, device=Q3.device)
+    check(lib.strata_bsr_sddmm_bf16(bsr.handle, _ptr(Q3), _ptr(K3), _ptr(S), H, d, _stream(stream)))
+    return S
+
+
+__all__ += ["bsr_sddmm"]
+
+
 # ---- ELL (storage.hpp:124, storage.cpp:190-227) --------------------------------------------
 
 def csr_to_ell(csr: DeviceCsr, w: int, stream=None):

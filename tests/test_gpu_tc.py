@@ -105,6 +105,32 @@ def test_bsr_spmm_batched_heads(cuda, heads, d):
     assert np.array_equal(Y1[0], one)
 
 
+@pytest.mark.parametrize("heads,d,shape", [(1, 64, (4096, 4096, 0.1)), (12, 64, (1024, 2048, 0.2)),
+                                           (3, 128, (512, 768, 0.3))])
+def test_bsr_sddmm_heads(cuda, heads, d, shape):
+    """Block-sparse SDDMM on tcgen05 (four key blocks per MMA): S = A (.) Q K^T on the stored
+    blocks, every head bitwise equal to an f64 restatement on integer operands (exact in bf16
+    and f32); partial last groups of a block row and empty block rows included."""
+    import torch
+    n, mcols, dens = shape
+    m = S.generate_matrix("blocksparse", n, mcols, dens, 0, 32, 0, 2)
+    bs = S.csr_to_bsr(m.to_device(cuda), 32)
+    a = bs.arrays()
+    jp, ji = a["bsr_JO_indptr"], a["bsr_JO_indices"]
+    A = a["values"].reshape(-1, 32, 32).astype(np.float64)
+    rng = np.random.default_rng(heads * 7 + d)
+    Q = rng.integers(-3, 4, (heads, bs.mb * 32, d)).astype(np.float32)
+    K = rng.integers(-3, 4, (heads, bs.nb * 32, d)).astype(np.float32)
+    Sg = S.bsr_sddmm(bs, bf16(torch.from_numpy(Q).to(cuda)), bf16(torch.from_numpy(K).to(cuda)))
+    Sg = Sg.cpu().numpy()
+    for h in range(heads):
+        for br in range(bs.mb):
+            qt = Q[h, br * 32:(br + 1) * 32].astype(np.float64)
+            for q in range(jp[br], jp[br + 1]):
+                kt = K[h, ji[q] * 32:(ji[q] + 1) * 32].astype(np.float64)
+                assert np.array_equal(Sg[h, q], (A[q] * (qt @ kt.T)).astype(np.float32)), (h, br, q)
+
+
 def test_bsr_empty_block_rows(cuda):
     import torch
     m = S.generate_matrix("blocksparse", 512, 256, 0.05, 0, 32, 0, 4)
