@@ -640,6 +640,9 @@ def run_ours(args):
             "kernel_ms": round(spmm_ms, 4),
             "algorithmic_bytes_per_launch": int(b_alg),
             "bytes_model": "nnz*8 + (m+1)*4 + nnz*d*4 (one X row per non-zero) + m*d*4"}
+    if traffic:  # measured DRAM bytes (ncu, profiles/) over the same launch time: frac > 1 on
+        # the algorithmic model means L2 served part of the X gathers (~10 % at C5)
+        roof["dram_traffic_frac"] = round(traffic / 1e9 / (spmm_ms * 1e-3) / hbm_peak, 4)
 
     # e2e: same metric through the C ABI with host buffers (pinned), copies inside the region:
     # strata_spmm_hyb_f32_host = H2D of X, the shard SpMM, D2H of this rank's rows.
