@@ -190,3 +190,48 @@ def rgms_refnum(R, m, i_indptr, i_indices, j_indptr, j_indices, A, X, W):
                          C.c_void_p(_p(X)),
                          C.c_void_p(_p(W)), C.c_void_p(_p(Y)))
     return Y
+
+
+def csr_to_dbsr(rows, cols, indptr, indices, values, b):
+    """storage.cpp:336-370: the BSR of the matrix plus its stored block rows.
+    Returns (IO_indices, JO_indptr over stored rows, JO_indices, values)."""
+    jp, ji, bv = csr_to_bsr(rows, cols, indptr, indices, values, b)
+    stored = np.flatnonzero(np.diff(jp) > 0).astype(np.int32)            # :342-344
+    jptr = np.r_[0, jp[stored + 1]].astype(np.int32)                      # :362-363
+    return stored, jptr, ji, bv
+
+
+def csr_to_srbcrs(rows, cols, indptr, indices, values, t, g):
+    """storage.cpp:372-440 (numpy restatement, small sizes): per tile row of t rows the sorted
+    distinct columns, cut into groups of g (last group padded with the last column, :411-420);
+    values slot-major [groups*g][t] placed by lower_bound (:421-436).
+    Returns (G_indptr, JT_indices, values)."""
+    if t < 1 or g < 1:
+        raise OracleError(6, "SR-BCRS requires t >= 1 and g >= 1")
+    indptr = np.asarray(indptr, np.int64)
+    mb = -(-rows // t)
+    tiles = []
+    gptr = np.zeros(mb + 1, np.int32)
+    for r in range(mb):
+        q0, q1 = indptr[min(r * t, rows)], indptr[min((r + 1) * t, rows)]
+        u = np.unique(indices[q0:q1])
+        tiles.append(u)
+        ng = -(-len(u) // g) if len(u) else 0
+        gptr[r + 1] = gptr[r] + ng
+    total = int(gptr[mb])
+    jt = np.zeros(total * g, np.int32)
+    vals = np.zeros(total * g * t, np.float32)
+    for r, u in enumerate(tiles):
+        base = int(gptr[r]) * g
+        n = (int(gptr[r + 1]) - int(gptr[r])) * g
+        if len(u):
+            jt[base:base + len(u)] = u
+            jt[base + len(u):base + n] = u[-1]
+    for i in range(rows):
+        r = i // t
+        u = tiles[r]
+        base = int(gptr[r]) * g
+        for q in range(indptr[i], indptr[i + 1]):
+            slot = int(np.searchsorted(u, indices[q]))
+            vals[(base + slot) * t + (i % t)] = values[q]
+    return gptr, jt, vals

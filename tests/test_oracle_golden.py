@@ -236,3 +236,31 @@ def test_generator_c1_matches_reference():
     assert mine.nnz == 1627136
     assert np.array_equal(mine.indices, st.aux("J_indices"))
     assert np.array_equal(mine.values, st.values().astype(np.float32))
+
+
+def test_golden_dbsr_srbcrs(G):
+    """The DBSR / SR-BCRS restatements (storage.cpp:336-440) against the reference library's
+    arrays, and the reference pipeline's SpMM for both formats equal to the CSR SpMM restatement
+    (integer operands: every format computes the same exact product)."""
+    for name in ("example", "bs128", "pl"):
+        meta = G[f"fmt/{name}/csr"]
+        rows, cols = int(meta[0]), int(meta[1])
+        ip, ix, v = meta[2:].astype(np.int32), G[f"fmt/{name}/indices"], G[f"fmt/{name}/values"]
+        for b in (2, 32):
+            key = f"dbsr/{name}_b{b}"
+            io, jp, ji, bv = port.csr_to_dbsr(rows, cols, ip, ix, v, b)
+            assert np.array_equal(io, G[key + "/IO_indices"]), key
+            assert np.array_equal(jp, G[key + "/JO_indptr"]), key
+            assert np.array_equal(ji, G[key + "/JO_indices"]), key
+            assert np.array_equal(bv, G[key + "/values"]), key
+        for t, g in ((2, 2), (3, 5), (8, 32)):
+            key = f"srbcrs/{name}_t{t}_g{g}"
+            gp, jt, sv = port.csr_to_srbcrs(rows, cols, ip, ix, v, t, g)
+            assert np.array_equal(gp, G[key + "/G_indptr"]), key
+            assert np.array_equal(jt, G[key + "/JT_indices"]), key
+            assert np.array_equal(sv, G[key + "/values"]), key
+        for fmt in ("dbsr", "srbcrs"):
+            X = G[f"fmtspmm/{name}/{fmt}/X"]
+            want = port.spmm_csr_refnum(rows, ip, ix, v, X[:cols])
+            Y = G[f"fmtspmm/{name}/{fmt}/Y"]
+            assert np.array_equal(Y[:rows], want) and not Y[rows:].any(), (name, fmt)
