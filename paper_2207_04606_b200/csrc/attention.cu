@@ -63,15 +63,22 @@ __device__ __forceinline__ float vw_allreduce(float v, unsigned mask) {
 
 // One virtual warp (L lanes, one float4 of the D features each) per work item.
 // Items from nlong_items_begin on are long-row chunks: they write their (acc, m, l) partial.
+#ifndef STRATA_ATTN_U  // A/B knobs: edges in flight per batch, CTAs per SM the registers allow
+#define STRATA_ATTN_U 4
+#endif
+#ifndef STRATA_ATTN_MINB
+#define STRATA_ATTN_MINB 1
+#endif
+
 template <int L>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, STRATA_ATTN_MINB)
 attn_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
             const float* __restrict__ A, const float* __restrict__ Q, const float* __restrict__ K,
             const float* __restrict__ V, const int2* __restrict__ items,
             const int32_t* __restrict__ item_len, long long nitems, long long nlong_items_begin,
             float* __restrict__ Z, float* __restrict__ partial) {
   constexpr int D = 4 * L;
-  constexpr int U = 8;  // edges in flight per batch
+  constexpr int U = STRATA_ATTN_U;  // edges in flight per batch
   const int wl = threadIdx.x & 31, lane = threadIdx.x & (L - 1);
   const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (wl & ~(L - 1)));
   const long long it = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
