@@ -194,7 +194,8 @@ struct RgmsWsSmem {
   static constexpr int kEpiBytes = 4 * 32 * kNC * 4;
   static constexpr int kIdxOff = kStagesWs * kStage;
   static constexpr int kEpiOff = kIdxOff + kIdxSlotsWs * kIdxBytes;
-  static constexpr int kBytes = kEpiOff + kEpiBytes + 1024;  // + alignment slack
+  static constexpr int kRunOff = kEpiOff + kEpiBytes;        // 4 warps x 32 int4 run records
+  static constexpr int kBytes = kRunOff + 4 * 32 * 16 + 1024;  // + alignment slack
   static constexpr int kAccCols = DOUT < 32 ? 32 : DOUT;
   static constexpr int kTmemCols = 2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
 };
@@ -216,7 +217,6 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
   constexpr uint32_t kIdesc = tc::make_idesc_bf16(kEdges, DOUT, /*A K-major*/ false, /*B MN-major*/ true);
   constexpr int kNC = SM::kNC;
   constexpr int kSPR = kNC / 4;    // float4 slots per row of a chunk
-  constexpr int kRPI = 32 / kSPR;  // lane groups per warp
   static_assert(DIN == 16 || DIN == 32 || DIN == 64, "d_in");
   static_assert(DOUT % 16 == 0 && DOUT <= 128, "d_out");
 
@@ -324,8 +324,9 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
   } else {
     // ---------------- epilogue (warps 3-6: TMEM lanes 32 * (warp % 4) ..) ----------------
     const int q = warp & 3;
-    float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + (warp - kMmaWarp - 1) * (32 * kSPR);
-    const int gi = lane / kSPR, sl = lane & (kSPR - 1);
+    const int ew = warp - kMmaWarp - 1;  // 0..3
+    float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + ew * (32 * kSPR);
+    int4* runs = reinterpret_cast<int4*>(smem + SM::kRunOff) + ew * 32;  // {r0, r1, T row, 0}
     for (long long j = 0; j < nt; ++j) {
       const int b = static_cast<int>(j & 1);
       // The accumulator being published implies the producer saw this tile's index block land
@@ -334,13 +335,17 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
       tc::fence_after_sync();
       const int32_t* si = idx_slot(j);
       const float a = __int_as_float(si[4 + 2 * kEdges + q * 32 + lane]);
-      const int32_t* spos = si + 4 + kEdges + q * 32;
-      const int myword = spos[lane];
+      const int myword = si[4 + kEdges + q * 32 + lane];
       const unsigned heads = __ballot_sync(0xffffffffu, myword >= 0);
       const unsigned pads = __ballot_sync(0xffffffffu, myword == -1);
       const int first_pad = pads ? __ffs(pads) - 1 : 32;
-      unsigned mine = heads;  // runs gi, gi + kRPI, ... belong to lane group gi
-      for (int i = 0; i < gi; ++i) mine &= mine - 1;
+      const int nruns = __popc(heads);
+      // Run table, once per tile: the head lane of the k-th run stores {r0, r1, T row} at k.
+      if (myword >= 0) {
+        const unsigned later = heads & ~((2u << lane) - 1u);
+        runs[__popc(heads & ((1u << lane) - 1u))] =
+            make_int4(lane, min(later ? __ffs(later) - 1 : 32, first_pad), myword, 0);
+      }
 #pragma unroll
       for (int c0 = 0; c0 < DOUT; c0 += kNC) {
         uint32_t v[kNC];
@@ -352,17 +357,15 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
               make_float4(a * __uint_as_float(v[4 * u]), a * __uint_as_float(v[4 * u + 1]),
                           a * __uint_as_float(v[4 * u + 2]), a * __uint_as_float(v[4 * u + 3]));
         __syncwarp();
-        unsigned m = mine;
-        while (m) {
-          const int r0 = __ffs(m) - 1;
-          const unsigned later = heads & ~((2u << r0) - 1u);
-          const int r1 = min(later ? __ffs(later) - 1 : 32, first_pad);
-          float4 acc = epi[r0 * kSPR + (sl ^ (r0 & (kSPR - 1)))];
-          for (int row = r0 + 1; row < r1; ++row)
+        // (run, float4 column slot) items, kSPR per run, spread over the lanes: a run's rows
+        // are summed in edge order, its slots leave as one contiguous kNC-float segment.
+        for (int it = lane; it < nruns * kSPR; it += 32) {
+          const int sl = it & (kSPR - 1);
+          const int4 rn = runs[it / kSPR];
+          float4 acc = epi[rn.x * kSPR + (sl ^ (rn.x & (kSPR - 1)))];
+          for (int row = rn.x + 1; row < rn.y; ++row)
             acc = add4(acc, epi[row * kSPR + (sl ^ (row & (kSPR - 1)))]);
-          __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(spos[r0]) * DOUT + c0) + sl, acc);
-#pragma unroll
-          for (int i = 0; i < kRPI; ++i) m &= m - 1;
+          __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(rn.z) * DOUT + c0) + sl, acc);
         }
         __syncwarp();
       }
@@ -409,9 +412,9 @@ struct RowSumShape {
 // walks that range in batches of 8 T rows issued together, flushing a row's sum when the walk
 // crosses its end.  Long rows are stepped over (at most one wasted batch each).
 template <int DOUT>
-__global__ void __launch_bounds__(256, STRATA_RGMS_SUM_MINB)
-rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ T, long long m,
-                    float* __restrict__ Y) {
+__device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, const float* __restrict__ T,
+                                             long long m, float* __restrict__ Y, long long blk,
+                                             long long nblk) {
   using RS = RowSumShape<DOUT>;
   constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
   constexpr int kRPV = 32 / kGrp;  // rows per lane group per block
@@ -419,9 +422,9 @@ rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ 
   __shared__ int sbnd[8][33];
   const int lane = threadIdx.x & 31, l = lane % kL, g = lane / kL, w = threadIdx.x >> 5;
   int* bnd = sbnd[w];
-  const long long nwarps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const long long nwarps = nblk * (blockDim.x >> 5);
   const float4* T4 = reinterpret_cast<const float4*>(T) + l;
-  for (long long b = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + w; b * 32 < m;
+  for (long long b = blk * (blockDim.x >> 5) + w; b * 32 < m;
        b += nwarps) {
     const long long i0 = b * 32;
     __syncwarp();
@@ -450,7 +453,7 @@ rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ 
       skip = r < rend && nb - bnd[r] > kLong;
     };
     while (q < qend) {
-      if (skip) {  // long row: its T rows are summed by rgms_long_chunk_kernel
+      if (skip) {  // long row: its T rows are summed by the chunk blocks (long_chunk_body)
         q = nb;
         flush();
         continue;
@@ -502,15 +505,16 @@ __device__ __forceinline__ float4 reduce_groups(float4 v) {
 // One warp per chunk of a long row: partial[c] = sum of T rows [q0, q1).  Lane group g sums
 // rows q0 + g, q0 + g + kGrp, ... (4 in flight), then the groups are combined.
 template <int DOUT>
-__global__ void __launch_bounds__(256)
-rgms_long_chunk_kernel(const int32_t* __restrict__ dptr, const int32_t* __restrict__ long_rows,
-                       const int32_t* __restrict__ chunk_off, int nlong, int nchunks,
-                       const float* __restrict__ T, float* __restrict__ partial) {
+__device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr,
+                                                const int32_t* __restrict__ long_rows,
+                                                const int32_t* __restrict__ chunk_off, int nlong,
+                                                int nchunks, const float* __restrict__ T,
+                                                float* __restrict__ partial, int blk, int nblk) {
   using RS = RowSumShape<DOUT>;
   constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
   const int lane = threadIdx.x & 31, l = lane % kL, grp = lane / kL;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nchunks; c += nwarps) {
+  const int nwarps = nblk * (blockDim.x >> 5);
+  for (int c = blk * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nchunks; c += nwarps) {
     int lo = 0, hi = nlong;  // long row owning chunk c: last li with chunk_off[li] <= c
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -548,6 +552,21 @@ rgms_long_chunk_kernel(const int32_t* __restrict__ dptr, const int32_t* __restri
       if (grp == 0) reinterpret_cast<float4*>(partial + static_cast<long long>(c) * DOUT)[g * kL + l] = v;
     }
   }
+}
+
+// Pass 2 in one launch: the first `cblk` blocks sum the long rows' chunks into partials (they
+// are dispatched first, so the hub rows' T ranges stream concurrently with the short rows
+// instead of after them), the remaining blocks run the short-row walk.
+template <int DOUT>
+__global__ void __launch_bounds__(256, STRATA_RGMS_SUM_MINB)
+rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ T, long long m,
+                    float* __restrict__ Y, const int32_t* __restrict__ long_rows,
+                    const int32_t* __restrict__ chunk_off, int nlong, int nchunks,
+                    float* __restrict__ partial, int cblk) {
+  if (static_cast<int>(blockIdx.x) < cblk)
+    long_chunk_body<DOUT>(dptr, long_rows, chunk_off, nlong, nchunks, T, partial, blockIdx.x, cblk);
+  else
+    row_sum_body<DOUT>(dptr, T, m, Y, blockIdx.x - cblk, gridDim.x - cblk);
 }
 
 // One warp per long row: Y[row] = sum of its chunks' partials (same fixed split as above).
@@ -615,12 +634,11 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
   STRATA_CUDA_CHECK(cudaGetLastError());
   const long long lanes = h.m * RowSumShape<DOUT>::kL;
   const long long blocks = std::min<long long>((lanes + 255) / 256, static_cast<long long>(num_sms()) * 8);
-  rgms_row_sum_kernel<DOUT><<<static_cast<unsigned>(std::max<long long>(blocks, 1)), 256, 0, s>>>(
-      h.dptr.p, h.T.p, h.m, Y);
+  const int wpb = 8;
+  const int cblk = h.nlong > 0 ? (h.nchunks + wpb - 1) / wpb : 0;
+  rgms_row_sum_kernel<DOUT><<<static_cast<unsigned>(std::max<long long>(blocks, 1) + cblk), 256, 0, s>>>(
+      h.dptr.p, h.T.p, h.m, Y, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks, h.partial.p, cblk);
   if (h.nlong > 0) {
-    const int wpb = 8;
-    rgms_long_chunk_kernel<DOUT><<<static_cast<unsigned>((h.nchunks + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
-        h.dptr.p, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks, h.T.p, h.partial.p);
     rgms_long_finish_kernel<DOUT><<<static_cast<unsigned>((h.nlong + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
         h.long_rows.p, h.chunk_off.p, h.nlong, h.partial.p, Y);
   }

@@ -155,13 +155,29 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread is parked until the phase completes (or
+// the hint expires) instead of re-issuing try_wait + branch.  Without the hint the waits of the
+// warp-specialised RGMS pass spun ~100M times per launch at C4 — 40 % of all issued warp
+// instructions, taken from the epilogue warps sharing the SM sub-partitions.
+#ifndef STRATA_MBAR_SUSPEND_NS  // A/B knob; 0 = no hint
+#define STRATA_MBAR_SUSPEND_NS 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+#if STRATA_MBAR_SUSPEND_NS
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n"
+      :: "r"(smem_u32(mbar)), "r"(parity), "n"(STRATA_MBAR_SUSPEND_NS) : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred done;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
       "@!done bra WAIT_%=;\n\t}\n"
       :: "r"(smem_u32(mbar)), "r"(parity) : "memory");
+#endif
 }
 
 // 16-byte asynchronous global -> shared copy (L1-bypassing).
