@@ -180,6 +180,9 @@ constexpr int kWsThreads = (kProdWarps + 1 + 4) * 32;  // then 4 epilogue warps
 #define STRATA_RGMS_WS_STAGES 4
 #endif
 constexpr int kStagesWs = STRATA_RGMS_WS_STAGES;
+#ifndef STRATA_RGMS_EPI_NC  // A/B knob: accumulator columns per tcgen05.ld / epilogue pass
+#define STRATA_RGMS_EPI_NC 32
+#endif
 constexpr int kIdxAheadWs = 3;
 constexpr int kIdxSlotsWs = kIdxAheadWs + kStagesWs + 2;
 
@@ -190,7 +193,7 @@ struct RgmsWsSmem {
   static constexpr int kWBytes = DIN * DOUT * 2;
   static constexpr int kStage = kABytes + kWBytes;   // keeps every A region swizzle-atom aligned
   static constexpr int kIdxBytes = kTileWords * 4;   // 1552
-  static constexpr int kNC = DOUT < 16 ? DOUT : 16;  // epilogue column chunk
+  static constexpr int kNC = DOUT < STRATA_RGMS_EPI_NC ? DOUT : STRATA_RGMS_EPI_NC;  // epilogue column chunk
   static constexpr int kEpiBytes = 4 * 32 * kNC * 4;
   static constexpr int kIdxOff = kStagesWs * kStage;
   static constexpr int kEpiOff = kIdxOff + kIdxSlotsWs * kIdxBytes;
@@ -388,10 +391,10 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
 // kChunk-edge chunks summed by a whole warp (fixed strided split + fixed shuffle tree) into
 // partials, and a finishing pass adds a row's partials in chunk order — deterministic.
 #ifndef STRATA_RGMS_SUM_MINB  // A/B knobs of the row-sum pass
-#define STRATA_RGMS_SUM_MINB 1
+#define STRATA_RGMS_SUM_MINB 5
 #endif
 #ifndef STRATA_RGMS_SUM_KB
-#define STRATA_RGMS_SUM_KB 8
+#define STRATA_RGMS_SUM_KB 6
 #endif
 #ifndef STRATA_RGMS_LONG
 #define STRATA_RGMS_LONG 64
@@ -424,13 +427,24 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
   int* bnd = sbnd[w];
   const long long nwarps = nblk * (blockDim.x >> 5);
   const float4* T4 = reinterpret_cast<const float4*>(T) + l;
-  for (long long b = blk * (blockDim.x >> 5) + w; b * 32 < m;
-       b += nwarps) {
+  // The next block's bounds are loaded while this block's T rows stream (one DRAM latency
+  // less on every block's dependency chain).
+  long long b = blk * (blockDim.x >> 5) + w;
+  int nb0 = 0, nb32 = 0;
+  if (b * 32 < m) {
+    nb0 = __ldg(dptr + min64(b * 32 + lane, m));
+    nb32 = __ldg(dptr + min64(b * 32 + 32, m));
+  }
+  for (; b * 32 < m; b += nwarps) {
     const long long i0 = b * 32;
     __syncwarp();
-    bnd[lane] = __ldg(dptr + min64(i0 + lane, m));
-    if (lane == 0) bnd[32] = __ldg(dptr + min64(i0 + 32, m));
+    bnd[lane] = nb0;
+    if (lane == 0) bnd[32] = nb32;
     __syncwarp();
+    if ((b + nwarps) * 32 < m) {
+      nb0 = __ldg(dptr + min64((b + nwarps) * 32 + lane, m));
+      nb32 = __ldg(dptr + min64((b + nwarps) * 32 + 32, m));
+    }
     int r = g * kRPV;
     const int rend = static_cast<int>(min64(r + kRPV, m - i0));
     if (r >= rend) continue;
