@@ -175,7 +175,15 @@ __global__ void tile_edges_kernel(const int32_t* __restrict__ rel_ptr, long long
 #endif
 constexpr int kProdWarps = STRATA_RGMS_PROD_WARPS;  // warps 0 .. kProdWarps-1: producers
 constexpr int kMmaWarp = kProdWarps;                // then the MMA issuer warp
-constexpr int kWsThreads = (kProdWarps + 1 + 4) * 32;  // then 4 epilogue warps
+#ifndef STRATA_RGMS_EPI_SETS  // A/B knob: epilogue warp sets (set e takes the tiles j = e mod sets)
+#define STRATA_RGMS_EPI_SETS 1
+#endif
+constexpr int kEpiSets = STRATA_RGMS_EPI_SETS;
+#ifndef STRATA_RGMS_CTAS  // A/B knob: cap on resident pass-1 CTAs per SM
+#define STRATA_RGMS_CTAS 3
+#endif
+static_assert(kEpiSets == 1 || kEpiSets == 2, "one set per TMEM accumulator at most");
+constexpr int kWsThreads = (kProdWarps + 1 + 4 * kEpiSets) * 32;  // then the epilogue warps
 #ifndef STRATA_RGMS_WS_STAGES
 #define STRATA_RGMS_WS_STAGES 4
 #endif
@@ -194,11 +202,11 @@ struct RgmsWsSmem {
   static constexpr int kStage = kABytes + kWBytes;   // keeps every A region swizzle-atom aligned
   static constexpr int kIdxBytes = kTileWords * 4;   // 1552
   static constexpr int kNC = DOUT < STRATA_RGMS_EPI_NC ? DOUT : STRATA_RGMS_EPI_NC;  // epilogue column chunk
-  static constexpr int kEpiBytes = 4 * 32 * kNC * 4;
+  static constexpr int kEpiBytes = 4 * kEpiSets * 32 * kNC * 4;
   static constexpr int kIdxOff = kStagesWs * kStage;
   static constexpr int kEpiOff = kIdxOff + kIdxSlotsWs * kIdxBytes;
-  static constexpr int kRunOff = kEpiOff + kEpiBytes;        // 4 warps x 32 int4 run records
-  static constexpr int kBytes = kRunOff + 4 * 32 * 16 + 1024;  // + alignment slack
+  static constexpr int kRunOff = kEpiOff + kEpiBytes;        // per epilogue warp 32 int4 run records
+  static constexpr int kBytes = kRunOff + 4 * kEpiSets * 32 * 16 + 1024;  // + alignment slack
   static constexpr int kAccCols = DOUT < 32 ? 32 : DOUT;
   static constexpr int kTmemCols = 2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
 };
@@ -325,12 +333,13 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue (warps 3-6: TMEM lanes 32 * (warp % 4) ..) ----------------
+    // ---------------- epilogue (warps 3..: TMEM lanes 32 * (warp % 4) ..) ----------------
+    // With two sets, set e owns accumulator e (tiles j = e mod 2): two tiles drain at once.
     const int q = warp & 3;
-    const int ew = warp - kMmaWarp - 1;  // 0..3
+    const int ew = warp - kMmaWarp - 1;  // 0 .. 4 * kEpiSets - 1
     float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + ew * (32 * kSPR);
     int4* runs = reinterpret_cast<int4*>(smem + SM::kRunOff) + ew * 32;  // {r0, r1, T row, 0}
-    for (long long j = 0; j < nt; ++j) {
+    for (long long j = ew / 4; j < nt; j += kEpiSets) {
       const int b = static_cast<int>(j & 1);
       // The accumulator being published implies the producer saw this tile's index block land
       // (idx_full -> gathers -> full -> MMA -> commit), so the block is read only after it.
@@ -639,8 +648,10 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  // Resident CTAs per SM: shared memory (~227 KB usable) and TMEM (512 columns) bound it.
-  const int per_sm = std::max(1, std::min({3, (227 * 1024) / (smem + 2048), 512 / SM::kTmemCols}));
+  // Resident CTAs per SM: shared memory (~227 KB usable) and TMEM (512 columns) bound it.  (The
+  // occupancy API reports 2 at C4's 74 KB; a grid of 3 per SM measured 0.398 vs 0.537 ms.)
+  const int per_sm = std::max(1, std::min({STRATA_RGMS_CTAS, (227 * 1024) / (smem + 2048),
+                                           512 / SM::kTmemCols}));
   const long long grid = std::min<long long>(h.ntiles, static_cast<long long>(num_sms()) * per_sm);
   const CUtensorMap wmap = make_tensor_map_bf16_2d(W, h.R * DIN, DOUT, 8, DIN, CU_TENSOR_MAP_SWIZZLE_NONE);
   k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kWsThreads, smem, s>>>(wmap, X, h.edges.p,
