@@ -131,6 +131,9 @@ constexpr int bsr_stages() {
   return (200 * 1024) / stage < 8 ? (200 * 1024) / stage : 8;
 }
 constexpr int kThreads = 128;
+#ifndef STRATA_BSR_PDL  // A/B knob: programmatic dependent launch of the BSR SpMM
+#define STRATA_BSR_PDL 1
+#endif
 constexpr int kMaxPre = 256;  // block-column indices of a block row preloaded into smem
 
 // Warp-specialised, mbarrier-pipelined block-row SpMM:
@@ -167,10 +170,8 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // CTA = (stored block row, head); DBSR maps stored row -> block row (IO_indices).
   const long long sr = blockIdx.x, head = blockIdx.y;
-  const long long br = rowmap ? rowmap[sr] : sr;
   BSR_TRACE(0);
-  const int q0 = jo_indptr[sr], nblk = jo_indptr[sr + 1] - q0;
-  for (int j = tid; j < nblk && j < kMaxPre; j += kThreads) s_cols[j] = jo_indices[q0 + j];
+  // Prologue that touches no input (overlaps the previous kernel under PDL).
   if (warp == 0) tc::tmem_alloc<kCols>(&tmem_slot);
   if (tid == 32) {
     for (int s = 0; s < kStages; ++s) {
@@ -180,16 +181,23 @@ bsr_spmm_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
     tc::mbar_init(&done, 1);
     tc::mbar_fence_init();
   }
+  if (tid == 64) {
+    tc::prefetch_tensormap(&amap);
+    tc::prefetch_tensormap(&xmap);
+  }
+  tc::pdl_wait();
+  const long long br = rowmap ? rowmap[sr] : sr;
+  const int q0 = jo_indptr[sr], nblk = jo_indptr[sr + 1] - q0;
+  for (int j = tid; j < nblk && j < kMaxPre; j += kThreads) s_cols[j] = jo_indices[q0 + j];
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  tc::pdl_launch();
   const uint32_t tmem = tmem_slot;
   BSR_TRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      tc::prefetch_tensormap(&amap);
-      tc::prefetch_tensormap(&xmap);
       for (int j = 0; j < nblk; ++j) {
         const int s = j % kStages;
         if (j >= kStages) tc::mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
@@ -280,10 +288,21 @@ void launch_bsr(const strata_bsr& h, const __nv_bfloat16* vals, long long heads,
   const CUtensorMap xmap = make_tensor_map_bf16_2d(X, heads * x_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap amap = make_tensor_map_bf16_2d(vals, heads * std::max<long long>(h.nblocks, 1) * kB,
                                                    kB, kB, kB, CU_TENSOR_MAP_SWIZZLE_64B);
-  const dim3 grid(static_cast<unsigned>(nrows), static_cast<unsigned>(heads));
-  bsr_spmm_tc_kernel<D><<<grid, kThreads, smem, s>>>(amap, xmap, jo_indptr, h.indices.p, rowmap,
-                                                     h.nblocks, x_rows, y_rows, Y);
-  STRATA_CUDA_CHECK(cudaGetLastError());
+  // Programmatic dependent launch: this grid's prologue may overlap the tail of the previous
+  // kernel on the stream (the kernel waits on griddepcontrol before reading any input).
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nrows), static_cast<unsigned>(heads));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = STRATA_BSR_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  STRATA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bsr_spmm_tc_kernel<D>, amap, xmap, jo_indptr,
+                                       static_cast<const int32_t*>(h.indices.p), rowmap,
+                                       static_cast<long long>(h.nblocks), x_rows, y_rows, Y));
 }
 
 // rows of a stored-row view: stored[i] = block rows with >= 1 block, jptr = compressed indptr

@@ -238,6 +238,13 @@ __device__ __forceinline__ void prefetch_tensormap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];\n" :: "l"(tmap) : "memory");
 }
 
+// Programmatic dependent launch (launched with cudaLaunchAttributeProgrammaticStreamSerialization):
+// pdl_wait() blocks until the preceding grid on the stream has completed and its memory is
+// visible — call it before the first global read of anything that grid may have written;
+// pdl_launch() lets the next grid start its prologue (TMEM alloc, barrier init) early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // Vector reduction into global memory (sm_90+): 4 consecutive f32 added atomically.
 __device__ __forceinline__ void red_add_v4(float* gaddr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n"
