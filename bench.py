@@ -390,6 +390,27 @@ def _time_graph_ms(torch, fn, calls=20, reps=10):
     return e0.elapsed_time(e1) / (reps * calls)
 
 
+def extra_gnn_layer(S, torch, dev, stream, h, X, nnz, spmm_ms):
+    """GNN layer step Z = A @ X @ W at C5 shape (GraphSAGE/GCN layer):
+    hyb SpMM + fp32 cuBLAS SGEMM (pedantic fp32), associated so the SpMM gathers the narrower
+    rows.  Integer operands, so the layer is exact."""
+    out = {}
+    rows, d_in = h.rows, X.shape[1]
+    for d_out in (128, 64):
+        W = torch.randint(-3, 4, (d_in, d_out), device=dev).to(torch.float32)
+        Z = torch.empty((rows, d_out), device=dev)
+        work = torch.empty(max(S.gnn_layer_work_floats(h, d_in, d_out), 1), device=dev)
+        ms = _time_ms(torch, stream, lambda: S.gnn_layer(h, X, W, Z, work, stream=stream))
+        agg_d = d_out if d_out < d_in else d_in
+        flops = 2.0 * nnz * agg_d + 2.0 * (h.cols if d_out < d_in else rows) * d_in * d_out
+        out[f"c5_gnn_layer_{d_in}x{d_out}"] = {
+            "ms": round(ms, 4), "gflops": round(flops / (ms * 1e-3) / 1e9, 1),
+            "order": "A@(X@W)" if d_out < d_in else "(A@X)@W",
+            "spmm_alone_ms_d128": round(spmm_ms, 4)}
+        del W, Z, work
+    return out
+
+
 def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     """C3 (BSR sparse attention, bf16, tcgen05) and C4 (RGCN, AM shape, tcgen05)."""
     out = {}
@@ -698,6 +719,10 @@ def run_ours(args):
             extra.update(extra_reddit(S, torch, dev, stream, hbm_peak))
         except Exception as e:  # informational only
             extra["reddit_error"] = str(e)
+        try:
+            extra.update(extra_gnn_layer(S, torch, dev, stream, h, X, m.nnz, spmm_ms))
+        except Exception as e:  # informational only
+            extra["gnn_layer_error"] = str(e)
         try:
             extra.update(extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak))
         except Exception as e:  # informational only

@@ -28,7 +28,7 @@ __all__ = [
     "StrataError", "CsrMatrix", "build_csr_device", "generate_matrix", "dense_int", "hyb_auto_k", "EllBucketPart",
     "HybDecomposition", "decompose_hyb", "hyb_rules", "spmm", "spmm_host", "spmm_host_batch",
     "spmm_multi", "ipc_handle", "ipc_open", "ipc_close",
-    "spmm_csr", "sddmm",
+    "spmm_csr", "sddmm", "gnn_layer", "gnn_layer_work_floats",
     "partition_rows", "device_ok",
 ]
 
@@ -259,6 +259,28 @@ def spmm(hyb: HybDecomposition, X, Y=None, stream=None):
         Y = torch.empty((hyb.rows, d), dtype=torch.float32, device=X.device)
     check(lib.strata_spmm_hyb_f32(hyb.handle, _ptr(X), _ptr(Y), d, _stream(stream)))
     return Y
+
+
+def gnn_layer_work_floats(hyb: HybDecomposition, d_in: int, d_out: int) -> int:
+    """Floats of the intermediate (T = X@W or Y = A@X) that gnn_layer needs."""
+    return int(lib.strata_gnn_layer_work_floats(hyb.handle, d_in, d_out))
+
+
+def gnn_layer(hyb: HybDecomposition, X, W, Z=None, work=None, stream=None):
+    """GNN layer step Z = A @ X @ W (f32, device): hyb SpMM aggregation + fp32 cuBLAS transform,
+    associated so the SpMM gathers the narrower rows (strata_gnn_layer_f32)."""
+    import torch
+    d_in, d_out = X.shape[1], W.shape[1]
+    if W.shape[0] != d_in:
+        raise StrataError(6, "gnn_layer: W must be [d_in][d_out]")
+    if Z is None:
+        Z = torch.empty((hyb.rows, d_out), dtype=torch.float32, device=X.device)
+    if work is None:
+        work = torch.empty(max(gnn_layer_work_floats(hyb, d_in, d_out), 1), dtype=torch.float32,
+                           device=X.device)
+    check(lib.strata_gnn_layer_f32(hyb.handle, _ptr(X), _ptr(W), _ptr(Z), _ptr(work), d_in, d_out,
+                                   _stream(stream)))
+    return Z
 
 
 def spmm_host(hyb: HybDecomposition, X_host, Y_host, stream=None):
