@@ -212,6 +212,15 @@ class DeviceHyb {
   void spmm(const float* X, float* Y, int64_t d, cudaStream_t s = nullptr) const {
     check(strata_spmm_hyb_f32(h_.get(), X, Y, d, s));
   }
+  // GNN layer step Z[rows][d_out] = A X W (X[cols][d_in], W[d_in][d_out]; device, f32).
+  // `work` holds gnn_layer_work_floats(d_in, d_out) floats.
+  int64_t gnn_layer_work_floats(int64_t d_in, int64_t d_out) const {
+    return strata_gnn_layer_work_floats(h_.get(), d_in, d_out);
+  }
+  void gnn_layer(const float* X, const float* W, float* Z, float* work, int64_t d_in,
+                 int64_t d_out, cudaStream_t s = nullptr) const {
+    check(strata_gnn_layer_f32(h_.get(), X, W, Z, work, d_in, d_out, s));
+  }
   HybDecomposition host(const std::string& prefix = "") const {
     HybDecomposition out;
     int n = 0;

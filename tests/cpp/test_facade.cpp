@@ -315,6 +315,24 @@ TEST_CASE("BSR tensor-core SpMM equals the dense oracle") {
   }
 }
 
+TEST_CASE("GNN layer step A*X*W equals the dense oracle in both associations") {  // §8f item 2
+  std::mt19937 rng(23);
+  CooMatrix a = generate_matrix("powerlaw", 900, 700, 0, 0, 0, 10.0, 5);
+  TensorStorage csr = build_csr(a);
+  DeviceCsr dc(csr);
+  DeviceHyb h(dc, 1, hyb_auto_k(csr));
+  for (auto [din, dout] : {std::pair<int64_t, int64_t>{64, 16}, {16, 64}}) {
+    DenseMatrix x = random_dense(rng, a.cols, din), w = random_dense(rng, din, dout);
+    DenseMatrix want = matmul(matmul(dense_from_coo(a), x), w);
+    std::vector<float> xf(x.v.begin(), x.v.end()), wf(w.v.begin(), w.v.end());
+    DeviceArray<float> X(xf), W(wf), Z(static_cast<size_t>(a.rows * dout)),
+        work(static_cast<size_t>(h.gnn_layer_work_floats(din, dout)));
+    h.gnn_layer(X.data(), W.data(), Z.data(), work.data(), din, dout);
+    std::vector<float> z = Z.host();
+    CHECK(std::vector<double>(z.begin(), z.end()) == want.v);
+  }
+}
+
 TEST_CASE("SpMM is bitwise deterministic") {  // exec :135-157
   std::mt19937 rng(17);
   CooMatrix a = generate_matrix("powerlaw", 3000, 3000, 0, 0, 0, 40.0, 3);
