@@ -24,7 +24,8 @@ KEEP = ("dram__bytes", "gpu__time_duration", "lts__t_sector_hit_rate", "l1tex__t
         "sm__throughput.avg.pct", "sm__warps_active", "launch__", "smsp__pcsamp_warps_issue",
         "smsp__pcsamp_sample_count", "sm__pipe_tensor", "sm__inst_executed_pipe_tc",
         "lts__t_bytes.sum", "dram__throughput", "gpu__compute_memory_throughput",
-        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg ")
+        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg ", "lts__throughput",
+        "lts__t_bytes", "l1tex__throughput", "lts__t_sectors_srcunit_tex_op_read.sum")
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
