@@ -39,7 +39,10 @@ struct strata_rgms {
   int device = 0;
   int64_t R = 0, m = 0, n = 0, nnz = 0;
   int64_t ntiles = 0;            // 128-edge tiles (tiles never straddle relations)
-  int64_t nruns = 0;             // message runs = T rows (see run_heads_kernel)
+  int64_t nruns = 0;             // message runs (see run_heads_kernel)
+  int64_t trows = 0;             // T rows: the runs of rows with >= 2 runs (the sole run of a
+                                 // row goes straight to Y from pass 1: a "direct" row)
+  DevBuf<uint32_t> dbits;        // [ceil(m/32)] bit r of word b: row 32b + r is direct
   DevBuf<int32_t> edges;         // [ntiles][kTileWords] per-tile edge blocks (see below)
   DevBuf<int32_t> dptr;          // [m+1] row pointer into the destination-sorted order
   int nlong = 0, nchunks = 0;     // rows with > kLong edges and their kChunk-edge chunks
@@ -128,8 +131,47 @@ __global__ void run_dst_kernel(const int32_t* __restrict__ head, const int32_t* 
     if (head[e]) run_dst[incl[e] - 1] = dst[e];
 }
 
-// Per-tile edge blocks; the pos word of an edge is its run's T row for a run head, -2 for a
-// run continuation and -1 for padding.
+// Direct rows: a row with exactly one run needs no T row — pass 1 writes its sum to Y.
+// dflag[q] = 1 when the run at destination-sorted position q is its row's only run.
+__global__ void direct_flags_kernel(const int32_t* __restrict__ keys, long long nr,
+                                    const int32_t* __restrict__ dptr, int32_t* __restrict__ dflag) {
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q <= nr;
+       q += static_cast<long long>(gridDim.x) * blockDim.x)
+    dflag[q] = q < nr && dptr[keys[q] + 1] - dptr[keys[q]] == 1 ? 1 : 0;
+}
+
+// Run r's pos word: -(3 + row) for a direct run, else its compacted T row.
+__global__ void direct_pos_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ dflag,
+                                  const int32_t* __restrict__ dbefore, long long nr,
+                                  int32_t* __restrict__ run_pos) {
+  for (long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; r < nr;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int q = run_pos[r];
+    run_pos[r] = dflag[q] ? -3 - keys[q] : q - dbefore[q];
+  }
+}
+
+// Direct-row bitmask (from the uncompacted dptr), then dptr[i] -= direct runs before it.
+__global__ void direct_bits_kernel(const int32_t* __restrict__ dptr, long long m,
+                                   uint32_t* __restrict__ dbits) {
+  const long long nw = (m + 31) / 32 * 32;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < nw;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const bool d = i < m && dptr[i + 1] - dptr[i] == 1;
+    const unsigned w = __ballot_sync(0xffffffffu, d);
+    if ((threadIdx.x & 31) == 0) dbits[i / 32] = w;
+  }
+}
+
+__global__ void compact_dptr_kernel(const int32_t* __restrict__ dbefore, long long m,
+                                    int32_t* __restrict__ dptr) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i <= m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dptr[i] -= dbefore[dptr[i]];
+}
+
+// Per-tile edge blocks; the pos word of an edge is its run's T row for a run head (or
+// -(3 + row) for a direct row's run), -2 for a run continuation and -1 for padding.
 __global__ void tile_edges_kernel(const int32_t* __restrict__ rel_ptr, long long R,
                                   const long long* __restrict__ tile_start,
                                   const int32_t* __restrict__ tile_rel, long long ntiles,
@@ -222,7 +264,8 @@ __device__ __forceinline__ uint64_t a_desc_kmajor(uint32_t saddr) {
 template <int DIN, int DOUT>
 __global__ void __launch_bounds__(kWsThreads, 1)
 rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloat16* __restrict__ X,
-                      const int32_t* __restrict__ ed, long long ntiles, float* __restrict__ T) {
+                      const int32_t* __restrict__ ed, long long ntiles, float* __restrict__ T,
+                      float* __restrict__ Y) {
   using SM = RgmsWsSmem<DIN, DOUT>;
   constexpr int kSboW = (DIN / 8) * 128;  // MN-major B (SWIZZLE_NONE): 8-column group stride
   constexpr uint32_t kIdesc = tc::make_idesc_bf16(kEdges, DOUT, /*A K-major*/ false, /*B MN-major*/ true);
@@ -348,12 +391,13 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
       const int32_t* si = idx_slot(j);
       const float a = __int_as_float(si[4 + 2 * kEdges + q * 32 + lane]);
       const int myword = si[4 + kEdges + q * 32 + lane];
-      const unsigned heads = __ballot_sync(0xffffffffu, myword >= 0);
+      const bool is_head = myword >= 0 || myword <= -3;  // T row or direct Y row
+      const unsigned heads = __ballot_sync(0xffffffffu, is_head);
       const unsigned pads = __ballot_sync(0xffffffffu, myword == -1);
       const int first_pad = pads ? __ffs(pads) - 1 : 32;
       const int nruns = __popc(heads);
       // Run table, once per tile: the head lane of the k-th run stores {r0, r1, T row} at k.
-      if (myword >= 0) {
+      if (is_head) {
         const unsigned later = heads & ~((2u << lane) - 1u);
         runs[__popc(heads & ((1u << lane) - 1u))] =
             make_int4(lane, min(later ? __ffs(later) - 1 : 32, first_pad), myword, 0);
@@ -377,7 +421,12 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
           float4 acc = epi[rn.x * kSPR + (sl ^ (rn.x & (kSPR - 1)))];
           for (int row = rn.x + 1; row < rn.y; ++row)
             acc = add4(acc, epi[row * kSPR + (sl ^ (row & (kSPR - 1)))]);
-          __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(rn.z) * DOUT + c0) + sl, acc);
+          if (rn.z >= 0) {
+            __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(rn.z) * DOUT + c0) + sl, acc);
+          } else {  // direct row: its only run is its sum (+0.f: the reference's 0 + x, no -0)
+            acc.x += 0.f; acc.y += 0.f; acc.z += 0.f; acc.w += 0.f;
+            __stcs(reinterpret_cast<float4*>(Y + static_cast<long long>(-3 - rn.z) * DOUT + c0) + sl, acc);
+          }
         }
         __syncwarp();
       }
@@ -425,7 +474,8 @@ struct RowSumShape {
 // crosses its end.  Long rows are stepped over (at most one wasted batch each).
 template <int DOUT>
 __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, const float* __restrict__ T,
-                                             long long m, float* __restrict__ Y, long long blk,
+                                             long long m, float* __restrict__ Y,
+                                             const uint32_t* __restrict__ dbits, long long blk,
                                              long long nblk) {
   using RS = RowSumShape<DOUT>;
   constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
@@ -440,19 +490,23 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
   // less on every block's dependency chain).
   long long b = blk * (blockDim.x >> 5) + w;
   int nb0 = 0, nb32 = 0;
+  uint32_t ndw = 0;  // direct rows of the block (written by pass 1, not here)
   if (b * 32 < m) {
     nb0 = __ldg(dptr + min64(b * 32 + lane, m));
     nb32 = __ldg(dptr + min64(b * 32 + 32, m));
+    ndw = __ldg(dbits + b);
   }
   for (; b * 32 < m; b += nwarps) {
     const long long i0 = b * 32;
     __syncwarp();
     bnd[lane] = nb0;
     if (lane == 0) bnd[32] = nb32;
+    const uint32_t dw = ndw;
     __syncwarp();
     if ((b + nwarps) * 32 < m) {
       nb0 = __ldg(dptr + min64((b + nwarps) * 32 + lane, m));
       nb32 = __ldg(dptr + min64((b + nwarps) * 32 + 32, m));
+      ndw = __ldg(dbits + b + nwarps);
     }
     int r = g * kRPV;
     const int rend = static_cast<int>(min64(r + kRPV, m - i0));
@@ -464,7 +518,7 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
 #pragma unroll
     for (int f = 0; f < kF; ++f) acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
     auto flush = [&] {
-      if (!skip) {
+      if (!skip && !((dw >> r) & 1u)) {
 #pragma unroll
         for (int f = 0; f < kF; ++f) {
           st_stream4(reinterpret_cast<float4*>(Y + (i0 + r) * DOUT) + f * kL + l, acc[f]);
@@ -583,13 +637,14 @@ __device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr
 template <int DOUT>
 __global__ void __launch_bounds__(256, STRATA_RGMS_SUM_MINB)
 rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ T, long long m,
-                    float* __restrict__ Y, const int32_t* __restrict__ long_rows,
+                    float* __restrict__ Y, const uint32_t* __restrict__ dbits,
+                    const int32_t* __restrict__ long_rows,
                     const int32_t* __restrict__ chunk_off, int nlong, int nchunks,
                     float* __restrict__ partial, int cblk) {
   if (static_cast<int>(blockIdx.x) < cblk)
     long_chunk_body<DOUT>(dptr, long_rows, chunk_off, nlong, nchunks, T, partial, blockIdx.x, cblk);
   else
-    row_sum_body<DOUT>(dptr, T, m, Y, blockIdx.x - cblk, gridDim.x - cblk);
+    row_sum_body<DOUT>(dptr, T, m, Y, dbits, blockIdx.x - cblk, gridDim.x - cblk);
 }
 
 // One warp per long row: Y[row] = sum of its chunks' partials (same fixed split as above).
@@ -655,14 +710,15 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
   const long long grid = std::min<long long>(h.ntiles, static_cast<long long>(num_sms()) * per_sm);
   const CUtensorMap wmap = make_tensor_map_bf16_2d(W, h.R * DIN, DOUT, 8, DIN, CU_TENSOR_MAP_SWIZZLE_NONE);
   k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kWsThreads, smem, s>>>(wmap, X, h.edges.p,
-                                                                                   h.ntiles, h.T.p);
+                                                                                   h.ntiles, h.T.p, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
   const long long lanes = h.m * RowSumShape<DOUT>::kL;
   const long long blocks = std::min<long long>((lanes + 255) / 256, static_cast<long long>(num_sms()) * 8);
   const int wpb = 8;
   const int cblk = h.nlong > 0 ? (h.nchunks + wpb - 1) / wpb : 0;
   rgms_row_sum_kernel<DOUT><<<static_cast<unsigned>(std::max<long long>(blocks, 1) + cblk), 256, 0, s>>>(
-      h.dptr.p, h.T.p, h.m, Y, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks, h.partial.p, cblk);
+      h.dptr.p, h.T.p, h.m, Y, h.dbits.p, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks,
+      h.partial.p, cblk);
   if (h.nlong > 0) {
     rgms_long_finish_kernel<DOUT><<<static_cast<unsigned>((h.nlong + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
         h.long_rows.p, h.chunk_off.p, h.nlong, h.partial.p, Y);
@@ -766,6 +822,24 @@ extern "C" int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, cons
       invert_kernel<<<gn, 256, 0, s>>>(order, nr, run_pos);
       const unsigned gr = static_cast<unsigned>(std::min<long long>((m + 1 + 255) / 256, num_sms() * 16LL));
       row_ptr_kernel<<<gr, 256, 0, s>>>(keys, nr, m, h->dptr.p);
+      // Direct rows (exactly one run): bitmask, then T rows compacted over the other runs.
+      h->dbits.alloc(static_cast<size_t>((m + 31) / 32) + 1);
+      direct_bits_kernel<<<gr, 256, 0, s>>>(h->dptr.p, m, h->dbits.p);
+      int32_t* dflag = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * (nr + 1) * 2, s));
+      int32_t* dbefore = dflag + nr + 1;
+      direct_flags_kernel<<<gn, 256, 0, s>>>(keys, nr, h->dptr.p, dflag);
+      size_t db = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, db, dflag, dbefore, nr + 1, s);
+      void* dtmp = workspace_alloc(db, s);
+      cub::DeviceScan::ExclusiveSum(dtmp, db, dflag, dbefore, nr + 1, s);
+      direct_pos_kernel<<<gn, 256, 0, s>>>(keys, dflag, dbefore, nr, run_pos);
+      compact_dptr_kernel<<<gr, 256, 0, s>>>(dbefore, m, h->dptr.p);
+      int32_t hd = 0;
+      STRATA_CUDA_CHECK(cudaMemcpyAsync(&hd, dbefore + nr, sizeof(hd), cudaMemcpyDeviceToHost, s));
+      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+      h->trows = nr - hd;
+      STRATA_CUDA_CHECK(cudaFreeAsync(dtmp, s));
+      STRATA_CUDA_CHECK(cudaFreeAsync(dflag, s));
       h->edges.alloc(static_cast<size_t>(h->ntiles) * kTileWords);
       tile_edges_kernel<<<ge, 256, 0, s>>>(rel_ptr, RR, tile_start, tile_rel, h->ntiles, src, head,
                                            incl, run_pos, A, h->edges.p);
@@ -819,6 +893,10 @@ extern "C" int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, cons
     } else if (m >= 0) {
       STRATA_CUDA_CHECK(cudaMemsetAsync(h->dptr.p, 0, sizeof(int32_t) * (m + 1), s));
     }
+    if (!h->dbits.p) {  // no runs: no direct rows
+      h->dbits.alloc(static_cast<size_t>((m + 31) / 32) + 1);
+      STRATA_CUDA_CHECK(cudaMemsetAsync(h->dbits.p, 0, sizeof(uint32_t) * ((m + 31) / 32 + 1), s));
+    }
     STRATA_CUDA_CHECK(cudaFreeAsync(tmp, s));
     STRATA_CUDA_CHECK(cudaFreeAsync(tile_rel, s));
     STRATA_CUDA_CHECK(cudaFreeAsync(tile_start, s));
@@ -839,7 +917,7 @@ extern "C" int strata_rgms_run_bf16(const strata_rgms* h, const void* X_bf16, co
       if (h->m > 0) STRATA_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(float) * h->m * d_out, s));
       return;
     }
-    const size_t need = static_cast<size_t>(h->nruns) * d_out;
+    const size_t need = static_cast<size_t>(std::max<int64_t>(h->trows, 1)) * d_out;
     const size_t pneed = static_cast<size_t>(h->nchunks) * d_out;
     if (h->T.n < need || h->partial.n < pneed) {
       STRATA_CUDA_CHECK(cudaStreamSynchronize(s));  // earlier runs may still read the old T
@@ -863,7 +941,7 @@ extern "C" int strata_rgms_info(const strata_rgms* h, int64_t* tiles_bound, int6
   return guarded([&] {
     if (!h) throw ApiError(STRATA_ERR_USAGE, "null rgms plan");
     if (tiles_bound) *tiles_bound = h->ntiles;
-    if (t_bytes_per_dout) *t_bytes_per_dout = h->nruns * 4;
+    if (t_bytes_per_dout) *t_bytes_per_dout = h->trows * 4;  // T rows (direct rows excluded)
   });
 }
 
