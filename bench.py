@@ -491,7 +491,8 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     flops = 2.0 * g.nnz * 32 * 32
     b_onchip = g.nnz * (4 + 4 + 2) + g.nnz * 32 * 2 + 133 * 32 * 32 * 2 + g.rows * 32 * 4
     # two-pass model actually executed: (src, pos, A) + X row gather + message-row write, then
-    # message-row read + dptr + Y; message rows = the plan's (relation, destination) runs
+    # message-row read + dptr + Y; message rows = the plan's (relation, destination) runs of
+    # rows with >= 2 runs (a row's sole run goes to Y from pass 1: counted in m*d_out*4)
     runs = plan.message_rows
     b_2pass = g.nnz * 12 + g.nnz * 32 * 2 + runs * 32 * 4 * 2 + (g.rows + 1) * 4 + g.rows * 32 * 4
     out["c4_rgcn"] = {"ms": round(ms, 4), "gflops": round(flops / (ms * 1e-3) / 1e9, 1),

@@ -645,7 +645,8 @@ class RgmsPlan:
 
     @property
     def message_rows(self) -> int:
-        """T rows a run writes and reads back: (relation, destination) runs of the plan."""
+        """T rows a run writes and reads back: the (relation, destination) runs of rows with two
+        or more runs (a row's sole run is written to Y directly by pass 1)."""
         t, b = C.c_int64(), C.c_int64()
         check(lib.strata_rgms_info(self._h, C.byref(t), C.byref(b)))
         return b.value // 4
