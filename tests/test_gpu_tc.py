@@ -263,3 +263,42 @@ def test_rgms_empty_relations_and_rows(cuda):
         S.rgms(rel.to_device(cuda), bf16(torch.ones((cols, 48), device=cuda)),
                bf16(torch.ones((R, 48, 16), device=cuda)))
     assert e.value.kind == "Usage"
+
+
+@pytest.mark.parametrize("case", ["all_direct", "no_direct", "mixed_hub"])
+def test_rgms_direct_rows(cuda, case):
+    """Rows whose edges form a single run are written to Y by pass 1 (no message row); the rest
+    go through message rows and pass 2.  Exercise a graph where every row is direct, one where
+    none is (every row has two relations), and a mix with a hub row above the long-row
+    threshold; plus the sign of zero (a direct row summing to 0 must read +0.0, as the
+    reference's 0 + x)."""
+    import torch
+    rng = np.random.default_rng(11)
+    R, rows, cols = 4, 2000, 1500
+    if case == "all_direct":      # one edge per row, relation = row % R
+        dst = np.arange(rows)
+        rel_of = dst % R
+    elif case == "no_direct":     # two edges per row in two different relations
+        dst = np.repeat(np.arange(rows), 2)
+        rel_of = (dst + np.tile([0, 1], rows)) % R
+    else:                         # light rows + one hub row with 5,000 edges in all relations
+        dst = np.r_[rng.integers(0, rows, 3000), np.full(5000, 7)]
+        rel_of = rng.integers(0, R, dst.size)
+    order = np.lexsort((dst, rel_of))
+    dst, rel_of = dst[order].astype(np.int32), rel_of[order]
+    rel_ptr = np.r_[0, np.cumsum(np.bincount(rel_of, minlength=R))].astype(np.int32)
+    src = rng.integers(0, cols, dst.size).astype(np.int32)
+    A = rng.integers(1, 10, dst.size).astype(np.float32)
+    rel = S.RelSparse(R, rows, cols, rel_ptr, dst, src, A)
+    X = S.dense_int((cols, 32), 7)
+    X[src[:50]] = 0  # some rows' messages are exactly zero
+    W = S.dense_int((R, 32, 32), 8)
+    plan = S.RgmsPlan(rel.to_device(cuda))
+    Y = plan.run(bf16(torch.from_numpy(X).to(cuda)), bf16(torch.from_numpy(W).to(cuda))).cpu().numpy()
+    want = _rgms_dense_f64(rel, X, W).astype(np.float32)
+    assert np.array_equal(Y, want)
+    assert not np.signbit(Y[Y == 0]).any()  # no -0.0
+    if case == "all_direct":
+        assert plan.message_rows == 0
+    if case == "no_direct":
+        assert plan.message_rows == dst.size
