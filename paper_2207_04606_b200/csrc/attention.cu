@@ -66,6 +66,9 @@ __device__ __forceinline__ float vw_allreduce(float v, unsigned mask) {
 #ifndef STRATA_ATTN_U  // A/B knobs: edges in flight per batch, CTAs per SM the registers allow
 #define STRATA_ATTN_U 4
 #endif
+#ifndef STRATA_ATTN_MB  // A/B knob: chunk partials in flight per merge step
+#define STRATA_ATTN_MB 8
+#endif
 #ifndef STRATA_ATTN_MINB
 #define STRATA_ATTN_MINB 1
 #endif
@@ -153,15 +156,40 @@ attn_merge_kernel(const int32_t* __restrict__ long_rows, const int32_t* __restri
   const long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
   if (r >= nlong) return;
   const int c0 = long_off[r], c1 = long_off[r + 1];
+  // Dense hub rows have ~900 chunks: the partials are read kMB at a time (independent loads in
+  // flight) and combined in chunk order — the same arithmetic as one chunk per step.
+  constexpr int kMB = STRATA_ATTN_MB;
   float M = -INFINITY;
-  for (int c = c0; c < c1; ++c) M = fmaxf(M, partial[static_cast<long long>(c) * (D + 4) + D]);
+  for (int c = c0; c < c1; c += kMB) {
+    float mv[kMB];
+#pragma unroll
+    for (int u = 0; u < kMB; ++u)
+      mv[u] = c + u < c1 ? partial[static_cast<long long>(c + u) * (D + 4) + D] : -INFINITY;
+#pragma unroll
+    for (int u = 0; u < kMB; ++u) M = fmaxf(M, mv[u]);
+  }
   float lsum = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int c = c0; c < c1; ++c) {
-    const float* pp = partial + static_cast<long long>(c) * (D + 4);
-    const float w = expf(pp[D] - M);
-    lsum += w * pp[D + 1];
-    fma4(acc, w, reinterpret_cast<const float4*>(pp)[lane]);
+  for (int c = c0; c < c1; c += kMB) {
+    float mv[kMB], lv[kMB];
+    float4 av[kMB];
+#pragma unroll
+    for (int u = 0; u < kMB; ++u) {
+      if (c + u < c1) {
+        const float* pp = partial + static_cast<long long>(c + u) * (D + 4);
+        mv[u] = pp[D];
+        lv[u] = pp[D + 1];
+        av[u] = reinterpret_cast<const float4*>(pp)[lane];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kMB; ++u) {
+      if (c + u < c1) {
+        const float w = expf(mv[u] - M);
+        lsum += w * lv[u];
+        fma4(acc, w, av[u]);
+      }
+    }
   }
   const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
   st_stream4(reinterpret_cast<float4*>(Z + static_cast<long long>(long_rows[r]) * D) + lane,
