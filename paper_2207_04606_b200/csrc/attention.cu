@@ -159,15 +159,23 @@ attn_merge_kernel(const int32_t* __restrict__ long_rows, const int32_t* __restri
   // Dense hub rows have ~900 chunks: the partials are read kMB at a time (independent loads in
   // flight) and combined in chunk order — the same arithmetic as one chunk per step.
   constexpr int kMB = STRATA_ATTN_MB;
+  // Row max: lane-strided over the chunks, then a max across the virtual warp (exact in any
+  // order, so identical to the sequential scan).
+  const int wl = threadIdx.x & 31;
+  const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (wl & ~(L - 1)));
   float M = -INFINITY;
-  for (int c = c0; c < c1; c += kMB) {
+  for (int c = c0; c < c1; c += L * kMB) {
     float mv[kMB];
 #pragma unroll
-    for (int u = 0; u < kMB; ++u)
-      mv[u] = c + u < c1 ? partial[static_cast<long long>(c + u) * (D + 4) + D] : -INFINITY;
+    for (int u = 0; u < kMB; ++u) {
+      const int q = c + u * L + lane;
+      mv[u] = q < c1 ? partial[static_cast<long long>(q) * (D + 4) + D] : -INFINITY;
+    }
 #pragma unroll
     for (int u = 0; u < kMB; ++u) M = fmaxf(M, mv[u]);
   }
+#pragma unroll
+  for (int o = L / 2; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(vmask, M, o, L));
   float lsum = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int c = c0; c < c1; c += kMB) {
