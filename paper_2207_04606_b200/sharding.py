@@ -86,21 +86,41 @@ class PeerAllGather:
     def __init__(self, y_full, rank: int, world: int, group=None):
         import torch.distributed as dist
         from .ops import ipc_handle, ipc_open
+        import torch
         self.y = y_full
         self.rank, self.world, self.group = rank, world, group
         self.d = int(y_full.shape[1])
-        mine = ipc_handle(y_full)
+        self.ptrs, self._opened = [], []
+
+        def agree(ok: bool, what: str, err):
+            # every rank takes the same branch: a failure on any rank raises on all of them,
+            # so callers that fall back to NCCL keep their collectives in step
+            t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=y_full.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            if int(t[0]) != 1:
+                self.close()
+                raise RuntimeError(f"{what} failed on a rank" + (f": {err}" if err else ""))
+
+        mine, err = None, None
+        try:
+            mine = ipc_handle(y_full)
+        except Exception as e:  # noqa: BLE001
+            err = e
+        agree(mine is not None, "CUDA IPC handle export", err)
         handles = [None] * world
         dist.all_gather_object(handles, mine, group=group)
-        self.ptrs, self._opened = [], []
-        for r, (hd, off) in enumerate(handles):
-            if r == rank:
-                self.ptrs.append(y_full.data_ptr())
-            else:
-                base = ipc_open(hd)
-                self._opened.append(base)
-                self.ptrs.append(base + off)
-        import torch
+        err = None
+        try:
+            for r, (hd, off) in enumerate(handles):
+                if r == rank:
+                    self.ptrs.append(y_full.data_ptr())
+                else:
+                    base = ipc_open(hd)
+                    self._opened.append(base)
+                    self.ptrs.append(base + off)
+        except Exception as e:  # noqa: BLE001
+            err = e
+        agree(err is None, "CUDA IPC peer mapping", err)
         self._flag = torch.zeros(1, dtype=torch.int32, device=y_full.device)
 
     def dsts(self, row0: int):
