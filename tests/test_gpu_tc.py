@@ -81,6 +81,29 @@ def test_bsr_spmm_c3_shape(cuda, d):
     assert close_ref_metric(Yr, dense @ Xr64, 1e-2)
 
 
+def test_bsr_spmm_pdl_producer_consumer(cuda):
+    """The BSR SpMM is launched with programmatic dependent launch; its inputs are read only
+    after griddepcontrol.wait.  Chain producer kernels (X written by torch on the same stream)
+    and back-to-back SpMMs whose output feeds the next X, without host syncs, and check every
+    result against the oracle chain."""
+    import torch
+    m = S.generate_matrix("blocksparse", 1024, 1024, 0.2, 0, 32, 0, 2)
+    bs = S.csr_to_bsr(m.to_device(cuda), 32)
+    jp, ji, bv = port.csr_to_bsr(m.rows, m.cols, m.indptr, m.indices, m.values, 32)
+    X0 = S.dense_int((1024, 64), 9)
+    Xd = bf16(torch.from_numpy(X0).to(cuda))
+    outs = []
+    for i in range(6):
+        Xd = (Xd.float() + i).remainder(5).sub(2).to(torch.bfloat16)  # producer kernels
+        Y = S.bsr_spmm(bs, Xd)                                       # consumer (PDL launch)
+        outs.append((Xd, Y))
+        Xd = Y.remainder(7).sub(3).to(torch.bfloat16)                 # next X from Y
+    torch.cuda.synchronize()
+    for Xi, Yi in outs:
+        want = port.bsr_spmm_refnum(32, 32, jp, ji, bv, Xi.float().cpu().numpy())
+        assert np.array_equal(Yi.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("heads,d", [(12, 64), (3, 128), (2, 512)])
 def test_bsr_spmm_batched_heads(cuda, heads, d):
     """Multi-head batched SpMM: 12 heads on the C3 mask, per-head block values
