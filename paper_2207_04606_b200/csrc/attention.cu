@@ -66,6 +66,14 @@ __device__ __forceinline__ float vw_allreduce(float v, unsigned mask) {
 #ifndef STRATA_ATTN_U  // A/B knobs: edges in flight per batch, CTAs per SM the registers allow
 #define STRATA_ATTN_U 4
 #endif
+#ifndef STRATA_ATTN_FASTEXP  // A/B knob: MUFU __expf in the edge loop (C2: 6.13 vs 6.18 ms; off)
+#define STRATA_ATTN_FASTEXP 0
+#endif
+#if STRATA_ATTN_FASTEXP
+#define ATTN_EXP(x) __expf(x)
+#else
+#define ATTN_EXP(x) expf(x)
+#endif
 #ifndef STRATA_ATTN_MB  // A/B knob: chunk partials in flight per merge step
 #define STRATA_ATTN_MB 8
 #endif
@@ -119,13 +127,13 @@ attn_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indi
       if (u < n) bm = fmaxf(bm, s[u]);
     }
     const float mn = fmaxf(m, bm);
-    const float scale = expf(m - mn);  // m = -inf on the first batch -> 0
+    const float scale = ATTN_EXP(m - mn);  // m = -inf on the first batch -> 0
     l *= scale;
     acc.x *= scale; acc.y *= scale; acc.z *= scale; acc.w *= scale;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (u < n) {
-        const float p = expf(s[u] - mn);
+        const float p = ATTN_EXP(s[u] - mn);
         l += p;
         fma4(acc, p, vv[u]);
       }
