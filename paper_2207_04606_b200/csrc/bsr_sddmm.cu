@@ -46,8 +46,7 @@ bsr_sddmm_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_const
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long br = blockIdx.x, head = blockIdx.y;
-  const int q0 = jo_indptr[br], nblk = jo_indptr[br + 1] - q0;
-  const int ngroups = (nblk + kGroup - 1) / kGroup;
+  // Prologue that touches no input (overlaps the previous kernel under PDL).
   if (warp == 0) tc::tmem_alloc<64>(&tmem_slot);
   if (threadIdx.x == 32) {
     for (int s = 0; s < kStages; ++s) {
@@ -61,15 +60,21 @@ bsr_sddmm_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_const
     }
     tc::mbar_fence_init();
   }
+  if (threadIdx.x == 64) {
+    tc::prefetch_tensormap(&qmap);
+    tc::prefetch_tensormap(&kmap);
+  }
+  tc::pdl_wait();  // inputs (Q, K, structure) may come from the previous kernel
+  const int q0 = jo_indptr[br], nblk = jo_indptr[br + 1] - q0;
+  const int ngroups = (nblk + kGroup - 1) / kGroup;
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  tc::pdl_launch();
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
     if (lane == 0 && ngroups > 0) {  // producer
-      tc::prefetch_tensormap(&qmap);
-      tc::prefetch_tensormap(&kmap);
       tc::mbar_arrive_expect_tx(&qbar, kQT);
       for (int a = 0; a < kAtoms; ++a)
         tc::tma_load_2d(sQ + a * (kB * 128), &qmap, a * 64, static_cast<int>(head * q_rows + br * kB), &qbar);
@@ -154,10 +159,23 @@ void launch_sddmm(const strata_bsr& h, const __nv_bfloat16* Q, const __nv_bfloat
   const long long q_rows = h.mb * kB, k_rows = h.nb * kB;
   const CUtensorMap qmap = make_tensor_map_bf16_2d(Q, heads * q_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap kmap = make_tensor_map_bf16_2d(K, heads * k_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);
-  const dim3 grid(static_cast<unsigned>(h.mb), static_cast<unsigned>(heads));
-  bsr_sddmm_tc_kernel<D><<<grid, kThreads, smem, s>>>(qmap, kmap, h.indptr.p, h.indices.p, h.values.p,
-                                                      h.nblocks, q_rows, k_rows, S);
-  STRATA_CUDA_CHECK(cudaGetLastError());
+  // Programmatic dependent launch, as the BSR SpMM (bsr.cu): the prologue overlaps the
+  // previous kernel; no input is read before griddepcontrol.wait.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(h.mb), static_cast<unsigned>(heads));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  STRATA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bsr_sddmm_tc_kernel<D>, qmap, kmap,
+                                       static_cast<const int32_t*>(h.indptr.p),
+                                       static_cast<const int32_t*>(h.indices.p),
+                                       static_cast<const float*>(h.values.p),
+                                       static_cast<long long>(h.nblocks), q_rows, k_rows, S));
 }
 
 }  // namespace

@@ -19,4 +19,11 @@ Vh = torch.randint(1, 10, (H, bs.nblocks, 32, 32), device=dev).to(torch.bfloat16
 Xh = torch.randint(-3, 4, (H, 4096, 64), device=dev).to(torch.bfloat16)
 Yh = torch.empty((H, 4096, 64), device=dev)
 out["c3_12head_graph_us"] = round(_time_graph_ms(torch, lambda: S.bsr_spmm_batched(bs, Vh, Xh, Yh)) * 1e3, 3)
+Qh = torch.randint(-3, 4, (H, 4096, 64), device=dev).to(torch.bfloat16)
+Kh = torch.randint(-3, 4, (H, 4096, 64), device=dev).to(torch.bfloat16)
+Sh = torch.empty((H, bs.nblocks, 32, 32), device=dev)
+try:
+    out["c3_sddmm_12head_graph_us"] = round(_time_graph_ms(torch, lambda: S.bsr_sddmm(bs, Qh, Kh, Sh)) * 1e3, 3)
+except Exception as e:  # noqa: BLE001
+    out["sddmm_error"] = str(e)[:80]
 print(json.dumps(out))
