@@ -458,7 +458,10 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
 #define STRATA_RGMS_LONG 64
 #endif
 constexpr int kLong = STRATA_RGMS_LONG;
-constexpr int kChunk = 1024;
+#ifndef STRATA_RGMS_CHUNK  // A/B knob: message rows per long-row chunk (128..1024 within 1 % at C4)
+#define STRATA_RGMS_CHUNK 1024
+#endif
+constexpr int kChunk = STRATA_RGMS_CHUNK;
 
 template <int DOUT>
 struct RowSumShape {
