@@ -458,6 +458,9 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
 #define STRATA_RGMS_LONG 64
 #endif
 constexpr int kLong = STRATA_RGMS_LONG;
+#ifndef STRATA_RGMS_SUM_WAVE  // A/B knob: cap on row-sum CTAs per SM in the grid
+#define STRATA_RGMS_SUM_WAVE 32  // C4: 5 -> 0.380, 8 -> 0.375, 16 -> 0.367, 32 -> 0.365, 64 -> 0.373 ms
+#endif
 #ifndef STRATA_RGMS_CHUNK  // A/B knob: message rows per long-row chunk (128..1024 within 1 % at C4)
 #define STRATA_RGMS_CHUNK 1024
 #endif
@@ -716,7 +719,11 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
                                                                                    h.ntiles, h.T.p, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
   const long long lanes = h.m * RowSumShape<DOUT>::kL;
-  const long long blocks = std::min<long long>((lanes + 255) / 256, static_cast<long long>(num_sms()) * 8);
+  // Grid: up to 32 CTAs per SM (~1.6 warp-blocks of 32 rows per warp at C4) — CTAs retire and
+  // are replaced as their rows finish, which balances the power-law row lengths better than a
+  // resident-only persistent grid (measured, knob above).
+  const long long blocks = std::min<long long>((lanes + 255) / 256,
+                                               static_cast<long long>(num_sms()) * STRATA_RGMS_SUM_WAVE);
   const int wpb = 8;
   const int cblk = h.nlong > 0 ? (h.nchunks + wpb - 1) / wpb : 0;
   rgms_row_sum_kernel<DOUT><<<static_cast<unsigned>(std::max<long long>(blocks, 1) + cblk), 256, 0, s>>>(
