@@ -449,10 +449,10 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
 // kChunk-edge chunks summed by a whole warp (fixed strided split + fixed shuffle tree) into
 // partials, and a finishing pass adds a row's partials in chunk order — deterministic.
 #ifndef STRATA_RGMS_SUM_MINB  // A/B knobs of the row-sum pass
-#define STRATA_RGMS_SUM_MINB 5
+#define STRATA_RGMS_SUM_MINB 6
 #endif
 #ifndef STRATA_RGMS_SUM_KB
-#define STRATA_RGMS_SUM_KB 6
+#define STRATA_RGMS_SUM_KB 4
 #endif
 #ifndef STRATA_RGMS_LONG
 #define STRATA_RGMS_LONG 64
