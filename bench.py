@@ -243,19 +243,58 @@ def cpu_baseline_port(m, d):
             "sample": f"rows [0,{rows}) ({nnz} nnz, d={d}) with the C restatement"}
 
 
+class RefCsr:
+    """CSR arrays of a graph built entirely by the reference library (oracle/_ref):
+    generate_matrix (driver.cpp:365-416) + build_csr (storage.cpp:89-124)."""
+
+    def __init__(self, cfg):
+        from oracle import ref
+        coo = ref.Coo.generate(cfg["kind"], cfg["n"], cfg["m"], 0.0, 0, 0, cfg["avg"], cfg["seed"])
+        st = ref.Storage.csr(coo, ref.F32)
+        self.coo = coo
+        self.rows, self.cols = st.rows, st.cols
+        self.indptr = st.aux("J_indptr")
+        self.indices = st.aux("J_indices")
+        self.values = st.values().astype(np.float32)
+        self.nnz = int(self.indices.shape[0])
+
+
+def reference_c1_full(d=32, runs=1, warm=0, X=None):
+    """BASELINE configs[0] at full size on the reference's own executor: power-law 65,536 nodes,
+    avg degree 16, seed 1 (1,048,664 nnz), hyb:c=1 SpMM, d = 32, F32 pipeline, X from the
+    tuner's seeding (tune.cpp:108-111) unless given; build_matrix_pipeline + interpret
+    (driver.cpp:173-217, interp.cpp:564-622), one core (hyb refuses to parallelise,
+    interp.cpp:21-49).  Returns (median seconds per run, nnz, Y of the last run as float64)."""
+    from oracle import ref
+    coo = ref.Coo.generate("powerlaw", 65536, 65536, 0.0, 0, 0, 16.0, 1)
+    pl = ref.Pipeline.matrix("spmm", coo, d, ref.F32, "hyb:c=1")
+    pl.set("X", ref.dense_int(coo.cols * d, 7) if X is None else np.asarray(X, np.float64))
+    for _ in range(warm):
+        pl.run_timed()
+    times, Y = [], None
+    for _ in range(max(runs, 1)):
+        t0 = time.perf_counter()
+        Y = pl.run_sized(coo.rows * d)  # one interpret(), output copied out by the same call
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times)), coo.nnz, Y
+
+
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU executor only (oracle/_ref = the unmodified
+    reference library).  Nothing from this repo's package is imported or loaded here."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import paper_2207_04606_b200 as S
     from oracle import ref
-    cfg = PRODUCTS
-    m = S.generate_matrix(cfg["kind"], cfg["n"], cfg["m"], 0, 0, 0, cfg["avg"], cfg["seed"])
-    d = cfg["d"]
-    threads = os.cpu_count() or 1
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstrata_ref.so not built"}))
         return 0
+    cfg = PRODUCTS
+    t0 = time.time()
+    m = RefCsr(cfg)  # reference generator + build_csr
+    gen_s = time.time() - t0
+    d = cfg["d"]
+    threads = os.cpu_count() or 1
     # size each thread's slice for ~2 s of interpretation per step
     pls, nnz = reference_sample_pipelines(m, d, 200, 1)
     per_mac = run_reference_step(pls) / max(1, nnz * d)
@@ -267,8 +306,19 @@ def run_reference_arm(args):
     t = float(np.median(times))
     gflops = 2.0 * nnz * d / t / 1e9
     sample = (f"{threads} concurrent reference pipelines (hyb:c=1, F32, build_matrix_pipeline + "
-              f"interpret), row slices of {rows} rows of the products-shape graph "
-              f"({nnz} nnz total, d={d}); median of {args.steps} steps; CPU: {cpu_model()}")
+              f"interpret), row slices of {rows} rows of the products-shape graph generated by "
+              f"the reference ({nnz} nnz total, d={d}); median of {args.steps} steps; "
+              f"CPU: {cpu_model()}")
+    extra = {"generate_and_build_csr_s": round(gen_s, 2), "graph_nnz": m.nnz}
+    if not args.no_extra:
+        # BASELINE configs[0] (C1) at full size, the same workload the device arm times in
+        # extra.c1_same_config: one core, whole graph.
+        t1, nnz1, _ = reference_c1_full(runs=2, warm=1)
+        extra["c1_same_config"] = {
+            "workload": "hyb SpMM fp32, power-law 65,536 nodes, avg 16, seed 1, d=32, hyb:c=1",
+            "nnz": nnz1, "ms": round(t1 * 1e3, 2), "gflops": round(2.0 * nnz1 * 32 / t1 / 1e9, 6),
+            "cores": 1, "same_config": True,
+            "how": "reference generate_matrix + build_matrix_pipeline + interpret, median of 2"}
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gflops, 6), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -280,6 +330,7 @@ def run_reference_arm(args):
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(gflops, 6), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "extra": extra,
     }
     print(json.dumps(line))
     return 0
@@ -513,6 +564,44 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     return out
 
 
+def extra_c1_same_config(S, torch, dev, stream):
+    """BASELINE configs[0] (C1) end to end on both executors, same workload, same operands:
+    power-law 65,536 nodes, avg 16, seed 1 (1,048,664 nnz), hyb:c=1 (k=5), d = 32, X from the
+    tuner's seeding (tune.cpp:108-111).  Device: decompose + SpMM through the C ABI (kernel time
+    by CUDA events; e2e with host X in / host Y out per call).  Reference: the unmodified
+    interpreter (oracle/_ref) on one core, timed around interpret(); its Y is compared bitwise."""
+    from oracle import ref
+    d = 32
+    m = S.generate_matrix("powerlaw", 65536, 65536, 0, 0, 0, 16.0, 1)
+    h = S.decompose_hyb(m.to_device(dev), 1, S.hyb_auto_k(m))
+    Xh = torch.from_numpy(S.dense_int((m.cols, d), 7)).pin_memory()
+    X = Xh.to(dev)
+    Y = torch.empty((m.rows, d), device=dev)
+    ms = _time_ms(torch, stream, lambda: S.spmm(h, X, Y, stream=stream), reps=50)
+    Yh = torch.empty((m.rows, d)).pin_memory()
+    S.spmm_host(h, Xh, Yh, stream=stream)
+    reps = 20
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        S.spmm_host(h, Xh, Yh, stream=stream)
+    e2e_ms = (time.perf_counter() - t0) / reps * 1e3
+    flops = 2.0 * m.nnz * d
+    out = {"workload": "hyb SpMM fp32, power-law 65,536 nodes, avg 16, seed 1, d=32, hyb:c=1",
+           "nnz": m.nnz, "device_ms": round(ms, 5), "device_gflops": round(flops / ms / 1e6, 2),
+           "e2e_ms": round(e2e_ms, 4), "e2e_gflops": round(flops / e2e_ms / 1e6, 2),
+           "e2e_path": "strata_spmm_hyb_f32_host (pinned X in, Y out, one call per step)",
+           "same_config": True}
+    if ref.available():
+        t_ref, nnz_ref, y_ref = reference_c1_full(runs=1, X=Xh.numpy())
+        out.update({"reference_ms": round(t_ref * 1e3, 2), "reference_cores": 1,
+                    "reference_nnz": nnz_ref,
+                    "ratio_device": round(t_ref * 1e3 / ms, 1),
+                    "ratio_e2e": round(t_ref * 1e3 / e2e_ms, 1),
+                    "bitwise_equal_to_reference": bool(np.array_equal(
+                        Yh.numpy().ravel(), y_ref.astype(np.float32)))})
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -520,8 +609,9 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        args.gpus = world
+    if world != args.gpus:  # main() re-execs through torch.distributed.run; never relabel N
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     # STRATA_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 with a gloo group, so the
     # N > 1 code path (sharding, IPC peer stores, fallbacks) runs on a one-GPU box.
     share = os.environ.get("STRATA_BENCH_SHARE_GPU") == "1"
@@ -746,12 +836,19 @@ def run_ours(args):
             extra.update(extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak))
         except Exception as e:  # informational only
             extra["tensor_core_error"] = str(e)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_extra:
+        try:
+            extra["c1_same_config"] = extra_c1_same_config(S, torch, dev, stream)
+        except Exception as e:  # informational only
+            extra["c1_error"] = str(e)
+    if rank == 0 and not args.no_cpu_baseline:  # every N: the other ranks wait at the barrier
         try:
             cpu = cpu_baseline_single(m, d)
         except Exception as e:
             cpu = {"value": None, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -788,6 +885,20 @@ def main():
     ap.add_argument("--allgather", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 reassembly of Y: fused peer stores (p2p) or NCCL all-gather")
     args = ap.parse_args()
+    if args.gpus < 1:
+        print("bench.py: --gpus must be >= 1", file=sys.stderr)
+        return 2
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # One process per GPU: re-launch this command under torch.distributed.run so that
+        # `python bench.py --gpus N` really runs N ranks (never a 1-GPU run labelled N).
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

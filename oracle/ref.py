@@ -276,6 +276,16 @@ class Pipeline:
         _chk(lib().sref_pipeline_run(self.h, _p(out), n.value, C.byref(n)))
         return out
 
+    def run_sized(self, n):
+        """One interpret() whose output (n elements, known to the caller) is copied out by the
+        same call."""
+        out = np.empty(n, np.float64)
+        got = i64()
+        _chk(lib().sref_pipeline_run(self.h, _p(out), n, C.byref(got)))
+        if got.value != n:
+            raise RefError(7, f"output has {got.value} elements, expected {n}")
+        return out
+
     def run_timed(self):
         """One interpret() of stage III (the reference tuner's timed call, tune.cpp:137)."""
         n = i64()

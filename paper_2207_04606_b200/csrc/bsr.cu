@@ -278,12 +278,11 @@ void launch_bsr(const strata_bsr& h, const __nv_bfloat16* vals, long long heads,
                 const __nv_bfloat16* X, float* Y, cudaStream_t s, const int32_t* jo_indptr,
                 const int32_t* rowmap, long long nrows) {
   constexpr int smem = bsr_stages<D>() * (kB * kB * 2 + kB * D * 2) + 1024;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce once;
+  once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(bsr_spmm_tc_kernel<D>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  });
   const long long x_rows = h.nb * kB, y_rows = h.mb * kB;
   const CUtensorMap xmap = make_tensor_map_bf16_2d(X, heads * x_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap amap = make_tensor_map_bf16_2d(vals, heads * std::max<long long>(h.nblocks, 1) * kB,

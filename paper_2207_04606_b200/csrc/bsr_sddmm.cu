@@ -150,12 +150,11 @@ template <int D>
 void launch_sddmm(const strata_bsr& h, const __nv_bfloat16* Q, const __nv_bfloat16* K,
                   long long heads, float* S, cudaStream_t s) {
   constexpr int smem = kStages * kGroup * kB * D * 2 + kB * D * 2 + 1024;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce once;
+  once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(bsr_sddmm_tc_kernel<D>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  });
   const long long q_rows = h.mb * kB, k_rows = h.nb * kB;
   const CUtensorMap qmap = make_tensor_map_bf16_2d(Q, heads * q_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap kmap = make_tensor_map_bf16_2d(K, heads * k_rows, D, 64, kB, CU_TENSOR_MAP_SWIZZLE_128B);

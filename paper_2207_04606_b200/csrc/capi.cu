@@ -355,6 +355,7 @@ int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_ho
     require_device();
     if (nbatch == 0) return;
     cudaStream_t s = as_stream(stream);
+    std::lock_guard<std::mutex> lock(H.stage_mu);  // the staging slots belong to the handle
     const size_t xn = static_cast<size_t>(H.cols) * d, yn = static_cast<size_t>(H.rows) * d;
     const int nslots = nbatch > 1 ? 2 : 1;
     for (int k = 0; k < nslots; ++k) {

@@ -5,7 +5,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -27,6 +29,34 @@ struct ApiError : std::runtime_error {
       throw ::strata_b200::ApiError(STRATA_ERR_CUDA, std::string(#expr) + ": " +         \
                                                          cudaGetErrorString(e_));        \
   } while (0)
+
+// Once-per-device guard for cudaFuncSetAttribute (function attributes are per device, so a
+// process driving several GPUs must set them on each):  static PerDeviceOnce once;
+// once([&] { cudaFuncSetAttribute(...); });
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  template <class F>
+  void operator()(F&& f) {
+    int dev = 0;
+    STRATA_CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    f();
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+};
+
+// Restores the caller's current device on scope exit (handles may live on another device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 struct CsrHost {
   int64_t rows = 0, cols = 0, nnz = 0;
@@ -123,10 +153,10 @@ struct strata_hyb_impl {
   DevBuf<FixRun> fix_runs;
   std::vector<FixRange> fix_ranges;    // per column partition, in partition order
   int64_t l2_slots = 0;
-  mutable DevBuf<double> carry;        // [total_chunks_carry][2][d] f64 scratch, grown on demand
-  mutable DevBuf<double> carry_l2;     // [l2_slots][d]
-  mutable DevBuf<double> yacc;         // c > 1: f64 [rows][d] accumulator across partitions
-  mutable int64_t carry_d = 0;
+  // Per-call scratch (split-row carries [total_chunks_carry][2][d] f64, level-2 partials
+  // [l2_slots][d] f64, the c > 1 f64 accumulator [rows][d]) is taken from the stream-ordered
+  // pool for each SpMM, so one handle may serve several streams / threads at once.
+  mutable std::mutex stage_mu;                   // guards the e2e staging buffers below
   mutable DevBuf<float> stage_x[2], stage_y[2];  // e2e staging (double-buffered)
 };
 

@@ -51,27 +51,55 @@ __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict
   }
 }
 
-template <int L>
-__device__ __forceinline__ float reduce_scatter(float (&v)[L], int lane, unsigned mask) {
+template <int L, class T>
+__device__ __forceinline__ T reduce_scatter(T (&v)[L], int lane, unsigned mask) {
 #pragma unroll
   for (int w = L / 2; w >= 1; w >>= 1) {
     const bool hi = (lane & w) != 0;
 #pragma unroll
     for (int i = 0; i < w; ++i) {
-      const float send = hi ? v[i] : v[i + w];
-      const float keep = hi ? v[i + w] : v[i];
+      const T send = hi ? v[i] : v[i + w];
+      const T keep = hi ? v[i + w] : v[i];
       v[i] = keep + __shfl_xor_sync(mask, send, w, L);
     }
   }
   return v[0];
 }
 
-template <int L>
+#ifndef STRATA_SDDMM_F64  // A/B knob: 1 = f64 dot products (default), 0 = f32
+#define STRATA_SDDMM_F64 1
+#endif
+
+// Dot-product numerics.  The reference accumulates sum_k A*X*Y in f64 and rounds each partial
+// to f32 (interp.cpp:88-94); the parity bar is |x - y| <= 1e-5 max(|x|, |y|, 1) against its F64
+// pipeline (driver.cpp:124-144).  An f32 dot of 64 N(0,1) terms misses that bar on cancelling
+// rows (measured 0.73-1.12e-5), so each lane forms its 4-feature partial with exact f64
+// products (f32 x f32 fits in 53 bits) and the butterfly reduces f64: one rounding, at B.
+// The X row fragment is converted once per row; Y values once per gathered element.
+template <bool kF64>
+struct DotT { using T = float; };
+template <>
+struct DotT<true> { using T = double; };
+
+template <bool kF64>
+__device__ __forceinline__ typename DotT<kF64>::T dot4(const float4& x, const float4& y) {
+  if constexpr (kF64) {
+    double s = static_cast<double>(x.x) * static_cast<double>(y.x);
+    s = fma(static_cast<double>(x.y), static_cast<double>(y.y), s);
+    s = fma(static_cast<double>(x.z), static_cast<double>(y.z), s);
+    return fma(static_cast<double>(x.w), static_cast<double>(y.w), s);
+  } else {
+    return x.x * y.x + x.y * y.y + x.z * y.z + x.w * y.w;
+  }
+}
+
+template <int L, bool kF64 = STRATA_SDDMM_F64>
 __global__ void __launch_bounds__(kBlock)
 sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
              const float* __restrict__ A, const float* __restrict__ X,
              const float* __restrict__ Yt, float* __restrict__ B, long long rows, long long nnz,
              long long d) {
+  using T = typename DotT<kF64>::T;
   constexpr int U = 8;
   const int wl = threadIdx.x & 31;
   const int lane = threadIdx.x & (L - 1);
@@ -118,7 +146,7 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   for (int g = 0; g < ne; g += L) {
     const int n = min(L, ne - g);
     const bool one_row = e0 + g + n <= row_end;  // VW-uniform: no row boundary in this group
-    float part[L];
+    T part[L];
 #pragma unroll
     for (int u0 = 0; u0 < L; u0 += U) {
       float4 yv[U];
@@ -133,8 +161,7 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
       }
       if (one_row) {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          part[u0 + u] = x.x * yv[u].x + x.y * yv[u].y + x.z * yv[u].z + x.w * yv[u].w;
+        for (int u = 0; u < U; ++u) part[u0 + u] = dot4<kF64>(x, yv[u]);
       } else {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -145,12 +172,12 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
               x = ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane);
             }
           }
-          part[u0 + u] = x.x * yv[u].x + x.y * yv[u].y + x.z * yv[u].z + x.w * yv[u].w;
+          part[u0 + u] = dot4<kF64>(x, yv[u]);
         }
       }
     }
-    const float dot = reduce_scatter<L>(part, lane, vmask);
-    if (lane < n) st_stream(B + e0 + g + lane, sA[g + lane] * dot);
+    const T dot = reduce_scatter<L, T>(part, lane, vmask);
+    if (lane < n) st_stream(B + e0 + g + lane, static_cast<float>(static_cast<T>(sA[g + lane]) * dot));
   }
 }
 
@@ -169,10 +196,28 @@ __global__ void sddmm_scalar_kernel(const int32_t* __restrict__ indptr,
     }
     const float* x = X + lo * d;
     const float* y = Yt + static_cast<long long>(indices[e]) * d;
-    float s = 0.f;
-    for (long long k = 0; k < d; ++k) s = fmaf(x[k], y[k], s);
-    B[e] = A[e] * s;
+    double s = 0.0;  // exact f32 products, f64 sum (see DotT)
+    for (long long k = 0; k < d; ++k) s = fma(static_cast<double>(x[k]), static_cast<double>(y[k]), s);
+    B[e] = static_cast<float>(static_cast<double>(A[e]) * s);
   }
+}
+
+// f64 accumulator of a float4 fragment: the CSR SpMM uses the hyb kernel's two-level numerics
+// (f32 FMAs over a batch of <= 8 non-zeros, folded into f64, one rounding at the store).
+struct D4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ void absorb4(D4& a, float4& p) {
+  a.x += static_cast<double>(p.x); a.y += static_cast<double>(p.y);
+  a.z += static_cast<double>(p.z); a.w += static_cast<double>(p.w);
+  p = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ float4 round4(const D4& a) {
+  return make_float4(static_cast<float>(a.x), static_cast<float>(a.y), static_cast<float>(a.z),
+                     static_cast<float>(a.w));
+}
+__device__ __forceinline__ void add_d4(D4& a, const double4& b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
 }
 
 // Row-split CSR SpMM: one virtual warp per row (the "csr" format of the reference pipeline).
@@ -190,7 +235,8 @@ spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ 
   if (r >= rows) return;
   const long long q0 = __ldg(indptr + r), q1 = __ldg(indptr + r + 1);
   if (q1 - q0 > kCsrLong) return;  // long row: spmm_csr_chunk_kernel + the two merge levels
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 part = make_float4(0.f, 0.f, 0.f, 0.f);
+  D4 acc{0.0, 0.0, 0.0, 0.0};
   for (long long g = q0; g < q1; g += L) {
     const long long q = g + lane;
     const int32_t col = q < q1 ? ld_stream(indices + q) : 0;
@@ -206,11 +252,12 @@ spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float vu = __shfl_sync(vmask, val, (u0 + u) & (L - 1), L);
-        if (u0 + u < n) fma4(acc, vu, xv[u]);
+        if (u0 + u < n) fma4(part, vu, xv[u]);
       }
+      absorb4(acc, part);
     }
   }
-  st_stream4(reinterpret_cast<float4*>(Y + r * d) + lane, acc);
+  st_stream4(reinterpret_cast<float4*>(Y + r * d) + lane, round4(acc));
 }
 
 // ---- long rows of the row-split CSR SpMM --------------------------------------------------
@@ -250,7 +297,7 @@ template <int L>
 __global__ void __launch_bounds__(kBlock)
 spmm_csr_chunk_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                       const float* __restrict__ A, const float* __restrict__ X,
-                      const long long* __restrict__ coff, long long rows, float* __restrict__ part) {
+                      const long long* __restrict__ coff, long long rows, double* __restrict__ part) {
   constexpr int U = 8, D = 4 * L;
   const int lane = threadIdx.x & (L - 1);
   const long long nvw = static_cast<long long>(gridDim.x) * kBlock / L;
@@ -260,7 +307,8 @@ spmm_csr_chunk_kernel(const int32_t* __restrict__ indptr, const int32_t* __restr
     const long long r = owner_row(coff, rows, c);
     const long long q0 = indptr[r] + (c - coff[r]) * kCsrChunk;
     const long long q1 = min64(q0 + kCsrChunk, static_cast<long long>(indptr[r + 1]));
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 pb = make_float4(0.f, 0.f, 0.f, 0.f);
+    D4 acc{0.0, 0.0, 0.0, 0.0};
     for (long long g = q0; g < q1; g += U) {
       float4 xv[U];
       float vv[U];
@@ -274,9 +322,10 @@ spmm_csr_chunk_kernel(const int32_t* __restrict__ indptr, const int32_t* __restr
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (g + u < q1) fma4(acc, vv[u], xv[u]);
+        if (g + u < q1) fma4(pb, vv[u], xv[u]);
+      absorb4(acc, pb);
     }
-    reinterpret_cast<float4*>(part + c * D)[lane] = acc;
+    reinterpret_cast<double4*>(part + c * D)[lane] = make_double4(acc.x, acc.y, acc.z, acc.w);
   }
 }
 
@@ -284,7 +333,7 @@ spmm_csr_chunk_kernel(const int32_t* __restrict__ indptr, const int32_t* __restr
 template <int L>
 __global__ void __launch_bounds__(kBlock)
 spmm_csr_group_kernel(const long long* __restrict__ coff, const long long* __restrict__ goff,
-                      long long rows, const float* __restrict__ part, float* __restrict__ l1) {
+                      long long rows, const double* __restrict__ part, double* __restrict__ l1) {
   constexpr int D = 4 * L;
   const int lane = threadIdx.x & (L - 1);
   const long long nvw = static_cast<long long>(gridDim.x) * kBlock / L;
@@ -294,9 +343,9 @@ spmm_csr_group_kernel(const long long* __restrict__ coff, const long long* __res
     const long long r = owner_row(goff, rows, g);
     const long long c0 = coff[r] + (g - goff[r]) * kCsrGroup;
     const long long c1 = min64(c0 + kCsrGroup, coff[r + 1]);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (long long c = c0; c < c1; ++c) acc = add4(acc, reinterpret_cast<const float4*>(part + c * D)[lane]);
-    reinterpret_cast<float4*>(l1 + g * D)[lane] = acc;
+    D4 acc{0.0, 0.0, 0.0, 0.0};
+    for (long long c = c0; c < c1; ++c) add_d4(acc, reinterpret_cast<const double4*>(part + c * D)[lane]);
+    reinterpret_cast<double4*>(l1 + g * D)[lane] = make_double4(acc.x, acc.y, acc.z, acc.w);
   }
 }
 
@@ -304,7 +353,7 @@ spmm_csr_group_kernel(const long long* __restrict__ coff, const long long* __res
 template <int L>
 __global__ void __launch_bounds__(kBlock)
 spmm_csr_rowsum_kernel(const long long* __restrict__ goff, long long rows,
-                       const float* __restrict__ l1, float* __restrict__ Y) {
+                       const double* __restrict__ l1, float* __restrict__ Y) {
   constexpr int D = 4 * L;
   const int lane = threadIdx.x & (L - 1);
   const long long nvw = static_cast<long long>(gridDim.x) * kBlock / L;
@@ -312,9 +361,9 @@ spmm_csr_rowsum_kernel(const long long* __restrict__ goff, long long rows,
        r += nvw) {
     const long long g0 = goff[r], g1 = goff[r + 1];
     if (g1 == g0) continue;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (long long g = g0; g < g1; ++g) acc = add4(acc, reinterpret_cast<const float4*>(l1 + g * D)[lane]);
-    st_stream4(reinterpret_cast<float4*>(Y + r * D) + lane, acc);
+    D4 acc{0.0, 0.0, 0.0, 0.0};
+    for (long long g = g0; g < g1; ++g) add_d4(acc, reinterpret_cast<const double4*>(l1 + g * D)[lane]);
+    st_stream4(reinterpret_cast<float4*>(Y + r * D) + lane, round4(acc));
   }
 }
 
@@ -325,10 +374,10 @@ __global__ void spmm_csr_scalar_kernel(const int32_t* __restrict__ indptr,
   const long long r = blockIdx.x;
   if (r >= rows) return;
   for (long long f = threadIdx.x; f < d; f += blockDim.x) {
-    float acc = 0.f;
+    double acc = 0.0;  // exact products, f64 sum, one rounding
     for (long long q = indptr[r]; q < indptr[r + 1]; ++q)
-      acc = fmaf(A[q], X[static_cast<long long>(indices[q]) * d + f], acc);
-    Y[r * d + f] = acc;
+      acc = fma(static_cast<double>(A[q]), static_cast<double>(X[static_cast<long long>(indices[q]) * d + f]), acc);
+    Y[r * d + f] = static_cast<float>(acc);
   }
 }
 
@@ -355,11 +404,10 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
   auto smem_for = [&](int L) { return (kBlock / L) * 2 * kNnzPerChunk * 4; };
   const bool staged = aligned && reinterpret_cast<uintptr_t>(indices) % 16 == 0 &&
                       reinterpret_cast<uintptr_t>(A) % 16 == 0;
-  static bool configured = false;
-  if (!configured) {  // d = 32: 64 KB per block
+  static PerDeviceOnce once;  // d = 32: 64 KB per block
+  once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8)));
-    configured = true;
-  }
+  });
   if (staged && d == 32)
     sddmm_kernel<8><<<blocks_for(8), kBlock, smem_for(8), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   else if (staged && d == 64)
@@ -411,8 +459,8 @@ void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float*
     STRATA_CUDA_CHECK(cudaFreeAsync(nch, s));
     return;
   }
-  float* part = static_cast<float*>(workspace_alloc(sizeof(float) * (max_chunks + max_groups) * d, s));
-  float* l1 = part + max_chunks * d;
+  double* part = static_cast<double*>(workspace_alloc(sizeof(double) * (max_chunks + max_groups) * d, s));
+  double* l1 = part + max_chunks * d;
   const unsigned gc = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((max_chunks * L + kBlock - 1) / kBlock, 148LL * 64)));
   const unsigned gg = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((max_groups * L + kBlock - 1) / kBlock, 148LL * 64)));
   const unsigned grr = static_cast<unsigned>(std::min<long long>((rows * L + kBlock - 1) / kBlock, 148LL * 64));

@@ -48,8 +48,6 @@ struct strata_rgms {
   int nlong = 0, nchunks = 0;     // rows with > kLong edges and their kChunk-edge chunks
   DevBuf<int32_t> long_rows;     // [nlong] ascending
   DevBuf<int32_t> chunk_off;     // [nlong+1] first chunk of long row li
-  mutable DevBuf<float> T;       // [nnz][d_out] message rows, grown on demand
-  mutable DevBuf<float> partial; // [nchunks][d_out] long-row chunk sums
 };
 
 namespace {
@@ -700,15 +698,14 @@ __global__ void gather_i32_kernel(const int32_t* __restrict__ idx, const int32_t
 
 template <int DIN, int DOUT>
 void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat16* W, float* Y,
-                 cudaStream_t s) {
+                 float* T, float* partial, cudaStream_t s) {
   using SM = RgmsWsSmem<DIN, DOUT>;
   constexpr int smem = SM::kBytes;
   auto* k1 = rgms_edge_gemm_kernel<DIN, DOUT>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce once;
+  once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  });
   // Resident CTAs per SM: shared memory (~227 KB usable) and TMEM (512 columns) bound it.  (The
   // occupancy API reports 2 at C4's 74 KB; a grid of 3 per SM measured 0.398 vs 0.537 ms.)
   const int per_sm = std::max(1, std::min({STRATA_RGMS_CTAS, (227 * 1024) / (smem + 2048),
@@ -716,7 +713,7 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
   const long long grid = std::min<long long>(h.ntiles, static_cast<long long>(num_sms()) * per_sm);
   const CUtensorMap wmap = make_tensor_map_bf16_2d(W, h.R * DIN, DOUT, 8, DIN, CU_TENSOR_MAP_SWIZZLE_NONE);
   k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kWsThreads, smem, s>>>(wmap, X, h.edges.p,
-                                                                                   h.ntiles, h.T.p, Y);
+                                                                                   h.ntiles, T, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
   const long long lanes = h.m * RowSumShape<DOUT>::kL;
   // Grid: up to 32 CTAs per SM (~1.6 warp-blocks of 32 rows per warp at C4) — CTAs retire and
@@ -727,11 +724,11 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
   const int wpb = 8;
   const int cblk = h.nlong > 0 ? (h.nchunks + wpb - 1) / wpb : 0;
   rgms_row_sum_kernel<DOUT><<<static_cast<unsigned>(std::max<long long>(blocks, 1) + cblk), 256, 0, s>>>(
-      h.dptr.p, h.T.p, h.m, Y, h.dbits.p, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks,
-      h.partial.p, cblk);
+      h.dptr.p, T, h.m, Y, h.dbits.p, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks,
+      partial, cblk);
   if (h.nlong > 0) {
     rgms_long_finish_kernel<DOUT><<<static_cast<unsigned>((h.nlong + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
-        h.long_rows.p, h.chunk_off.p, h.nlong, h.partial.p, Y);
+        h.long_rows.p, h.chunk_off.p, h.nlong, partial, Y);
   }
   STRATA_CUDA_CHECK(cudaGetLastError());
 }
@@ -929,21 +926,21 @@ extern "C" int strata_rgms_run_bf16(const strata_rgms* h, const void* X_bf16, co
     }
     const size_t need = static_cast<size_t>(std::max<int64_t>(h->trows, 1)) * d_out;
     const size_t pneed = static_cast<size_t>(h->nchunks) * d_out;
-    if (h->T.n < need || h->partial.n < pneed) {
-      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));  // earlier runs may still read the old T
-      if (h->T.n < need) h->T.alloc(need);
-      if (h->partial.n < pneed) h->partial.alloc(pneed);
-    }
+    // Per-run scratch from the stream-ordered pool (cached there), so a plan may be run on
+    // several streams at once: message rows T, then the long rows' chunk partials.
+    float* T = static_cast<float*>(workspace_alloc(sizeof(float) * (need + pneed), s));
+    float* partial = T + need;
     const auto* X = static_cast<const __nv_bfloat16*>(X_bf16);
     const auto* W = static_cast<const __nv_bfloat16*>(W_bf16);
 #define STRATA_RGMS_CASE(I, O) \
-  case I * 1000 + O: launch_rgms<I, O>(*h, X, W, Y, s); break;
+  case I * 1000 + O: launch_rgms<I, O>(*h, X, W, Y, T, partial, s); break;
     switch (d_in * 1000 + d_out) {
       STRATA_RGMS_CASE(16, 16) STRATA_RGMS_CASE(16, 32) STRATA_RGMS_CASE(32, 16)
       STRATA_RGMS_CASE(32, 32) STRATA_RGMS_CASE(32, 64) STRATA_RGMS_CASE(64, 32)
       STRATA_RGMS_CASE(64, 64) STRATA_RGMS_CASE(32, 128) STRATA_RGMS_CASE(64, 128)
     }
 #undef STRATA_RGMS_CASE
+    STRATA_CUDA_CHECK(cudaFreeAsync(T, s));
   });
 }
 
@@ -958,7 +955,7 @@ extern "C" int strata_rgms_info(const strata_rgms* h, int64_t* tiles_bound, int6
 extern "C" int strata_rgms_destroy(strata_rgms* h) {
   return guarded([&] {
     if (h) {
-      cudaSetDevice(h->device);
+      DeviceGuard g(h->device);  // free on the plan's device, then restore the caller's
       delete h;
     }
   });

@@ -251,13 +251,14 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
       put_f64<L, VEC, kScalar, false>(a.carry + ((P.carry_off + c) * 2 + 1) * d, acc, d, lane, feat0);
     } else {
       const long long dest = cur_dest;
-      if (a.yacc)  // c > 1: partitions accumulate in f64, rounded once at the end
+      if (a.yacc) {  // c > 1: partitions accumulate in f64, rounded once at the end
         put_f64<L, VEC, kScalar, true>(a.yacc + dest * d, acc, d, lane, feat0);
-      else
+      } else {
         put_row<L, VEC, kScalar>(a.Y.p[0] + dest * d, acc, d, lane, feat0);
         if constexpr (kMulti)  // replicas of the fused all-gather (separate instantiation:
           for (int i = 1; i < a.Y.n; ++i)  // the single-output kernels keep their registers)
             put_row<L, VEC, kScalar>(a.Y.p[i] + dest * d, acc, d, lane, feat0);
+      }
     }
     acc.zero();
     first_group = false;
@@ -540,14 +541,13 @@ void launch_variant_m(const SpmmArgs& args, long long total_chunks, long long d,
   dim3 grid(blocks, kScalar ? static_cast<unsigned>((d + 31) / 32) : 1u);
   constexpr int smem = (kBlock / L) * 3 * kPiece * 4;  // 3 KB staging per virtual warp
   auto* kern = spmm_hyb_kernel<L, VEC, kScalar, kMulti>;
-  static bool configured = false;  // host-side, once per instantiation
-  if (!configured) {
+  static PerDeviceOnce once;  // per instantiation and device
+  once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 #ifdef STRATA_SPMM_CARVEOUT  // A/B knob: prefer the largest shared-memory carveout
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 #endif
-    configured = true;
-  }
+  });
   kern<<<grid, kBlock, smem, s>>>(args);
 }
 
@@ -582,17 +582,21 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     else if (d == 512) { L = 32; VEC = 4; scalar = false; }
   }
 
-  if (h.carry_d != d) {
-    h.carry.alloc(static_cast<size_t>(h.total_chunks_carry) * 2 * d);
-    h.carry_l2.alloc(static_cast<size_t>(h.l2_slots) * d);
-    h.carry_d = d;
-  }
-  // c > 1: partitions accumulate into an f64 [rows][d] workspace, rounded to Y once at the end.
-  double* yacc = nullptr;
-  if (h.c > 1 && h.rows > 0) {
-    if (h.yacc.n < static_cast<size_t>(h.rows * d)) h.yacc.alloc(static_cast<size_t>(h.rows * d));
-    yacc = h.yacc.p;
-    STRATA_CUDA_CHECK(cudaMemsetAsync(yacc, 0, sizeof(double) * h.rows * d, s));
+  // Per-call scratch from the stream-ordered pool (cached there): split-row carries, level-2
+  // partials and, for c > 1, the f64 [rows][d] accumulator the partitions add into (rounded to
+  // Y once at the end).  Nothing mutable lives in the handle, so calls on different streams
+  // do not share scratch.
+  const size_t n_carry = static_cast<size_t>(h.total_chunks_carry) * 2 * d;
+  const size_t n_l2 = static_cast<size_t>(h.l2_slots) * d;
+  const size_t n_yacc = (h.c > 1 && h.rows > 0) ? static_cast<size_t>(h.rows) * d : 0;
+  double* scratch = (n_carry + n_l2 + n_yacc) > 0
+                        ? static_cast<double*>(workspace_alloc(sizeof(double) * (n_carry + n_l2 + n_yacc), s))
+                        : nullptr;
+  double* carry = scratch;
+  double* carry_l2 = scratch ? scratch + n_carry : nullptr;
+  double* yacc = n_yacc ? scratch + n_carry + n_l2 : nullptr;
+  if (yacc) {
+    STRATA_CUDA_CHECK(cudaMemsetAsync(yacc, 0, sizeof(double) * n_yacc, s));
   } else if (h.n_empty > 0) {
     const long long total = h.n_empty * d;
     const unsigned blocks = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 4096));
@@ -607,7 +611,7 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     const int part_id = h.parts[pi].partition;
     SpmmArgs args{};
     args.I = h.I.p; args.J = h.J.p; args.V = h.V.p; args.X = X; args.Y = Y;
-    args.carry = h.carry.p; args.yacc = yacc; args.d = d;
+    args.carry = carry; args.yacc = yacc; args.d = d;
     long long chunks = 0;
     int np = 0;
     for (; pi < h.parts.size() && h.parts[pi].partition == part_id; ++pi) {
@@ -637,19 +641,19 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
       if (nt > 0) {
         if (vec2)
           spmm_fixup_tiles_kernel<2><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
-              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, yacc, d);
+              h.fix_tiles.p + R.tile_begin, carry, carry_l2, Y, yacc, d);
         else
           spmm_fixup_tiles_kernel<1><<<static_cast<unsigned>(nt), kFixBlock, 0, s>>>(
-              h.fix_tiles.p + R.tile_begin, h.carry.p, h.carry_l2.p, Y, yacc, d);
+              h.fix_tiles.p + R.tile_begin, carry, carry_l2, Y, yacc, d);
         STRATA_CUDA_CHECK(cudaGetLastError());
       }
       if (nr > 0) {
         if (vec2)
           spmm_fixup_runs_kernel<2><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
-              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, yacc, d);
+              h.fix_runs.p + R.run_begin, carry_l2, Y, yacc, d);
         else
           spmm_fixup_runs_kernel<1><<<static_cast<unsigned>(nr), kFixBlock, 0, s>>>(
-              h.fix_runs.p + R.run_begin, h.carry_l2.p, Y, yacc, d);
+              h.fix_runs.p + R.run_begin, carry_l2, Y, yacc, d);
         STRATA_CUDA_CHECK(cudaGetLastError());
       }
     }
@@ -660,6 +664,7 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
         yacc, Y, n);
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
+  if (scratch) STRATA_CUDA_CHECK(cudaFreeAsync(scratch, s));
 }
 
 }  // namespace strata_b200

@@ -242,12 +242,11 @@ void launch_srbcrs(const strata_srbcrs& h, const __nv_bfloat16* X, float* Y, cud
   constexpr int kM = D == 64 ? 64 : 128;
   constexpr int kN = kM == 64 ? 8 : 16;
   constexpr int smem = kStages * (kG * D * 2 + kG * kN * 2) + 1024;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce once;
+  once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(srbcrs_spmm_tc_kernel<D>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  });
   const CUtensorMap xmap = make_tensor_map_bf16_2d(X, h.cols, D, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   srbcrs_spmm_tc_kernel<D><<<static_cast<unsigned>(h.mb), kThreads, smem, s>>>(
       xmap, h.gptr.p, h.jt.p, h.vals_bf.p, h.rows, Y);

@@ -46,6 +46,29 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def _dense(t, name: str, shape, dtype: str, device=None):
+    """Binding check of a dense device operand before its raw pointer crosses the C ABI (which
+    cannot see shapes): the reference's interpret() rejects a wrongly sized binding with
+    ErrKind::Exec "binding size mismatch for <name>: got <n>, declared <m>" (interp.cpp:576-582);
+    dtype, layout (row-major contiguous) and device are checked the same way."""
+    import torch
+    want = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}[dtype]
+    if not isinstance(t, torch.Tensor):
+        raise StrataError(7, f"binding for {name} must be a torch tensor")
+    got_n, want_n = int(t.numel()), int(np.prod(shape))
+    if tuple(t.shape) != tuple(shape):
+        raise StrataError(7, f"binding size mismatch for {name}: got {got_n} "
+                             f"{list(t.shape)}, declared {want_n} {list(shape)}")
+    if t.dtype != want:
+        raise StrataError(7, f"binding dtype mismatch for {name}: got {t.dtype}, declared {dtype}")
+    if not t.is_contiguous():
+        raise StrataError(7, f"binding for {name} must be row-major contiguous")
+    if t.device.type != "cuda" or (device is not None and t.device != device):
+        raise StrataError(7, f"binding for {name} is on {t.device}, expected "
+                             f"{device if device is not None else 'a CUDA device'}")
+    return t
+
+
 def _stream(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -254,9 +277,13 @@ def hyb_rules(csr: DeviceCsr, c: int, k: int, name: str = "hyb"):
 def spmm(hyb: HybDecomposition, X, Y=None, stream=None):
     """Y = A @ X over the hyb decomposition (device tensors, f32).  Y is overwritten."""
     import torch
-    d = X.shape[1]
+    if getattr(X, "dim", lambda: 0)() != 2:
+        raise StrataError(7, "binding for X must be a [cols][d] matrix")
+    d = int(X.shape[1])
+    _dense(X, "X", (hyb.cols, d), "f32")
     if Y is None:
         Y = torch.empty((hyb.rows, d), dtype=torch.float32, device=X.device)
+    _dense(Y, "Y", (hyb.rows, d), "f32", X.device)
     check(lib.strata_spmm_hyb_f32(hyb.handle, _ptr(X), _ptr(Y), d, _stream(stream)))
     return Y
 
@@ -270,22 +297,43 @@ def gnn_layer(hyb: HybDecomposition, X, W, Z=None, work=None, stream=None):
     """GNN layer step Z = A @ X @ W (f32, device): hyb SpMM aggregation + fp32 cuBLAS transform,
     associated so the SpMM gathers the narrower rows (strata_gnn_layer_f32)."""
     import torch
-    d_in, d_out = X.shape[1], W.shape[1]
+    d_in, d_out = int(X.shape[1]), int(W.shape[1])
     if W.shape[0] != d_in:
         raise StrataError(6, "gnn_layer: W must be [d_in][d_out]")
+    _dense(X, "X", (hyb.cols, d_in), "f32")
+    _dense(W, "W", (d_in, d_out), "f32", X.device)
     if Z is None:
         Z = torch.empty((hyb.rows, d_out), dtype=torch.float32, device=X.device)
+    _dense(Z, "Z", (hyb.rows, d_out), "f32", X.device)
+    need = max(gnn_layer_work_floats(hyb, d_in, d_out), 1)
     if work is None:
-        work = torch.empty(max(gnn_layer_work_floats(hyb, d_in, d_out), 1), dtype=torch.float32,
-                           device=X.device)
+        work = torch.empty(need, dtype=torch.float32, device=X.device)
+    if work.numel() < need or work.dtype != torch.float32 or not work.is_contiguous():
+        raise StrataError(7, f"binding size mismatch for work: got {work.numel()}, declared {need}")
     check(lib.strata_gnn_layer_f32(hyb.handle, _ptr(X), _ptr(W), _ptr(Z), _ptr(work), d_in, d_out,
                                    _stream(stream)))
     return Z
 
 
+def _host(t, name: str, shape):
+    """Binding check of a host (pinned) f32 operand of the end-to-end entry points."""
+    import torch
+    if isinstance(t, torch.Tensor):
+        ok = t.device.type == "cpu" and t.dtype == torch.float32 and t.is_contiguous()
+    else:
+        ok = isinstance(t, np.ndarray) and t.dtype == np.float32 and t.flags.c_contiguous
+    if not ok:
+        raise StrataError(7, f"binding for {name} must be a contiguous f32 host array")
+    if tuple(t.shape) != tuple(shape):
+        raise StrataError(7, f"binding size mismatch for {name}: got {int(np.prod(t.shape))}, "
+                             f"declared {int(np.prod(shape))}")
+
+
 def spmm_host(hyb: HybDecomposition, X_host, Y_host, stream=None):
     """End-to-end form: host (pinned) X in, host Y out, copies inside the call."""
-    d = X_host.shape[1]
+    d = int(X_host.shape[1])
+    _host(X_host, "X", (hyb.cols, d))
+    _host(Y_host, "Y", (hyb.rows, d))
     check(lib.strata_spmm_hyb_f32_host(hyb.handle, _ptr(X_host), _ptr(Y_host), d,
                                        _stream(stream)))
     return Y_host
@@ -294,7 +342,8 @@ def spmm_host(hyb: HybDecomposition, X_host, Y_host, stream=None):
 def spmm_multi(hyb: HybDecomposition, X, dst_ptrs, stream=None):
     """Y rows of ``hyb`` stored to every device address in ``dst_ptrs`` (ints: row-major
     [rows][d] f32 buffers, possibly peer-mapped; see sharding.PeerAllGather)."""
-    d = X.shape[1]
+    d = int(X.shape[1])
+    _dense(X, "X", (hyb.cols, d), "f32")
     n = len(dst_ptrs)
     arr = (C.c_void_p * n)(*dst_ptrs)
     check(lib.strata_spmm_hyb_f32_multi(hyb.handle, _ptr(X), C.cast(arr, C.c_void_p), n, d,
@@ -328,7 +377,10 @@ def spmm_host_batch(hyb: HybDecomposition, X_hosts, Y_hosts, stream=None):
     n = len(X_hosts)
     if n == 0:
         return Y_hosts
-    d = X_hosts[0].shape[1]
+    d = int(X_hosts[0].shape[1])
+    for x, y in zip(X_hosts, Y_hosts):
+        _host(x, "X", (hyb.cols, d))
+        _host(y, "Y", (hyb.rows, d))
     xs = (C.c_void_p * n)(*[_ptr(x) for x in X_hosts])
     ys = (C.c_void_p * n)(*[_ptr(y) for y in Y_hosts])
     check(lib.strata_spmm_hyb_f32_host_batch(hyb.handle, C.cast(xs, C.c_void_p),
@@ -338,9 +390,11 @@ def spmm_host_batch(hyb: HybDecomposition, X_hosts, Y_hosts, stream=None):
 
 def spmm_csr(csr: DeviceCsr, X, Y=None, stream=None):
     import torch
-    d = X.shape[1]
+    d = int(X.shape[1])
+    _dense(X, "X", (csr.cols, d), "f32")
     if Y is None:
         Y = torch.empty((csr.rows, d), dtype=torch.float32, device=X.device)
+    _dense(Y, "Y", (csr.rows, d), "f32", X.device)
     check(lib.strata_spmm_csr_f32(_ptr(csr.indptr), _ptr(csr.indices), _ptr(csr.values), _ptr(X),
                                   _ptr(Y), csr.rows, csr.cols, d, _stream(stream)))
     return Y
@@ -349,9 +403,12 @@ def spmm_csr(csr: DeviceCsr, X, Y=None, stream=None):
 def sddmm(csr: DeviceCsr, X, Yt_dn, B=None, stream=None):
     """B[nnz] = A .* (X @ Y) on the pattern; X [rows][d], Y [d][cols] (reference layout)."""
     import torch
-    d = X.shape[1]
+    d = int(X.shape[1])
+    _dense(X, "X", (csr.rows, d), "f32")
+    _dense(Yt_dn, "Y", (d, csr.cols), "f32", X.device)
     if B is None:
         B = torch.empty((csr.nnz,), dtype=torch.float32, device=X.device)
+    _dense(B, "B", (csr.nnz,), "f32", X.device)
     check(lib.strata_sddmm_csr_f32(_ptr(csr.indptr), _ptr(csr.indices), _ptr(csr.values), _ptr(X),
                                    _ptr(Yt_dn), _ptr(B), csr.rows, csr.cols, csr.nnz, d,
                                    _stream(stream)))
@@ -412,9 +469,11 @@ def csr_to_bsr(csr: DeviceCsr, b: int, stream=None) -> BsrMatrix:
 def bsr_spmm(bsr: BsrMatrix, X_bf16, Y=None, stream=None):
     """Y[mb*b][d] (f32) = A_bsr @ X on tcgen05 tensor cores; X is bf16 [nb*b][d]."""
     import torch
-    d = X_bf16.shape[1]
+    d = int(X_bf16.shape[1])
+    _dense(X_bf16, "X", (bsr.nb * bsr.b, d), "bf16")
     if Y is None:
         Y = torch.empty((bsr.mb * bsr.b, d), dtype=torch.float32, device=X_bf16.device)
+    _dense(Y, "Y", (bsr.mb * bsr.b, d), "f32", X_bf16.device)
     check(lib.strata_bsr_spmm_bf16(bsr.handle, _ptr(X_bf16), _ptr(Y), d, _stream(stream)))
     return Y
 
@@ -425,11 +484,14 @@ def bsr_spmm_batched(bsr: BsrMatrix, values_bf16, X_bf16, Y=None, stream=None):
     values_bf16 [H][nblocks][b][b] (row-major blocks, the reference's A_bsr layout per head),
     X_bf16 [H][nb*b][d] -> Y [H][mb*b][d] f32, Y[h] = A_h @ X[h]."""
     import torch
-    H, _, d = X_bf16.shape
+    H, _, d = (int(x) for x in X_bf16.shape)
     if tuple(values_bf16.shape) != (H, bsr.nblocks, bsr.b, bsr.b):
         raise StrataError(6, "bsr_spmm_batched: values must be [heads][nblocks][b][b]")
+    _dense(X_bf16, "X", (H, bsr.nb * bsr.b, d), "bf16")
+    _dense(values_bf16, "A_bsr", (H, bsr.nblocks, bsr.b, bsr.b), "bf16", X_bf16.device)
     if Y is None:
         Y = torch.empty((H, bsr.mb * bsr.b, d), dtype=torch.float32, device=X_bf16.device)
+    _dense(Y, "Y", (H, bsr.mb * bsr.b, d), "f32", X_bf16.device)
     check(lib.strata_bsr_spmm_bf16_batched(bsr.handle, _ptr(values_bf16), _ptr(X_bf16), _ptr(Y),
                                            H, d, _stream(stream)))
     return Y
@@ -478,9 +540,11 @@ def csr_to_dbsr(csr: DeviceCsr, b: int, stream=None) -> DbsrMatrix:
 def dbsr_spmm(dbsr: DbsrMatrix, X_bf16, Y=None, stream=None):
     """Y[mb*b][d] (f32) = A_dbsr @ X on tcgen05 (stored block rows only)."""
     import torch
-    d = X_bf16.shape[1]
+    d = int(X_bf16.shape[1])
+    _dense(X_bf16, "X", (dbsr.nb * dbsr.b, d), "bf16")
     if Y is None:
         Y = torch.empty((dbsr.mb * dbsr.b, d), dtype=torch.float32, device=X_bf16.device)
+    _dense(Y, "Y", (dbsr.mb * dbsr.b, d), "f32", X_bf16.device)
     check(lib.strata_dbsr_spmm_bf16(dbsr.handle, _ptr(X_bf16), _ptr(Y), d, _stream(stream)))
     return Y
 
@@ -522,9 +586,12 @@ def csr_to_srbcrs(csr: DeviceCsr, t: int, g: int, stream=None) -> SrbcrsMatrix:
 def srbcrs_spmm(sr: SrbcrsMatrix, X_bf16, Y=None, stream=None):
     """Y[mb*t][d] (f32) = A_srbcrs @ X on tcgen05 (t = 8, g = 32)."""
     import torch
-    d = X_bf16.shape[1]
+    d = int(X_bf16.shape[1])
+    if X_bf16.dtype != torch.bfloat16 or not X_bf16.is_contiguous() or X_bf16.dim() != 2:
+        raise StrataError(7, "binding for X must be a contiguous bf16 [cols][d] matrix")
     if Y is None:
         Y = torch.empty((sr.mb * sr.t, d), dtype=torch.float32, device=X_bf16.device)
+    _dense(Y, "Y", (sr.mb * sr.t, d), "f32", X_bf16.device)
     check(lib.strata_srbcrs_spmm_bf16(sr.handle, _ptr(X_bf16), _ptr(Y), d, _stream(stream)))
     return Y
 
@@ -549,8 +616,12 @@ class AttentionPlan:
         """Z[i] = sum_j softmax_j(A_ij <Q_i, K_j>) V_j over the stored j of row i."""
         import torch
         d = int(Q.shape[1])
+        _dense(Q, "Q", (self.csr.rows, d), "f32")
+        _dense(K, "K", (self.csr.cols, d), "f32", Q.device)
+        _dense(V, "V", (self.csr.cols, d), "f32", Q.device)
         if Z is None:
             Z = torch.empty((self.csr.rows, d), dtype=torch.float32, device=Q.device)
+        _dense(Z, "Z", (self.csr.rows, d), "f32", Q.device)
         check(lib.strata_attn_csr_f32(self._h, _ptr(self.csr.indptr), _ptr(self.csr.indices),
                                       _ptr(self.csr.values), _ptr(Q), _ptr(K), _ptr(V), _ptr(Z), d,
                                       _stream(stream)))
@@ -572,9 +643,12 @@ def bsr_sddmm(bsr: BsrMatrix, Q_bf16, K_bf16, S=None, stream=None):
     import torch
     Q3 = Q_bf16 if Q_bf16.dim() == 3 else Q_bf16.unsqueeze(0)
     K3 = K_bf16 if K_bf16.dim() == 3 else K_bf16.unsqueeze(0)
-    H, _, d = Q3.shape
+    H, _, d = (int(x) for x in Q3.shape)
+    _dense(Q3, "Q", (H, bsr.mb * bsr.b, d), "bf16")
+    _dense(K3, "K", (H, bsr.nb * bsr.b, d), "bf16", Q3.device)
     if S is None:
         S = torch.empty((H, bsr.nblocks, bsr.b, bsr.b), dtype=torch.float32, device=Q3.device)
+    _dense(S, "S", (H, bsr.nblocks, bsr.b, bsr.b), "f32", Q3.device)
     check(lib.strata_bsr_sddmm_bf16(bsr.handle, _ptr(Q3), _ptr(K3), _ptr(S), H, d, _stream(stream)))
     return S
 
@@ -654,8 +728,11 @@ class RgmsPlan:
     def run(self, X_bf16, W_bf16, Y=None, stream=None):
         import torch
         d_in, d_out = int(W_bf16.shape[1]), int(W_bf16.shape[2])
+        _dense(X_bf16, "X", (self.cols, d_in), "bf16")
+        _dense(W_bf16, "W", (self.relations, d_in, d_out), "bf16", X_bf16.device)
         if Y is None:
             Y = torch.empty((self.rows, d_out), dtype=torch.float32, device=X_bf16.device)
+        _dense(Y, "Y", (self.rows, d_out), "f32", X_bf16.device)
         check(lib.strata_rgms_run_bf16(self._h, _ptr(X_bf16), _ptr(W_bf16), _ptr(Y), d_in, d_out,
                                        _stream(stream)))
         return Y
@@ -676,8 +753,11 @@ def rgms(rel, X_bf16, W_bf16, Y=None, stream=None):
     if isinstance(rel, RgmsPlan):
         return rel.run(X_bf16, W_bf16, Y, stream)
     d_in, d_out = int(W_bf16.shape[1]), int(W_bf16.shape[2])
+    _dense(X_bf16, "X", (rel.cols, d_in), "bf16")
+    _dense(W_bf16, "W", (rel.relations, d_in, d_out), "bf16", X_bf16.device)
     if Y is None:
         Y = torch.empty((rel.rows, d_out), dtype=torch.float32, device=X_bf16.device)
+    _dense(Y, "Y", (rel.rows, d_out), "f32", X_bf16.device)
     check(lib.strata_rgms_bf16(_ptr(rel.rel_ptr), _ptr(rel.dst), _ptr(rel.src), _ptr(rel.A),
                                rel.relations, rel.rows, rel.cols, rel.nnz, _ptr(X_bf16),
                                _ptr(W_bf16), _ptr(Y), d_in, d_out, _stream(stream)))

@@ -69,3 +69,26 @@ def test_partition_rows_balanced_by_nnz():
             target = (m.nnz * p) // parts
             assert m.indptr[b[p]] >= target
             assert b[p] == 0 or m.indptr[b[p] - 1] < target
+
+
+def test_python_binding_checks_reject_bad_operands():
+    """ops.py checks shape / dtype / layout / device before a raw pointer crosses the C ABI,
+    with the reference's ErrKind::Exec wording (interp.cpp:576-582)."""
+    import torch
+    from paper_2207_04606_b200 import ops
+    X = torch.zeros(4, 8)
+    with pytest.raises(ops.StrataError) as e:          # host tensor where device memory is due
+        ops._dense(X, "X", (4, 8), "f32")
+    assert e.value.kind == "Exec"
+    with pytest.raises(ops.StrataError) as e:
+        ops._dense(X, "X", (5, 8), "f32")
+    assert "binding size mismatch for X: got 32" in str(e.value)
+    with pytest.raises(ops.StrataError) as e:
+        ops._dense(X.to(torch.float64), "X", (4, 8), "f32")
+    assert "dtype mismatch" in str(e.value)
+    with pytest.raises(ops.StrataError) as e:
+        ops._dense(X.t(), "X", (8, 4), "f32")
+    assert "contiguous" in str(e.value)
+    ops._host(X, "X", (4, 8))
+    with pytest.raises(ops.StrataError):
+        ops._host(X, "X", (4, 9))

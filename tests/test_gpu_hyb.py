@@ -36,11 +36,13 @@ def close_ref_metric(got, want, tol=TOL):
     return ref_metric_err(got, want) <= tol
 
 
-def close_to_f64(got, want64, ref_f32):
-    """Real-valued parity bar: within 1e-5 of the reference's F64 pipeline (the north_star's
-    rel-err), or — where the reference's own F32 pipeline (ref_f32, bit-exact via the oracle)
-    is itself further than 1e-5 from F64 (long rows / cancellation) — no worse than it."""
-    return ref_metric_err(got, want64) <= max(TOL, ref_metric_err(ref_f32, want64))
+def close_to_f64(got, want64):
+    """Real-valued parity bar, strict: |x - y| <= 1e-5 * max(|x|, |y|, 1) against the
+    reference's F64 pipeline (driver.cpp:124-144 metric; the north_star's rel-err), with no
+    allowance for the reference F32 pipeline's own drift."""
+    err = ref_metric_err(got, want64)
+    assert err <= TOL, f"rel-err {err:.3e} > {TOL:g} vs the F64 reference"
+    return True
 
 
 def csr_of(G, name):
@@ -125,7 +127,7 @@ def test_spmm_golden(cuda, G):
                     if tag == "int":
                         assert np.array_equal(Y, G[key + "/Y"]), (key, c, k)
                     else:
-                        assert close_to_f64(Y, G[key + "/Y64"], G[key + "/Y"]), (key, c, k)
+                        assert close_to_f64(Y, G[key + "/Y64"]), (key, c, k)
             Yc = S.spmm_csr(dcsr, torch.from_numpy(G[f"{name}/spmm_d32_int/X"]).to(cuda))
             assert np.array_equal(Yc.cpu().numpy(), G[f"{name}/spmm_d32_int/Y"])
 
@@ -163,7 +165,7 @@ def test_spmm_long_split_rows_deterministic(cuda):
             xr = Xr.cpu().numpy()
             want64 = port.spmm_csr_f64(m.rows, m.indptr, m.indices, m.values, xr)
             ref32 = port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, xr)
-            assert close_to_f64(r1, want64, ref32), (c, k, d)
+            assert close_to_f64(r1, want64), (c, k, d)
             # and clearly better than the reference's own f32 accumulation on long rows
             assert ref_metric_err(r1, want64) <= ref_metric_err(ref32, want64)
 
@@ -253,4 +255,6 @@ def test_spmm_csr_long_rows(cuda, d):
     Yr = S.spmm_csr(dm, torch.from_numpy(xr).to(cuda)).cpu().numpy()
     want64 = port.spmm_csr_f64(m.rows, m.indptr, m.indices, m.values, xr)
     ref32 = port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, xr)
-    assert close_to_f64(Yr, want64, ref32)
+    assert close_to_f64(Yr, want64)
+    # the reference F32 order itself drifts on these hub rows; ours must not be worse
+    assert ref_metric_err(Yr, want64) <= max(ref_metric_err(ref32, want64), 1e-7)

@@ -29,7 +29,7 @@ def test_sddmm_golden(cuda, G):
             key = f"{name}/sddmm_d{d}"
             B = S.sddmm(dcsr, torch.from_numpy(G[key + "/X"]).to(cuda),
                         torch.from_numpy(G[key + "/Yd"]).to(cuda)).cpu().numpy()
-            assert close_to_f64(B, G[key + "/B64"], G[key + "/B"]), key
+            assert close_to_f64(B, G[key + "/B64"]), key
 
 
 @pytest.mark.parametrize("d", [32, 64, 128, 16, 7])
@@ -44,19 +44,43 @@ def test_sddmm_integer_exact(cuda, d):
     assert np.array_equal(got, want)
 
 
-def test_sddmm_empty_rows_and_real(cuda):
+@pytest.mark.parametrize("seed", range(8))
+def test_sddmm_real_strict(cuda, seed):
+    """Real-valued N(0,1) operands, the reference generator's A in 1..9, many empty rows: the
+    64-term dots cancel, so f32 dot products miss the bar (measured 0.73-1.12e-5, and the
+    reference's own F32 pipeline 0.95-2.14e-5); ours (exact f64 products and f64 reduction,
+    one rounding) must be within 1e-5 of the reference F64 pipeline, asserted strictly."""
     import torch
     m = S.generate_matrix("powerlaw", 3000, 3000, 0, 0, 0, 2.0, 9)  # many empty rows
     assert (np.diff(m.indptr) == 0).any()
-    # Seeded: 64-term dots of N(0,1) data cancel, and both f32 pipelines sit near the 1e-5
-    # line (measured over seeds 0-7: ours 0.73-1.12e-5, the reference F32 0.95-2.14e-5).
-    for seed in (0, 1, 2):
+    for d in (32, 64, 128):
         gen = torch.Generator(device=cuda)
-        gen.manual_seed(seed)
-        X = torch.randn(m.rows, 64, device=cuda, generator=gen)
-        Yd = torch.randn(64, m.cols, device=cuda, generator=gen)
+        gen.manual_seed(seed * 7 + d)
+        X = torch.randn(m.rows, d, device=cuda, generator=gen)
+        Yd = torch.randn(d, m.cols, device=cuda, generator=gen)
         got = S.sddmm(m.to_device(cuda), X, Yd).cpu().numpy()
         x, yd = X.cpu().numpy(), Yd.cpu().numpy()
         want = port.sddmm_csr_f64(m.rows, m.cols, m.indptr, m.indices, m.values, x, yd)
-        ref32 = port.sddmm_csr_refnum(m.rows, m.cols, m.indptr, m.indices, m.values, x, yd)
-        assert close_to_f64(got, want, ref32), seed
+        assert close_to_f64(got, want), (seed, d)
+
+
+def test_sddmm_c2_row_sample_real(cuda):
+    """BASELINE configs[1] (Reddit shape, 114.6M nnz, d = 64) on real-valued operands: the whole
+    SDDMM on the device, checked strictly against the F64 oracle on a sample of rows that
+    includes the densest hub rows (232,965 non-zeros each) and a stride over the rest."""
+    import torch
+    m = S.generate_matrix("powerlaw", 232965, 232965, 0, 0, 0, 567.5267, 1)
+    assert m.nnz == 114615895
+    d = 64
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(11)
+    X = torch.randn(m.rows, d, device=cuda, generator=gen)
+    Yd = torch.randn(d, m.cols, device=cuda, generator=gen)
+    B = S.sddmm(m.to_device(cuda), X, Yd).cpu().numpy()
+    lens = np.diff(m.indptr)
+    rows = np.unique(np.r_[np.argsort(lens)[-3:], np.arange(0, m.rows, 997)])
+    sub_ptr = np.r_[0, np.cumsum(lens[rows])].astype(np.int32)
+    sel = np.concatenate([np.arange(m.indptr[r], m.indptr[r + 1]) for r in rows])
+    x, yd = X.cpu().numpy(), Yd.cpu().numpy()
+    want = port.sddmm_csr_f64(len(rows), m.cols, sub_ptr, m.indices[sel], m.values[sel], x[rows], yd)
+    assert close_to_f64(B[sel], want)
