@@ -131,15 +131,22 @@ int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_ho
                                    float* const* Y_host, int64_t nbatch, int64_t d, void* stream);
 
 /* ---- GNN layer step: Z = A · X · W (GraphSAGE/GCN layer)
- * Sparse aggregation on the hyb SpMM, dense transform as a plain fp32 cuBLAS SGEMM (pedantic
- * fp32 math, no TF32).  Associated so the SpMM gathers the narrower rows: d_out < d_in computes
- * T = X·W then Z = A·T, otherwise Y = A·X then Z = Y·W.  X[cols][d_in], W[d_in][d_out],
- * Z[rows][d_out] f32 row-major (device); `work` holds strata_gnn_layer_work_floats() floats
- * (T or Y).  Exact on integer operands whose partial sums fit f32; otherwise within
- * 1e-5 * max(|x|, |y|, 1) of the f64 product. */
+ * Sparse aggregation on the hyb SpMM, dense transform on the tensor cores (strata_gemm_f32).
+ * Associated so the SpMM gathers the narrower rows: d_out < d_in computes T = X·W then Z = A·T,
+ * otherwise Y = A·X then Z = Y·W.  X[cols][d_in], W[d_in][d_out], Z[rows][d_out] f32 row-major
+ * (device); `work` holds strata_gnn_layer_work_floats() floats (T or Y).  Exact on integer
+ * operands whose partial sums fit f32; otherwise within 1e-5 * max(|x|, |y|, 1) of the f64
+ * product. */
 int64_t strata_gnn_layer_work_floats(const strata_hyb* h, int64_t d_in, int64_t d_out);
 int strata_gnn_layer_f32(const strata_hyb* h, const float* X, const float* W, float* Z,
                          float* work, int64_t d_in, int64_t d_out, void* stream);
+
+/* Dense transform Z[M][N] = Y[M][K] · W[K][N] (f32, row-major, device): tcgen05.mma kind::tf32
+ * with the 3xTF32 split (a = a_hi + a_lo, products a_lo·w_hi + a_hi·w_lo + a_hi·w_hi accumulated
+ * in f32 in TMEM), persistent 128-row tiles, W's tile resident in shared memory.  Tensor-core
+ * path for K % 32 == 0 and N % 16 == 0; other shapes run an f64-accumulating CUDA-core kernel. */
+int strata_gemm_f32(const float* Y, const float* W, float* Z, int64_t M, int64_t K, int64_t N,
+                    void* stream);
 
 /* Multi-destination form — the fused SpMM + all-gather of a row-sharded multi-GPU run: every
  * output row of h (local row i) is stored to Y_dsts[0 .. ndst-1][i][0 .. d-1] (ndst <= 8).  The

@@ -80,6 +80,7 @@ _sig("strata_hyb_dims", C.c_int, vp, i64p, i64p, C.POINTER(C.c_int), C.POINTER(C
 _sig("strata_hyb_destroy", C.c_int, vp)
 _sig("strata_hyb_schedule_info", C.c_int, vp, i64p, i64p, i64p, i64p, C.POINTER(C.c_int))
 _sig("strata_hyb_row_work_balance", C.c_int, vp, C.POINTER(C.c_double), vp)
+_sig("strata_gemm_f32", C.c_int, vp, vp, vp, i64, i64, i64, vp)
 _sig("strata_gnn_layer_work_floats", i64, vp, i64, i64)
 _sig("strata_gnn_layer_f32", C.c_int, vp, vp, vp, vp, vp, i64, i64, vp)
 _sig("strata_spmm_hyb_f32", C.c_int, vp, vp, vp, i64, vp)
@@ -131,7 +132,7 @@ EXPORTED = [
     "strata_hyb_dims", "strata_hyb_destroy", "strata_hyb_schedule_info",
     "strata_hyb_row_work_balance", "strata_spmm_hyb_f32", "strata_spmm_hyb_f32_host",
     "strata_spmm_hyb_f32_host_batch", "strata_spmm_hyb_f32_multi", "strata_gnn_layer_work_floats",
-    "strata_gnn_layer_f32", "strata_ipc_get_handle",
+    "strata_gnn_layer_f32", "strata_gemm_f32", "strata_ipc_get_handle",
     "strata_ipc_open_handle", "strata_ipc_close",
     "strata_spmm_csr_f32", "strata_sddmm_csr_f32", "strata_bsr_from_csr", "strata_bsr_info",
     "strata_bsr_read", "strata_bsr_destroy", "strata_bsr_spmm_bf16",

@@ -10,7 +10,6 @@
 
 #include <cudaTypedefs.h>
 
-#include <cublas_v2.h>
 
 #include "capi_internal.h"
 
@@ -405,38 +404,10 @@ int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_ho
 }
 
 // GNN layer step (the GraphSAGE/GCN end-to-end pattern PAPER.md:457-460):
-// Z = A · X · W with the sparse aggregation on the hyb SpMM and the dense transform as a plain
-// fp32 cuBLAS SGEMM (no TF32).  The product is associated so the SpMM gathers the narrower
-// feature matrix: d_out < d_in -> T = X·W first, then Z = A·T; otherwise Y = A·X, Z = Y·W.
-namespace {
-cublasHandle_t cublas_for_device() {
-  static thread_local cublasHandle_t handles[64] = {};
-  int dev = 0;
-  STRATA_CUDA_CHECK(cudaGetDevice(&dev));
-  require(dev >= 0 && dev < 64, STRATA_ERR_CUDA, "device ordinal out of range");
-  if (!handles[dev]) {
-    if (cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS)
-      throw ApiError(STRATA_ERR_CUDA, "cublasCreate failed");
-    cublasSetMathMode(handles[dev], CUBLAS_PEDANTIC_MATH);  // true fp32, never TF32
-  }
-  return handles[dev];
-}
-
-// Row-major C[m][n] = A[m][k] · B[k][n]  (column-major view: C^T = B^T · A^T).
-void sgemm_rowmajor(const float* A, const float* B, float* C, int64_t m, int64_t k, int64_t n,
-                    cudaStream_t s) {
-  if (m == 0 || n == 0) return;
-  require(m <= INT32_MAX && k <= INT32_MAX && n <= INT32_MAX, STRATA_ERR_USAGE, "gemm dims");
-  cublasHandle_t hb = cublas_for_device();
-  cublasSetStream(hb, s);
-  const float one = 1.f, zero = 0.f;
-  if (cublasSgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(m),
-                  static_cast<int>(k), &one, B, static_cast<int>(n), A, static_cast<int>(k), &zero,
-                  C, static_cast<int>(n)) != CUBLAS_STATUS_SUCCESS)
-    throw ApiError(STRATA_ERR_CUDA, "cublasSgemm failed");
-}
-}  // namespace
-
+// Z = A · X · W with the sparse aggregation on the hyb SpMM and the dense transform on the
+// tensor cores (gemm_tf32.cu: tcgen05 kind::tf32 with the 3xTF32 split, fp32-accurate).  The
+// product is associated so the SpMM gathers the narrower feature matrix: d_out < d_in ->
+// T = X·W first, then Z = A·T; otherwise Y = A·X, Z = Y·W.
 int64_t strata_gnn_layer_work_floats(const strata_hyb* h, int64_t d_in, int64_t d_out) {
   if (!h || d_in < 1 || d_out < 1) return -1;
   return d_out < d_in ? h->cols * d_out : h->rows * d_in;
@@ -447,17 +418,30 @@ int strata_gnn_layer_f32(const strata_hyb* h, const float* X, const float* W, fl
   return guard([&] {
     const auto& H = hyb_of(h);
     require(d_in >= 1 && d_out >= 1, STRATA_ERR_USAGE, "gnn_layer: d_in and d_out must be >= 1");
+    require(d_in <= INT32_MAX && d_out <= INT32_MAX, STRATA_ERR_USAGE, "gnn_layer: d_in and d_out must fit int32");
     require((H.cols == 0 || X) && (H.rows == 0 || Z) && W && work, STRATA_ERR_USAGE,
             "gnn_layer: null operand");
     require_device();
     cudaStream_t s = as_stream(stream);
     if (d_out < d_in) {  // transform, then aggregate the narrower rows
-      sgemm_rowmajor(X, W, work, H.cols, d_in, d_out, s);
+      gemm_f32_launch(X, W, work, H.cols, static_cast<int>(d_in), static_cast<int>(d_out), s);
       spmm_hyb_launch(H, work, &Z, 1, d_out, s);
     } else {             // aggregate, then transform
       spmm_hyb_launch(H, X, &work, 1, d_in, s);
-      sgemm_rowmajor(work, W, Z, H.rows, d_in, d_out, s);
+      gemm_f32_launch(work, W, Z, H.rows, static_cast<int>(d_in), static_cast<int>(d_out), s);
     }
+  });
+}
+
+// Dense transform on its own (the GEMM half of the GNN layer step): tcgen05 3xTF32.
+int strata_gemm_f32(const float* Y, const float* W, float* Z, int64_t M, int64_t K, int64_t N,
+                    void* stream) {
+  return guard([&] {
+    require(M >= 0 && K >= 1 && N >= 1, STRATA_ERR_USAGE, "gemm: M >= 0, K >= 1, N >= 1 required");
+    require(K <= INT32_MAX && N <= INT32_MAX, STRATA_ERR_USAGE, "gemm: K and N must fit int32");
+    require(M == 0 || (Y && W && Z), STRATA_ERR_USAGE, "gemm: null operand");
+    require_device();
+    gemm_f32_launch(Y, W, Z, M, static_cast<int>(K), static_cast<int>(N), as_stream(stream));
   });
 }
 

@@ -171,6 +171,11 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
                      int64_t d, cudaStream_t s);
 void spmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,
                      const float* X, float* Y, int64_t rows, int64_t d, cudaStream_t s);
+// Z[M][N] = Y[M][K] · W[K][N] (f32, row-major) on tcgen05 kind::tf32 with the 3xTF32 split
+// (gemm_tf32.cu); shapes outside its tiling go to an f64-accumulating CUDA-core kernel.
+void gemm_f32_launch(const float* Y, const float* W, float* Z, long long M, int K, int N,
+                     cudaStream_t s);
+int gemm_tf32_tile_n(int K, int N);
 void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float* A,
                       const float* X, const float* Y, float* B, int64_t rows, int64_t cols,
                       int64_t nnz, int64_t d, cudaStream_t s);

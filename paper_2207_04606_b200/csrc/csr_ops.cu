@@ -77,17 +77,28 @@ __device__ __forceinline__ T reduce_scatter(T (&v)[L], int lane, unsigned mask) 
 // products (f32 x f32 fits in 53 bits) and the butterfly reduces f64: one rounding, at B.
 // The X row fragment is converted once per row; Y values once per gathered element.
 template <bool kF64>
-struct DotT { using T = float; };
+struct DotT { using T = float; using XV = float4; };
 template <>
-struct DotT<true> { using T = double; };
+struct DotT<true> { using T = double; using XV = double4; };
+
+// The row's X fragment in the dot's precision: converted once per row, not per non-zero.
+template <bool kF64>
+__device__ __forceinline__ typename DotT<kF64>::XV xfrag(const float4& x) {
+  if constexpr (kF64) {
+    return make_double4(static_cast<double>(x.x), static_cast<double>(x.y), static_cast<double>(x.z),
+                        static_cast<double>(x.w));
+  } else {
+    return x;
+  }
+}
 
 template <bool kF64>
-__device__ __forceinline__ typename DotT<kF64>::T dot4(const float4& x, const float4& y) {
+__device__ __forceinline__ typename DotT<kF64>::T dot4(const typename DotT<kF64>::XV& x, const float4& y) {
   if constexpr (kF64) {
-    double s = static_cast<double>(x.x) * static_cast<double>(y.x);
-    s = fma(static_cast<double>(x.y), static_cast<double>(y.y), s);
-    s = fma(static_cast<double>(x.z), static_cast<double>(y.z), s);
-    return fma(static_cast<double>(x.w), static_cast<double>(y.w), s);
+    double s = x.x * static_cast<double>(y.x);
+    s = fma(x.y, static_cast<double>(y.y), s);
+    s = fma(x.z, static_cast<double>(y.z), s);
+    return fma(x.w, static_cast<double>(y.w), s);
   } else {
     return x.x * y.x + x.y * y.y + x.z * y.z + x.w * y.w;
   }
@@ -137,7 +148,8 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   }
   int row = static_cast<int>(lo);
   long long row_end = __ldg(indptr + row + 1);
-  float4 x = ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane);
+  typename DotT<kF64>::XV x =
+      xfrag<kF64>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane));
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncwarp(vmask);
 
@@ -169,7 +181,7 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
             const long long e = e0 + g + u0 + u;
             if (e >= row_end) {  // next non-empty row containing e
               do { ++row; row_end = __ldg(indptr + row + 1); } while (e >= row_end);
-              x = ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane);
+              x = xfrag<kF64>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane));
             }
           }
           part[u0 + u] = dot4<kF64>(x, yv[u]);
@@ -202,15 +214,17 @@ __global__ void sddmm_scalar_kernel(const int32_t* __restrict__ indptr,
   }
 }
 
-// f64 accumulator of a float4 fragment: the CSR SpMM uses the hyb kernel's two-level numerics
-// (f32 FMAs over a batch of <= 8 non-zeros, folded into f64, one rounding at the store).
+// f64 accumulator of a float4 fragment: the CSR SpMM uses the hyb kernel's numerics (every
+// product a * x exact in f64 and added in f64, one rounding at the store).
 struct D4 {
   double x, y, z, w;
 };
-__device__ __forceinline__ void absorb4(D4& a, float4& p) {
-  a.x += static_cast<double>(p.x); a.y += static_cast<double>(p.y);
-  a.z += static_cast<double>(p.z); a.w += static_cast<double>(p.w);
-  p = make_float4(0.f, 0.f, 0.f, 0.f);
+__device__ __forceinline__ void fma_d4(D4& a, float v, const float4& x) {
+  const double vd = static_cast<double>(v);
+  a.x = fma(vd, static_cast<double>(x.x), a.x);
+  a.y = fma(vd, static_cast<double>(x.y), a.y);
+  a.z = fma(vd, static_cast<double>(x.z), a.z);
+  a.w = fma(vd, static_cast<double>(x.w), a.w);
 }
 __device__ __forceinline__ float4 round4(const D4& a) {
   return make_float4(static_cast<float>(a.x), static_cast<float>(a.y), static_cast<float>(a.z),
@@ -235,7 +249,6 @@ spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ 
   if (r >= rows) return;
   const long long q0 = __ldg(indptr + r), q1 = __ldg(indptr + r + 1);
   if (q1 - q0 > kCsrLong) return;  // long row: spmm_csr_chunk_kernel + the two merge levels
-  float4 part = make_float4(0.f, 0.f, 0.f, 0.f);
   D4 acc{0.0, 0.0, 0.0, 0.0};
   for (long long g = q0; g < q1; g += L) {
     const long long q = g + lane;
@@ -252,9 +265,8 @@ spmm_csr_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float vu = __shfl_sync(vmask, val, (u0 + u) & (L - 1), L);
-        if (u0 + u < n) fma4(part, vu, xv[u]);
+        if (u0 + u < n) fma_d4(acc, vu, xv[u]);
       }
-      absorb4(acc, part);
     }
   }
   st_stream4(reinterpret_cast<float4*>(Y + r * d) + lane, round4(acc));
@@ -307,7 +319,6 @@ spmm_csr_chunk_kernel(const int32_t* __restrict__ indptr, const int32_t* __restr
     const long long r = owner_row(coff, rows, c);
     const long long q0 = indptr[r] + (c - coff[r]) * kCsrChunk;
     const long long q1 = min64(q0 + kCsrChunk, static_cast<long long>(indptr[r + 1]));
-    float4 pb = make_float4(0.f, 0.f, 0.f, 0.f);
     D4 acc{0.0, 0.0, 0.0, 0.0};
     for (long long g = q0; g < q1; g += U) {
       float4 xv[U];
@@ -322,8 +333,7 @@ spmm_csr_chunk_kernel(const int32_t* __restrict__ indptr, const int32_t* __restr
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (g + u < q1) fma4(pb, vv[u], xv[u]);
-      absorb4(acc, pb);
+        if (g + u < q1) fma_d4(acc, vv[u], xv[u]);
     }
     reinterpret_cast<double4*>(part + c * D)[lane] = make_double4(acc.x, acc.y, acc.z, acc.w);
   }

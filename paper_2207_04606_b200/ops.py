@@ -28,7 +28,7 @@ __all__ = [
     "StrataError", "CsrMatrix", "build_csr_device", "generate_matrix", "dense_int", "hyb_auto_k", "EllBucketPart",
     "HybDecomposition", "decompose_hyb", "hyb_rules", "spmm", "spmm_host", "spmm_host_batch",
     "spmm_multi", "ipc_handle", "ipc_open", "ipc_close",
-    "spmm_csr", "sddmm", "gnn_layer", "gnn_layer_work_floats",
+    "spmm_csr", "sddmm", "gnn_layer", "gnn_layer_work_floats", "gemm",
     "partition_rows", "device_ok",
 ]
 
@@ -294,8 +294,8 @@ def gnn_layer_work_floats(hyb: HybDecomposition, d_in: int, d_out: int) -> int:
 
 
 def gnn_layer(hyb: HybDecomposition, X, W, Z=None, work=None, stream=None):
-    """GNN layer step Z = A @ X @ W (f32, device): hyb SpMM aggregation + fp32 cuBLAS transform,
-    associated so the SpMM gathers the narrower rows (strata_gnn_layer_f32)."""
+    """GNN layer step Z = A @ X @ W (f32, device): hyb SpMM aggregation + the tcgen05 3xTF32
+    transform, associated so the SpMM gathers the narrower rows (strata_gnn_layer_f32)."""
     import torch
     d_in, d_out = int(X.shape[1]), int(W.shape[1])
     if W.shape[0] != d_in:
@@ -312,6 +312,22 @@ def gnn_layer(hyb: HybDecomposition, X, W, Z=None, work=None, stream=None):
         raise StrataError(7, f"binding size mismatch for work: got {work.numel()}, declared {need}")
     check(lib.strata_gnn_layer_f32(hyb.handle, _ptr(X), _ptr(W), _ptr(Z), _ptr(work), d_in, d_out,
                                    _stream(stream)))
+    return Z
+
+
+def gemm(Y, W, Z=None, stream=None):
+    """Dense transform Z = Y @ W (f32, device, row-major) on the tensor cores (strata_gemm_f32:
+    tcgen05 kind::tf32 with the 3xTF32 split, fp32-accurate)."""
+    import torch
+    if Y.dim() != 2 or W.dim() != 2 or W.shape[0] != Y.shape[1]:
+        raise StrataError(6, "gemm: Y must be [M][K] and W [K][N]")
+    M, K, N = int(Y.shape[0]), int(Y.shape[1]), int(W.shape[1])
+    _dense(Y, "Y", (M, K), "f32")
+    _dense(W, "W", (K, N), "f32", Y.device)
+    if Z is None:
+        Z = torch.empty((M, N), dtype=torch.float32, device=Y.device)
+    _dense(Z, "Z", (M, N), "f32", Y.device)
+    check(lib.strata_gemm_f32(_ptr(Y), _ptr(W), _ptr(Z), M, K, N, _stream(stream)))
     return Z
 
 

@@ -42,6 +42,13 @@ def main():
             out["C2_sddmm_ms"] = round(timeit(lambda: S.sddmm(dcsr, Xs, Yd, B)), 4)
         del h, X, Y, dcsr
         torch.cuda.empty_cache()
+    # dense transform of the GNN layer at C5 shape (strata_gemm_f32, 3xTF32 tcgen05)
+    Yg = torch.randn(2449029, 128, device=dev)
+    for n_out in (128, 64):
+        Wg = torch.randn(128, n_out, device=dev)
+        Zg = torch.empty(2449029, n_out, device=dev)
+        if hasattr(S, "gemm"):
+            out[f"gemm_c5_128x{n_out}_ms"] = round(timeit(lambda: S.gemm(Yg, Wg, Zg)), 4)
     print(json.dumps(out))
 
 
