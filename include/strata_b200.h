@@ -316,6 +316,32 @@ int strata_attn_csr_f32(const strata_attn_plan* p, const int32_t* indptr, const 
                         const float* A, const float* Q, const float* K, const float* V, float* Z,
                         int64_t d, void* stream);
 
+/* ---- Matrix Market ingest (device) ---------------------------------------------------
+ * Replaces: read_matrix_market(std::istream&) and read_matrix_market_file(path)
+ * (mmio.hpp:22-23, mmio.cpp:17-62).  text[bytes] holds the file's bytes in host memory; the
+ * banner, comment and size lines are read on the host, the nnz entry lines are segmented and
+ * parsed on the device (one thread per line; libstdc++ istream grammar for int64 / double,
+ * decimals correctly rounded to double like strtod; "pattern" gives 1.0; "symmetric" pushes
+ * the mirrored (j, i) of an off-diagonal entry right after it, mmio.cpp:50-51).  The handle
+ * owns device triplets in the reference's order: row/col int32 (0-based), value f64 (the
+ * reference's Triplet.value) and its f32 rounding (what build_csr stores for F32,
+ * storage.cpp:57-61), ready for strata_csr_from_coo.  Errors are STRATA_ERR_USAGE with the
+ * reference's messages for the first failing line in file order: "empty matrix market
+ * stream", "unsupported matrix market header: <line>", "unsupported matrix market field: <f>",
+ * "bad matrix market size line", "bad matrix market entry: <line>", "matrix market entry out of
+ * range: <line>", "truncated matrix market entries", "cannot open <path>".  Two host syncs
+ * (newline count, verdict). */
+typedef struct strata_mtx strata_mtx;
+int strata_mtx_parse(const char* text, int64_t bytes, strata_mtx** out, void* stream);
+int strata_mtx_read_file(const char* path, strata_mtx** out, void* stream);
+int strata_mtx_info(const strata_mtx* h, int64_t* rows, int64_t* cols, int64_t* ntriplets);
+/* Device arrays owned by the handle (valid until strata_mtx_destroy). */
+int strata_mtx_device(const strata_mtx* h, const int32_t** row, const int32_t** col,
+                      const double** val64, const float** val32);
+/* Host readback of the triplets (the reference CooMatrix.triplets), any pointer may be null. */
+int strata_mtx_read(const strata_mtx* h, int64_t* row, int64_t* col, double* val);
+int strata_mtx_destroy(strata_mtx* h);
+
 /* ---- multi-GPU helpers (host logic, no device work) -----------------------------------
  * Row-partition into `parts` contiguous row ranges balanced by nnz: cut p is the first row
  * r with indptr[r] >= nnz*p/parts (binary search on the HOST indptr).  bounds[parts+1]. */

@@ -40,6 +40,9 @@ def lib():
         L.sref_coo_info.argtypes = [vp, vp, vp, vp]
         L.sref_coo_triplets.argtypes = [vp, vp, vp, vp]
         L.sref_coo_free.argtypes = [vp]
+        L.sref_read_matrix_market.argtypes = [C.c_char_p, i64, C.POINTER(vp)]
+        L.sref_write_matrix_market.argtypes = [vp, C.c_char_p, i64]
+        L.sref_write_matrix_market.restype = i64
         L.sref_split_relations.argtypes = [vp, i64, C.c_uint64, vp]
         L.sref_dense_int.argtypes = [i64, C.c_uint64, vp]
         L.sref_build_csr.argtypes = [vp, C.c_int, C.POINTER(vp)]
@@ -115,6 +118,20 @@ class Coo:
         v = np.empty(self.nnz, np.float64)
         lib().sref_coo_triplets(self.h, _p(r), _p(c), _p(v))
         return r, c, v
+
+    @staticmethod
+    def read_matrix_market(text: bytes):
+        """mmio.cpp:17-55 over an in-memory stream; raises RefError like the reference."""
+        h = vp()
+        _chk(lib().sref_read_matrix_market(text, len(text), C.byref(h)))
+        return Coo(h)
+
+    def write_matrix_market(self) -> bytes:
+        """mmio.cpp:63-72 (sorted triplets, precision 17)."""
+        n = lib().sref_write_matrix_market(self.h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        lib().sref_write_matrix_market(self.h, buf, n + 1)
+        return buf.raw[:n]
 
     def split_relations(self, R, seed):
         outs = (vp * R)()

@@ -15,7 +15,10 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
 #include "strata/driver.hpp"
+#include "strata/mmio.hpp"
 #include "strata/interp.hpp"
 #include "strata/kernels.hpp"
 #include "strata/storage.hpp"
@@ -92,6 +95,23 @@ void sref_coo_triplets(void* h, int64_t* r, int64_t* c, double* v) {
 }
 
 void sref_coo_free(void* h) { delete static_cast<CooMatrix*>(h); }
+
+// mmio.cpp:17-55 read_matrix_market over an in-memory stream, and :63-72 write_matrix_market.
+int sref_read_matrix_market(const char* text, int64_t len, void** out) {
+  return guard([&] {
+    std::istringstream in(std::string(text, static_cast<size_t>(len)));
+    *out = new CooMatrix(read_matrix_market(in));
+  });
+}
+
+// Writes into buf (capacity cap); returns the full text length (call again with a larger buf).
+int64_t sref_write_matrix_market(void* coo, char* buf, int64_t cap) {
+  std::ostringstream os;
+  write_matrix_market(os, *static_cast<CooMatrix*>(coo));
+  const std::string s = os.str();
+  if (static_cast<int64_t>(s.size()) <= cap) memcpy(buf, s.data(), s.size());
+  return static_cast<int64_t>(s.size());
+}
 
 // strata_cli.cpp:70-82 split_relations lives in the CLI (not the library, and the CLI needs the
 // absent CLI11), so this is a two-line restatement of it: triplet t goes to relation

@@ -120,6 +120,12 @@ _sig("strata_rgms_run_bf16", C.c_int, vp, vp, vp, vp, i64, i64, vp)
 _sig("strata_rgms_info", C.c_int, vp, i64p, i64p)
 _sig("strata_rgms_destroy", C.c_int, vp)
 _sig("strata_partition_rows", C.c_int, vp, i64, C.c_int, vp)
+_sig("strata_mtx_parse", C.c_int, vp, i64, C.POINTER(vp), vp)
+_sig("strata_mtx_read_file", C.c_int, C.c_char_p, C.POINTER(vp), vp)
+_sig("strata_mtx_info", C.c_int, vp, i64p, i64p, i64p)
+_sig("strata_mtx_device", C.c_int, vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp))
+_sig("strata_mtx_read", C.c_int, vp, vp, vp, vp)
+_sig("strata_mtx_destroy", C.c_int, vp)
 
 # Every symbol include/strata_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = [
@@ -143,4 +149,6 @@ EXPORTED = [
     "strata_attn_plan_destroy", "strata_attn_csr_f32", "strata_ell_from_csr",
     "strata_rgms_bf16", "strata_rgms_plan", "strata_rgms_run_bf16", "strata_rgms_info",
     "strata_rgms_destroy", "strata_partition_rows",
+    "strata_mtx_parse", "strata_mtx_read_file", "strata_mtx_info", "strata_mtx_device",
+    "strata_mtx_read", "strata_mtx_destroy",
 ]

@@ -29,7 +29,8 @@ __all__ = [
     "HybDecomposition", "decompose_hyb", "hyb_rules", "spmm", "spmm_host", "spmm_host_batch",
     "spmm_multi", "ipc_handle", "ipc_open", "ipc_close",
     "spmm_csr", "sddmm", "gnn_layer", "gnn_layer_work_floats", "gemm",
-    "partition_rows", "device_ok",
+    "partition_rows", "device_ok", "MatrixMarket", "read_matrix_market",
+    "read_matrix_market_file",
 ]
 
 
@@ -73,6 +74,15 @@ def _stream(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def _stream_if_device(stream=None) -> int:
+    """The caller's stream, or the legacy default stream where no device is visible (host-only
+    errors of an ingest call can still be reported then)."""
+    import torch
+    if stream is None and not torch.cuda.is_available():
+        return 0
+    return _stream(stream)
 
 
 @dataclass
@@ -129,6 +139,70 @@ def build_csr_device(rows: int, cols: int, row, col, val, stream=None) -> "Devic
     check(lib.strata_csr_from_coo(_ptr(row), _ptr(col), _ptr(val), nnz, rows, cols, _ptr(indptr),
                                   _ptr(indices), _ptr(values), _stream(stream)))
     return DeviceCsr(rows, cols, indptr, indices[:nnz], values[:nnz])
+
+
+class MatrixMarket:
+    """Device COO parsed from a Matrix Market file: the reference CooMatrix (storage.hpp:45-54)
+    that read_matrix_market returns, with its triplets in the reference's order (symmetric
+    files: the mirrored entry right after its off-diagonal entry, mmio.cpp:50-51) resident in
+    HBM as int32 row / col, f64 value and its f32 rounding."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        r, c, z = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.strata_mtx_info(handle, C.byref(r), C.byref(c), C.byref(z)))
+        self.rows, self.cols, self.ntriplets = r.value, c.value, z.value
+
+    def triplets(self):
+        """Host copy (row int64, col int64, value float64) of CooMatrix.triplets."""
+        n = self.ntriplets
+        r, c, v = np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n, np.float64)
+        check(lib.strata_mtx_read(self._h, r.ctypes.data, c.ctypes.data, v.ctypes.data))
+        return r, c, v
+
+    def to_csr(self, device="cuda", stream=None) -> "DeviceCsr":
+        """build_csr (storage.cpp:89-124) of the parsed triplets, on the device (F32 values)."""
+        import torch
+        rp, cp, v64, v32 = (C.c_void_p() for _ in range(4))
+        check(lib.strata_mtx_device(self._h, C.byref(rp), C.byref(cp), C.byref(v64), C.byref(v32)))
+        nnz = self.ntriplets
+        indptr = torch.empty(self.rows + 1, dtype=torch.int32, device=device)
+        indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=device)
+        values = torch.empty(max(nnz, 1), dtype=torch.float32, device=device)
+        check(lib.strata_csr_from_coo(rp.value or 0, cp.value or 0, v32.value or 0, nnz, self.rows,
+                                      self.cols, _ptr(indptr), _ptr(indices), _ptr(values),
+                                      _stream(stream)))
+        return DeviceCsr(self.rows, self.cols, indptr, indices[:nnz], values[:nnz])
+
+    def close(self):
+        if self._h:
+            lib.strata_mtx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def read_matrix_market(text, stream=None) -> MatrixMarket:
+    """read_matrix_market(std::istream&) (mmio.hpp:22, mmio.cpp:17-55): the stream's bytes
+    (bytes or str) parsed on the device.  StrataError(kind='Usage') with the reference's
+    messages."""
+    if isinstance(text, str):
+        text = text.encode()
+    buf = C.create_string_buffer(text, len(text))
+    h = C.c_void_p()
+    check(lib.strata_mtx_parse(buf, len(text), C.byref(h), _stream_if_device(stream)))
+    return MatrixMarket(h)
+
+
+def read_matrix_market_file(path: str, stream=None) -> MatrixMarket:
+    """read_matrix_market_file(path) (mmio.hpp:23, mmio.cpp:57-61)."""
+    h = C.c_void_p()
+    check(lib.strata_mtx_read_file(str(path).encode(), C.byref(h), _stream_if_device(stream)))
+    return MatrixMarket(h)
 
 
 def generate_matrix(kind: str, n: int, m: int, density: float = 0.0, band: int = 0,
