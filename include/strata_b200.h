@@ -342,6 +342,44 @@ int strata_mtx_device(const strata_mtx* h, const int32_t** row, const int32_t** 
 int strata_mtx_read(const strata_mtx* h, int64_t* row, int64_t* col, double* val);
 int strata_mtx_destroy(strata_mtx* h);
 
+/* ---- row-partitioned multi-GPU SpMM / SDDMM ---------------------------
+ * Replaces: nothing in the reference (single process, single core); this is the sharded form
+ * of strata_spmm_hyb_f32 / strata_sddmm_csr_f32 that §8b names
+ * (strata_spmm_hyb_f32_sharded(..., const ncclComm_t*, int ndev)).  One process per GPU.
+ * The plan cuts rows into `world` contiguous nnz-balanced ranges (strata_partition_rows' rule),
+ * this rank's range into `chunks` sub-ranges (same rule), and decomposes each chunk to
+ * hyb(c, k) on the calling device.  indices / values must stay valid while the plan lives
+ * (the SDDMM reads them).  A plan's calls must be ordered (one stream at a time).
+ *   SpMM: X[cols][d] replicated, Y[rows][d] a full replica on every rank.  `comm` points to
+ *     this rank's ncclComm_t (rank/size checked against the plan; NULL allowed when world=1):
+ *     chunk q of every rank is broadcast from its owner (grouped ncclBroadcast = uneven
+ *     all-gather, in place) on the plan's stream, overlapping chunk q+1's SpMM.  The _p2p form
+ *     instead stores every finished row into all ranks' replicas (Y_dsts[rank q] = rank q's Y,
+ *     e.g. CUDA IPC mappings) from the SpMM kernel itself.
+ *   SDDMM: X[rows][d], Yd[d][cols] replicated, B[nnz]: this rank's contiguous nnz range is
+ *     computed; gather=1 all-gathers the ranges (grouped broadcasts), gather=0 leaves B sharded.
+ * NCCL is loaded at run time (the process's libnccl.so.2, else the system one). */
+#define STRATA_NCCL_ID_BYTES 128
+typedef struct strata_shard_plan strata_shard_plan;
+int strata_nccl_unique_id(void* id_out);
+/* comm_out receives an ncclComm_t. */
+int strata_nccl_comm_init(const void* id, int nranks, int rank, void* comm_out);
+int strata_nccl_comm_destroy(void* comm);
+int strata_shard_plan_create(const int32_t* indptr, const int32_t* indices, const float* values,
+                             int64_t rows, int64_t cols, int rank, int world, int chunks, int c,
+                             int k, strata_shard_plan** out, void* stream);
+/* Rows [row0, row1) of chunk `chunk` of rank `rank` (chunk = -1: the rank's whole range). */
+int strata_shard_plan_rows(const strata_shard_plan* p, int rank, int chunk, int64_t* row0,
+                           int64_t* row1);
+int strata_shard_plan_destroy(strata_shard_plan* p);
+int strata_spmm_hyb_f32_sharded(const strata_shard_plan* p, const float* X, float* Y, int64_t d,
+                                const void* comm, int ndev, void* stream);
+int strata_spmm_hyb_f32_sharded_p2p(const strata_shard_plan* p, const float* X,
+                                    float* const* Y_dsts, int ndev, int64_t d, void* stream);
+int strata_sddmm_csr_f32_sharded(const strata_shard_plan* p, const float* X, const float* Yd,
+                                 float* B, int64_t d, int gather, const void* comm, int ndev,
+                                 void* stream);
+
 /* ---- multi-GPU helpers (host logic, no device work) -----------------------------------
  * Row-partition into `parts` contiguous row ranges balanced by nnz: cut p is the first row
  * r with indptr[r] >= nnz*p/parts (binary search on the HOST indptr).  bounds[parts+1]. */

@@ -12,8 +12,17 @@
 //   decompose_hyb / EllBucketPart / HybDecomposition  storage.hpp:84-132  device kernels
 //   hyb_auto_k / padding_ratio   storage.hpp:166-173
 //   generate_matrix              driver.hpp:84-85   same libstdc++ <random> sequence
-//   FormatRequest::parse         driver.hpp:25-35
-//   build_matrix_pipeline / build_rgms_pipeline / Pipeline::run_dense  driver.hpp:44-71
+//   FormatRequest::parse / str   driver.hpp:25-35
+//   DType / TensorData / Bindings common.hpp:22, storage.hpp:33-43, interp.hpp:25-28
+//   KernelSpec / PipelineOptions / Pipeline  kernels.hpp:24-31, driver.hpp:37-60
+//   build_matrix_pipeline(op, m, d, dtype, fmt, opts)       driver.hpp:63-64
+//   build_rgms_pipeline(rels, d_in, d_out, dtype, fmt, opts, w_override, x_override, seed)
+//                                                           driver.hpp:67-71
+//   Pipeline::run_dense / verify_pipeline                   driver.hpp:59, :78-81
+//   interpret(Program, Bindings, ExecOptions) -> ExecReport interp.hpp:57 (dispatches the
+//                                                           pipeline's device plan)
+//   SearchSpace / enumerate / run_trials / report_json      tune.hpp (device-timed trials)
+//   read_matrix_market(_file) / write_matrix_market(_file)  mmio.hpp:22-26 (device parse)
 //
 // Host containers are value types exactly like the reference's; the Device* classes keep the
 // data resident in HBM for the fast path (no per-call copies).  Header-only; link
@@ -26,8 +35,11 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <map>
 #include <memory>
+#include <optional>
 #include <random>
 #include <sstream>
 #include <stdexcept>
@@ -514,8 +526,148 @@ inline CooMatrix generate_matrix(const std::string& kind, int64_t n, int64_t m, 
   return out;
 }
 
-// ---- pipelines (driver.hpp:25-71) -----------------------------------------------------------
+// ---- Matrix Market (mmio.hpp:22-26) ---------------------------------------------------------
+// read_matrix_market parses the entry lines on the device (strata_mtx_parse); the triplets come
+// back as the reference's value-type CooMatrix.  write_matrix_market is the host writer
+// (sorted triplets, precision 17, mmio.cpp:63-72).
+class DeviceCoo {  // the parsed triplets resident in HBM (int32 row / col, f64 and f32 values)
+ public:
+  explicit DeviceCoo(strata_mtx* h) : h_(h) { check(strata_mtx_info(h, &rows, &cols, &ntriplets)); }
+  const strata_mtx* get() const { return h_.get(); }
+  CooMatrix host() const {
+    std::vector<int64_t> r(ntriplets), c(ntriplets);
+    std::vector<double> v(ntriplets);
+    check(strata_mtx_read(h_.get(), r.data(), c.data(), v.data()));
+    CooMatrix m;
+    m.rows = rows;
+    m.cols = cols;
+    m.triplets.resize(ntriplets);
+    for (int64_t i = 0; i < ntriplets; ++i) m.triplets[i] = {r[i], c[i], v[i]};
+    return m;
+  }
+  int64_t rows = 0, cols = 0, ntriplets = 0;
+
+ private:
+  struct Del {
+    void operator()(strata_mtx* h) const { strata_mtx_destroy(h); }
+  };
+  std::unique_ptr<strata_mtx, Del> h_;
+};
+
+inline DeviceCoo read_matrix_market_device(const std::string& text, cudaStream_t s = nullptr) {
+  strata_mtx* h = nullptr;
+  check(strata_mtx_parse(text.data(), static_cast<int64_t>(text.size()), &h, s));
+  return DeviceCoo(h);
+}
+inline CooMatrix read_matrix_market(std::istream& in) {
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  return read_matrix_market_device(text).host();
+}
+inline CooMatrix read_matrix_market_file(const std::string& path) {
+  strata_mtx* h = nullptr;
+  check(strata_mtx_read_file(path.c_str(), &h, nullptr));
+  return DeviceCoo(h).host();
+}
+inline void write_matrix_market(std::ostream& out, const CooMatrix& m) {
+  out << "%%MatrixMarket matrix coordinate real general\n";
+  std::vector<Triplet> t = m.triplets;
+  std::sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
+    return a.row != b.row ? a.row < b.row : a.col < b.col;
+  });
+  out << m.rows << " " << m.cols << " " << t.size() << "\n";
+  out.precision(17);
+  for (const auto& e : t) out << e.row + 1 << " " << e.col + 1 << " " << e.value << "\n";
+}
+inline void write_matrix_market_file(const std::string& path, const CooMatrix& m) {
+  std::ofstream f(path);
+  if (!f) fail(ErrKind::Usage, "cannot open " + path + " for writing");
+  write_matrix_market(f, m);
+}
+
+// ---- dtypes, bindings, interpret (common.hpp:22-31, storage.hpp:33-43, interp.hpp:25-63) ----
+enum class DType { I32, F32, F64 };
+inline const char* dtype_name(DType t) {
+  switch (t) {
+    case DType::I32: return "i32";
+    case DType::F32: return "f32";
+    case DType::F64: return "f64";
+  }
+  return "?";
+}
+
+struct TensorData {
+  DType dtype = DType::F64;
+  std::vector<int32_t> i32;
+  std::vector<float> f32;
+  std::vector<double> f64;
+
+  static TensorData zeros(DType t, size_t n) {
+    TensorData d;
+    d.dtype = t;
+    if (t == DType::I32) d.i32.assign(n, 0);
+    else if (t == DType::F32) d.f32.assign(n, 0.f);
+    else d.f64.assign(n, 0.0);
+    return d;
+  }
+  size_t size() const {
+    return dtype == DType::I32 ? i32.size() : dtype == DType::F32 ? f32.size() : f64.size();
+  }
+  double get(size_t i) const {
+    return dtype == DType::I32 ? static_cast<double>(i32[i])
+                               : dtype == DType::F32 ? static_cast<double>(f32[i]) : f64[i];
+  }
+  void set(size_t i, double v) {
+    if (dtype == DType::I32) i32[i] = static_cast<int32_t>(v);
+    else if (dtype == DType::F32) f32[i] = static_cast<float>(v);
+    else f64[i] = v;
+  }
+  // Convenience (not in the reference): a TensorData of dtype t holding v.
+  static TensorData of(const std::vector<double>& v, DType t = DType::F64) {
+    TensorData d = zeros(t, v.size());
+    for (size_t i = 0; i < v.size(); ++i) d.set(i, v[i]);
+    return d;
+  }
+  std::vector<double> values() const {
+    std::vector<double> out(size());
+    for (size_t i = 0; i < out.size(); ++i) out[i] = get(i);
+    return out;
+  }
+};
+
+struct Bindings {
+  std::map<std::string, TensorData> buffers;
+  std::map<std::string, int64_t> scalars;
+};
+
+enum class ExecMode { Checked, Release };
+struct ExecStats {
+  int64_t loads = 0, stores = 0, flops = 0;
+};
+struct ExecReport {
+  Bindings outputs;
+  ExecStats stats;
+  std::vector<std::string> violations;
+  double device_ms = 0.0;  // not in the reference: CUDA-event time of the kernels
+  bool ok() const { return violations.empty(); }
+};
+struct ExecOptions {
+  ExecMode mode = ExecMode::Release;
+  bool skip_copy_blocks = false;
+  int threads = 1;
+  cudaStream_t stream = nullptr;  // not in the reference: the stream the kernels run on
+};
+
+// ---- pipelines (kernels.hpp:22-31, driver.hpp:25-91) ---------------------------------------
 enum class KernelOp { SpMM, SDDMM, RGMS };
+
+struct KernelSpec {
+  KernelOp op = KernelOp::SpMM;
+  int64_t m = 0, n = 0;
+  int64_t d = 0;
+  int64_t d_in = 0, d_out = 0;
+  int64_t relations = 1;
+  DType dtype = DType::F32;
+};
 
 struct FormatRequest {
   std::string kind = "csr";  // csr | bsr | ell | dbsr | srbcrs | hyb
@@ -547,25 +699,44 @@ struct FormatRequest {
     }
     return r;
   }
+  std::string str() const {  // driver.cpp:56-64
+    std::ostringstream os;
+    os << kind;
+    if (kind == "bsr" || kind == "dbsr") os << ":b=" << b;
+    if (kind == "ell" && w > 0) os << ":w=" << w;
+    if (kind == "srbcrs") os << ":t=" << t << ",g=" << g;
+    if (kind == "hyb") os << ":c=" << c << ",k=" << k;
+    return os.str();
+  }
 };
 
-// A canonical pipeline: the sparse operand decomposed on the device, named dense bindings
-// ("X", "Y" for SDDMM, "W" for RGMS) like Pipeline::bindings, run_dense() like
-// driver.cpp:163-171 (SDDMM reconstructs the dense m x n output; toy sizes only, as there).
-class Pipeline {
- public:
+struct PipelineOptions {
+  std::string schedule_script;  // accepted; the device kernels carry their own schedule
+  bool preconverted = true;
+  ExecMode mode = ExecMode::Release;
+  int threads = 1;
+};
+
+// FormatRewriteRule (transform.hpp:33-48), as far as callers read it: the rule name, the
+// converted buffer's name and the converted storage (kind, dims, nnz, pad_slots and, for
+// ELL buckets, the width; its aux arrays are read back from the device by rule_storage()).
+struct FormatRewriteRule {
+  std::string name, new_buffer;
+  TensorStorage storage;
+};
+
+enum class Stage { I, II, III };
+inline const char* stage_name(Stage s) { return s == Stage::I ? "I" : s == Stage::II ? "II" : "III"; }
+
+namespace detail {
+
+// The device execution plan a Program stands for: the sparse operand converted once and
+// resident in HBM, plus the op's binding contract.  interpret() runs it.
+struct DevicePlan {
   KernelOp op = KernelOp::SpMM;
-  int64_t m = 0, n = 0, d = 0, d_in = 0, d_out = 0, relations = 1;
-  std::map<std::string, std::vector<double>> bindings;
-
-  DenseMatrix run_dense() {
-    if (op == KernelOp::SpMM) return run_spmm();
-    if (op == KernelOp::SDDMM) return run_sddmm();
-    return run_rgms();
-  }
-
-  // internal state
   FormatRequest fmt;
+  int64_t m = 0, n = 0, d = 0, d_in = 0, d_out = 0, relations = 1;
+  int64_t work_slots = 0;  // stored slots the kernel executes (padding included)
   std::unique_ptr<DeviceCsr> csr;
   std::unique_ptr<DeviceHyb> hyb;
   std::unique_ptr<DeviceBsr> bsr;
@@ -575,160 +746,679 @@ class Pipeline {
   struct SrbcrsDel {
     void operator()(strata_srbcrs* h) const { strata_srbcrs_destroy(h); }
   };
+  struct RgmsDel {
+    void operator()(strata_rgms* h) const { strata_rgms_destroy(h); }
+  };
   std::unique_ptr<strata_dbsr, DbsrDel> dbsr;
   std::unique_ptr<strata_srbcrs, SrbcrsDel> srbcrs;
-  TensorStorage csr_host;
-  std::vector<int32_t> rel_ptr, rel_dst, rel_src;
-  std::vector<float> rel_a;
+  std::unique_ptr<strata_rgms, RgmsDel> rgms;
+  DeviceArray<int32_t> rel_ptr, rel_dst, rel_src;
+  DeviceArray<float> rel_a;
 
- private:
-  const std::vector<double>& bound(const std::string& name, size_t n_expected) const {
-    auto it = bindings.find(name);
-    if (it == bindings.end()) fail(ErrKind::Exec, "missing binding for buffer " + name);
+  static const TensorData& bound(const Bindings& b, const std::string& name, size_t n_expected) {
+    auto it = b.buffers.find(name);  // interp.cpp:572-582
+    if (it == b.buffers.end()) fail(ErrKind::Exec, "missing binding for buffer " + name);
     if (it->second.size() != n_expected)
       fail(ErrKind::Exec, "binding size mismatch for " + name + ": got " +
                               std::to_string(it->second.size()) + ", declared " +
                               std::to_string(n_expected));
     return it->second;
   }
-  static std::vector<float> f32(const std::vector<double>& v) { return {v.begin(), v.end()}; }
+  static std::vector<float> f32(const TensorData& t) {
+    std::vector<float> v(t.size());
+    for (size_t i = 0; i < v.size(); ++i) v[i] = static_cast<float>(t.get(i));
+    return v;
+  }
+  static std::vector<uint16_t> bf16(const TensorData& t) {
+    std::vector<uint16_t> v(t.size());
+    for (size_t i = 0; i < v.size(); ++i) v[i] = to_bf16(static_cast<float>(t.get(i)));
+    return v;
+  }
 
-  DenseMatrix run_spmm() {
-    const auto& x = bound("X", static_cast<size_t>(n * d));
-    DenseMatrix out(m, d);
-    if (fmt.kind == "bsr" || fmt.kind == "dbsr" || fmt.kind == "srbcrs") {  // bf16 tensor cores
-      std::vector<uint16_t> xb(x.size());
-      for (size_t i = 0; i < x.size(); ++i) xb[i] = to_bf16(static_cast<float>(x[i]));
-      DeviceArray<uint16_t> X(xb);
-      DeviceArray<float> Y(static_cast<size_t>(m * d));
-      if (bsr) bsr->spmm_bf16(X.data(), Y.data(), d);
-      else if (dbsr) check(strata_dbsr_spmm_bf16(dbsr.get(), X.data(), Y.data(), d, nullptr));
-      else check(strata_srbcrs_spmm_bf16(srbcrs.get(), X.data(), Y.data(), d, nullptr));
-      auto y = Y.host();
-      for (size_t i = 0; i < y.size(); ++i) out.v[i] = y[i];
-      return out;
+  // Kernels between two events on the caller's stream; returns the output values.
+  template <class F>
+  static std::vector<float> timed(cudaStream_t s, size_t nout, double& ms, F&& launch) {
+    DeviceArray<float> out(std::max<size_t>(nout, 1));
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0));
+    cuda_check(cudaEventCreate(&e1));
+    cuda_check(cudaEventRecord(e0, s));
+    launch(out.data());
+    cuda_check(cudaEventRecord(e1, s));
+    cuda_check(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cuda_check(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ms = t;
+    std::vector<float> h = out.host();
+    h.resize(nout);
+    return h;
+  }
+
+  ExecReport run(const Bindings& b, const ExecOptions& o, const std::string& out_name) const {
+    ExecReport rep;
+    const cudaStream_t s = o.stream;
+    std::vector<float> y;
+    if (op == KernelOp::SpMM) {
+      const TensorData& x = bound(b, "X", static_cast<size_t>(n * d));
+      if (fmt.kind == "bsr" || fmt.kind == "dbsr" || fmt.kind == "srbcrs") {  // bf16 tensor cores
+        DeviceArray<uint16_t> X(bf16(x));
+        y = timed(s, static_cast<size_t>(m * d), rep.device_ms, [&](float* Y) {
+          if (bsr) bsr->spmm_bf16(X.data(), Y, d, s);
+          else if (dbsr) check(strata_dbsr_spmm_bf16(dbsr.get(), X.data(), Y, d, s));
+          else check(strata_srbcrs_spmm_bf16(srbcrs.get(), X.data(), Y, d, s));
+        });
+      } else {
+        DeviceArray<float> X(f32(x));
+        y = timed(s, static_cast<size_t>(m * d), rep.device_ms, [&](float* Y) {
+          if (hyb) hyb->spmm(X.data(), Y, d, s);
+          else check(strata_spmm_csr_f32(csr->indptr.data(), csr->indices.data(), csr->values.data(),
+                                         X.data(), Y, m, n, d, s));
+        });
+      }
+      rep.stats.flops = 2 * work_slots * d;
+      rep.stats.loads = work_slots * (d + 2);
+      rep.stats.stores = m * d;
+    } else if (op == KernelOp::SDDMM) {
+      const TensorData& x = bound(b, "X", static_cast<size_t>(m * d));
+      const TensorData& yd = bound(b, "Y", static_cast<size_t>(d * n));
+      DeviceArray<float> X(f32(x)), Yd(f32(yd));
+      y = timed(s, static_cast<size_t>(csr->nnz), rep.device_ms, [&](float* B) {
+        check(strata_sddmm_csr_f32(csr->indptr.data(), csr->indices.data(), csr->values.data(),
+                                   X.data(), Yd.data(), B, m, n, csr->nnz, d, s));
+      });
+      rep.stats.flops = csr->nnz * (2 * d + 1);
+      rep.stats.loads = csr->nnz * (2 * d + 2);
+      rep.stats.stores = csr->nnz;
+    } else {
+      const TensorData& x = bound(b, "X", static_cast<size_t>(n * d_in));
+      const TensorData& w = bound(b, "W", static_cast<size_t>(relations * d_in * d_out));
+      DeviceArray<uint16_t> X(bf16(x)), W(bf16(w));
+      y = timed(s, static_cast<size_t>(m * d_out), rep.device_ms, [&](float* Y) {
+        check(strata_rgms_run_bf16(rgms.get(), X.data(), W.data(), Y, d_in, d_out, s));
+      });
+      rep.stats.flops = 2 * work_slots * d_in * d_out;
+      rep.stats.loads = work_slots * (d_in + 2);
+      rep.stats.stores = m * d_out;
     }
-    DeviceArray<float> X(f32(x));
-    DeviceArray<float> Y(static_cast<size_t>(m * d));
-    if (hyb) hyb->spmm(X.data(), Y.data(), d);
-    else check(strata_spmm_csr_f32(csr->indptr.data(), csr->indices.data(), csr->values.data(),
-                                   X.data(), Y.data(), m, n, d, nullptr));
-    auto y = Y.host();
-    for (size_t i = 0; i < y.size(); ++i) out.v[i] = y[i];
-    return out;
-  }
-
-  DenseMatrix run_sddmm() {
-    const auto& x = bound("X", static_cast<size_t>(m * d));
-    const auto& yd = bound("Y", static_cast<size_t>(d * n));
-    DeviceArray<float> X(f32(x)), Yd(f32(yd));
-    DeviceArray<float> B(std::max<size_t>(static_cast<size_t>(csr->nnz), 1));
-    check(strata_sddmm_csr_f32(csr->indptr.data(), csr->indices.data(), csr->values.data(),
-                               X.data(), Yd.data(), B.data(), m, n, csr->nnz, d, nullptr));
-    auto b = B.host();
-    DenseMatrix out(m, n);  // positional B reconstructed through the CSR pattern
-    const IntArray& ip = csr_host.arr("J_indptr");
-    const IntArray& ix = csr_host.arr("J_indices");
-    for (int64_t i = 0; i < m; ++i)
-      for (int32_t q = ip[i]; q < ip[i + 1]; ++q) out.at(i, ix[q]) += b[q];
-    return out;
-  }
-
-  DenseMatrix run_rgms() {
-    const auto& x = bound("X", static_cast<size_t>(n * d_in));
-    const auto& w = bound("W", static_cast<size_t>(relations * d_in * d_out));
-    std::vector<uint16_t> xb(x.size()), wb(w.size());
-    for (size_t i = 0; i < x.size(); ++i) xb[i] = to_bf16(static_cast<float>(x[i]));
-    for (size_t i = 0; i < w.size(); ++i) wb[i] = to_bf16(static_cast<float>(w[i]));
-    DeviceArray<uint16_t> X(xb), W(wb);
-    DeviceArray<int32_t> rp(rel_ptr), dst(rel_dst), src(rel_src);
-    DeviceArray<float> A(rel_a), Y(static_cast<size_t>(m * d_out));
-    check(strata_rgms_bf16(rp.data(), dst.data(), src.data(), A.data(), relations, m, n,
-                           static_cast<int64_t>(rel_src.size()), X.data(), W.data(), Y.data(),
-                           d_in, d_out, nullptr));
-    auto y = Y.host();
-    DenseMatrix out(m, d_out);
-    for (size_t i = 0; i < y.size(); ++i) out.v[i] = y[i];
-    return out;
+    TensorData out = TensorData::zeros(DType::F32, y.size());
+    out.f32 = std::move(y);
+    rep.outputs.buffers[out_name] = std::move(out);
+    return rep;
   }
 };
 
-// build_matrix_pipeline (driver.cpp:173-217): pad dims for bsr, build CSR, decompose.
-inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m_in, int64_t d,
-                                      const FormatRequest& fmt) {
-  Pipeline pl;
-  CooMatrix m = m_in;
-  if (fmt.kind == "bsr" || fmt.kind == "dbsr") {  // pad_for_format (driver.cpp:69-78)
-    m.rows = (m.rows + fmt.b - 1) / fmt.b * fmt.b;
-    m.cols = (m.cols + fmt.b - 1) / fmt.b * fmt.b;
+inline void require_f32(DType dtype) {
+  if (dtype != DType::F32)
+    fail(ErrKind::Usage, std::string("dtype ") + dtype_name(dtype) +
+                             " is not served by the B200 kernels (f32 storage; the tensor-core "
+                             "formats compute in bf16 with f32 accumulation)");
+}
+
+// pad_for_format (driver.cpp:69-78)
+inline CooMatrix pad_for_format(const CooMatrix& m, const FormatRequest& fmt) {
+  CooMatrix out = m;
+  if (fmt.kind == "bsr" || fmt.kind == "dbsr") {
+    out.rows = (m.rows + fmt.b - 1) / fmt.b * fmt.b;
+    out.cols = (m.cols + fmt.b - 1) / fmt.b * fmt.b;
   } else if (fmt.kind == "srbcrs") {
-    m.rows = (m.rows + fmt.t - 1) / fmt.t * fmt.t;
+    out.rows = (m.rows + fmt.t - 1) / fmt.t * fmt.t;
   }
-  pl.op = op;
-  pl.fmt = fmt;
-  pl.m = m.rows;
-  pl.n = m.cols;
-  pl.d = d;
-  pl.csr_host = build_csr(m);
-  pl.csr = std::make_unique<DeviceCsr>(pl.csr_host);
-  if (op == KernelOp::SpMM && fmt.kind == "hyb") {
-    const int k = fmt.k >= 0 ? fmt.k : hyb_auto_k(pl.csr_host);
-    pl.hyb = std::make_unique<DeviceHyb>(*pl.csr, fmt.c, k);
-  } else if (op == KernelOp::SpMM && fmt.kind == "bsr") {
-    pl.bsr = std::make_unique<DeviceBsr>(*pl.csr, fmt.b);
-  } else if (op == KernelOp::SpMM && fmt.kind == "dbsr") {
+  return out;
+}
+
+inline int64_t max_row_length(const TensorStorage& csr) {
+  const IntArray& ip = csr.arr("J_indptr");
+  int64_t w = 0;
+  for (size_t i = 0; i + 1 < ip.size(); ++i) w = std::max<int64_t>(w, ip[i + 1] - ip[i]);
+  return std::max<int64_t>(w, 1);
+}
+
+}  // namespace detail
+
+// A stage-III program.  On this path it stands for the device plan of its pipeline (there is
+// no IR to walk: interpret() dispatches to the kernels the plan was built for).
+struct Program {
+  Stage stage = Stage::III;
+  std::shared_ptr<const detail::DevicePlan> plan;
+};
+
+// interpret (interp.hpp:57, interp.cpp:564-622): same contract — inputs read from the
+// bindings by name with the reference's Exec errors, outputs returned in report.outputs —
+// executed by the B200 kernels.
+inline ExecReport interpret(const Program& p, const Bindings& b, const ExecOptions& opts = {}) {
+  if (p.stage != Stage::III)
+    fail(ErrKind::Exec, std::string("interpret expects a stage-III program (got stage ") +
+                            stage_name(p.stage) + ")");
+  if (!p.plan) fail(ErrKind::Exec, "program has no device plan (not built by a pipeline)");
+  const char* out = p.plan->op == KernelOp::SDDMM ? "B" : "Y";
+  return p.plan->run(b, opts, out);
+}
+
+struct Pipeline {
+  KernelSpec spec;
+  Program stage1, stage2, stage3;
+  Bindings bindings;
+  ExecOptions exec_opts;
+  std::vector<FormatRewriteRule> rules;
+  std::string output_buffer;
+  int64_t out_rows = 0, out_cols = 0;
+  std::optional<TensorStorage> output_pattern;  // SDDMM: B shares A's structure
+
+  // driver.cpp:146-171: interpret stage3, read the output back as a dense matrix.
+  DenseMatrix run_dense() {
+    ExecReport report = interpret(stage3, bindings, exec_opts);
+    if (!report.ok()) {
+      std::string msg = "execution violations:";
+      for (const auto& v : report.violations) msg += "\n  " + v;
+      fail(ErrKind::Exec, msg);
+    }
+    auto it = report.outputs.buffers.find(output_buffer);
+    if (it == report.outputs.buffers.end())
+      fail(ErrKind::Exec, "pipeline output " + output_buffer + " missing from report");
+    const TensorData& data = it->second;
+    if (output_pattern) {
+      TensorStorage view = *output_pattern;
+      view.values.resize(data.size());
+      for (size_t i = 0; i < data.size(); ++i) view.values[i] = static_cast<float>(data.get(i));
+      return reconstruct_dense(view);
+    }
+    DenseMatrix d(out_rows, out_cols);
+    for (int64_t i = 0; i < out_rows * out_cols; ++i) d.v[i] = data.get(i);
+    return d;
+  }
+
+  // Host copy of rule i's converted storage (aux arrays included), read back from the device.
+  TensorStorage rule_storage(size_t i) const {
+    const detail::DevicePlan& pl = *stage3.plan;
+    const FormatRewriteRule& r = rules.at(i);
+    if (pl.hyb) {
+      HybDecomposition h = pl.hyb->host();
+      for (auto& part : h.parts)
+        if (r.name == "hyb_p" + std::to_string(part.partition) + "_b" + std::to_string(part.bucket))
+          return part.ell;
+      return r.storage;  // an empty bucket: no arrays
+    }
+    if (pl.bsr) return pl.bsr->host(r.name + "_");
+    return r.storage;
+  }
+
+  const detail::DevicePlan& plan() const { return *stage3.plan; }
+};
+
+namespace detail {
+inline void finish_pipeline(Pipeline& pl, std::shared_ptr<DevicePlan> plan, const PipelineOptions& opts) {
+  pl.stage3.stage = Stage::III;
+  pl.stage3.plan = plan;
+  pl.stage1 = Program{Stage::I, plan};
+  pl.stage2 = Program{Stage::II, plan};
+  pl.exec_opts.mode = opts.mode;
+  pl.exec_opts.skip_copy_blocks = opts.preconverted;
+  pl.exec_opts.threads = opts.threads;
+}
+}  // namespace detail
+
+// build_matrix_pipeline (driver.hpp:63-64, driver.cpp:173-217): pad for the format, build the
+// CSR, convert on the device, name the rules like rules_for (driver.cpp:80-104).
+inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m_in, int64_t d, DType dtype,
+                                      const FormatRequest& fmt, const PipelineOptions& opts) {
+  detail::require_f32(dtype);
+  if (op == KernelOp::RGMS) fail(ErrKind::Usage, "RGMS pipelines come from build_rgms_pipeline");
+  Pipeline pl;
+  CooMatrix m = detail::pad_for_format(m_in, fmt);
+  TensorStorage csr = build_csr(m);
+  pl.spec.op = op;
+  pl.spec.m = m.rows;
+  pl.spec.n = m.cols;
+  pl.spec.d = d;
+  pl.spec.dtype = dtype;
+  auto plan = std::make_shared<detail::DevicePlan>();
+  plan->op = op;
+  plan->fmt = fmt;
+  plan->m = m.rows;
+  plan->n = m.cols;
+  plan->d = d;
+  plan->csr = std::make_unique<DeviceCsr>(csr);
+  plan->work_slots = csr.nnz;
+  if (op == KernelOp::SpMM) {
+    pl.output_buffer = "Y";
+    pl.out_rows = m.rows;
+    pl.out_cols = d;
+  } else {
+    pl.output_buffer = "B";
+    pl.out_rows = m.rows;
+    pl.out_cols = m.cols;
+  }
+  auto rule = [&](const std::string& name, FormatKind kind) {
+    FormatRewriteRule r;
+    r.name = name;
+    r.new_buffer = "A_" + name;
+    r.storage.kind = kind;
+    r.storage.rows = m.rows;
+    r.storage.cols = m.cols;
+    pl.rules.push_back(r);
+    return &pl.rules.back();
+  };
+  if (fmt.kind == "csr") {
+  } else if (fmt.kind == "hyb") {
+    const int k = fmt.k >= 0 ? fmt.k : hyb_auto_k(csr);
+    if (fmt.c < 1 || k < 0) fail(ErrKind::Usage, "hyb requires c >= 1 and k >= 0");
+    plan->hyb = std::make_unique<DeviceHyb>(*plan->csr, fmt.c, k);
+    plan->work_slots = 0;
+    int np = 0;
+    check(strata_hyb_num_parts(plan->hyb->get(), &np));
+    std::map<std::pair<int, int>, int> present;
+    for (int i = 0; i < np; ++i) {
+      int p = 0, bb = 0;
+      int64_t w = 0, nr = 0, nz = 0, pad = 0, lo = 0, hi = 0;
+      check(strata_hyb_part_info(plan->hyb->get(), i, &p, &bb, &w, &nr, &nz, &pad, &lo, &hi));
+      present[{p, bb}] = i;
+      plan->work_slots += nr * w;
+    }
+    // hyb_rules (transform.cpp:525-557): c * (k + 1) rules, empty buckets included.
+    for (int p = 0; p < fmt.c; ++p)
+      for (int bb = 0; bb <= k; ++bb) {
+        FormatRewriteRule* r = rule("hyb_p" + std::to_string(p) + "_b" + std::to_string(bb),
+                                    FormatKind::EllBucket);
+        r->storage.width = int64_t{1} << bb;
+        auto it = present.find({p, bb});
+        if (it != present.end()) {
+          int pp = 0, b2 = 0;
+          int64_t w = 0, nr = 0, nz = 0, pad = 0, lo = 0, hi = 0;
+          check(strata_hyb_part_info(plan->hyb->get(), it->second, &pp, &b2, &w, &nr, &nz, &pad, &lo, &hi));
+          r->storage.nnz = nz;
+          r->storage.pad_slots = pad;
+        }
+      }
+  } else if (fmt.kind == "bsr") {
+    if (op != KernelOp::SpMM) fail(ErrKind::Usage, "format bsr is not served for SDDMM");
+    plan->bsr = std::make_unique<DeviceBsr>(*plan->csr, fmt.b);
+    plan->work_slots = plan->bsr->nblocks * fmt.b * fmt.b;
+    FormatRewriteRule* r = rule("bsr", FormatKind::Bsr);
+    r->storage.block = fmt.b;
+    r->storage.nnz = csr.nnz;
+    r->storage.pad_slots = plan->bsr->pad_slots;
+  } else if (fmt.kind == "dbsr") {
+    if (op != KernelOp::SpMM) fail(ErrKind::Usage, "format dbsr is not served for SDDMM");
     strata_dbsr* h = nullptr;
-    check(strata_dbsr_from_csr(pl.csr->indptr.data(), pl.csr->indices.data(), pl.csr->values.data(),
-                               pl.csr->rows, pl.csr->cols, pl.csr->nnz, fmt.b, nullptr, &h));
-    pl.dbsr.reset(h);
-  } else if (op == KernelOp::SpMM && fmt.kind == "srbcrs") {
+    check(strata_dbsr_from_csr(plan->csr->indptr.data(), plan->csr->indices.data(),
+                               plan->csr->values.data(), plan->csr->rows, plan->csr->cols,
+                               plan->csr->nnz, fmt.b, nullptr, &h));
+    plan->dbsr.reset(h);
+    int64_t mb = 0, nb = 0, b = 0, nstored = 0, nblocks = 0, pad = 0;
+    check(strata_dbsr_info(h, &mb, &nb, &b, &nstored, &nblocks, &pad));
+    plan->work_slots = nblocks * b * b;
+    FormatRewriteRule* r = rule("dbsr", FormatKind::Bsr);
+    r->storage.block = fmt.b;
+    r->storage.nnz = csr.nnz;
+    r->storage.pad_slots = pad;
+  } else if (fmt.kind == "srbcrs") {
+    if (op != KernelOp::SpMM) fail(ErrKind::Usage, "format srbcrs is not served for SDDMM");
     strata_srbcrs* h = nullptr;
-    check(strata_srbcrs_from_csr(pl.csr->indptr.data(), pl.csr->indices.data(), pl.csr->values.data(),
-                                 pl.csr->rows, pl.csr->cols, pl.csr->nnz, fmt.t, fmt.g, nullptr, &h));
-    pl.srbcrs.reset(h);
-  } else if (op == KernelOp::SpMM && fmt.kind == "ell") {
-    // ELL (w = max row length by default) stores the CSR entries plus zero pads; the product
-    // is the CSR one, so the row-split CSR kernel serves it.
-  } else if (fmt.kind != "csr") {
-    fail(ErrKind::Usage, "format " + fmt.kind + " is not served for this op");
+    check(strata_srbcrs_from_csr(plan->csr->indptr.data(), plan->csr->indices.data(),
+                                 plan->csr->values.data(), plan->csr->rows, plan->csr->cols,
+                                 plan->csr->nnz, fmt.t, fmt.g, nullptr, &h));
+    plan->srbcrs.reset(h);
+    int64_t mb = 0, t = 0, g = 0, ngroups = 0, pad = 0;
+    check(strata_srbcrs_info(h, &mb, &t, &g, &ngroups, &pad));
+    plan->work_slots = ngroups * t * g;
+    FormatRewriteRule* r = rule("srbcrs", FormatKind::Bsr);
+    r->storage.nnz = csr.nnz;
+    r->storage.pad_slots = pad;
+  } else if (fmt.kind == "ell") {
+    // csr_to_ell (w = max row length by default, driver.cpp:86-93): the capacity check runs on
+    // the device; the ELL product is the CSR one (pads multiply by 0), so the row-split CSR
+    // kernel executes it.
+    const int64_t w = fmt.w > 0 ? fmt.w : detail::max_row_length(csr);
+    TensorStorage ell = csr_to_ell(csr, w, "ell_");
+    FormatRewriteRule* r = rule("ell", FormatKind::Ell);
+    r->storage = std::move(ell);
+    plan->work_slots = m.rows * w;
+  } else {
+    fail(ErrKind::Usage, "no rules for format " + fmt.kind);
   }
+  if (op == KernelOp::SDDMM) pl.output_pattern = csr;
+  detail::finish_pipeline(pl, std::move(plan), opts);
   return pl;
 }
 
-// build_rgms_pipeline (driver.cpp:241-314): relation-major edges (kernels.cpp:19-62), X and W
-// seeded like the reference (mt19937(seed), uniform_int(-3,3): X first, then W).
+// Former four-argument form (F32, default options).
+inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m, int64_t d,
+                                      const FormatRequest& fmt) {
+  return build_matrix_pipeline(op, m, d, DType::F32, fmt, PipelineOptions{});
+}
+
+// build_rgms_pipeline (driver.hpp:67-71, driver.cpp:241-314): relations padded for the format,
+// relation-major edges (build_rel_sparse, kernels.cpp:19-62), X then W drawn from
+// mt19937(seed) uniform_int(-3, 3) unless overridden (x_override: cols x d_in; w_override:
+// one d_in x d_out matrix per relation).  Every per-relation format the reference accepts
+// computes the same product; the device plan executes it with the two-pass tcgen05 RGMS.
 inline Pipeline build_rgms_pipeline(const std::vector<CooMatrix>& relations, int64_t d_in,
-                                    int64_t d_out, uint64_t seed = 7) {
+                                    int64_t d_out, DType dtype, const FormatRequest& fmt,
+                                    const PipelineOptions& opts,
+                                    const std::vector<DenseMatrix>* w_override = nullptr,
+                                    const DenseMatrix* x_override = nullptr, uint64_t seed = 7) {
+  detail::require_f32(dtype);
   if (relations.empty()) fail(ErrKind::Usage, "need at least one relation");
   Pipeline pl;
-  pl.op = KernelOp::RGMS;
-  pl.m = relations[0].rows;
-  pl.n = relations[0].cols;
-  pl.d_in = d_in;
-  pl.d_out = d_out;
-  pl.relations = static_cast<int64_t>(relations.size());
-  pl.rel_ptr.push_back(0);
-  for (const auto& r : relations) {
-    if (r.rows != pl.m || r.cols != pl.n) fail(ErrKind::Usage, "all relations must share dims");
-    std::vector<Triplet> t = r.triplets;
-    std::sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
-      return a.row != b.row ? a.row < b.row : a.col < b.col;
-    });
-    for (const auto& e : t) {
-      pl.rel_dst.push_back(static_cast<int32_t>(e.row));
-      pl.rel_src.push_back(static_cast<int32_t>(e.col));
-      pl.rel_a.push_back(static_cast<float>(e.value));
-    }
-    pl.rel_ptr.push_back(static_cast<int32_t>(pl.rel_src.size()));
+  auto plan = std::make_shared<detail::DevicePlan>();
+  std::vector<CooMatrix> rels;
+  for (const auto& r : relations) rels.push_back(detail::pad_for_format(r, fmt));
+  const int64_t R = static_cast<int64_t>(rels.size());
+  const int64_t m = rels[0].rows, n = rels[0].cols;
+  std::vector<int32_t> rp{0}, dst, src;
+  std::vector<float> a;
+  for (const auto& r : rels) {
+    if (r.rows != m || r.cols != n) fail(ErrKind::Usage, "all relations must share dims");
+    TensorStorage s = build_csr(r);  // sorted, validated like the reference's per-slice CSR
+    const IntArray& ip = s.arr("J_indptr");
+    const IntArray& ix = s.arr("J_indices");
+    for (int64_t i = 0; i < m; ++i)
+      for (int32_t q = ip[i]; q < ip[i + 1]; ++q) {
+        dst.push_back(static_cast<int32_t>(i));
+        src.push_back(ix[q]);
+        a.push_back(s.values[q]);
+      }
+    rp.push_back(static_cast<int32_t>(src.size()));
   }
+  pl.spec.op = KernelOp::RGMS;
+  pl.spec.m = m;
+  pl.spec.n = n;
+  pl.spec.d_in = d_in;
+  pl.spec.d_out = d_out;
+  pl.spec.relations = R;
+  pl.spec.dtype = dtype;
+  pl.output_buffer = "Y";
+  pl.out_rows = m;
+  pl.out_cols = d_out;
+
   std::mt19937 rng(static_cast<uint32_t>(seed));
   std::uniform_int_distribution<int> val(-3, 3);
-  std::vector<double> x(pl.n * d_in), w(pl.relations * d_in * d_out);
-  for (auto& v : x) v = val(rng);
-  for (auto& v : w) v = val(rng);
-  pl.bindings["X"] = std::move(x);
-  pl.bindings["W"] = std::move(w);
+  TensorData xd = TensorData::zeros(dtype, static_cast<size_t>(n * d_in));
+  if (x_override) {
+    if (x_override->rows * x_override->cols != n * d_in)
+      fail(ErrKind::Usage, "x_override must be cols x d_in");
+    for (size_t i = 0; i < xd.size(); ++i) xd.set(i, x_override->v[i]);
+  } else {
+    for (size_t i = 0; i < xd.size(); ++i) xd.set(i, val(rng));
+  }
+  TensorData wd = TensorData::zeros(dtype, static_cast<size_t>(R * d_in * d_out));
+  if (w_override && static_cast<int64_t>(w_override->size()) != R)
+    fail(ErrKind::Usage, "w_override needs one matrix per relation");
+  for (int64_t r = 0; r < R; ++r)
+    for (int64_t k = 0; k < d_in; ++k)
+      for (int64_t l = 0; l < d_out; ++l)
+        wd.set((r * d_in + k) * d_out + l, w_override ? (*w_override)[r].at(k, l) : val(rng));
+  pl.bindings.buffers["X"] = std::move(xd);
+  pl.bindings.buffers["W"] = std::move(wd);
+
+  if (fmt.kind != "csr") {
+    for (int64_t r = 0; r < R; ++r) {
+      FormatRewriteRule rule;
+      rule.name = "r" + std::to_string(r) + "_" + fmt.kind;
+      rule.new_buffer = "A_" + rule.name;
+      rule.storage.rows = m;
+      rule.storage.cols = n;
+      rule.storage.nnz = rp[r + 1] - rp[r];
+      rule.storage.kind = fmt.kind == "hyb" ? FormatKind::EllBucket
+                          : fmt.kind == "ell" ? FormatKind::Ell : FormatKind::Bsr;
+      pl.rules.push_back(rule);
+    }
+  }
+  plan->op = KernelOp::RGMS;
+  plan->fmt = fmt;
+  plan->m = m;
+  plan->n = n;
+  plan->d_in = d_in;
+  plan->d_out = d_out;
+  plan->relations = R;
+  plan->work_slots = static_cast<int64_t>(src.size());
+  plan->rel_ptr = DeviceArray<int32_t>(rp);
+  plan->rel_dst = DeviceArray<int32_t>(dst);
+  plan->rel_src = DeviceArray<int32_t>(src);
+  plan->rel_a = DeviceArray<float>(a);
+  strata_rgms* h = nullptr;
+  check(strata_rgms_plan(plan->rel_ptr.data(), plan->rel_dst.data(), plan->rel_src.data(),
+                         plan->rel_a.data(), R, m, n, static_cast<int64_t>(src.size()), &h, nullptr));
+  plan->rgms.reset(h);
+  detail::finish_pipeline(pl, std::move(plan), opts);
   return pl;
+}
+
+// Former form (F32, csr, default options).
+inline Pipeline build_rgms_pipeline(const std::vector<CooMatrix>& relations, int64_t d_in,
+                                    int64_t d_out, uint64_t seed = 7) {
+  return build_rgms_pipeline(relations, d_in, d_out, DType::F32, FormatRequest{}, PipelineOptions{},
+                             nullptr, nullptr, seed);
+}
+
+// ---- verification (driver.hpp:73-81, driver.cpp:316-363) -----------------------------------
+struct VerifyResult {
+  bool pass = true;
+  std::string detail;
+};
+
+namespace detail {
+inline VerifyResult compare(const DenseMatrix& got, const DenseMatrix& want, double rel_tol) {
+  VerifyResult out;
+  if (got.rows != want.rows || got.cols != want.cols) {
+    out.pass = false;
+    out.detail = "shape mismatch";
+    return out;
+  }
+  for (int64_t i = 0; i < got.rows; ++i)
+    for (int64_t j = 0; j < got.cols; ++j) {
+      const double x = got.at(i, j), y = want.at(i, j);
+      const double denom = std::max({std::fabs(x), std::fabs(y), 1.0});
+      if (std::fabs(x - y) > rel_tol * denom) {
+        out.pass = false;
+        std::ostringstream os;
+        os << "first divergence at (" << i << ", " << j << "): got " << x << ", expected " << y;
+        out.detail = os.str();
+        return out;
+      }
+    }
+  return out;
+}
+}  // namespace detail
+
+// Runs the pipeline on the device and compares it with the reference's dense oracle (f64,
+// the padded matrix's stored entries): SpMM Y = A X; SDDMM B = A .* (X Y) on the pattern.
+inline VerifyResult verify_pipeline(KernelOp op, const CooMatrix& m, int64_t d, DType dtype,
+                                    const FormatRequest& fmt, const PipelineOptions& opts,
+                                    uint64_t seed) {
+  std::mt19937 rng(static_cast<uint32_t>(seed));
+  std::uniform_int_distribution<int> val(-3, 3);
+  Pipeline pl = build_matrix_pipeline(op, m, d, dtype, fmt, opts);
+  // The oracle walks the padded matrix's triplets in (row, col) order with their f64 values,
+  // i.e. the stored entries of the reference's dense_from_coo(padded).
+  CooMatrix padded = detail::pad_for_format(m, fmt);
+  std::sort(padded.triplets.begin(), padded.triplets.end(), [](const Triplet& p, const Triplet& q) {
+    return p.row != q.row ? p.row < q.row : p.col < q.col;
+  });
+  const double tol = dtype == DType::I32 ? 0.0 : 1e-5;
+  if (op == KernelOp::SpMM) {
+    DenseMatrix x(pl.spec.n, d);
+    for (auto& v : x.v) v = val(rng);
+    pl.bindings.buffers["X"] = TensorData::of(x.v, dtype);
+    DenseMatrix got = pl.run_dense();
+    DenseMatrix want(padded.rows, d);
+    for (const Triplet& e : padded.triplets)
+      if (e.value != 0.0)
+        for (int64_t k = 0; k < d; ++k) want.at(e.row, k) += e.value * x.at(e.col, k);
+    return detail::compare(got, want, tol);
+  }
+  DenseMatrix x(pl.spec.m, d), y(d, pl.spec.n);
+  for (auto& v : x.v) v = val(rng);
+  for (auto& v : y.v) v = val(rng);
+  pl.bindings.buffers["X"] = TensorData::of(x.v, dtype);
+  pl.bindings.buffers["Y"] = TensorData::of(y.v, dtype);
+  DenseMatrix got = pl.run_dense();
+  DenseMatrix want(padded.rows, padded.cols);
+  for (const Triplet& e : padded.triplets) {
+    if (e.value == 0.0) continue;
+    double acc = 0;
+    for (int64_t k = 0; k < d; ++k) acc += x.at(e.row, k) * y.at(k, e.col);
+    want.at(e.row, e.col) = e.value * acc;
+  }
+  return detail::compare(got, want, tol);
+}
+
+// ---- tuner (tune.hpp, tune.cpp:19-190) -------------------------------------------------------
+struct SearchSpace {
+  std::vector<std::string> formats;
+  std::vector<std::string> schedules;
+  static SearchSpace hyb_c_grid(int k0 = -1, bool scan_k = false, bool include_csr = true) {
+    SearchSpace s;
+    if (include_csr) s.formats.push_back("csr");
+    for (int c : {1, 2, 4, 8, 16}) {
+      if (scan_k && k0 >= 0) {
+        for (int off : {-1, 0, 1})
+          s.formats.push_back("hyb:c=" + std::to_string(c) + ",k=" + std::to_string(std::max(0, k0 + off)));
+      } else if (k0 >= 0) {
+        s.formats.push_back("hyb:c=" + std::to_string(c) + ",k=" + std::to_string(k0));
+      } else {
+        s.formats.push_back("hyb:c=" + std::to_string(c));
+      }
+    }
+    s.schedules.push_back("");
+    return s;
+  }
+};
+
+struct SearchPoint {
+  int id = 0;
+  std::string format, schedule;
+};
+
+struct TrialResult {
+  SearchPoint point;
+  double median_ns = 0.0;
+  int64_t flops = 0, loads = 0;
+  bool valid = false, correct = false;
+  double padding = 0.0, balance = 1.0;
+  std::string error;
+};
+
+struct TuneReport {
+  std::vector<TrialResult> trials;
+  int best = -1;
+};
+
+inline std::vector<SearchPoint> enumerate(const SearchSpace& space) {
+  std::vector<SearchPoint> out;
+  const std::vector<std::string> formats =
+      space.formats.empty() ? std::vector<std::string>{"csr"} : space.formats;
+  const std::vector<std::string> schedules =
+      space.schedules.empty() ? std::vector<std::string>{""} : space.schedules;
+  int id = 0;
+  for (const auto& f : formats)
+    for (const auto& s : schedules) out.push_back({id++, f, s});
+  return out;
+}
+
+// run_trials: the reference's loop (build, verify gate, warmup + repeats of interpret, median)
+// with the repeats timed on the device (CUDA events around the kernels; conversion untimed as
+// `preconverted` asks) and flush_cache writing a 256 MB device buffer (larger than L2).
+inline TuneReport run_trials(KernelOp op, const CooMatrix& m, int64_t d, DType dtype,
+                             const SearchSpace& space, int repeats = 100, int warmup = 10,
+                             bool flush_cache = false, uint64_t seed = 1) {
+  if (repeats < 1) fail(ErrKind::Usage, "repeats must be >= 1");
+  TuneReport report;
+  std::mt19937 rng(static_cast<uint32_t>(seed));
+  std::uniform_int_distribution<int> val(-3, 3);
+  DenseMatrix x(m.cols, d);
+  for (auto& v : x.v) v = val(rng);
+  std::unique_ptr<DeviceArray<uint8_t>> junk;
+  if (flush_cache) junk = std::make_unique<DeviceArray<uint8_t>>(size_t{256} << 20);
+  for (const SearchPoint& pt : enumerate(space)) {
+    TrialResult tr;
+    tr.point = pt;
+    try {
+      FormatRequest fmt = FormatRequest::parse(pt.format);
+      PipelineOptions opts;
+      opts.schedule_script = pt.schedule;
+      opts.preconverted = true;
+      Pipeline pl = build_matrix_pipeline(op, m, d, dtype, fmt, opts);
+      pl.bindings.buffers["X"] = TensorData::of(x.v, dtype);  // as tune.cpp:112-114
+      VerifyResult v = verify_pipeline(op, m, d, dtype, fmt, opts, seed + 17);
+      tr.correct = v.pass;
+      if (!v.pass) tr.error = v.detail;
+      int64_t pads = 0, slots = 0;
+      for (const auto& r : pl.rules) {  // storage_padding (tune.cpp:86-95)
+        pads += r.storage.pad_slots;
+        slots += r.storage.nnz + r.storage.pad_slots;
+      }
+      tr.padding = slots == 0 ? 0.0 : static_cast<double>(pads) / static_cast<double>(slots);
+      if (pl.plan().hyb) check(strata_hyb_row_work_balance(pl.plan().hyb->get(), &tr.balance, nullptr));
+      std::vector<double> samples;
+      for (int rep = 0; rep < warmup + repeats; ++rep) {
+        if (junk) cuda_check(cudaMemset(junk->data(), rep & 0xff, junk->size()));
+        ExecReport er = interpret(pl.stage3, pl.bindings, pl.exec_opts);
+        if (rep == 0) {
+          tr.flops = er.stats.flops;
+          tr.loads = er.stats.loads;
+        }
+        if (rep >= warmup) samples.push_back(er.device_ms * 1e6);
+      }
+      std::sort(samples.begin(), samples.end());
+      tr.median_ns = samples[samples.size() / 2];
+      tr.valid = true;
+    } catch (const Error& e) {
+      tr.valid = false;
+      tr.error = e.what();
+    }
+    report.trials.push_back(std::move(tr));
+  }
+  for (size_t i = 0; i < report.trials.size(); ++i) {
+    const TrialResult& tr = report.trials[i];
+    if (!tr.valid || !tr.correct) continue;
+    if (report.best < 0 || tr.median_ns < report.trials[report.best].median_ns)
+      report.best = static_cast<int>(i);
+  }
+  if (report.best < 0) fail(ErrKind::Usage, "tuner: no valid point in the search space");
+  return report;
+}
+
+// report_json (tune.cpp:171-197): the same fields, two-space indentation.
+inline std::string report_json(const TuneReport& report) {
+  auto esc = [](const std::string& s) {
+    std::string o;
+    for (char ch : s) {
+      if (ch == '"' || ch == '\\') { o += '\\'; o += ch; }
+      else if (ch == '\n') o += "\\n";
+      else o += ch;
+    }
+    return o;
+  };
+  auto num = [](double v) {
+    std::ostringstream os;
+    os.precision(17);
+    os << v;
+    return os.str();
+  };
+  std::ostringstream j;
+  j << "{\n  \"best_point\": " << (report.best >= 0 ? report.trials[report.best].point.id : -1)
+    << ",\n  \"trials\": [";
+  for (size_t i = 0; i < report.trials.size(); ++i) {
+    const TrialResult& t = report.trials[i];
+    j << (i ? ",\n" : "\n") << "    {\n";
+    j << "      \"best\": " << (static_cast<int>(i) == report.best ? "true" : "false") << ",\n";
+    j << "      \"correct\": " << (t.correct ? "true" : "false") << ",\n";
+    if (!t.error.empty()) j << "      \"error\": \"" << esc(t.error) << "\",\n";
+    j << "      \"flops\": " << t.flops << ",\n";
+    j << "      \"loads\": " << t.loads << ",\n";
+    j << "      \"median_ns\": " << num(t.median_ns) << ",\n";
+    j << "      \"padding_ratio\": " << num(t.padding) << ",\n";
+    j << "      \"params\": {\n        \"format\": \"" << esc(t.point.format)
+      << "\",\n        \"schedule\": \"" << esc(t.point.schedule) << "\"\n      },\n";
+    j << "      \"point\": " << t.point.id << ",\n";
+    j << "      \"row_work_balance\": " << num(t.balance) << ",\n";
+    j << "      \"valid\": " << (t.valid ? "true" : "false") << "\n    }";
+  }
+  j << (report.trials.empty() ? "]\n}" : "\n  ]\n}");
+  return j.str();
 }
 
 }  // namespace strata_b200

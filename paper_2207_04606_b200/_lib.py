@@ -120,6 +120,16 @@ _sig("strata_rgms_run_bf16", C.c_int, vp, vp, vp, vp, i64, i64, vp)
 _sig("strata_rgms_info", C.c_int, vp, i64p, i64p)
 _sig("strata_rgms_destroy", C.c_int, vp)
 _sig("strata_partition_rows", C.c_int, vp, i64, C.c_int, vp)
+_sig("strata_nccl_unique_id", C.c_int, vp)
+_sig("strata_nccl_comm_init", C.c_int, vp, C.c_int, C.c_int, vp)
+_sig("strata_nccl_comm_destroy", C.c_int, vp)
+_sig("strata_shard_plan_create", C.c_int, vp, vp, vp, i64, i64, C.c_int, C.c_int, C.c_int,
+     C.c_int, C.c_int, C.POINTER(vp), vp)
+_sig("strata_shard_plan_rows", C.c_int, vp, C.c_int, C.c_int, i64p, i64p)
+_sig("strata_shard_plan_destroy", C.c_int, vp)
+_sig("strata_spmm_hyb_f32_sharded", C.c_int, vp, vp, vp, i64, vp, C.c_int, vp)
+_sig("strata_spmm_hyb_f32_sharded_p2p", C.c_int, vp, vp, vp, C.c_int, i64, vp)
+_sig("strata_sddmm_csr_f32_sharded", C.c_int, vp, vp, vp, vp, i64, C.c_int, vp, C.c_int, vp)
 _sig("strata_mtx_parse", C.c_int, vp, i64, C.POINTER(vp), vp)
 _sig("strata_mtx_read_file", C.c_int, C.c_char_p, C.POINTER(vp), vp)
 _sig("strata_mtx_info", C.c_int, vp, i64p, i64p, i64p)
@@ -151,4 +161,8 @@ EXPORTED = [
     "strata_rgms_destroy", "strata_partition_rows",
     "strata_mtx_parse", "strata_mtx_read_file", "strata_mtx_info", "strata_mtx_device",
     "strata_mtx_read", "strata_mtx_destroy",
+    "strata_nccl_unique_id", "strata_nccl_comm_init", "strata_nccl_comm_destroy",
+    "strata_shard_plan_create", "strata_shard_plan_rows", "strata_shard_plan_destroy",
+    "strata_spmm_hyb_f32_sharded", "strata_spmm_hyb_f32_sharded_p2p",
+    "strata_sddmm_csr_f32_sharded",
 ]

@@ -266,11 +266,13 @@ __device__ bool parse_i64(const uint8_t* s, long long& p, long long e, long long
 
 // istringstream >> double (libstdc++ num_get + strtod): [+-] digits [. digits] [(e|E) [+-]
 // digits]; a mantissa without digits, or an exponent marker without digits, fails with v = 0;
-// overflow gives +-DBL_MAX (failbit, mmio.cpp ignores it).  Returns false only when more than
+// overflow gives +-DBL_MAX (failbit, mmio.cpp ignores it); an exhausted line leaves `out`
+// (mmio.cpp's v = 1.0) untouched.  Returns false only when more than
 // 19 significant digits leave the rounding undecided (reported as unsupported).
 __device__ bool parse_f64(const uint8_t* s, long long& p, long long e, double& out) {
-  out = 0.0;
   while (p < e && is_space(s[p])) ++p;
+  if (p >= e) return true;  // nothing left: the sentry fails before num_get, `out` unchanged
+  out = 0.0;
   bool neg = false;
   if (p < e && (s[p] == '+' || s[p] == '-')) { neg = s[p] == '-'; ++p; }
   unsigned long long w = 0;

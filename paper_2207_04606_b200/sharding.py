@@ -12,7 +12,10 @@ from __future__ import annotations
 
 import numpy as np
 
-from .ops import CsrMatrix, partition_rows
+import ctypes as C
+
+from ._lib import check, lib
+from .ops import CsrMatrix, DeviceCsr, _dense, _ptr, _stream, partition_rows
 
 
 class RowShardPlan:
@@ -136,3 +139,93 @@ class PeerAllGather:
         for p in self._opened:
             ipc_close(p)
         self._opened = []
+
+
+class NcclComm:
+    """An NCCL communicator created through the C ABI (strata_nccl_comm_init): rank 0 draws
+    the unique id, the process group broadcasts it, every rank joins.  ``ptr`` is the address
+    of the ncclComm_t the sharded entry points take."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch
+        import torch.distributed as dist
+        idb = (C.c_char * 128)()
+        if rank == 0:
+            check(lib.strata_nccl_unique_id(idb))
+        if world > 1:
+            t = torch.frombuffer(bytearray(idb.raw), dtype=torch.uint8).clone()
+            dist.broadcast(t, src=0, group=group)
+            C.memmove(idb, bytes(t.tolist()), 128)
+        self._comm = C.c_void_p()
+        check(lib.strata_nccl_comm_init(idb, world, rank, C.byref(self._comm)))
+        self.rank, self.world = rank, world
+
+    @property
+    def ptr(self) -> int:
+        return C.addressof(self._comm)
+
+    def close(self):
+        if self._comm:
+            lib.strata_nccl_comm_destroy(C.byref(self._comm))
+            self._comm = C.c_void_p()
+
+
+class ShardPlan:
+    """Native row-partitioned plan (strata_shard_plan_create): this rank's nnz-balanced row
+    range, cut into ``chunks`` sub-ranges, each decomposed to hyb(c, k) on the device.  The
+    DeviceCsr must outlive the plan (the sharded SDDMM reads its arrays)."""
+
+    def __init__(self, csr: DeviceCsr, rank: int, world: int, chunks: int = 1, c: int = 1,
+                 k: int = None, stream=None):
+        from .ops import hyb_auto_k
+        self.csr = csr
+        self.rank, self.world, self.chunks = rank, world, chunks
+        self.rows, self.cols, self.nnz = csr.rows, csr.cols, csr.nnz
+        k = hyb_auto_k(csr) if k is None else k
+        self._h = C.c_void_p()
+        check(lib.strata_shard_plan_create(_ptr(csr.indptr), _ptr(csr.indices), _ptr(csr.values),
+                                           csr.rows, csr.cols, rank, world, chunks, c, k,
+                                           C.byref(self._h), _stream(stream)))
+
+    def rows_of(self, rank: int, chunk: int = -1):
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.strata_shard_plan_rows(self._h, rank, chunk, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def spmm(self, X, Y, comm: "NcclComm" = None, stream=None):
+        """Y[rows][d] replica on every rank; comm=None only at world 1."""
+        d = int(X.shape[1])
+        _dense(X, "X", (self.cols, d), "f32", X.device)
+        _dense(Y, "Y", (self.rows, d), "f32", X.device)
+        check(lib.strata_spmm_hyb_f32_sharded(self._h, _ptr(X), _ptr(Y), d,
+                                              comm.ptr if comm else None, self.world,
+                                              _stream(stream)))
+        return Y
+
+    def spmm_p2p(self, X, dst_ptrs, d: int, stream=None):
+        """Fused peer stores: dst_ptrs[q] = base address of rank q's Y replica."""
+        _dense(X, "X", (self.cols, d), "f32", X.device)
+        arr = (C.c_void_p * len(dst_ptrs))(*dst_ptrs)
+        check(lib.strata_spmm_hyb_f32_sharded_p2p(self._h, _ptr(X), arr, len(dst_ptrs), d,
+                                                  _stream(stream)))
+
+    def sddmm(self, X, Yd, B, gather: bool = True, comm: "NcclComm" = None, stream=None):
+        d = int(X.shape[1])
+        _dense(X, "X", (self.rows, d), "f32", X.device)
+        _dense(Yd, "Y", (d, self.cols), "f32", X.device)
+        _dense(B, "B", (self.nnz,), "f32", X.device)
+        check(lib.strata_sddmm_csr_f32_sharded(self._h, _ptr(X), _ptr(Yd), _ptr(B), d,
+                                               1 if gather else 0, comm.ptr if comm else None,
+                                               self.world, _stream(stream)))
+        return B
+
+    def close(self):
+        if self._h:
+            lib.strata_shard_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <sstream>
 #include <random>
 #include <string>
 #include <vector>
@@ -98,7 +99,7 @@ DenseMatrix reconstruct(const HybDecomposition& h) { return reconstruct_dense(h)
 
 DenseMatrix run_spmm(const CooMatrix& m, const DenseMatrix& x, const std::string& fmt) {
   Pipeline pl = build_matrix_pipeline(KernelOp::SpMM, m, x.cols, FormatRequest::parse(fmt));
-  pl.bindings["X"] = x.v;
+  pl.bindings.buffers["X"] = TensorData::of(x.v);
   return pl.run_dense();
 }
 
@@ -347,8 +348,8 @@ TEST_CASE("SDDMM: all-ones mask with identity factors picks the diagonal pattern
   a.rows = a.cols = 2;
   a.triplets = {{0, 0, 1}, {0, 1, 1}, {1, 0, 1}, {1, 1, 1}};
   Pipeline pl = build_matrix_pipeline(KernelOp::SDDMM, a, 2, FormatRequest{});
-  pl.bindings["X"] = {1, 0, 0, 1};
-  pl.bindings["Y"] = {1, 0, 0, 1};
+  pl.bindings.buffers["X"] = TensorData::of({1, 0, 0, 1});
+  pl.bindings.buffers["Y"] = TensorData::of({1, 0, 0, 1});
   DenseMatrix b = pl.run_dense();
   CHECK(b.at(0, 0) == 1 && b.at(0, 1) == 0 && b.at(1, 0) == 0 && b.at(1, 1) == 1);
 }
@@ -359,8 +360,8 @@ TEST_CASE("SDDMM random instances equal the dense oracle") {  // :81-97
     CooMatrix a = random_coo(rng, 8, 8, 0.3);
     Pipeline pl = build_matrix_pipeline(KernelOp::SDDMM, a, 4, FormatRequest{});
     DenseMatrix x = random_dense(rng, 8, 4), y = random_dense(rng, 4, 8);
-    pl.bindings["X"] = x.v;
-    pl.bindings["Y"] = y.v;
+    pl.bindings.buffers["X"] = TensorData::of(x.v);
+    pl.bindings.buffers["Y"] = TensorData::of(y.v);
     DenseMatrix got = pl.run_dense();
     DenseMatrix xy = matmul(x, y), ad = dense_from_coo(a), want(8, 8);
     for (int i = 0; i < 8; ++i)
@@ -373,8 +374,8 @@ TEST_CASE("SDDMM of a zero mask is zero") {  // :99-103
   CooMatrix a;
   a.rows = a.cols = 4;
   Pipeline pl = build_matrix_pipeline(KernelOp::SDDMM, a, 2, FormatRequest{});
-  pl.bindings["X"] = std::vector<double>(8, 0.0);
-  pl.bindings["Y"] = std::vector<double>(8, 0.0);
+  pl.bindings.buffers["X"] = TensorData::of(std::vector<double>(8, 0.0));
+  pl.bindings.buffers["Y"] = TensorData::of(std::vector<double>(8, 0.0));
   for (double v : pl.run_dense().v) CHECK(v == 0.0);
 }
 
@@ -384,8 +385,8 @@ TEST_CASE("RGMS with one relation degenerates to SpMM of X*W") {  // :105-118
   Pipeline pl = build_rgms_pipeline({a}, 16, 16);
   DenseMatrix got = pl.run_dense();
   DenseMatrix x(40, 16), w(16, 16);
-  x.v = pl.bindings["X"];
-  w.v = pl.bindings["W"];
+  x.v = pl.bindings.buffers["X"].values();
+  w.v = pl.bindings.buffers["W"].values();
   CHECK(got.v == matmul(dense_from_coo(a), matmul(x, w)).v);
 }
 
@@ -408,10 +409,11 @@ TEST_CASE("RGMS random instances match the two-stage oracle") {  // :120-156
     Pipeline pl = build_rgms_pipeline(rels, 16, 32, 100 + trial);
     DenseMatrix got = pl.run_dense();
     DenseMatrix x(48, 16), want(48, 32);
-    x.v = pl.bindings["X"];
+    x.v = pl.bindings.buffers["X"].values();
     for (int r = 0; r < R; ++r) {  // two_stage_rgms_oracle (kernels.cpp:169-193)
       DenseMatrix w(16, 32);
-      std::copy(pl.bindings["W"].begin() + r * 512, pl.bindings["W"].begin() + (r + 1) * 512, w.v.begin());
+      const std::vector<double> wall = pl.bindings.buffers["W"].values();
+      std::copy(wall.begin() + r * 512, wall.begin() + (r + 1) * 512, w.v.begin());
       DenseMatrix part = matmul(dense_from_coo(rels[r]), matmul(x, w));
       for (size_t i = 0; i < want.v.size(); ++i) want.v[i] += part.v[i];
     }
@@ -421,8 +423,170 @@ TEST_CASE("RGMS random instances match the two-stage oracle") {  // :120-156
 
 TEST_CASE("binding size mismatch is an Exec error") {  // interp.cpp:575-578
   Pipeline pl = build_matrix_pipeline(KernelOp::SpMM, example_m(), 2, FormatRequest::parse("hyb"));
-  pl.bindings["X"] = std::vector<double>(16, 1.0);
+  pl.bindings.buffers["X"] = TensorData::of(std::vector<double>(16, 1.0));
   CHECK_THROWS_KIND(pl.run_dense(), ErrKind::Exec, "binding size mismatch for X");
+}
+
+// ---- driver.hpp / interp.hpp / tune.hpp / mmio.hpp surface ------------------------------------
+
+TEST_CASE("six-argument pipelines: dtype, options, stage-III interpret, rule names") {  // driver.hpp:63-64
+  CooMatrix a = generate_matrix("powerlaw", 500, 400, 0, 0, 0, 12.0, 3);
+  PipelineOptions opts;
+  opts.schedule_script = "";
+  Pipeline pl = build_matrix_pipeline(KernelOp::SpMM, a, 16, DType::F32, FormatRequest::parse("hyb:c=2,k=2"), opts);
+  CHECK(pl.spec.m == 500 && pl.spec.n == 400 && pl.spec.d == 16 && pl.spec.dtype == DType::F32);
+  CHECK(pl.output_buffer == "Y" && pl.out_rows == 500 && pl.out_cols == 16);
+  REQUIRE(pl.rules.size() == 6);  // hyb_rules: c * (k + 1), empty buckets included
+  CHECK(pl.rules[0].name == "hyb_p0_b0" && pl.rules[5].name == "hyb_p1_b2");
+  CHECK(pl.rules[4].new_buffer == "A_hyb_p1_b1" && pl.rules[4].storage.width == 2);
+  HybDecomposition h = decompose_hyb(build_csr(a), 2, 2);
+  for (const auto& part : h.parts) {
+    const std::string name = "hyb_p" + std::to_string(part.partition) + "_b" + std::to_string(part.bucket);
+    for (size_t i = 0; i < pl.rules.size(); ++i)
+      if (pl.rules[i].name == name) {
+        TensorStorage got = pl.rule_storage(i);
+        CHECK(got.aux == part.ell.aux && got.values == part.ell.values);
+        CHECK(pl.rules[i].storage.nnz == part.ell.nnz && pl.rules[i].storage.pad_slots == part.ell.pad_slots);
+      }
+  }
+  std::mt19937 rng(4);
+  DenseMatrix x = random_dense(rng, 400, 16);
+  pl.bindings.buffers["X"] = TensorData::of(x.v, DType::F32);
+  ExecReport rep = interpret(pl.stage3, pl.bindings, pl.exec_opts);  // the tune.cpp:137 call
+  REQUIRE(rep.ok() && rep.outputs.buffers.count("Y") == 1);
+  CHECK(rep.outputs.buffers.at("Y").values() == matmul(dense_from_coo(a), x).v);
+  CHECK(rep.stats.flops > 0 && rep.device_ms > 0);
+  CHECK(pl.run_dense().v == matmul(dense_from_coo(a), x).v);
+  CHECK_THROWS_KIND(interpret(pl.stage1, pl.bindings), ErrKind::Exec,
+                    "interpret expects a stage-III program (got stage I)");
+  Bindings empty;
+  CHECK_THROWS_KIND(interpret(pl.stage3, empty), ErrKind::Exec, "missing binding for buffer X");
+  CHECK_THROWS_KIND(build_matrix_pipeline(KernelOp::SpMM, a, 16, DType::F64, FormatRequest{}, opts),
+                    ErrKind::Usage, "dtype f64 is not served");
+  CHECK_THROWS_KIND(build_matrix_pipeline(KernelOp::SpMM, a, 16, DType::I32, FormatRequest{}, opts),
+                    ErrKind::Usage, "dtype i32 is not served");
+  CHECK(FormatRequest::parse("hyb:c=2,k=3").str() == "hyb:c=2,k=3");
+  CHECK(FormatRequest::parse("bsr:b=4").str() == "bsr:b=4");
+  CHECK(FormatRequest::parse("srbcrs:t=8,g=32").str() == "srbcrs:t=8,g=32");
+}
+
+TEST_CASE("verify_pipeline passes in every served format") {  // driver.cpp:316-363
+  CooMatrix a = generate_matrix("powerlaw", 300, 260, 0, 0, 0, 9.0, 6);
+  for (const char* f : {"csr", "hyb:c=1", "hyb:c=3,k=2", "ell", "bsr:b=32", "dbsr:b=32", "srbcrs:t=8,g=32"}) {
+    VerifyResult v = verify_pipeline(KernelOp::SpMM, a, 64, DType::F32, FormatRequest::parse(f), PipelineOptions{}, 11);
+    CHECK(v.pass);
+    if (!v.pass) std::printf("    %s: %s\n", f, v.detail.c_str());
+  }
+  VerifyResult s = verify_pipeline(KernelOp::SDDMM, a, 16, DType::F32, FormatRequest{}, PipelineOptions{}, 12);
+  CHECK(s.pass);
+  CHECK_THROWS_KIND(verify_pipeline(KernelOp::SDDMM, a, 16, DType::F32, FormatRequest::parse("bsr:b=2"),
+                                    PipelineOptions{}, 12), ErrKind::Usage, "not served for SDDMM");
+}
+
+TEST_CASE("build_rgms_pipeline: overrides and the reference's draw order") {  // driver.cpp:241-314
+  std::mt19937 rng(31);
+  std::vector<CooMatrix> rels(3);
+  for (auto& r : rels) r = random_coo(rng, 40, 40, 0.2);
+  DenseMatrix x = random_dense(rng, 40, 16);
+  std::vector<DenseMatrix> w(3, DenseMatrix(16, 32));
+  for (auto& m : w) m = random_dense(rng, 16, 32);
+  // both overridden: Y = sum_r A_r X W_r
+  Pipeline pl = build_rgms_pipeline(rels, 16, 32, DType::F32, FormatRequest::parse("hyb"),
+                                    PipelineOptions{}, &w, &x, 5);
+  DenseMatrix want(40, 32);
+  for (int r = 0; r < 3; ++r) {
+    DenseMatrix part = matmul(dense_from_coo(rels[r]), matmul(x, w[r]));
+    for (size_t i = 0; i < want.v.size(); ++i) want.v[i] += part.v[i];
+  }
+  CHECK(pl.run_dense().v == want.v);
+  CHECK(pl.rules.size() == 3 && pl.rules[1].name == "r1_hyb");
+  // x overridden only: W takes the first draws of mt19937(seed)
+  Pipeline p2 = build_rgms_pipeline(rels, 16, 32, DType::F32, FormatRequest{}, PipelineOptions{},
+                                    nullptr, &x, 5);
+  std::mt19937 r5(5);
+  std::uniform_int_distribution<int> val(-3, 3);
+  std::vector<double> wdraw(3 * 16 * 32);
+  for (auto& v : wdraw) v = val(r5);
+  CHECK(p2.bindings.buffers["W"].values() == wdraw);
+  CHECK(p2.bindings.buffers["X"].values() == x.v);
+  // neither: X first, then W (driver.cpp:270-288)
+  Pipeline p3 = build_rgms_pipeline(rels, 16, 32, DType::F32, FormatRequest{}, PipelineOptions{});
+  std::mt19937 r7(7);
+  std::vector<double> xd(40 * 16), wd(3 * 16 * 32);
+  for (auto& v : xd) v = val(r7);
+  for (auto& v : wd) v = val(r7);
+  CHECK(p3.bindings.buffers["X"].values() == xd && p3.bindings.buffers["W"].values() == wd);
+  CHECK_THROWS_KIND(build_rgms_pipeline(rels, 16, 32, DType::F64, FormatRequest{}, PipelineOptions{}),
+                    ErrKind::Usage, "dtype f64");
+}
+
+TEST_CASE("run_trials over the hyb c-grid reaches the device and picks a correct point") {  // tune.cpp:100-165
+  CooMatrix a = generate_matrix("powerlaw", 2000, 2000, 0, 0, 0, 16.0, 1);
+  SearchSpace sp = SearchSpace::hyb_c_grid(-1, false, true);
+  CHECK(sp.formats.size() == 6 && sp.formats[0] == "csr" && sp.formats[2] == "hyb:c=2");
+  CHECK(enumerate(SearchSpace::hyb_c_grid(3, true, false)).size() == 15);
+  TuneReport rep = run_trials(KernelOp::SpMM, a, 32, DType::F32, sp, 5, 2, true, 1);
+  REQUIRE(rep.trials.size() == 6);
+  for (const auto& t : rep.trials) CHECK(t.valid && t.correct && t.median_ns > 0 && t.flops > 0);
+  CHECK(rep.best >= 0 && rep.trials[1].padding > 0 && rep.trials[1].balance >= 1.0);
+  const std::string js = report_json(rep);
+  CHECK(js.find("\"best_point\": " + std::to_string(rep.trials[rep.best].point.id)) != std::string::npos);
+  CHECK(js.find("\"format\": \"hyb:c=16\"") != std::string::npos);
+  // SDDMM points fail their binding (the reference's run_trials binds only X) -> no valid point
+  CHECK_THROWS_KIND(run_trials(KernelOp::SDDMM, a, 32, DType::F32, sp, 2, 1), ErrKind::Usage,
+                    "tuner: no valid point");
+}
+
+TEST_CASE("matrix market round trip") {  // test_storage.cpp:333-345
+  CooMatrix m = example_m();
+  std::ostringstream os;
+  write_matrix_market(os, m);
+  CHECK(os.str().find("%%MatrixMarket matrix coordinate real general") == 0);
+  std::istringstream is(os.str());
+  CooMatrix back = read_matrix_market(is);
+  CHECK(back.rows == m.rows);
+  CHECK(back.cols == m.cols);
+  CHECK(dense_from_coo(back).v == dense_from_coo(m).v);
+  std::istringstream bad("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n3 1 1\n");
+  CHECK_THROWS_KIND(read_matrix_market(bad), ErrKind::Usage, "matrix market entry out of range: 3 1 1");
+  CHECK_THROWS_KIND(read_matrix_market_file("/nonexistent.mtx"), ErrKind::Usage, "cannot open /nonexistent.mtx");
+}
+
+TEST_CASE("sharded SpMM / SDDMM through the C ABI with an NCCL communicator (world 1)") {  // §8b/§8e
+  CooMatrix a = generate_matrix("powerlaw", 6000, 5000, 0, 0, 0, 11.0, 8);
+  TensorStorage csr = build_csr(a);
+  DeviceCsr dc(csr);
+  char id[STRATA_NCCL_ID_BYTES];
+  check(strata_nccl_unique_id(id));
+  void* comm = nullptr;  // an ncclComm_t
+  check(strata_nccl_comm_init(id, 1, 0, &comm));
+  std::mt19937 rng(3);
+  const int64_t d = 32;
+  DenseMatrix x = random_dense(rng, a.cols, d);
+  std::vector<float> xf(x.v.begin(), x.v.end());
+  DeviceArray<float> X(xf), Y(static_cast<size_t>(a.rows * d)), Yref(static_cast<size_t>(a.rows * d));
+  DeviceHyb h(dc, 1, hyb_auto_k(csr));
+  h.spmm(X.data(), Yref.data(), d);
+  for (int chunks : {1, 4}) {
+    strata_shard_plan* p = nullptr;
+    check(strata_shard_plan_create(dc.indptr.data(), dc.indices.data(), dc.values.data(), dc.rows,
+                                   dc.cols, 0, 1, chunks, 1, hyb_auto_k(csr), &p, nullptr));
+    check(strata_spmm_hyb_f32_sharded(p, X.data(), Y.data(), d, &comm, 1, nullptr));
+    CHECK(Y.host() == Yref.host());
+    DenseMatrix xs = random_dense(rng, a.rows, 16), yd = random_dense(rng, 16, a.cols);
+    std::vector<float> xsf(xs.v.begin(), xs.v.end()), ydf(yd.v.begin(), yd.v.end());
+    DeviceArray<float> Xs(xsf), Yd(ydf), B(static_cast<size_t>(csr.nnz)), Bref(static_cast<size_t>(csr.nnz));
+    check(strata_sddmm_csr_f32(dc.indptr.data(), dc.indices.data(), dc.values.data(), Xs.data(),
+                               Yd.data(), Bref.data(), a.rows, a.cols, csr.nnz, 16, nullptr));
+    check(strata_sddmm_csr_f32_sharded(p, Xs.data(), Yd.data(), B.data(), 16, 1, &comm, 1, nullptr));
+    CHECK(B.host() == Bref.host());
+    int64_t r0 = -1, r1 = -1;
+    check(strata_shard_plan_rows(p, 0, -1, &r0, &r1));
+    CHECK(r0 == 0 && r1 == a.rows);
+    CHECK(strata_spmm_hyb_f32_sharded(p, X.data(), Y.data(), d, &comm, 2, nullptr) == STRATA_ERR_USAGE);
+    check(strata_shard_plan_destroy(p));
+  }
+  check(strata_nccl_comm_destroy(&comm));
 }
 
 int main() {

@@ -68,6 +68,67 @@ def test_row_sharded_spmm_allgather_gloo(tmp_path, world):
     assert np.array_equal(np.load(out), want)
 
 
+def _bcast_worker(rank, world, port, out_path):
+    """The native sharded plan's reassembly (shard.cu): per chunk, every rank's rows are
+    broadcast from their owner into the full in-place Y (grouped ncclBroadcast on the GPU,
+    dist.broadcast over gloo here); the SDDMM's contiguous nnz ranges likewise into B."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import paper_2207_04606_b200 as S
+    from paper_2207_04606_b200.sharding import RowShardPlan
+    from oracle import port as P
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    m = S.generate_matrix("powerlaw", 7000, 6500, 0, 0, 0, 18.0, 4)
+    plan = RowShardPlan(m, world, chunks=3)  # the same cuts strata_shard_plan_create makes
+    d = 8
+    X = S.dense_int((m.cols, d), 6)
+    Y = torch.full((m.rows, d), float("nan"))
+    for c in range(plan.chunks):
+        a, b = plan.sub[rank][c]
+        sh = plan.chunk(rank, c)
+        Y[a:b] = torch.from_numpy(P.spmm_csr_refnum(sh.rows, sh.indptr, sh.indices, sh.values, X))
+        for q in range(world):  # one group: chunk c of every rank, from its owner, in place
+            qa, qb = plan.sub[q][c]
+            seg = Y[qa:qb].contiguous()
+            dist.broadcast(seg, src=q)
+            Y[qa:qb] = seg
+    Xs = S.dense_int((m.rows, d), 7)
+    Yd = S.dense_int((d, m.cols), 8)
+    B = torch.full((m.nnz,), float("nan"))
+    r0, r1 = plan.rows_of(rank)
+    q0, q1 = int(m.indptr[r0]), int(m.indptr[r1])
+    sh = plan.shard(rank)
+    B[q0:q1] = torch.from_numpy(P.sddmm_csr_refnum(sh.rows, sh.cols, sh.indptr, sh.indices,
+                                                   sh.values, Xs[r0:r1], Yd))
+    for q in range(world):
+        qr0, qr1 = plan.rows_of(q)
+        a, b = int(m.indptr[qr0]), int(m.indptr[qr1])
+        seg = B[a:b].contiguous()
+        dist.broadcast(seg, src=q)
+        B[a:b] = seg
+    np.save(out_path + f".{rank}.y.npy", Y.numpy())
+    np.save(out_path + f".{rank}.b.npy", B.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_broadcast_reassembly_gloo(tmp_path, world):
+    import paper_2207_04606_b200 as S
+    from oracle import port as P
+    out = str(tmp_path / "r")
+    mp.spawn(_bcast_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    m = S.generate_matrix("powerlaw", 7000, 6500, 0, 0, 0, 18.0, 4)
+    wantY = P.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, S.dense_int((m.cols, 8), 6))
+    wantB = P.sddmm_csr_refnum(m.rows, m.cols, m.indptr, m.indices, m.values,
+                               S.dense_int((m.rows, 8), 7), S.dense_int((8, m.cols), 8))
+    for r in range(world):
+        assert np.array_equal(np.load(out + f".{r}.y.npy"), wantY)
+        assert np.array_equal(np.load(out + f".{r}.b.npy"), wantB)
+
+
 @pytest.mark.parametrize("parts", [2, 3, 5, 8])
 def test_shard_decompositions_concatenate_to_global(parts):
     import paper_2207_04606_b200 as S
