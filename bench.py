@@ -405,6 +405,49 @@ def extra_reddit(S, torch, dev, stream, peak):
     return out
 
 
+def extra_sddmm_sharded(S, torch, dist, dev, stream, rank, world, comm):
+    """N > 1: BASELINE configs[1]'s SDDMM (C2, d = 64) row-sharded through the native plan —
+    each rank computes its contiguous nnz range, then the ranges are all-gathered (grouped
+    ncclBroadcast) so every rank holds B[nnz]; device time max over ranks."""
+    from paper_2207_04606_b200.sharding import ShardPlan
+    cfg = REDDIT
+    m = S.generate_matrix(cfg["kind"], cfg["n"], cfg["m"], 0, 0, 0, cfg["avg"], cfg["seed"])
+    d = cfg["d"]
+    dcsr = m.to_device(dev)
+    plan = ShardPlan(dcsr, rank, world, chunks=1, stream=stream)
+    g = torch.Generator(device=dev)
+    g.manual_seed(2)
+    Xs = torch.randint(-3, 4, (m.rows, d), device=dev, dtype=torch.float32, generator=g)
+    Yd = torch.randint(-3, 4, (d, m.cols), device=dev, dtype=torch.float32, generator=g)
+    B = torch.empty((m.nnz,), device=dev)
+    out = {}
+    for name, gather in (("gathered", True), ("compute_only", False)):
+        for _ in range(3):
+            plan.sddmm(Xs, Yd, B, gather=gather, comm=comm, stream=stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record(stream)
+        for _ in range(reps):
+            plan.sddmm(Xs, Yd, B, gather=gather, comm=comm, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        out[name + "_ms"] = round(ms, 4)
+        out[name + "_gflops"] = round((2.0 * m.nnz * d + m.nnz) / (ms * 1e-3) / 1e9, 1)
+    ref = S.sddmm(dcsr, Xs, Yd)
+    plan.sddmm(Xs, Yd, B, gather=True, comm=comm, stream=stream)
+    torch.cuda.synchronize()
+    ok = torch.tensor([1 if torch.equal(B, ref) else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    out["equals_single_gpu"] = bool(int(ok[0]))
+    out["nnz"] = m.nnz
+    return out
+
+
 def _time_ms(torch, stream, fn, reps=20):
     for _ in range(3):
         fn()
@@ -489,22 +532,32 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     Yh = torch.empty((H, 4096, d), device=dev)
     msh = _time_graph_ms(torch, lambda: S.bsr_spmm_batched(bs, Vh, Xh, Yh))
     flops_h = H * flops
+    # B_min: every head's block values, X and Y move once; the gather model charges a 32 x d
+    # X tile per stored block, most of which are L2 re-reads (ncu: 45 MB DRAM per call).
+    b_min_h = H * (bs.nblocks * 32 * 32 * 2 + 4096 * d * 2 + 4096 * d * 4) + bs.nblocks * 4 + 129 * 4
     b_alg_h = H * (bs.nblocks * 32 * 32 * 2 + bs.nblocks * 32 * d * 2 + 4096 * d * 4) + bs.nblocks * 4 + 129 * 4
     out["c3_bsr_spmm_12head"] = {"ms": round(msh, 5), "gflops": round(flops_h / (msh * 1e-3) / 1e9, 1),
                                  "tensor_frac": round(flops_h / (msh * 1e-3) / 1e12 / bf16_peak, 5),
-                                 "hbm_frac": round(b_alg_h / (msh * 1e-3) / 1e9 / hbm_peak, 4),
-                                 "bytes_model": "heads*(blocks*2KB + blocks*32*d*2 + 4096*d*4)"}
+                                 "hbm_frac": round(b_min_h / (msh * 1e-3) / 1e9 / hbm_peak, 4),
+                                 "bytes_model": "B_min = heads*(blocks*2KB + 4096*d*2 + 4096*d*4)",
+                                 "hbm_frac_gather_model_l2_assisted":
+                                     round(b_alg_h / (msh * 1e-3) / 1e9 / hbm_peak, 4)}
     # 12-head block-sparse SDDMM (sparse-attention scores) on tcgen05, C3 mask.
     Qh = torch.randint(-3, 4, (H, 4096, d), device=dev).to(torch.bfloat16)
     Kh = torch.randint(-3, 4, (H, 4096, d), device=dev).to(torch.bfloat16)
     Sh = torch.empty((H, bs.nblocks, 32, 32), device=dev)
     ms_sd = _time_graph_ms(torch, lambda: S.bsr_sddmm(bs, Qh, Kh, Sh))
     fl_sd = H * bs.nblocks * 2.0 * 32 * 32 * d
-    b_sd = H * (bs.nblocks * 32 * 32 * 4 * 2 + bs.nblocks * 32 * d * 2 + 4096 * d * 2)
+    # B_min: the mask's block values (f32, shared by the heads) once, per head S out, Q and K
+    # once; the gather model charges a 32 x d K tile per stored block (L2 re-reads).
+    b_sd = bs.nblocks * 32 * 32 * 4 + H * (bs.nblocks * 32 * 32 * 4 + 2 * 4096 * d * 2)
+    b_sd_g = bs.nblocks * 32 * 32 * 4 + H * (bs.nblocks * 32 * 32 * 4 + bs.nblocks * 32 * d * 2 + 4096 * d * 2)
     out["c3_bsr_sddmm_12head"] = {"ms": round(ms_sd, 5), "gflops": round(fl_sd / (ms_sd * 1e-3) / 1e9, 1),
                                   "tensor_frac": round(fl_sd / (ms_sd * 1e-3) / 1e12 / bf16_peak, 5),
                                   "hbm_frac": round(b_sd / (ms_sd * 1e-3) / 1e9 / hbm_peak, 4),
-                                  "bytes_model": "heads*(blocks*4KB A in + 4KB S out + blocks*32*d*2 K + 4096*d*2 Q)",
+                                  "bytes_model": "B_min = blocks*4KB (A, shared) + heads*(blocks*4KB S out + 4096*d*2 Q + 4096*d*2 K)",
+                                  "hbm_frac_gather_model_l2_assisted":
+                                      round(b_sd_g / (ms_sd * 1e-3) / 1e9 / hbm_peak, 4),
                                   "timing": "CUDA graph of 20 calls"}
     # Pruned-weight formats: a 4096 x 4096 weight pruned
     # to 5 % density (unstructured, "random") as SR-BCRS(8, 32) and a 2 %-dense block mask as
@@ -633,70 +686,71 @@ def run_ours(args):
     m = S.generate_matrix(cfg["kind"], cfg["n"], cfg["m"], 0, 0, 0, cfg["avg"], cfg["seed"])
     gen_s = time.time() - t0
     k = S.hyb_auto_k(m)
-    from paper_2207_04606_b200.sharding import RowShardPlan
-    # N > 1, --allgather p2p (default): the fused SpMM + all-gather — every rank's SpMM stores
-    # its rows straight into all ranks' full Y replicas over NVLink (strata_spmm_hyb_f32_multi,
-    # CUDA IPC mappings), verified once against the NCCL path below, which it falls back to.
-    # --allgather nccl: each rank's rows are cut into sub-chunks so chunk c's NCCL all-gather
-    # overlaps the SpMM of chunk c+1 (sharding.py).  N = 1 runs the whole graph as one chunk.
+    from paper_2207_04606_b200.sharding import NcclComm, PeerAllGather, RowShardPlan, ShardPlan
+    # The native row-partitioned plan (strata_shard_plan_create): this rank's nnz-balanced row
+    # range, cut into chunks, each decomposed to hyb on this GPU; X replicated, Y a full
+    # replica on every rank.  N > 1 reassembly (--allgather):
+    #   p2p (default)  strata_spmm_hyb_f32_sharded_p2p — the SpMM stores every finished row into
+    #                  all ranks' replicas over NVLink (CUDA IPC), verified once against nccl;
+    #   nccl           strata_spmm_hyb_f32_sharded with an NCCL communicator made by the C ABI —
+    #                  per chunk a grouped ncclBroadcast from every owner (an uneven all-gather),
+    #                  overlapping the next chunk's SpMM on the plan's stream.
     p2p = world > 1 and args.allgather == "p2p"
     chunks = 4 if (world > 1 and not p2p) else 1
-    plan = RowShardPlan(m, world, chunks)
-    r0, r1 = plan.rows_of(rank)
-    shard = plan.shard(rank)
     stream = torch.cuda.current_stream()
-
-    hs, up_s, decomp_s = [], 0.0, 0.0
-    for c in range(chunks):
-        t0 = time.time()
-        dsub = plan.chunk(rank, c).to_device(dev)
-        torch.cuda.synchronize()
-        t1 = time.time()
-        hs.append(S.decompose_hyb(dsub, 1, k))
-        torch.cuda.synchronize()
-        up_s += t1 - t0
-        decomp_s += time.time() - t1
-        if c == 0:  # warm (second) decomposition of the same device CSR
-            t1 = time.time()
-            h_warm = S.decompose_hyb(dsub, 1, k)
-            torch.cuda.synchronize()
-            decomp_warm_s = time.time() - t1
-            del h_warm
-        del dsub
-    sched = hs[0].schedule_info()
-    launches_per_step = sum(h.schedule_info()["launches_per_spmm"] for h in hs)
+    t0 = time.time()
+    dcsr = m.to_device(dev)  # the full CSR on every rank (the plan slices it)
+    torch.cuda.synchronize()
+    up_s = time.time() - t0
+    t0 = time.time()
+    plan = ShardPlan(dcsr, rank, world, chunks=chunks, c=1, k=k, stream=stream)
+    torch.cuda.synchronize()
+    plan_s = time.time() - t0
+    r0, r1 = plan.rows_of(rank)
+    shard = RowShardPlan(m, world).shard(rank)  # the same cuts, host copy for the byte model
+    # The shard's decomposition alone, first and warm (second) call, for the plan-cost record.
+    dsh = shard.to_device(dev)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    h = S.decompose_hyb(dsh, 1, k)
+    torch.cuda.synchronize()
+    decomp_s = time.time() - t0
+    t0 = time.time()
+    h_warm = S.decompose_hyb(dsh, 1, k)
+    torch.cuda.synchronize()
+    decomp_warm_s = time.time() - t0
+    del h_warm, dsh
+    sched = h.schedule_info()
+    launches_per_step = sched["launches_per_spmm"] * chunks
 
     # X replicated on every rank (BASELINE: "dense features replicated"); integer operands in
     # [-3, 3] like the reference tuner's (tune.cpp:108-111).
     gx = torch.Generator(device=dev)
     gx.manual_seed(1)
     X = torch.randint(-3, 4, (m.cols, d), device=dev, dtype=torch.float32, generator=gx)
-    Yfull = torch.empty((plan.padded_rows, d), device=dev, dtype=torch.float32)
-    Yloc = torch.empty((chunks, plan.max_rows, d), device=dev, dtype=torch.float32)
-    ys = []
-    for c in range(chunks):
-        n_c = plan.chunk_rows(rank, c)
-        if world == 1:
-            ys.append(Yfull[plan.slot(c, rank): plan.slot(c, rank) + n_c])
-        else:
-            ys.append(Yloc[c, :n_c])
-    gviews = [Yfull[plan.slot(c, 0): plan.slot(c, 0) + world * plan.max_rows] for c in range(chunks)]
+    Yrep = torch.empty((m.rows, d), device=dev, dtype=torch.float32)
+    # NCCL refuses two ranks on one device: the shared-GPU test mode runs p2p only.
+    comm = NcclComm(rank, world) if world > 1 and not share else None
+    if share and not p2p:
+        print("bench.py: STRATA_BENCH_SHARE_GPU runs the p2p reassembly only", file=sys.stderr)
+        return 2
 
     pag, p2p_note = None, None
     if p2p:
-        from paper_2207_04606_b200.sharding import PeerAllGather
-        Yrep = torch.empty((m.rows, d), device=dev, dtype=torch.float32)
         try:
             pag = PeerAllGather(Yrep, rank, world)
-            # one-time check against the NCCL path: local rows + all_gather + unpad
-            S.spmm(hs[0], X, ys[0], stream=stream)
-            dist.all_gather_into_tensor(gviews[0], Yloc[0])
-            S.spmm_multi(hs[0], X, pag.dsts(r0), stream=stream)
+            # one-time check against the NCCL path (bitwise), then fall back if it differs
+            Ychk = torch.empty_like(Yrep)
+            if comm is not None:
+                plan.spmm(X, Ychk, comm, stream=stream)
+            else:  # shared-GPU test mode: the single-GPU SpMM of the whole graph
+                S.spmm(S.decompose_hyb(dcsr, 1, k), X, Ychk, stream=stream)
+            plan.spmm_p2p(X, pag.dsts(0), d, stream=stream)
             pag.fence()
             torch.cuda.synchronize()
-            same = torch.equal(Yrep, plan.unpad(Yfull))
-            ok = torch.tensor([1 if same else 0], device=dev)
+            ok = torch.tensor([1 if torch.equal(Yrep, Ychk) else 0], device=dev)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            del Ychk
             if int(ok[0]) != 1:
                 raise RuntimeError("peer all-gather differs from the NCCL all-gather")
         except Exception as e:  # noqa: BLE001 — fall back to the NCCL collective
@@ -704,26 +758,15 @@ def run_ours(args):
             pag = None
             p2p = False
 
-    def step(evs=None):
+    def step():
         if pag is not None:
-            if evs is not None:
-                evs[0][0].record(stream)
-            S.spmm_multi(hs[0], X, pag.dsts(r0), stream=stream)
-            if evs is not None:
-                evs[0][1].record(stream)
+            plan.spmm_p2p(X, pag.dsts(0), d, stream=stream)
             pag.fence()
-            return
-        works = []
-        for c in range(chunks):
-            if evs is not None:
-                evs[c][0].record(stream)
-            S.spmm(hs[c], X, ys[c], stream=stream)
-            if evs is not None:
-                evs[c][1].record(stream)
-            if world > 1:  # overlaps the next chunk's SpMM (NCCL stream)
-                works.append(dist.all_gather_into_tensor(gviews[c], Yloc[c], async_op=True))
-        for w in works:
-            w.wait()
+        else:
+            plan.spmm(X, Yrep, comm, stream=stream)
+
+    def compute_only():  # the same kernels, no reassembly (this rank's rows)
+        plan.spmm(X, Yrep, None, stream=stream)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -733,22 +776,28 @@ def run_ours(args):
 
     sampler = ClockSampler(local)
     sampler.start()
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(chunks)] for _ in range(args.steps)]
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e_start.record(stream)
     for i in range(args.steps):
-        step(ev[i])
+        step()
     e_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
     total_ms = e_start.elapsed_time(e_end)
-    spmm_ms = float(np.mean([sum(a.elapsed_time(b) for a, b in evs) for evs in ev]))
+    # compute-only launches, CUDA events around each (the kernel time of the roofline)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for a_, b_ in ev:
+        a_.record(stream)
+        compute_only()
+        b_.record(stream)
+    torch.cuda.synchronize()
+    spmm_ms = float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev]))
     t = torch.tensor([total_ms, spmm_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -756,6 +805,12 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
     flops = 2.0 * m.nnz * d
     gflops = flops / (ms_per_step * 1e-3) / 1e9
+    sddmm_sharded = None
+    if comm is not None and not args.no_extra:
+        try:
+            sddmm_sharded = extra_sddmm_sharded(S, torch, dist, dev, stream, rank, world, comm)
+        except Exception as e:  # informational only
+            sddmm_sharded = {"error": str(e)}
 
     # roofline of the dominant kernel on this rank's shard
     b_alg = b_alg_spmm(shard.nnz, shard.rows, m.cols, d)
@@ -773,11 +828,7 @@ def run_ours(args):
 
     # e2e: same metric through the C ABI with host buffers (pinned), copies inside the region:
     # strata_spmm_hyb_f32_host = H2D of X, the shard SpMM, D2H of this rank's rows.
-    h_e2e = hs[0]
-    if chunks > 1:
-        dsh = shard.to_device(dev)
-        h_e2e = S.decompose_hyb(dsh, 1, k)
-        del dsh
+    h_e2e = h  # this rank's shard as one hyb
     # Batched form (strata_spmm_hyb_f32_host_batch): e2e_steps independent feature matrices,
     # each copied in from pinned host memory and its Y copied back; copy-in of step b+1 and
     # copy-out of step b-1 overlap step b's SpMM.  Two host buffer pairs alternate.
@@ -808,14 +859,14 @@ def run_ours(args):
            "path": "strata_spmm_hyb_f32_host_batch (pinned host X in, host Y rows out, per "
                    "step; copy-in/compute/copy-out pipelined across steps, wall clock)"}
     del Xh, Yh
-    h = hs[0]
 
     cpu = None
     extra = {"generate_s": round(gen_s, 2), "csr_upload_ms": round(up_s * 1e3, 1),
+             "shard_plan_ms": round(plan_s * 1e3, 1),
              "decompose_ms": round(decomp_s * 1e3, 1),
-             "decompose_warm_ms_chunk0": round(decomp_warm_s * 1e3, 1),
-             "hyb_parts_rows_chunk0": [P.nrows for P in h.parts],
-             "padding_ratio_chunk0": round(h.padding_ratio, 5),
+             "decompose_warm_ms": round(decomp_warm_s * 1e3, 1),
+             "hyb_parts_rows": [P.nrows for P in h.parts],
+             "padding_ratio": round(h.padding_ratio, 5),
              "schedule": sched, "spmm_ms_max_over_ranks": round(spmm_ms_max, 4),
              "allgather_exposed_ms": round(ms_per_step - spmm_ms_max, 4) if world > 1 else 0.0,
              "chunks_per_rank": chunks,
@@ -823,6 +874,8 @@ def run_ours(args):
              "allgather_note": p2p_note,
              "compute_only_gflops": round(flops / (spmm_ms_max * 1e-3) / 1e9, 2),
              "frac_of_8tbs_nameplate": round(achieved / 8000.0, 4)}
+    if sddmm_sharded is not None:
+        extra["sddmm_sharded_c2"] = sddmm_sharded
     if rank == 0 and world == 1 and not args.no_extra:
         try:
             extra.update(extra_reddit(S, torch, dev, stream, hbm_peak))
@@ -862,13 +915,17 @@ def run_ours(args):
                        "parallelism": ("single GPU" if world == 1 else
                                        f"row-sharded x{world} (nnz-balanced) + " +
                                        ("fused peer-store all-gather (NVLink, CUDA IPC)" if pag is not None
-                                        else "NCCL all-gather (4 chunks overlapped)")),
+                                        else "NCCL grouped-broadcast all-gather (4 chunks overlapped)")),
                        "l2": "no flush: inputs larger than L2 (X 1.25 GB, ELL 0.57 GB)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "extra": extra,
         }
         print(json.dumps(line))
+    if pag is not None:
+        pag.close()
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -351,7 +351,8 @@ int strata_mtx_destroy(strata_mtx* h);
  * hyb(c, k) on the calling device.  indices / values must stay valid while the plan lives
  * (the SDDMM reads them).  A plan's calls must be ordered (one stream at a time).
  *   SpMM: X[cols][d] replicated, Y[rows][d] a full replica on every rank.  `comm` points to
- *     this rank's ncclComm_t (rank/size checked against the plan; NULL allowed when world=1):
+ *     this rank's ncclComm_t (rank/size checked against the plan; NULL = no reassembly: only
+ *     this rank's rows of Y are written, as at world 1):
  *     chunk q of every rank is broadcast from its owner (grouped ncclBroadcast = uneven
  *     all-gather, in place) on the plan's stream, overlapping chunk q+1's SpMM.  The _p2p form
  *     instead stores every finished row into all ranks' replicas (Y_dsts[rank q] = rank q's Y,

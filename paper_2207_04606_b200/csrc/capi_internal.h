@@ -71,29 +71,51 @@ void generate_csr(const std::string& kind, int64_t n, int64_t m, double density,
                   int64_t block, double avg_degree, uint64_t seed, CsrHost& out);
 void dense_int(int64_t count, uint64_t seed, float* out);
 
-// RAII device buffer (stream-ordered free is not needed: handles are destroyed by the
-// caller after its stream work completes, as with the reference's value semantics).
+// RAII device buffer.  alloc() = cudaMalloc (freed with cudaFree); alloc_async(n, s) takes
+// the memory from the device's stream-ordered pool (workspace_alloc: freed blocks stay cached,
+// so rebuilding a plan of the same size costs no driver mapping).  A temporary returns it with
+// cudaFreeAsync on `s`; a handle-owned (persistent) buffer on the legacy stream, i.e. after all
+// work queued on blocking streams — handles are destroyed by the caller after its work on them,
+// as with the reference's value semantics.
+void* workspace_alloc(size_t bytes, cudaStream_t s);
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool pooled = false;
+  cudaStream_t free_stream = nullptr;
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(size_t count, cudaStream_t s) { alloc_async(count, s); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), pooled(o.pooled), free_stream(o.free_stream) {
+    o.p = nullptr;
+    o.n = 0;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     reset();
-    p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+    p = o.p; n = o.n; pooled = o.pooled; free_stream = o.free_stream;
+    o.p = nullptr; o.n = 0;
     return *this;
   }
   void alloc(size_t count) {
     reset();
     n = count;
+    pooled = false;
     if (count) STRATA_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
   }
+  void alloc_async(size_t count, cudaStream_t s, bool persistent = false) {
+    reset();
+    n = count;
+    pooled = true;
+    free_stream = persistent ? nullptr : s;
+    if (count) p = static_cast<T*>(workspace_alloc(count * sizeof(T), s));
+  }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, free_stream); else cudaFree(p);
+    }
     p = nullptr;
     n = 0;
   }
@@ -192,8 +214,6 @@ int num_sms();
 // (cuTensorMapEncodeTiled through the runtime's driver entry point).
 CUtensorMap make_tensor_map_bf16_2d(const void* base, long long rows, long long cols,
                                     int box_cols, int box_rows, CUtensorMapSwizzle swizzle);
-// Stream-ordered scratch from the device pool (kept cached across calls); free with cudaFreeAsync.
-void* workspace_alloc(size_t bytes, cudaStream_t s);
 // Thread-local message returned by strata_last_error() (shared by every translation unit).
 void set_last_error(const std::string& msg);
 

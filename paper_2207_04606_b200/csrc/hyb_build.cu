@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "capi_internal.h"
 #include "common.cuh"
@@ -235,8 +236,65 @@ __global__ void cross_flags_kernel(const int32_t* __restrict__ I, long long nrow
   fend[c] = xp && !(xc && uniform);
 }
 
+// ---- SpMM fix-up schedule, built on the device -------------------------------------------
+// Per split part (bucket k), after the crossing runs are selected (rs[j], re[j]: first / last
+// chunk of run j, j < nruns): a run of n = re - rs + 1 contributions needs ceil(n / kFixTile)
+// level-1 tiles and, when that is more than one, a level-2 run entry with as many slots.
+// Counts per run -> exclusive scans over all split parts in part order -> entries.  Runs of
+// part pi live at [carry_off, carry_off + nchunks) of the concatenated per-chunk arrays.
+__global__ void run_counts_kernel(const long long* __restrict__ rs, const long long* __restrict__ re,
+                                  const long long* __restrict__ nsel, long long nchunks,
+                                  long long* __restrict__ ntile, long long* __restrict__ nl2,
+                                  long long* __restrict__ isrun) {
+  const long long nruns = nsel[0];
+  for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < nchunks;
+       j += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long nt = 0;
+    if (j < nruns) nt = (re[j] - rs[j] + 1 + kFixTile - 1) / kFixTile;
+    ntile[j] = nt;
+    nl2[j] = nt > 1 ? nt : 0;
+    isrun[j] = nt > 1 ? 1 : 0;
+  }
+}
+
+__global__ void fix_fill_kernel(const long long* __restrict__ rs, const long long* __restrict__ re,
+                                const long long* __restrict__ nsel, const int32_t* __restrict__ I,
+                                int rpc_log2, long long carry_off,
+                                const long long* __restrict__ tile_off,
+                                const long long* __restrict__ l2_off,
+                                const long long* __restrict__ run_off, FixTile* __restrict__ tiles,
+                                FixRun* __restrict__ runs) {
+  const long long nruns = nsel[0];
+  for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < nruns;
+       j += static_cast<long long>(gridDim.x) * blockDim.x) {
+    // Run j: chunks rs..re; contributions in order = tail carry of rs, then the head carries
+    // of rs+1 .. re.  Its output row is the last row of chunk rs.
+    const long long ca = rs[j], n = re[j] - ca + 1;
+    const long long row = I[((ca + 1) << rpc_log2) - 1];
+    const long long nt = (n + kFixTile - 1) / kFixTile;
+    const long long t0 = tile_off[j], l2 = l2_off[j];
+    for (long long u = 0; u < nt; ++u) {
+      FixTile t;
+      t.carry0 = carry_off + ca + u * kFixTile;
+      t.count = static_cast<int>(min64(kFixTile, n - u * kFixTile));
+      t.first_slot = u == 0 ? 1 : 0;
+      t.out = nt == 1 ? row : -(l2 + u + 1);
+      tiles[t0 + u] = t;
+    }
+    if (nt > 1) runs[run_off[j]] = FixRun{l2, row, static_cast<int>(nt), 0};
+  }
+}
+
+unsigned grid_of(long long n) {
+  return static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 16)));
+}
+
 }  // namespace
 
+// Two host synchronisations, both to size allocations: the per-bin totals (part table, ELL
+// arrays) and the fix-up schedule totals.  Temporaries come from the stream-ordered pool and
+// are released in stream order; the handle's arrays are pooled too (no cudaMalloc/cudaFree
+// device-wide syncs), so a rebuilt plan of the same size reuses cached memory.
 void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32_t* indices,
                           const float* values, cudaStream_t s) {
   const int c = h.c, k = h.k;
@@ -246,12 +304,15 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
   const int64_t part_w = (cols + c - 1) / c;  // storage.cpp:280
 
   h.parts.clear();
+  h.fix_ranges.clear();
   h.n_empty = 0;
   h.padding_ratio = 0.0;
+  h.total_chunks_carry = 0;
+  h.l2_slots = 0;
   if (rows == 0) return;
 
-  DevBuf<long long> cnt(static_cast<size_t>(nbins) * ntiles + 1), off(cnt.n);
-  DevBuf<unsigned long long> nnz_bin(nbins);
+  DevBuf<long long> cnt(static_cast<size_t>(nbins) * ntiles + 1, s), off(cnt.n, s);
+  DevBuf<unsigned long long> nnz_bin(nbins, s);
   STRATA_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, cnt.n * sizeof(long long), s));
   STRATA_CUDA_CHECK(cudaMemsetAsync(nnz_bin.p, 0, nnz_bin.n * sizeof(unsigned long long), s));
   hyb_count_kernel<<<static_cast<unsigned>(ntiles), kTile, 2 * nbins * sizeof(unsigned long long),
@@ -260,11 +321,13 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
 
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.p, off.p, static_cast<int64_t>(cnt.n), s);
-  DevBuf<unsigned char> tmp(tmp_bytes);
-  cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, cnt.p, off.p, static_cast<int64_t>(cnt.n), s);
-  STRATA_CUDA_CHECK(cudaGetLastError());
+  {
+    DevBuf<unsigned char> tmp(tmp_bytes, s);
+    cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, cnt.p, off.p, static_cast<int64_t>(cnt.n), s);
+    STRATA_CUDA_CHECK(cudaGetLastError());
+  }
 
-  // Per-bin start positions (bin * ntiles), plus the grand total at index nbins * ntiles.
+  // Sync 1: per-bin start positions (bin * ntiles) + the grand total, and per-bin entries.
   std::vector<long long> bin_start(nbins + 1);
   std::vector<unsigned long long> bin_nnz(nbins);
   STRATA_CUDA_CHECK(cudaMemcpy2DAsync(bin_start.data(), sizeof(long long), off.p,
@@ -302,12 +365,20 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
   }
   h.padding_ratio = slots == 0 ? 0.0 : static_cast<double>(pads) / static_cast<double>(slots);
 
-  h.I.alloc(total_segs);
-  h.J.alloc(slot_cursor);
-  h.V.alloc(slot_cursor);
-  h.empty_rows.alloc(h.n_empty);
-  DevBuf<long long> seg_src(total_segs);
-  DevBuf<int32_t> seg_len(total_segs);
+  static const bool pooled = getenv("STRATA_HYB_POOL") && atoi(getenv("STRATA_HYB_POOL")) == 1;  // A/B knob
+  if (pooled) {
+    h.I.alloc_async(total_segs, s, true);
+    h.J.alloc_async(slot_cursor, s, true);
+    h.V.alloc_async(slot_cursor, s, true);
+    h.empty_rows.alloc_async(h.n_empty, s, true);
+  } else {
+    h.I.alloc(total_segs);
+    h.J.alloc(slot_cursor);
+    h.V.alloc(slot_cursor);
+    h.empty_rows.alloc(h.n_empty);
+  }
+  DevBuf<long long> seg_src(total_segs, s);
+  DevBuf<int32_t> seg_len(total_segs, s);
   if (ntiles > 0) {
     hyb_scatter_kernel<<<static_cast<unsigned>(ntiles), kTile, 0, s>>>(
         indptr, indices, rows, c, k, part_w, cols, ntiles, cnt.p, off.p, h.I.p, seg_src.p,
@@ -317,95 +388,131 @@ void hyb_decompose_device(strata_hyb_impl& h, const int32_t* indptr, const int32
   if (slot_cursor > 0) {
     std::vector<FillPart> fp;
     for (const auto& P : h.parts) fp.push_back({P.slot_off, P.row_off, P.nrows * P.width, P.bucket});
-    DevBuf<FillPart> dfp(fp.size());
+    DevBuf<FillPart> dfp(fp.size(), s);
     STRATA_CUDA_CHECK(cudaMemcpyAsync(dfp.p, fp.data(), fp.size() * sizeof(FillPart),
                                       cudaMemcpyHostToDevice, s));
+    const size_t smem = std::max<size_t>(fp.size() * sizeof(FillPart), 1);
+    if (smem > 48 * 1024)
+      STRATA_CUDA_CHECK(cudaFuncSetAttribute(hyb_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
     const long long blocks = std::min<long long>((slot_cursor + 255) / 256, 148LL * 64);
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(hyb_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(std::max<size_t>(fp.size() * sizeof(FillPart), 1))));
-    hyb_fill_kernel<<<static_cast<unsigned>(blocks), 256, fp.size() * sizeof(FillPart), s>>>(
+    hyb_fill_kernel<<<static_cast<unsigned>(blocks), 256, smem, s>>>(
         indices, values, seg_src.p, seg_len.p, h.J.p, h.V.p, slot_cursor, dfp.p,
         static_cast<int>(fp.size()));
     STRATA_CUDA_CHECK(cudaGetLastError());
-    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));  // dfp / seg_* are freed on return
+    // (a pageable-source cudaMemcpyAsync returns once `fp` is staged: no sync needed for it)
   }
 
-  // SpMM schedule.
-  std::vector<FixTile> tiles;
-  std::vector<FixRun> runs;
-  h.fix_ranges.clear();
-  int64_t carry_chunks = 0, l2_slots = 0;
-  for (auto& P : h.parts) {
+  // SpMM schedule: rows per chunk per part; the bucket-k part (the only one whose I_indices
+  // may repeat) gets its crossing runs, selected and expanded into fix-up tiles on the device.
+  std::vector<size_t> split;  // indices of split parts with >= 2 chunks
+  int64_t carry_chunks = 0;
+  for (size_t pi = 0; pi < h.parts.size(); ++pi) {
+    HybPart& P = h.parts[pi];
     P.rpc_log2 = std::max(0, 8 - P.bucket);  // kSlotsPerChunk = 256 slots per chunk
     static_assert(kSlotsPerChunk == 256, "rpc rule assumes 256-slot chunks");
     P.nchunks = (P.nrows + (int64_t{1} << P.rpc_log2) - 1) >> P.rpc_log2;
-    P.may_split = (P.bucket == k);  // only bucket k may hold several segments of one row
+    P.may_split = (P.bucket == k);
     P.nruns = 0;
     P.carry_off = 0;
-    if (h.fix_ranges.empty() || h.fix_ranges.back().partition != P.partition)
-      h.fix_ranges.push_back({P.partition, (long long)tiles.size(), (long long)tiles.size(),
-                              (long long)runs.size(), (long long)runs.size()});
     if (!P.may_split || P.nchunks < 2) continue;
-    DevBuf<unsigned char> fs(P.nchunks), fe(P.nchunks);
-    cross_flags_kernel<<<static_cast<unsigned>((P.nchunks + 255) / 256), 256, 0, s>>>(
-        h.I.p + P.row_off, P.nrows, P.rpc_log2, P.nchunks, fs.p, fe.p);
-    STRATA_CUDA_CHECK(cudaGetLastError());
-    DevBuf<long long> rs(P.nchunks), re(P.nchunks);
-    DevBuf<long long> nsel(2);
-    cub::CountingInputIterator<long long> it(0);
-    size_t tb = 0, tb2 = 0;
-    cub::DeviceSelect::Flagged(nullptr, tb, it, fs.p, rs.p, nsel.p, P.nchunks, s);
-    cub::DeviceSelect::Flagged(nullptr, tb2, it, fe.p, re.p, nsel.p + 1, P.nchunks, s);
-    DevBuf<unsigned char> t2(std::max(tb, tb2));
-    cub::DeviceSelect::Flagged(t2.p, tb, it, fs.p, rs.p, nsel.p, P.nchunks, s);
-    cub::DeviceSelect::Flagged(t2.p, tb2, it, fe.p, re.p, nsel.p + 1, P.nchunks, s);
-    STRATA_CUDA_CHECK(cudaGetLastError());
-    long long hn[2];
-    STRATA_CUDA_CHECK(cudaMemcpyAsync(hn, nsel.p, sizeof(hn), cudaMemcpyDeviceToHost, s));
-    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
-    if (hn[0] != hn[1]) throw ApiError(STRATA_ERR_INTERNAL, "hyb: unbalanced split runs");
-    P.nruns = hn[0];
     P.carry_off = carry_chunks;
     carry_chunks += P.nchunks;
-    if (!P.nruns) continue;
-    std::vector<long long> a(P.nruns), b(P.nruns);
-    std::vector<int32_t> Ih(P.nrows);
-    STRATA_CUDA_CHECK(cudaMemcpy(a.data(), rs.p, P.nruns * sizeof(long long), cudaMemcpyDeviceToHost));
-    STRATA_CUDA_CHECK(cudaMemcpy(b.data(), re.p, P.nruns * sizeof(long long), cudaMemcpyDeviceToHost));
-    STRATA_CUDA_CHECK(cudaMemcpy(Ih.data(), h.I.p + P.row_off, P.nrows * sizeof(int32_t),
-                                 cudaMemcpyDeviceToHost));
-    for (long long j = 0; j < P.nruns; ++j) {
-      // Run j: chunks a[j]..b[j]; contributions in order = tail carry of a[j], then the head
-      // carries of a[j]+1 .. b[j].  Its output row is the last row of chunk a[j].
-      const long long ca = a[j], n = b[j] - a[j] + 1;
-      const long long row = Ih[((ca + 1) << P.rpc_log2) - 1];
-      const long long nt = (n + kFixTile - 1) / kFixTile;
-      for (long long u = 0; u < nt; ++u) {
-        FixTile t;
-        t.carry0 = P.carry_off + ca + u * kFixTile;
-        t.count = static_cast<int>(std::min<long long>(kFixTile, n - u * kFixTile));
-        t.first_slot = u == 0 ? 1 : 0;
-        t.out = nt == 1 ? row : -(l2_slots + u + 1);
-        tiles.push_back(t);
-      }
-      if (nt > 1) {
-        runs.push_back({l2_slots, row, static_cast<int>(nt), 0});
-        l2_slots += nt;
-      }
-    }
-    h.fix_ranges.back().tile_end = static_cast<long long>(tiles.size());
-    h.fix_ranges.back().run_end = static_cast<long long>(runs.size());
+    split.push_back(pi);
   }
   h.total_chunks_carry = carry_chunks;
-  h.l2_slots = l2_slots;
-  h.fix_tiles.alloc(tiles.size());
-  h.fix_runs.alloc(runs.size());
-  if (!tiles.empty())
-    STRATA_CUDA_CHECK(cudaMemcpy(h.fix_tiles.p, tiles.data(), tiles.size() * sizeof(FixTile),
-                                 cudaMemcpyHostToDevice));
-  if (!runs.empty())
-    STRATA_CUDA_CHECK(cudaMemcpy(h.fix_runs.p, runs.data(), runs.size() * sizeof(FixRun),
-                                 cudaMemcpyHostToDevice));
+
+  DevBuf<long long> rs, re, nsel, ntile, nl2, isrun, tile_off, l2_off, run_off;
+  if (!split.empty()) {
+    const size_t tot = static_cast<size_t>(carry_chunks);
+    rs.alloc_async(tot, s);
+    re.alloc_async(tot, s);
+    nsel.alloc_async(2 * split.size(), s);
+    ntile.alloc_async(tot + 1, s);
+    nl2.alloc_async(tot + 1, s);
+    isrun.alloc_async(tot + 1, s);
+    tile_off.alloc_async(tot + 1, s);
+    l2_off.alloc_async(tot + 1, s);
+    run_off.alloc_async(tot + 1, s);
+    DevBuf<unsigned char> fs(tot, s), fe(tot, s);
+    cub::CountingInputIterator<long long> it(0);
+    size_t tb = 0;
+    for (size_t si = 0; si < split.size(); ++si) {
+      const HybPart& P = h.parts[split[si]];
+      size_t t1 = 0;
+      cub::DeviceSelect::Flagged(nullptr, t1, it, fs.p, rs.p, nsel.p, P.nchunks, s);
+      tb = std::max(tb, t1);
+    }
+    DevBuf<unsigned char> t2(tb, s);
+    for (size_t si = 0; si < split.size(); ++si) {
+      const HybPart& P = h.parts[split[si]];
+      const long long o = P.carry_off;
+      cross_flags_kernel<<<grid_of(P.nchunks), 256, 0, s>>>(h.I.p + P.row_off, P.nrows, P.rpc_log2,
+                                                            P.nchunks, fs.p + o, fe.p + o);
+      size_t t1 = tb;
+      cub::DeviceSelect::Flagged(t2.p, t1, it, fs.p + o, rs.p + o, nsel.p + 2 * si, P.nchunks, s);
+      t1 = tb;
+      cub::DeviceSelect::Flagged(t2.p, t1, it, fe.p + o, re.p + o, nsel.p + 2 * si + 1, P.nchunks, s);
+      run_counts_kernel<<<grid_of(P.nchunks), 256, 0, s>>>(rs.p + o, re.p + o, nsel.p + 2 * si,
+                                                           P.nchunks, ntile.p + o, nl2.p + o,
+                                                           isrun.p + o);
+    }
+    STRATA_CUDA_CHECK(cudaGetLastError());
+    for (DevBuf<long long>* a : {&ntile, &nl2, &isrun})
+      STRATA_CUDA_CHECK(cudaMemsetAsync(a->p + tot, 0, sizeof(long long), s));
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, ntile.p, tile_off.p, static_cast<int64_t>(tot + 1), s);
+    DevBuf<unsigned char> t3(sb, s);
+    for (auto [in, out] : {std::pair{&ntile, &tile_off}, {&nl2, &l2_off}, {&isrun, &run_off}}) {
+      size_t sb2 = sb;
+      cub::DeviceScan::ExclusiveSum(t3.p, sb2, in->p, out->p, static_cast<int64_t>(tot + 1), s);
+    }
+    STRATA_CUDA_CHECK(cudaGetLastError());
+    // Sync 2: per split part its run counts (selected starts / ends) and the scan positions
+    // at its first chunk, plus the totals.
+    std::vector<long long> hsel(2 * split.size());
+    STRATA_CUDA_CHECK(cudaMemcpyAsync(hsel.data(), nsel.p, hsel.size() * sizeof(long long),
+                                      cudaMemcpyDeviceToHost, s));
+    std::vector<long long> tb_h(split.size() + 1), rb_h(split.size() + 1), l2_h(split.size() + 1);
+    for (size_t si = 0; si <= split.size(); ++si) {
+      const long long o = si < split.size() ? h.parts[split[si]].carry_off : carry_chunks;
+      STRATA_CUDA_CHECK(cudaMemcpyAsync(&tb_h[si], tile_off.p + o, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      STRATA_CUDA_CHECK(cudaMemcpyAsync(&rb_h[si], run_off.p + o, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      STRATA_CUDA_CHECK(cudaMemcpyAsync(&l2_h[si], l2_off.p + o, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    }
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+    for (size_t si = 0; si < split.size(); ++si) {
+      if (hsel[2 * si] != hsel[2 * si + 1]) throw ApiError(STRATA_ERR_INTERNAL, "hyb: unbalanced split runs");
+      h.parts[split[si]].nruns = hsel[2 * si];
+    }
+    h.l2_slots = l2_h[split.size()];
+    h.fix_tiles.alloc_async(tb_h[split.size()], s, true);
+    h.fix_runs.alloc_async(rb_h[split.size()], s, true);
+    for (size_t si = 0; si < split.size(); ++si) {
+      const HybPart& P = h.parts[split[si]];
+      if (!P.nruns) continue;
+      const long long o = P.carry_off;
+      fix_fill_kernel<<<grid_of(P.nruns), 256, 0, s>>>(rs.p + o, re.p + o, nsel.p + 2 * si,
+                                                       h.I.p + P.row_off, P.rpc_log2, o,
+                                                       tile_off.p + o, l2_off.p + o, run_off.p + o,
+                                                       h.fix_tiles.p, h.fix_runs.p);
+    }
+    STRATA_CUDA_CHECK(cudaGetLastError());
+    // per column partition, in partition order: its split part's tiles / runs (empty ranges
+    // for partitions without one)
+    size_t si = 0;
+    for (const auto& P : h.parts) {
+      if (!h.fix_ranges.empty() && h.fix_ranges.back().partition == P.partition) continue;
+      while (si < split.size() && h.parts[split[si]].partition < P.partition) ++si;
+      const bool has = si < split.size() && h.parts[split[si]].partition == P.partition;
+      const size_t b0 = si, b1 = has ? si + 1 : si;
+      h.fix_ranges.push_back({P.partition, tb_h[b0], tb_h[b1], rb_h[b0], rb_h[b1]});
+    }
+  } else {
+    for (const auto& P : h.parts)
+      if (h.fix_ranges.empty() || h.fix_ranges.back().partition != P.partition)
+        h.fix_ranges.push_back({P.partition, 0, 0, 0, 0});
+  }
 }
 
 

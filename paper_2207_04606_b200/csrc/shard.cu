@@ -150,8 +150,7 @@ const strata_shard_plan& plan_of(const strata_shard_plan* p) {
 ncclComm_t comm_of(const void* comm, int ndev, const strata_shard_plan& P) {
   require(ndev == P.world, STRATA_ERR_USAGE,
           "sharded call: ndev " + std::to_string(ndev) + " != plan world " + std::to_string(P.world));
-  if (P.world == 1 && comm == nullptr) return nullptr;
-  require(comm != nullptr, STRATA_ERR_USAGE, "sharded call: null communicator");
+  if (comm == nullptr) return nullptr;  // no reassembly: this rank's rows / range only
   ncclComm_t c = *static_cast<const ncclComm_t*>(comm);
   int n = 0, r = 0;
   nccl_check(nccl().CommCount(c, &n), "ncclCommCount");

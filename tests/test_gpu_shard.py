@@ -66,9 +66,11 @@ def test_sharded_errors(cuda, comm1):
     with pytest.raises(S.StrataError) as e:  # a one-rank communicator for a world-2 plan
         check(lib.strata_spmm_hyb_f32_sharded(p2._h, X.data_ptr(), Y.data_ptr(), 32, comm1.ptr, 2, 0))
     assert e.value.kind == "Usage" and "communicator is rank 0 of 1" in str(e.value)
-    with pytest.raises(S.StrataError) as e:
-        p2.spmm(X, Y, None)
-    assert e.value.kind == "Usage" and "null communicator" in str(e.value)
+    # comm = None: no reassembly, only this rank's rows are written
+    Y.fill_(float("nan"))
+    p2.spmm(X, Y, None)
+    r0, r1 = p2.rows_of(1)
+    assert not torch.isnan(Y[r0:r1]).any() and torch.isnan(Y[:r0]).all()
     with pytest.raises(S.StrataError) as e:
         check(lib.strata_spmm_hyb_f32_sharded(p2._h, X.data_ptr(), Y.data_ptr(), 32, None, 1, 0))
     assert "ndev 1 != plan world 2" in str(e.value)

@@ -12,6 +12,9 @@ for w in ${WORKLOADS:-products reddit_spmm reddit_sddmm bsr bsr12 rgcn rgcn_sum 
     rgcn_sum) k=rgms_row_sum_kernel; run=rgcn ;;
     srbcrs) k=srbcrs_spmm_tc_kernel ;;
     attention) k=attn_kernel ;;
+    bsr12_sddmm) k=bsr_sddmm_tc_kernel ;;
+    dbsr) k=bsr_spmm_tc_kernel ;;
+    gnn) k=gemm_tf32 ;;
   esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
     -o gpurun_out/prof_$w -f python tools/prof_workloads.py $run 4 > gpurun_out/ncu_$w.log 2>&1

@@ -1,5 +1,6 @@
 """Run one BASELINE workload a few times (for ncu captures): python tools/prof_workloads.py
-{products|reddit_spmm|reddit_sddmm|bsr|bsr12|rgcn|srbcrs|attention} [reps]"""
+{products|reddit_spmm|reddit_sddmm|bsr|bsr12|bsr12_sddmm|dbsr|gnn|rgcn|srbcrs|attention}
+[reps]"""
 import os
 import sys
 
@@ -58,6 +59,23 @@ def main():
         X = torch.randint(-3, 4, (m.cols, 32), device=dev).to(torch.bfloat16)
         W = torch.randint(-3, 4, (133, 32, 32), device=dev).to(torch.bfloat16)
         fn = lambda: plan.run(X, W)
+    elif which == "bsr12_sddmm":  # 12-head block-sparse SDDMM (sparse-attention scores)
+        m = S.generate_matrix("blocksparse", 4096, 4096, 0.1, 0, 32, 0, 1)
+        bs = S.csr_to_bsr(m.to_device(dev), 32)
+        Q = torch.randint(-3, 4, (12, 4096, 64), device=dev).to(torch.bfloat16)
+        K = torch.randint(-3, 4, (12, 4096, 64), device=dev).to(torch.bfloat16)
+        fn = lambda: S.bsr_sddmm(bs, Q, K)
+    elif which == "dbsr":  # DBSR(32) pruned-weight SpMM, 2 % block mask, d = 128
+        m = S.generate_matrix("blocksparse", 8192, 8192, 0.02, 0, 32, 0, 4)
+        db = S.csr_to_dbsr(m.to_device(dev), 32)
+        X = torch.randint(-3, 4, (8192, 128), device=dev).to(torch.bfloat16)
+        fn = lambda: S.dbsr_spmm(db, X)
+    elif which == "gnn":  # C5 GNN layer 128 -> 128: hyb SpMM then the tcgen05 3xTF32 transform
+        m = S.generate_matrix("powerlaw", 2449029, 2449029, 0, 0, 0, 25.3, 1)
+        h = S.decompose_hyb(m.to_device(dev), 1, S.hyb_auto_k(m))
+        X = torch.randint(-3, 4, (m.cols, 128), device=dev, dtype=torch.float32)
+        W = torch.randint(-3, 4, (128, 128), device=dev, dtype=torch.float32)
+        fn = lambda: S.gnn_layer(h, X, W)
     else:
         raise SystemExit(f"unknown workload {which}")
     for _ in range(reps):

@@ -26,9 +26,13 @@ for name, n, avg in [("C5", 2449029, 25.3), ("C2", 232965, 567.5267)]:
     m = S.generate_matrix("powerlaw", n, n, 0, 0, 0, avg, 1)
     dm = m.to_device(dev)
     k = S.hyb_auto_k(m)
-    _, t1 = wall(lambda: S.decompose_hyb(dm, 1, k))
-    _, t2 = wall(lambda: S.decompose_hyb(dm, 1, k))
-    out[name + "_decompose_ms"] = [round(t1, 1), round(t2, 1)]
+    h1, t1 = wall(lambda: S.decompose_hyb(dm, 1, k))
+    h2, t2 = wall(lambda: S.decompose_hyb(dm, 1, k))  # second handle alive beside the first
+    del h1, h2
+    torch.cuda.synchronize()
+    h3, t3 = wall(lambda: S.decompose_hyb(dm, 1, k))  # rebuilt after release: pooled memory
+    out[name + "_decompose_ms"] = [round(t1, 1), round(t2, 1), round(t3, 1)]
+    del h3
 m = S.generate_matrix("blocksparse", 4096, 4096, 0.1, 0, 32, 0, 1)
 dm = m.to_device(dev)
 _, t1 = wall(lambda: S.csr_to_bsr(dm, 32))
