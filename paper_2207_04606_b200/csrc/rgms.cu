@@ -420,7 +420,11 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
           for (int row = rn.x + 1; row < rn.y; ++row)
             acc = add4(acc, epi[row * kSPR + (sl ^ (row & (kSPR - 1)))]);
           if (rn.z >= 0) {
+#if STRATA_RGMS_T_L2
+            reinterpret_cast<float4*>(T + static_cast<long long>(rn.z) * DOUT + c0)[sl] = acc;
+#else
             __stcs(reinterpret_cast<float4*>(T + static_cast<long long>(rn.z) * DOUT + c0) + sl, acc);
+#endif
           } else {  // direct row: its only run is its sum (+0.f: the reference's 0 + x, no -0)
             acc.x += 0.f; acc.y += 0.f; acc.z += 0.f; acc.w += 0.f;
             __stcs(reinterpret_cast<float4*>(Y + static_cast<long long>(-3 - rn.z) * DOUT + c0) + sl, acc);
@@ -463,6 +467,21 @@ constexpr int kLong = STRATA_RGMS_LONG;
 #define STRATA_RGMS_CHUNK 1024
 #endif
 constexpr int kChunk = STRATA_RGMS_CHUNK;
+#ifndef STRATA_RGMS_T_L2  // A/B knob: T rows written with the default L2 policy and dropped from L2
+#define STRATA_RGMS_T_L2 0  // (discard.global.L2, no write-back) once pass 2 has summed them
+#endif
+
+// Pass 2 has consumed T row q: with STRATA_RGMS_T_L2 its 128-byte L2 lines are invalidated
+// without write-back (the row is dead), one line per lane of the row's lane group.
+template <int DOUT>
+__device__ __forceinline__ void t_row_consumed(const float* T, long long q, int l) {
+#if STRATA_RGMS_T_L2
+  if constexpr ((DOUT * 4) % 128 == 0) {
+    if (l < DOUT * 4 / 128)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(T + q * DOUT + l * 32) : "memory");
+  }
+#endif
+}
 
 template <int DOUT>
 struct RowSumShape {
@@ -564,6 +583,9 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
           }
         }
       }
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+        if (j < used) t_row_consumed<DOUT>(T, q + j, l);
       q += used;
     }
     while (r < rend) flush();  // trailing rows (their sums, or zeros for empty rows)
@@ -620,12 +642,15 @@ __device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int g = 0; g < kF; ++g) acc[g] = add4(acc[g], u[j][g]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t_row_consumed<DOUT>(T, q + j * kGrp, l);
     }
     for (; q < q1; q += kGrp) {
 #pragma unroll
       for (int g = 0; g < kF; ++g)
         acc[g] = add4(acc[g], __ldcs(reinterpret_cast<const float4*>(T) +
                                      static_cast<long long>(q) * kF4 + g * kL + l));
+      t_row_consumed<DOUT>(T, q, l);
     }
 #pragma unroll
     for (int g = 0; g < kF; ++g) {

@@ -1,2 +1,8 @@
-for pool in 0 1; do STRATA_HYB_POOL=$pool timeout 600 python tools/time_decompose.py > gpurun_out/time_decompose_$pool.json 2>&1; echo pool=$pool; cat gpurun_out/time_decompose_$pool.json; done
-SAN_ONLY="hyb bsr" bash tools/gpu_sanitize.sh
+# Full round check: smoke, the whole GPU suite, default bench + reference arm, sanitizer over
+# every pipeline, ncu launch list of the bench and full captures of the kernels DESIGN cites.
+REF=1 bash tools/gpu_round.sh
+bash tools/gpu_sanitize.sh
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/launches_bench.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra > gpurun_out/ncu_bench.log 2>&1
+WORKLOADS="rgcn rgcn_sum bsr12_sddmm dbsr gnn" bash tools/gpu_prof.sh > /dev/null 2>&1
+ls gpurun_out
