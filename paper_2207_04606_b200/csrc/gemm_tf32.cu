@@ -43,6 +43,9 @@ constexpr int kThreads = 320;        // 10 warps
 constexpr int kMaxStages = 6;
 constexpr uint32_t kHiMask = 0xFFFFE000u;  // tf32: 10 explicit mantissa bits
 constexpr int kChunkK = 64;                // K per big-product accumulator
+#ifndef STRATA_GEMM_MIN_STAGES  // A/B knob: pipeline stages the N tile must leave room for
+#define STRATA_GEMM_MIN_STAGES 2    // (4 at C5 128->128 = two N tiles, Y read twice: 0.74 -> 1.07 ms)
+#endif
 
 // f32 -> (nearest tf32, exact f32 remainder).  Rounding half away from zero in magnitude; a
 // carry into the exponent is still exact (the remainder absorbs it).
@@ -330,7 +333,7 @@ constexpr int kSmemStatic = 1024;   // barriers + TMEM slot (+ alignment slack b
 int gemm_tf32_tile_n(int K, int N) {
   if (K < kKB || K % kKB != 0 || N < 16 || N % 16 != 0) return 0;
   const int nchunk = (K + kChunkK - 1) / kChunkK;
-  const int budget = kSmemLimit - 1024 - kSmemStatic - 2 * 2 * kStageBytes;
+  const int budget = kSmemLimit - 1024 - kSmemStatic - STRATA_GEMM_MIN_STAGES * 2 * kStageBytes;
   int nt = std::min({256 / nchunk, budget / (8 * K)}) / 16 * 16;
   if (nt < 16) return 0;
   nt = std::min(nt, N);

@@ -48,6 +48,10 @@ struct strata_rgms {
   int nlong = 0, nchunks = 0;     // rows with > kLong edges and their kChunk-edge chunks
   DevBuf<int32_t> long_rows;     // [nlong] ascending
   DevBuf<int32_t> chunk_off;     // [nlong+1] first chunk of long row li
+  // Pass 2's work list: the rows it writes (>= 2 runs, or no edge at all), ascending, and
+  // their T-row pointer (cptr[j] = dptr[rowlist[j]], cptr[nlist] = trows).
+  int64_t nlist = 0;
+  DevBuf<int32_t> rowlist, cptr;
 };
 
 namespace {
@@ -166,6 +170,20 @@ __global__ void compact_dptr_kernel(const int32_t* __restrict__ dbefore, long lo
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i <= m;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     dptr[i] -= dbefore[dptr[i]];
+}
+
+__global__ void nondirect_flags_kernel(const uint32_t* __restrict__ dbits, long long m,
+                                       uint8_t* __restrict__ flag) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    flag[i] = ((dbits[i >> 5] >> (i & 31)) & 1u) ? 0 : 1;
+}
+
+__global__ void list_ptr_kernel(const int32_t* __restrict__ rowlist, const int32_t* __restrict__ dptr,
+                                long long n, long long m, int32_t* __restrict__ cptr) {
+  for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j <= n;
+       j += static_cast<long long>(gridDim.x) * blockDim.x)
+    cptr[j] = dptr[j < n ? rowlist[j] : m];
 }
 
 // Per-tile edge blocks; the pos word of an edge is its run's T row for a run head (or
@@ -467,6 +485,9 @@ constexpr int kLong = STRATA_RGMS_LONG;
 #define STRATA_RGMS_CHUNK 1024
 #endif
 constexpr int kChunk = STRATA_RGMS_CHUNK;
+#ifndef STRATA_RGMS_COMPACT  // A/B knob: pass 2 walks the plan's compacted row list (1) or all rows (0)
+#define STRATA_RGMS_COMPACT 1
+#endif
 #ifndef STRATA_RGMS_T_L2  // A/B knob: T rows written with the default L2 policy and dropped from L2
 #define STRATA_RGMS_T_L2 0  // (discard.global.L2, no write-back) once pass 2 has summed them
 #endif
@@ -495,16 +516,21 @@ struct RowSumShape {
 // smem); lane group g owns rows g*kRPV .. g*kRPV + kRPV - 1, whose T rows are contiguous, and
 // walks that range in batches of 8 T rows issued together, flushing a row's sum when the walk
 // crosses its end.  Long rows are stepped over (at most one wasted batch each).
-template <int DOUT>
+// kCompact (the plan's compacted list of the rows pass 2 must write — rows with >= 2 runs and
+// empty rows; the direct rows pass 1 wrote are absent): `m` is the list length, `dptr` the
+// list's T-row pointer (cptr[j] = first T row of rowlist[j]) and Y row j is rowlist[j].
+template <int DOUT, bool kCompact>
 __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, const float* __restrict__ T,
                                              long long m, float* __restrict__ Y,
-                                             const uint32_t* __restrict__ dbits, long long blk,
+                                             const uint32_t* __restrict__ dbits,
+                                             const int32_t* __restrict__ rowlist, long long blk,
                                              long long nblk) {
   using RS = RowSumShape<DOUT>;
   constexpr int kF4 = RS::kF4, kL = RS::kL, kF = RS::kF, kGrp = RS::kGrp;
   constexpr int kRPV = 32 / kGrp;  // rows per lane group per block
   constexpr int kB = STRATA_RGMS_SUM_KB;  // T rows in flight per lane group
   __shared__ int sbnd[8][33];
+  __shared__ int srow[kCompact ? 8 : 1][32];
   const int lane = threadIdx.x & 31, l = lane % kL, g = lane / kL, w = threadIdx.x >> 5;
   int* bnd = sbnd[w];
   const long long nwarps = nblk * (blockDim.x >> 5);
@@ -512,24 +538,27 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
   // The next block's bounds are loaded while this block's T rows stream (one DRAM latency
   // less on every block's dependency chain).
   long long b = blk * (blockDim.x >> 5) + w;
-  int nb0 = 0, nb32 = 0;
+  int nb0 = 0, nb32 = 0, nrow = 0;
   uint32_t ndw = 0;  // direct rows of the block (written by pass 1, not here)
   if (b * 32 < m) {
     nb0 = __ldg(dptr + min64(b * 32 + lane, m));
     nb32 = __ldg(dptr + min64(b * 32 + 32, m));
-    ndw = __ldg(dbits + b);
+    if constexpr (kCompact) nrow = __ldg(rowlist + min64(b * 32 + lane, m - 1));
+    else ndw = __ldg(dbits + b);
   }
   for (; b * 32 < m; b += nwarps) {
     const long long i0 = b * 32;
     __syncwarp();
     bnd[lane] = nb0;
     if (lane == 0) bnd[32] = nb32;
+    if constexpr (kCompact) srow[w][lane] = nrow;
     const uint32_t dw = ndw;
     __syncwarp();
     if ((b + nwarps) * 32 < m) {
       nb0 = __ldg(dptr + min64((b + nwarps) * 32 + lane, m));
       nb32 = __ldg(dptr + min64((b + nwarps) * 32 + 32, m));
-      ndw = __ldg(dbits + b + nwarps);
+      if constexpr (kCompact) nrow = __ldg(rowlist + min64((b + nwarps) * 32 + lane, m - 1));
+      else ndw = __ldg(dbits + b + nwarps);
     }
     int r = g * kRPV;
     const int rend = static_cast<int>(min64(r + kRPV, m - i0));
@@ -541,10 +570,11 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
 #pragma unroll
     for (int f = 0; f < kF; ++f) acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
     auto flush = [&] {
-      if (!skip && !((dw >> r) & 1u)) {
+      if (!skip && (kCompact || !((dw >> r) & 1u))) {
+        const long long yr = kCompact ? static_cast<long long>(srow[w][r]) : i0 + r;
 #pragma unroll
         for (int f = 0; f < kF; ++f) {
-          st_stream4(reinterpret_cast<float4*>(Y + (i0 + r) * DOUT) + f * kL + l, acc[f]);
+          st_stream4(reinterpret_cast<float4*>(Y + yr * DOUT) + f * kL + l, acc[f]);
           acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
@@ -583,9 +613,11 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
           }
         }
       }
+#if STRATA_RGMS_T_L2
 #pragma unroll
       for (int j = 0; j < kB; ++j)
         if (j < used) t_row_consumed<DOUT>(T, q + j, l);
+#endif
       q += used;
     }
     while (r < rend) flush();  // trailing rows (their sums, or zeros for empty rows)
@@ -642,15 +674,19 @@ __device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int g = 0; g < kF; ++g) acc[g] = add4(acc[g], u[j][g]);
+#if STRATA_RGMS_T_L2
 #pragma unroll
       for (int j = 0; j < 4; ++j) t_row_consumed<DOUT>(T, q + j * kGrp, l);
+#endif
     }
     for (; q < q1; q += kGrp) {
 #pragma unroll
       for (int g = 0; g < kF; ++g)
         acc[g] = add4(acc[g], __ldcs(reinterpret_cast<const float4*>(T) +
                                      static_cast<long long>(q) * kF4 + g * kL + l));
+#if STRATA_RGMS_T_L2
       t_row_consumed<DOUT>(T, q, l);
+#endif
     }
 #pragma unroll
     for (int g = 0; g < kF; ++g) {
@@ -663,17 +699,20 @@ __device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr
 // Pass 2 in one launch: the first `cblk` blocks sum the long rows' chunks into partials (they
 // are dispatched first, so the hub rows' T ranges stream concurrently with the short rows
 // instead of after them), the remaining blocks run the short-row walk.
-template <int DOUT>
-__global__ void __launch_bounds__(256, STRATA_RGMS_SUM_MINB)
+template <int DOUT, bool kCompact>
+__global__ void __launch_bounds__(256, DOUT <= 32 ? STRATA_RGMS_SUM_MINB : 4)  // wider rows: more registers
 rgms_row_sum_kernel(const int32_t* __restrict__ dptr, const float* __restrict__ T, long long m,
                     float* __restrict__ Y, const uint32_t* __restrict__ dbits,
                     const int32_t* __restrict__ long_rows,
                     const int32_t* __restrict__ chunk_off, int nlong, int nchunks,
-                    float* __restrict__ partial, int cblk) {
+                    float* __restrict__ partial, int cblk, const int32_t* __restrict__ cptr,
+                    const int32_t* __restrict__ rowlist, long long nlist) {
   if (static_cast<int>(blockIdx.x) < cblk)
     long_chunk_body<DOUT>(dptr, long_rows, chunk_off, nlong, nchunks, T, partial, blockIdx.x, cblk);
+  else if constexpr (kCompact)
+    row_sum_body<DOUT, true>(cptr, T, nlist, Y, dbits, rowlist, blockIdx.x - cblk, gridDim.x - cblk);
   else
-    row_sum_body<DOUT>(dptr, T, m, Y, dbits, blockIdx.x - cblk, gridDim.x - cblk);
+    row_sum_body<DOUT, false>(dptr, T, m, Y, dbits, nullptr, blockIdx.x - cblk, gridDim.x - cblk);
 }
 
 // One warp per long row: Y[row] = sum of its chunks' partials (same fixed split as above).
@@ -740,7 +779,7 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
   k1<<<static_cast<unsigned>(std::max<long long>(grid, 1)), kWsThreads, smem, s>>>(wmap, X, h.edges.p,
                                                                                    h.ntiles, T, Y);
   STRATA_CUDA_CHECK(cudaGetLastError());
-  const long long lanes = h.m * RowSumShape<DOUT>::kL;
+  const long long lanes = (STRATA_RGMS_COMPACT ? h.nlist : h.m) * RowSumShape<DOUT>::kL;
   // Grid: up to 32 CTAs per SM (~1.6 warp-blocks of 32 rows per warp at C4) — CTAs retire and
   // are replaced as their rows finish, which balances the power-law row lengths better than a
   // resident-only persistent grid (measured, knob above).
@@ -748,9 +787,9 @@ void launch_rgms(const strata_rgms& h, const __nv_bfloat16* X, const __nv_bfloat
                                                static_cast<long long>(num_sms()) * STRATA_RGMS_SUM_WAVE);
   const int wpb = 8;
   const int cblk = h.nlong > 0 ? (h.nchunks + wpb - 1) / wpb : 0;
-  rgms_row_sum_kernel<DOUT><<<static_cast<unsigned>(std::max<long long>(blocks, 1) + cblk), 256, 0, s>>>(
+  rgms_row_sum_kernel<DOUT, STRATA_RGMS_COMPACT != 0><<<static_cast<unsigned>(std::max<long long>(blocks, 1) + cblk), 256, 0, s>>>(
       h.dptr.p, T, h.m, Y, h.dbits.p, h.long_rows.p, h.chunk_off.p, h.nlong, h.nchunks,
-      partial, cblk);
+      partial, cblk, h.cptr.p, h.rowlist.p, h.nlist);
   if (h.nlong > 0) {
     rgms_long_finish_kernel<DOUT><<<static_cast<unsigned>((h.nlong + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
         h.long_rows.p, h.chunk_off.p, h.nlong, partial, Y);
@@ -879,6 +918,34 @@ extern "C" int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, cons
       STRATA_CUDA_CHECK(cudaFreeAsync(ids, s));
       STRATA_CUDA_CHECK(cudaFreeAsync(itmp, s));
       STRATA_CUDA_CHECK(cudaFreeAsync(head, s));
+      // Pass 2's work list (one host sync sizes it).
+      if (m > 0) {
+        uint8_t* flag = static_cast<uint8_t*>(workspace_alloc(m, s));
+        int32_t* sel = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t) * (m + 1), s));
+        int32_t* cnt = static_cast<int32_t*>(workspace_alloc(sizeof(int32_t), s));
+        const unsigned gm = static_cast<unsigned>(std::min<long long>((m + 255) / 256, num_sms() * 16LL));
+        nondirect_flags_kernel<<<gm, 256, 0, s>>>(h->dbits.p, m, flag);
+        cub::CountingInputIterator<int32_t> it(0);
+        size_t fb = 0;
+        cub::DeviceSelect::Flagged(nullptr, fb, it, flag, sel, cnt, m, s);
+        void* ftmp = workspace_alloc(fb, s);
+        cub::DeviceSelect::Flagged(ftmp, fb, it, flag, sel, cnt, m, s);
+        int32_t hn = 0;
+        STRATA_CUDA_CHECK(cudaMemcpyAsync(&hn, cnt, sizeof(hn), cudaMemcpyDeviceToHost, s));
+        STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
+        h->nlist = hn;
+        h->rowlist.alloc(std::max<int32_t>(hn, 1));
+        h->cptr.alloc(hn + 1);
+        if (hn > 0)
+          STRATA_CUDA_CHECK(cudaMemcpyAsync(h->rowlist.p, sel, sizeof(int32_t) * hn, cudaMemcpyDeviceToDevice, s));
+        list_ptr_kernel<<<static_cast<unsigned>(std::min<long long>((hn + 256) / 256, num_sms() * 16LL)), 256, 0, s>>>(
+            sel, h->dptr.p, hn, m, h->cptr.p);
+        STRATA_CUDA_CHECK(cudaGetLastError());
+        STRATA_CUDA_CHECK(cudaFreeAsync(ftmp, s));
+        STRATA_CUDA_CHECK(cudaFreeAsync(cnt, s));
+        STRATA_CUDA_CHECK(cudaFreeAsync(sel, s));
+        STRATA_CUDA_CHECK(cudaFreeAsync(flag, s));
+      }
       // Long rows (> kLong edges) and their chunk offsets; one host sync sizes the partials.
       if (m > 0) {
         uint8_t* flag = static_cast<uint8_t*>(workspace_alloc(m, s));

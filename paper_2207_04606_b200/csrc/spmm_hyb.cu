@@ -232,7 +232,9 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 //   3. consume: batches of 8 real slots are read with broadcast 128-bit shared loads (no
 //      shuffles), their X rows gathered UG at a time (128-bit per lane), and accumulated.
 template <int L, int VEC, bool kScalar, bool kMulti>
-__global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2)))
+// (the multi-destination instantiation keeps the 3-CTA budget only for one destination's worth
+// of registers: it gets the 2-CTA budget, so its replica stores do not spill)
+__global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar && !kMulti) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2)))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int kT = 8;  // real slots per consume batch / slots per lane per compaction round
 #ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
