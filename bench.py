@@ -730,9 +730,15 @@ def run_ours(args):
     X = torch.randint(-3, 4, (m.cols, d), device=dev, dtype=torch.float32, generator=gx)
     Yrep = torch.empty((m.rows, d), device=dev, dtype=torch.float32)
     # NCCL refuses two ranks on one device: the shared-GPU test mode runs p2p only.
-    comm = NcclComm(rank, world) if world > 1 and not share else None
-    if share and not p2p:
-        print("bench.py: STRATA_BENCH_SHARE_GPU runs the p2p reassembly only", file=sys.stderr)
+    comm, comm_note = None, None
+    if world > 1 and not share:
+        try:
+            comm = NcclComm(rank, world)
+        except Exception as e:  # noqa: BLE001 — p2p still runs; its check uses a local SpMM
+            comm_note = f"NCCL communicator unavailable ({e})"
+    if comm is None and world > 1 and not p2p:
+        print(f"bench.py: --allgather nccl needs an NCCL communicator ({comm_note or 'shared GPU'})",
+              file=sys.stderr)
         return 2
 
     pag, p2p_note = None, None
@@ -871,7 +877,7 @@ def run_ours(args):
              "allgather_exposed_ms": round(ms_per_step - spmm_ms_max, 4) if world > 1 else 0.0,
              "chunks_per_rank": chunks,
              "allgather": ("none" if world == 1 else ("p2p" if pag is not None else "nccl")),
-             "allgather_note": p2p_note,
+             "allgather_note": p2p_note or comm_note,
              "compute_only_gflops": round(flops / (spmm_ms_max * 1e-3) / 1e9, 2),
              "frac_of_8tbs_nameplate": round(achieved / 8000.0, 4)}
     if sddmm_sharded is not None:

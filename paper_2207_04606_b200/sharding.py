@@ -146,16 +146,27 @@ class NcclComm:
     the unique id, the process group broadcasts it, every rank joins.  ``ptr`` is the address
     of the ncclComm_t the sharded entry points take."""
 
-    def __init__(self, rank: int, world: int, group=None):
-        import torch
+    @staticmethod
+    def exchange_unique_id(rank: int, world: int, group=None, make_id=None) -> bytes:
+        """Rank 0's ncclUniqueId (128 bytes) on every rank (an object broadcast: works on gloo
+        and NCCL process groups alike)."""
         import torch.distributed as dist
-        idb = (C.c_char * 128)()
+        uid = b""
         if rank == 0:
-            check(lib.strata_nccl_unique_id(idb))
+            if make_id is not None:
+                uid = make_id()
+            else:
+                idb = (C.c_char * 128)()
+                check(lib.strata_nccl_unique_id(idb))
+                uid = bytes(idb.raw)
         if world > 1:
-            t = torch.frombuffer(bytearray(idb.raw), dtype=torch.uint8).clone()
-            dist.broadcast(t, src=0, group=group)
-            C.memmove(idb, bytes(t.tolist()), 128)
+            box = [uid]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = box[0]
+        return uid
+
+    def __init__(self, rank: int, world: int, group=None):
+        idb = (C.c_char * 128).from_buffer_copy(self.exchange_unique_id(rank, world, group))
         self._comm = C.c_void_p()
         check(lib.strata_nccl_comm_init(idb, world, rank, C.byref(self._comm)))
         self.rank, self.world = rank, world

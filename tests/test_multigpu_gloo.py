@@ -129,6 +129,27 @@ def test_sharded_broadcast_reassembly_gloo(tmp_path, world):
         assert np.array_equal(np.load(out + f".{r}.b.npy"), wantB)
 
 
+def _id_worker(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2207_04606_b200.sharding import NcclComm
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    uid = NcclComm.exchange_unique_id(rank, world, make_id=lambda: bytes(range(128)))
+    with open(out_path + f".{rank}", "wb") as f:
+        f.write(uid)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_exchange_gloo(tmp_path):
+    """The NCCL bootstrap of the native sharded path: rank 0's ncclUniqueId reaches every rank."""
+    out = str(tmp_path / "id")
+    mp.spawn(_id_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    for r in range(3):
+        assert open(out + f".{r}", "rb").read() == bytes(range(128))
+
+
 @pytest.mark.parametrize("parts", [2, 3, 5, 8])
 def test_shard_decompositions_concatenate_to_global(parts):
     import paper_2207_04606_b200 as S
