@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "capi_internal.h"
 #include "common.cuh"
@@ -35,7 +36,8 @@ constexpr long long kCsrLong = 2048;  // row-split CSR SpMM: longer rows are chu
 constexpr long long kCsrChunk = 256;  // non-zeros per chunk of a long row
 constexpr long long kCsrGroup = 64;   // chunk partials summed per level-1 group
 
-__global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out,
+template <class TO>
+__global__ void transpose_kernel(const float* __restrict__ in, TO* __restrict__ out,
                                  long long rows, long long cols) {
   // in[rows][cols] -> out[cols][rows]
   __shared__ float tile[32][33];
@@ -47,7 +49,7 @@ __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const long long c = c0 + i, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+    if (r < rows && c < cols) out[c * rows + r] = static_cast<TO>(tile[threadIdx.x][i]);
   }
 }
 
@@ -68,6 +70,9 @@ __device__ __forceinline__ T reduce_scatter(T (&v)[L], int lane, unsigned mask) 
 
 #ifndef STRATA_SDDMM_F64  // A/B knob: 1 = f64 dot products (default), 0 = f32
 #define STRATA_SDDMM_F64 1
+#endif
+#ifndef STRATA_SDDMM_YT64  // A/B knob: Y transposed once per call into f64 (no per-gather
+#define STRATA_SDDMM_YT64 0  // F32->F64 conversions; twice the gathered bytes)
 #endif
 
 // Dot-product numerics.  The reference accumulates sum_k A*X*Y in f64 and rounds each partial
@@ -92,6 +97,13 @@ __device__ __forceinline__ typename DotT<kF64>::XV xfrag(const float4& x) {
   }
 }
 
+__device__ __forceinline__ double dot4(const double4& x, const double4& y) {
+  double s = x.x * y.x;
+  s = fma(x.y, y.y, s);
+  s = fma(x.z, y.z, s);
+  return fma(x.w, y.w, s);
+}
+
 template <bool kF64>
 __device__ __forceinline__ typename DotT<kF64>::T dot4(const typename DotT<kF64>::XV& x, const float4& y) {
   if constexpr (kF64) {
@@ -104,13 +116,15 @@ __device__ __forceinline__ typename DotT<kF64>::T dot4(const typename DotT<kF64>
   }
 }
 
-template <int L, bool kF64 = STRATA_SDDMM_F64>
+template <int L, bool kF64 = STRATA_SDDMM_F64, bool kY64 = (STRATA_SDDMM_YT64 != 0)>
 __global__ void __launch_bounds__(kBlock)
 sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
              const float* __restrict__ A, const float* __restrict__ X,
-             const float* __restrict__ Yt, float* __restrict__ B, long long rows, long long nnz,
+             const void* __restrict__ Yt_, float* __restrict__ B, long long rows, long long nnz,
              long long d) {
+  static_assert(!kY64 || kF64, "an f64 Yt only serves the f64 dot");
   using T = typename DotT<kF64>::T;
+  using YV = std::conditional_t<kY64, double4, float4>;
   constexpr int U = 8;
   const int wl = threadIdx.x & 31;
   const int lane = threadIdx.x & (L - 1);
@@ -153,27 +167,39 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncwarp(vmask);
 
-  const float4* Y4 = reinterpret_cast<const float4*>(Yt) + lane;
+  const float4* Y4 = reinterpret_cast<const float4*>(Yt_) + lane;
+  const double2* Y8 = reinterpret_cast<const double2*>(Yt_) + 2 * lane;
   const int d4 = static_cast<int>(d / 4);
+  auto gather_y = [&](int col) -> YV {
+    if constexpr (kY64) {
+      const double2* p = Y8 + static_cast<long long>(col) * (2 * d4);
+      const double2 a = __ldg(p), b = __ldg(p + 1);
+      return make_double4(a.x, a.y, b.x, b.y);
+    } else {
+      return ld_gather4(Y4 + static_cast<long long>(col) * d4);
+    }
+  };
   for (int g = 0; g < ne; g += L) {
     const int n = min(L, ne - g);
     const bool one_row = e0 + g + n <= row_end;  // VW-uniform: no row boundary in this group
     T part[L];
 #pragma unroll
     for (int u0 = 0; u0 < L; u0 += U) {
-      float4 yv[U];
+      YV yv[U];
 #pragma unroll
       for (int u = 0; u < U; u += 4) {
         const int4 c = *reinterpret_cast<const int4*>(sJ + g + u0 + u);  // broadcast LDS.128
         const int cc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
         for (int v = 0; v < 4; ++v)
-          yv[u + v] = (u0 + u + v < n) ? ld_gather4(Y4 + static_cast<long long>(cc[v]) * d4)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+          yv[u + v] = (u0 + u + v < n) ? gather_y(cc[v]) : YV{};
       }
+      auto dot = [&](const YV& y) -> T {
+        if constexpr (kY64) return dot4(x, y); else return dot4<kF64>(x, y);
+      };
       if (one_row) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) part[u0 + u] = dot4<kF64>(x, yv[u]);
+        for (int u = 0; u < U; ++u) part[u0 + u] = dot(yv[u]);
       } else {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -184,12 +210,12 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
               x = xfrag<kF64>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane));
             }
           }
-          part[u0 + u] = dot4<kF64>(x, yv[u]);
+          part[u0 + u] = dot(yv[u]);
         }
       }
     }
-    const T dot = reduce_scatter<L, T>(part, lane, vmask);
-    if (lane < n) st_stream(B + e0 + g + lane, static_cast<float>(static_cast<T>(sA[g + lane]) * dot));
+    const T dsum = reduce_scatter<L, T>(part, lane, vmask);
+    if (lane < n) st_stream(B + e0 + g + lane, static_cast<float>(static_cast<T>(sA[g + lane]) * dsum));
   }
 }
 
@@ -398,11 +424,15 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
                       int64_t nnz, int64_t d, cudaStream_t s) {
   if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "sddmm: d must be >= 1");
   if (nnz == 0) return;
-  float* Yt = nullptr;
-  Yt = static_cast<float*>(workspace_alloc(sizeof(float) * cols * d, s));
+  // Y[d][n] -> Yt[n][d] once per call (f64 with STRATA_SDDMM_YT64 for the vectorised kernels;
+  // the scalar fallback always reads f32).
+  const bool vec = (d == 32 || d == 64 || d == 128);
+  const bool y64 = STRATA_SDDMM_YT64 && vec;
+  void* Yt = workspace_alloc((y64 ? sizeof(double) : sizeof(float)) * cols * d, s);
   {
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((d + 31) / 32));
-    transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(Y, Yt, d, cols);
+    if (y64) transpose_kernel<double><<<grid, dim3(32, 8), 0, s>>>(Y, static_cast<double*>(Yt), d, cols);
+    else transpose_kernel<float><<<grid, dim3(32, 8), 0, s>>>(Y, static_cast<float*>(Yt), d, cols);
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
   const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0;
@@ -418,6 +448,7 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
   once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8)));
   });
+  if (y64 && !staged) throw ApiError(STRATA_ERR_INTERNAL, "sddmm: f64 Yt needs 16-byte aligned operands");
   if (staged && d == 32)
     sddmm_kernel<8><<<blocks_for(8), kBlock, smem_for(8), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   else if (staged && d == 64)
@@ -426,7 +457,7 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
     sddmm_kernel<32><<<blocks_for(32), kBlock, smem_for(32), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   else {
     const unsigned blocks = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, 148 * 32));
-    sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+    sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, static_cast<const float*>(Yt), B, rows, nnz, d);
   }
   STRATA_CUDA_CHECK(cudaGetLastError());
   STRATA_CUDA_CHECK(cudaFreeAsync(Yt, s));
