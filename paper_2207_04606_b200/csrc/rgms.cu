@@ -246,6 +246,9 @@ constexpr int kWsThreads = (kProdWarps + 1 + 4 * kEpiSets) * 32;  // then the ep
 #define STRATA_RGMS_WS_STAGES 4
 #endif
 constexpr int kStagesWs = STRATA_RGMS_WS_STAGES;
+#ifndef STRATA_RGMS_EPI_PAD  // A/B knob: padded (1) or XOR-swizzled (0) epilogue transpose buffer
+#define STRATA_RGMS_EPI_PAD 0  // (measured +1 % at C4: 0.347 vs 0.344 ms)
+#endif
 #ifndef STRATA_RGMS_EPI_NC  // A/B knob: accumulator columns per tcgen05.ld / epilogue pass
 #define STRATA_RGMS_EPI_NC 32
 #endif
@@ -260,11 +263,15 @@ struct RgmsWsSmem {
   static constexpr int kStage = kABytes + kWBytes;   // keeps every A region swizzle-atom aligned
   static constexpr int kIdxBytes = kTileWords * 4;   // 1552
   static constexpr int kNC = DOUT < STRATA_RGMS_EPI_NC ? DOUT : STRATA_RGMS_EPI_NC;  // epilogue column chunk
-  static constexpr int kEpiBytes = 4 * kEpiSets * 32 * kNC * 4;
+  // Epilogue transpose buffer per warp: 32 rows of kNC floats.  STRATA_RGMS_EPI_PAD: rows
+  // padded by one float4 (conflict-free without the XOR swizzle, one IMAD per row address),
+  // the pad column holding the warp's run table — the same bytes as swizzle + separate table.
+  static constexpr int kRowF4 = kNC / 4 + (STRATA_RGMS_EPI_PAD ? 1 : 0);
+  static constexpr int kEpiBytes = 4 * kEpiSets * 32 * kRowF4 * 16;
   static constexpr int kIdxOff = kStagesWs * kStage;
   static constexpr int kEpiOff = kIdxOff + kIdxSlotsWs * kIdxBytes;
   static constexpr int kRunOff = kEpiOff + kEpiBytes;        // per epilogue warp 32 int4 run records
-  static constexpr int kBytes = kRunOff + 4 * kEpiSets * 32 * 16 + 1024;  // + alignment slack
+  static constexpr int kBytes = kRunOff + (STRATA_RGMS_EPI_PAD ? 0 : 4 * kEpiSets * 32 * 16) + 1024;  // + alignment slack
   static constexpr int kAccCols = DOUT < 32 ? 32 : DOUT;
   static constexpr int kTmemCols = 2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : 256));
 };
@@ -396,8 +403,12 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
     // With two sets, set e owns accumulator e (tiles j = e mod 2): two tiles drain at once.
     const int q = warp & 3;
     const int ew = warp - kMmaWarp - 1;  // 0 .. 4 * kEpiSets - 1
-    float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + ew * (32 * kSPR);
-    int4* runs = reinterpret_cast<int4*>(smem + SM::kRunOff) + ew * 32;  // {r0, r1, T row, 0}
+    constexpr int kRow = SM::kRowF4;  // float4 per buffer row
+    float4* epi = reinterpret_cast<float4*>(smem + SM::kEpiOff) + ew * (32 * kRow);
+    // run table {r0, r1, T row, 0}: in the pad column of row k (padded), else its own array
+    int4* runs = STRATA_RGMS_EPI_PAD ? reinterpret_cast<int4*>(epi + kSPR)
+                                     : reinterpret_cast<int4*>(smem + SM::kRunOff) + ew * 32;
+    constexpr int kRunStride = STRATA_RGMS_EPI_PAD ? kRow : 1;  // int4 between run records
     for (long long j = ew / 4; j < nt; j += kEpiSets) {
       const int b = static_cast<int>(j & 1);
       // The accumulator being published implies the producer saw this tile's index block land
@@ -415,7 +426,7 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
       // Run table, once per tile: the head lane of the k-th run stores {r0, r1, T row} at k.
       if (is_head) {
         const unsigned later = heads & ~((2u << lane) - 1u);
-        runs[__popc(heads & ((1u << lane) - 1u))] =
+        runs[__popc(heads & ((1u << lane) - 1u)) * kRunStride] =
             make_int4(lane, min(later ? __ffs(later) - 1 : 32, first_pad), myword, 0);
       }
 #pragma unroll
@@ -425,7 +436,7 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
         tc::tmem_ld_wait();
 #pragma unroll
         for (int u = 0; u < kSPR; ++u)
-          epi[lane * kSPR + (u ^ (lane & (kSPR - 1)))] =
+          epi[lane * kRow + (STRATA_RGMS_EPI_PAD ? u : (u ^ (lane & (kSPR - 1))))] =
               make_float4(a * __uint_as_float(v[4 * u]), a * __uint_as_float(v[4 * u + 1]),
                           a * __uint_as_float(v[4 * u + 2]), a * __uint_as_float(v[4 * u + 3]));
         __syncwarp();
@@ -433,10 +444,16 @@ rgms_edge_gemm_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloa
         // are summed in edge order, its slots leave as one contiguous kNC-float segment.
         for (int it = lane; it < nruns * kSPR; it += 32) {
           const int sl = it & (kSPR - 1);
-          const int4 rn = runs[it / kSPR];
+          const int4 rn = runs[(it / kSPR) * kRunStride];
+#if STRATA_RGMS_EPI_PAD
+          const float4* er = epi + sl + rn.x * kRow;
+          float4 acc = *er;
+          for (int row = rn.x + 1; row < rn.y; ++row) acc = add4(acc, *(er += kRow));
+#else
           float4 acc = epi[rn.x * kSPR + (sl ^ (rn.x & (kSPR - 1)))];
           for (int row = rn.x + 1; row < rn.y; ++row)
             acc = add4(acc, epi[row * kSPR + (sl ^ (row & (kSPR - 1)))]);
+#endif
           if (rn.z >= 0) {
 #if STRATA_RGMS_T_L2
             reinterpret_cast<float4*>(T + static_cast<long long>(rn.z) * DOUT + c0)[sl] = acc;

@@ -1,8 +1,9 @@
 mkdir -p gpurun_out
-: > gpurun_out/ab4.jsonl
-for v in default ab/y64; do
+: > gpurun_out/ab5.jsonl
+for v in default ab/nopad default ab/nopad; do
   if [ "$v" = default ]; then unset STRATA_B200_LIB; else export STRATA_B200_LIB=$v/libstrata_b200.so; fi
-  python tools/ab_spmm.py >> gpurun_out/ab4.jsonl 2>/dev/null
-  timeout 900 python -m pytest tests/test_gpu_sddmm.py tests/test_gpu_c2.py tests/test_gpu_shard.py -q 2>&1 | tail -1 | sed "s|^|$v: |" >> gpurun_out/ab4_tests.log
+  python tools/ab_rgcn.py >> gpurun_out/ab5.jsonl 2>/dev/null
 done
-cat gpurun_out/ab4.jsonl gpurun_out/ab4_tests.log
+unset STRATA_B200_LIB
+timeout 900 python -m pytest tests/test_gpu_tc.py -q -k "rgms" 2>&1 | tail -1
+cat gpurun_out/ab5.jsonl
