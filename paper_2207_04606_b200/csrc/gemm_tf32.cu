@@ -43,6 +43,9 @@ constexpr int kThreads = 320;        // 10 warps
 constexpr int kMaxStages = 6;
 constexpr uint32_t kHiMask = 0xFFFFE000u;  // tf32: 10 explicit mantissa bits
 constexpr int kChunkK = 64;                // K per big-product accumulator
+#ifndef STRATA_GEMM_ST256  // A/B knob: 256-bit epilogue stores (when Z is 32-byte aligned)
+#define STRATA_GEMM_ST256 1
+#endif
 #ifndef STRATA_GEMM_MIN_STAGES  // A/B knob: pipeline stages the N tile must leave room for
 #define STRATA_GEMM_MIN_STAGES 2    // (4 at C5 128->128 = two N tiles, Y read twice: 0.74 -> 1.07 ms)
 #endif
@@ -81,6 +84,7 @@ struct GemmArgs {
   float* Z;        // [M][N]
   long long M;
   int K, N, Nt, stages;
+  int st256;  // Z 32-byte aligned: 256-bit epilogue stores
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -262,10 +266,25 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_consta
           if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
         }
         if (row < a.M) {
+#if STRATA_GEMM_ST256
+          // 256-bit stores (sm_100 STG.256): each lane writes whole 32-byte sectors of its row
+          // (the 16-byte form left every warp store 32 half-sectors: 0.74 -> 0.57 ms at C5)
+          if (a.st256) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                         ::"l"(zr + c + 8 * q), "f"(z[8 * q]), "f"(z[8 * q + 1]), "f"(z[8 * q + 2]),
+                           "f"(z[8 * q + 3]), "f"(z[8 * q + 4]), "f"(z[8 * q + 5]), "f"(z[8 * q + 6]),
+                           "f"(z[8 * q + 7])
+                         : "memory");
+          } else
+#endif
+          {
           float4* zp = reinterpret_cast<float4*>(zr + c);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             st_stream4(zp + q, make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]));
+          }
         }
       }
     }
@@ -363,7 +382,7 @@ void gemm_f32_launch(const float* Y, const float* W, float* Z, long long M, int 
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit - kSmemStatic));
   });
   const CUtensorMap ymap = make_tensor_map_f32_2d(Y, M, K, kKB, kBM);
-  GemmArgs a{W, Z, M, K, N, nt, stages};
+  GemmArgs a{W, Z, M, K, N, nt, stages, reinterpret_cast<uintptr_t>(Z) % 32 == 0 ? 1 : 0};
   const long long tiles = (M + kBM - 1) / kBM;
   const int ntiles = (N + nt - 1) / nt;
   const long long per_y = std::max<long long>(1, num_sms() / ntiles);

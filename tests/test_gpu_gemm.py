@@ -44,6 +44,21 @@ def test_gemm_real_valued(cuda, M, K, N):
     assert _err(Z, Y.astype(np.float64) @ W.astype(np.float64)) <= TOL
 
 
+@pytest.mark.parametrize("offset", [0, 4])
+def test_gemm_output_alignment(cuda, offset):
+    """Z at a 32-byte (256-bit stores) and a 16-byte-only aligned address (16-byte stores)."""
+    import torch
+    M, K, N = 1000, 128, 128
+    rng = np.random.default_rng(3)
+    Y = rng.integers(-3000, 3000, (M, K)).astype(np.float32)
+    W = rng.integers(-3, 4, (K, N)).astype(np.float32)
+    buf = torch.full((M * N + 8,), float("nan"), device=cuda)
+    Z = buf[offset: offset + M * N].view(M, N)
+    S.gemm(torch.from_numpy(Y).to(cuda), torch.from_numpy(W).to(cuda), Z)
+    assert np.array_equal(Z.cpu().numpy().astype(np.float64), Y.astype(np.float64) @ W.astype(np.float64))
+    assert torch.isnan(buf[:offset]).all() and torch.isnan(buf[offset + M * N:]).all()
+
+
 def _f32_sequential(Y, W):
     """An IEEE f32 GEMM: one f32 rounding per multiply-add, k ascending (SGEMM's numerics)."""
     acc = np.zeros((Y.shape[0], W.shape[1]), np.float32)

@@ -1,9 +1,9 @@
 mkdir -p gpurun_out
-: > gpurun_out/ab5.jsonl
-for v in default ab/nopad default ab/nopad; do
+: > gpurun_out/ab6.jsonl
+for v in default ab/st256 default ab/st256; do
   if [ "$v" = default ]; then unset STRATA_B200_LIB; else export STRATA_B200_LIB=$v/libstrata_b200.so; fi
-  python tools/ab_rgcn.py >> gpurun_out/ab5.jsonl 2>/dev/null
+  python tools/ab_spmm.py >> gpurun_out/ab6.jsonl 2>/dev/null
 done
-unset STRATA_B200_LIB
-timeout 900 python -m pytest tests/test_gpu_tc.py -q -k "rgms" 2>&1 | tail -1
-cat gpurun_out/ab5.jsonl
+export STRATA_B200_LIB=ab/st256/libstrata_b200.so
+timeout 900 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_gnn_layer.py -q 2>&1 | tail -1
+cat gpurun_out/ab6.jsonl
