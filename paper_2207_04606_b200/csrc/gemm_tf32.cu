@@ -43,6 +43,9 @@ constexpr int kThreads = 320;        // 10 warps
 constexpr int kMaxStages = 6;
 constexpr uint32_t kHiMask = 0xFFFFE000u;  // tf32: 10 explicit mantissa bits
 constexpr int kChunkK = 64;                // K per big-product accumulator
+#ifndef STRATA_GEMM_EPI32  // A/B knob: 32-column epilogue steps, both K chunks loaded per wait
+#define STRATA_GEMM_EPI32 0
+#endif
 #ifndef STRATA_GEMM_ST256  // A/B knob: 256-bit epilogue stores (when Z is 32-byte aligned)
 #define STRATA_GEMM_ST256 1
 #endif
@@ -247,6 +250,36 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_consta
       const long long row = t * kBM + quarter * 32 + lane;
       float* zr = a.Z + row * N + n0;
       const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * acc_stride;
+#if STRATA_GEMM_ST256 && STRATA_GEMM_EPI32
+      // Two K chunks, 32 columns per step: both chunks' TMEM loads in flight, one wait, then
+      // four 256-bit stores (same f32 sum order as the general path below).
+      if (nchunk == 2 && nt % 32 == 0 && a.st256) {
+        for (int c = 0; c < nt; c += 32) {
+          uint32_t r0[32], r1[32];
+          tc::tmem_ld_32x32b_x32(taddr + static_cast<uint32_t>(c), r0);
+          tc::tmem_ld_32x32b_x32(taddr + static_cast<uint32_t>(Nt + c), r1);
+          tc::tmem_ld_wait();
+          float z[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) z[q] = __uint_as_float(r0[q]) + __uint_as_float(r1[q]);
+          if (c + 32 >= nt) {
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
+          }
+          if (row < a.M) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                           ::"l"(zr + c + 8 * q), "f"(z[8 * q]), "f"(z[8 * q + 1]), "f"(z[8 * q + 2]),
+                             "f"(z[8 * q + 3]), "f"(z[8 * q + 4]), "f"(z[8 * q + 5]), "f"(z[8 * q + 6]),
+                             "f"(z[8 * q + 7])
+                           : "memory");
+          }
+        }
+        continue;
+      }
+#endif
       for (int c = 0; c < nt; c += 16) {
         uint32_t r[16];
         float z[16];
