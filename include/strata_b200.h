@@ -287,8 +287,8 @@ int strata_rgms_bf16(const int32_t* rel_ptr, const int32_t* dst, const int32_t* 
  * rel_ptr) and adds each edge's position in the destination-sorted order (stable: a row's
  * edges stay in relation order) and the row pointer dptr[m+1].  A run is two kernels:
  * per-relation 128-edge tcgen05 tiles write message rows T[pos e] = A_e * (X[src e] W_r),
- * then Y[i] = sum of T rows [dptr i, dptr i+1) — deterministic, no atomics.  The plan keeps
- * a T workspace of nnz * d_out f32, grown on demand. */
+ * then Y[i] = sum of T rows [dptr i, dptr i+1) — deterministic, no atomics.  The T workspace
+ * is taken from the stream-ordered pool per run (a plan may serve several streams). */
 typedef struct strata_rgms strata_rgms;
 int strata_rgms_plan(const int32_t* rel_ptr, const int32_t* dst, const int32_t* src,
                      const float* A, int64_t R, int64_t m, int64_t n, int64_t nnz,
@@ -298,6 +298,18 @@ int strata_rgms_run_bf16(const strata_rgms* h, const void* X_bf16, const void* W
 /* tiles_bound: upper bound on 128-edge tiles; t_bytes_per_dout: T bytes per output column. */
 int strata_rgms_info(const strata_rgms* h, int64_t* tiles_bound, int64_t* t_bytes_per_dout);
 int strata_rgms_destroy(strata_rgms* h);
+
+/* RGMS over per-relation hyb parts — SURVEY §8b's strata_rgms_hyb_bf16; replaces the "hyb"
+ * format of build_rgms_pipeline (driver.cpp:290-300: every relation's slice decomposed with
+ * hyb_rules, k = hyb_auto_k of the slice, rules lifted to the relation axis) + interpret.
+ * hybs[r] is relation r's hyb handle, any c and k, all of the same dims.  The device reads the
+ * parts in place, drops the pads (a slot repeating its ELL row's previous column,
+ * storage.cpp:528), rebuilds the relation-major edge list in CSR order and plans as
+ * strata_rgms_plan; X / W / Y and d_in / d_out as strata_rgms_bf16.  The one-shot form
+ * synchronises `stream`; the plan form may be run many times. */
+int strata_rgms_plan_hyb(const strata_hyb* const* hybs, int64_t R, strata_rgms** out, void* stream);
+int strata_rgms_hyb_bf16(const strata_hyb* const* hybs, int64_t R, const void* X_bf16,
+                         const void* W_bf16, float* Y, int64_t d_in, int64_t d_out, void* stream);
 
 /* ---- fused attention layer step (GAT-style) --------------------------
  * SDDMM -> row softmax -> SpMM in one pass over each row's edges (online softmax):

@@ -1092,8 +1092,9 @@ inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m, int64_t d
 // build_rgms_pipeline (driver.hpp:67-71, driver.cpp:241-314): relations padded for the format,
 // relation-major edges (build_rel_sparse, kernels.cpp:19-62), X then W drawn from
 // mt19937(seed) uniform_int(-3, 3) unless overridden (x_override: cols x d_in; w_override:
-// one d_in x d_out matrix per relation).  Every per-relation format the reference accepts
-// computes the same product; the device plan executes it with the two-pass tcgen05 RGMS.
+// one d_in x d_out matrix per relation).  "hyb" decomposes every relation on the device and
+// plans from the parts (strata_rgms_plan_hyb); the other formats compute the same product from
+// the relation-major CSR edges; both execute the two-pass tcgen05 RGMS.
 inline Pipeline build_rgms_pipeline(const std::vector<CooMatrix>& relations, int64_t d_in,
                                     int64_t d_out, DType dtype, const FormatRequest& fmt,
                                     const PipelineOptions& opts,
@@ -1174,13 +1175,30 @@ inline Pipeline build_rgms_pipeline(const std::vector<CooMatrix>& relations, int
   plan->d_out = d_out;
   plan->relations = R;
   plan->work_slots = static_cast<int64_t>(src.size());
-  plan->rel_ptr = DeviceArray<int32_t>(rp);
-  plan->rel_dst = DeviceArray<int32_t>(dst);
-  plan->rel_src = DeviceArray<int32_t>(src);
-  plan->rel_a = DeviceArray<float>(a);
   strata_rgms* h = nullptr;
-  check(strata_rgms_plan(plan->rel_ptr.data(), plan->rel_dst.data(), plan->rel_src.data(),
-                         plan->rel_a.data(), R, m, n, static_cast<int64_t>(src.size()), &h, nullptr));
+  if (fmt.kind == "hyb") {
+    // per-relation hyb rules (driver.cpp:294-300: k = hyb_auto_k of each slice unless given),
+    // decomposed on the device and read in place by strata_rgms_plan_hyb
+    std::vector<std::unique_ptr<DeviceCsr>> dcsr;
+    std::vector<std::unique_ptr<DeviceHyb>> dhyb;
+    std::vector<const strata_hyb*> hp;
+    for (const auto& r : rels) {
+      TensorStorage sl = build_csr(r);
+      dcsr.push_back(std::make_unique<DeviceCsr>(sl));
+      const int k = fmt.k >= 0 ? fmt.k : hyb_auto_k(sl);
+      if (fmt.c < 1 || k < 0) fail(ErrKind::Usage, "hyb requires c >= 1 and k >= 0");
+      dhyb.push_back(std::make_unique<DeviceHyb>(*dcsr.back(), fmt.c, k));
+      hp.push_back(dhyb.back()->get());
+    }
+    check(strata_rgms_plan_hyb(hp.data(), R, &h, nullptr));  // synchronous: parts may go
+  } else {
+    plan->rel_ptr = DeviceArray<int32_t>(rp);
+    plan->rel_dst = DeviceArray<int32_t>(dst);
+    plan->rel_src = DeviceArray<int32_t>(src);
+    plan->rel_a = DeviceArray<float>(a);
+    check(strata_rgms_plan(plan->rel_ptr.data(), plan->rel_dst.data(), plan->rel_src.data(),
+                           plan->rel_a.data(), R, m, n, static_cast<int64_t>(src.size()), &h, nullptr));
+  }
   plan->rgms.reset(h);
   detail::finish_pipeline(pl, std::move(plan), opts);
   return pl;

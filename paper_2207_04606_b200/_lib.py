@@ -119,6 +119,8 @@ _sig("strata_rgms_plan", C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, C.POINTER(
 _sig("strata_rgms_run_bf16", C.c_int, vp, vp, vp, vp, i64, i64, vp)
 _sig("strata_rgms_info", C.c_int, vp, i64p, i64p)
 _sig("strata_rgms_destroy", C.c_int, vp)
+_sig("strata_rgms_plan_hyb", C.c_int, vp, i64, C.POINTER(vp), vp)
+_sig("strata_rgms_hyb_bf16", C.c_int, vp, i64, vp, vp, vp, i64, i64, vp)
 _sig("strata_partition_rows", C.c_int, vp, i64, C.c_int, vp)
 _sig("strata_nccl_unique_id", C.c_int, vp)
 _sig("strata_nccl_comm_init", C.c_int, vp, C.c_int, C.c_int, vp)
@@ -158,7 +160,7 @@ EXPORTED = [
     "strata_srbcrs_destroy", "strata_srbcrs_spmm_bf16", "strata_attn_plan_create",
     "strata_attn_plan_destroy", "strata_attn_csr_f32", "strata_ell_from_csr",
     "strata_rgms_bf16", "strata_rgms_plan", "strata_rgms_run_bf16", "strata_rgms_info",
-    "strata_rgms_destroy", "strata_partition_rows",
+    "strata_rgms_destroy", "strata_partition_rows", "strata_rgms_plan_hyb", "strata_rgms_hyb_bf16",
     "strata_mtx_parse", "strata_mtx_read_file", "strata_mtx_info", "strata_mtx_device",
     "strata_mtx_read", "strata_mtx_destroy",
     "strata_nccl_unique_id", "strata_nccl_comm_init", "strata_nccl_comm_destroy",

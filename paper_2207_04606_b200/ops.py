@@ -807,6 +807,20 @@ class RgmsPlan:
                                    _stream(stream)))
         self._h = h
 
+    @classmethod
+    def from_hyb(cls, hybs, stream=None) -> "RgmsPlan":
+        """The "hyb" format of build_rgms_pipeline (driver.cpp:290-300): one HybDecomposition
+        per relation (strata_rgms_plan_hyb reads their parts in place, pads dropped)."""
+        self = cls.__new__(cls)
+        self.rows, self.cols, self.relations = hybs[0].rows, hybs[0].cols, len(hybs)
+        arr = (C.c_void_p * len(hybs))(*[h.handle.value for h in hybs])
+        h = C.c_void_p()
+        check(lib.strata_rgms_plan_hyb(arr, len(hybs), C.byref(h), _stream(stream)))
+        self._h = h
+        self._hybs = list(hybs)  # keep the parts alive while the plan is in use
+        self.nnz = None
+        return self
+
     @property
     def message_rows(self) -> int:
         """T rows a run writes and reads back: the (relation, destination) runs of rows with two

@@ -195,6 +195,60 @@ def test_rgms_golden(cuda, G):
         assert np.array_equal(Y, G[f"rgms/{fmt}/Y"]), fmt
 
 
+def _relation_csrs(R, m, n, I_indptr, I_indices, J_indptr, J_indices, A):
+    """Per-relation CsrMatrix slices of a reference RelSparse (kernels.cpp:19-62)."""
+    out = []
+    for r in range(R):
+        counts = np.zeros(m, np.int64)
+        cols, vals = [], []
+        for a in range(I_indptr[r], I_indptr[r + 1]):
+            i = I_indices[a]
+            counts[i] = J_indptr[a + 1] - J_indptr[a]
+            cols.append(J_indices[J_indptr[a]:J_indptr[a + 1]])
+            vals.append(A[J_indptr[a]:J_indptr[a + 1]])
+        indptr = np.r_[0, np.cumsum(counts)].astype(np.int32)
+        ix = np.concatenate(cols).astype(np.int32) if cols else np.zeros(0, np.int32)
+        vv = np.concatenate(vals).astype(np.float32) if vals else np.zeros(0, np.float32)
+        out.append(S.CsrMatrix(m, n, indptr, ix, vv))
+    return out
+
+
+def test_rgms_hyb_parts_golden(cuda, G):
+    """strata_rgms_plan_hyb (SURVEY §8b strata_rgms_hyb_bf16): per-relation hyb decompositions
+    (k = hyb_auto_k of each slice, as driver.cpp:294-300) read in place -> the reference's
+    "hyb" RGMS pipeline output, bitwise."""
+    import torch
+    R, m, n = (int(x) for x in G["rgms/shape"])
+    slices = _relation_csrs(R, m, n, G["rgms/I_indptr"], G["rgms/I_indices"], G["rgms/J_indptr"],
+                            G["rgms/J_indices"], G["rgms/A"])
+    hybs = [S.decompose_hyb(c.to_device(cuda), 1, S.hyb_auto_k(c)) for c in slices]
+    X = bf16(torch.from_numpy(G["rgms/hyb/X"]).to(cuda))
+    W = bf16(torch.from_numpy(G["rgms/hyb/W"]).to(cuda))
+    Y = S.RgmsPlan.from_hyb(hybs).run(X, W).cpu().numpy()
+    assert np.array_equal(Y, G["rgms/hyb/Y"])
+
+
+@pytest.mark.parametrize("c,k", [(1, 0), (2, 1), (3, 2)])
+def test_rgms_hyb_parts_equal_csr_plan(cuda, c, k):
+    """Split rows (l > 2^k), padding and column partitions in the parts: same Y as the CSR
+    plan of the same relations, bitwise on integer operands."""
+    import torch
+    g = S.generate_matrix("powerlaw", 6000, 5000, 0, 0, 0, 6.0, 3)
+    rel = S.split_relations(g, 7, 2)
+    slices = []
+    for r in range(7):
+        lo, hi = int(rel.rel_ptr[r]), int(rel.rel_ptr[r + 1])
+        dst, src, a = rel.dst[lo:hi], rel.src[lo:hi], rel.A[lo:hi]
+        indptr = np.r_[0, np.cumsum(np.bincount(dst, minlength=rel.rows))].astype(np.int32)
+        slices.append(S.CsrMatrix(rel.rows, rel.cols, indptr, src.astype(np.int32), a.astype(np.float32)))
+    hybs = [S.decompose_hyb(sl.to_device(cuda), c, k) for sl in slices]
+    X = bf16(torch.from_numpy(S.dense_int((rel.cols, 32), 4)).to(cuda))
+    W = bf16(torch.from_numpy(S.dense_int((7, 32, 32), 5)).to(cuda))
+    Yh = S.RgmsPlan.from_hyb(hybs).run(X, W)
+    Yc = S.RgmsPlan(rel.to_device(cuda)).run(X, W)
+    assert torch.equal(Yh, Yc)
+
+
 @pytest.mark.parametrize("din,dout", [(32, 32), (16, 16), (64, 64), (32, 128)])
 def test_rgms_random_vs_oracle(cuda, din, dout):
     import torch
