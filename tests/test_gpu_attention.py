@@ -52,6 +52,26 @@ def test_attention_power_law_with_hub_rows(cuda, d, avg):
     assert np.array_equal(Z, Z2)  # deterministic
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_attention_16_byte_aligned_operands(cuda, d):
+    """K at a 16-byte-only aligned address takes the 128-bit path; same result within the bar
+    and the 256-bit path's result on aligned copies."""
+    m = S.generate_matrix("powerlaw", 2000, 1800, 0, 0, 0, 30.0, 5)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(3)
+    Q = torch.randn(m.rows, d, device=cuda, generator=g) * 0.3
+    K = torch.randn(m.cols, d, device=cuda, generator=g) * 0.3
+    V = torch.randn(m.cols, d, device=cuda, generator=g)
+    buf = torch.empty(m.cols * d + 4, device=cuda)
+    K16 = buf[4: 4 + m.cols * d].view(m.cols, d)
+    K16.copy_(K)
+    plan = S.AttentionPlan(m.to_device(cuda))
+    Za = plan(Q, K, V).cpu().numpy()
+    Zu = plan(Q, K16, V).cpu().numpy()
+    want = attention_f64(m, Q.cpu().numpy(), K.cpu().numpy(), V.cpu().numpy())
+    assert close_ref_metric(Za, want, 2e-5) and close_ref_metric(Zu, want, 2e-5)
+
+
 def test_attention_usage_errors(cuda):
     m = S.generate_matrix("powerlaw", 100, 100, 0, 0, 0, 4.0, 1)
     plan = S.AttentionPlan(m.to_device(cuda))
