@@ -62,7 +62,7 @@ __device__ __forceinline__ float vw_allreduce(float v, unsigned mask) {
 // One virtual warp (L lanes, one float4 of the D features each) per work item.
 // Items from nlong_items_begin on are long-row chunks: they write their (acc, m, l) partial.
 #ifndef STRATA_ATTN_U  // A/B knobs: edges in flight per batch, CTAs per SM the registers allow
-#define STRATA_ATTN_U 4
+#define STRATA_ATTN_U 2  // C2 with 256-bit slices: U = 1 / 2 / 3 / 4 / 8 -> 6.18 / 5.41 / 5.87 / 5.67 / 9.82 ms
 #endif
 #ifndef STRATA_ATTN_FASTEXP  // A/B knob: MUFU __expf in the edge loop (C2: 6.13 vs 6.18 ms; off)
 #define STRATA_ATTN_FASTEXP 0
