@@ -71,8 +71,8 @@ __device__ __forceinline__ T reduce_scatter(T (&v)[L], int lane, unsigned mask) 
 #ifndef STRATA_SDDMM_F64  // A/B knob: 1 = f64 dot products (default), 0 = f32
 #define STRATA_SDDMM_F64 1
 #endif
-#ifndef STRATA_SDDMM_YT64  // A/B knob: Y transposed once per call into f64 (no per-gather
-#define STRATA_SDDMM_YT64 0  // F32->F64 conversions; twice the gathered bytes)
+#ifndef STRATA_SDDMM_VEC64  // A/B knob: d = 64 as 8 lanes x 256-bit slices (2) or 16 x 128-bit (1)
+#define STRATA_SDDMM_VEC64 2
 #endif
 
 // Dot-product numerics.  The reference accumulates sum_k A*X*Y in f64 and rounds each partial
@@ -97,13 +97,6 @@ __device__ __forceinline__ typename DotT<kF64>::XV xfrag(const float4& x) {
   }
 }
 
-__device__ __forceinline__ double dot4(const double4& x, const double4& y) {
-  double s = x.x * y.x;
-  s = fma(x.y, y.y, s);
-  s = fma(x.z, y.z, s);
-  return fma(x.w, y.w, s);
-}
-
 template <bool kF64>
 __device__ __forceinline__ typename DotT<kF64>::T dot4(const typename DotT<kF64>::XV& x, const float4& y) {
   if constexpr (kF64) {
@@ -116,15 +109,21 @@ __device__ __forceinline__ typename DotT<kF64>::T dot4(const typename DotT<kF64>
   }
 }
 
-template <int L, bool kF64 = STRATA_SDDMM_F64, bool kY64 = (STRATA_SDDMM_YT64 != 0)>
+// VEC float4 per lane (VEC = 2: 8 consecutive features, one 256-bit gather per Yt row slice,
+// half the lanes per non-zero and half the reduce-scatter shuffles).
+template <int VEC>
+struct YSlice {
+  float4 v[VEC];
+};
+
+template <int L, int VEC = 1, bool kF64 = STRATA_SDDMM_F64>
 __global__ void __launch_bounds__(kBlock)
 sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
              const float* __restrict__ A, const float* __restrict__ X,
-             const void* __restrict__ Yt_, float* __restrict__ B, long long rows, long long nnz,
+             const float* __restrict__ Yt, float* __restrict__ B, long long rows, long long nnz,
              long long d) {
-  static_assert(!kY64 || kF64, "an f64 Yt only serves the f64 dot");
   using T = typename DotT<kF64>::T;
-  using YV = std::conditional_t<kY64, double4, float4>;
+  using YV = YSlice<VEC>;
   constexpr int U = 8;
   const int wl = threadIdx.x & 31;
   const int lane = threadIdx.x & (L - 1);
@@ -162,22 +161,32 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   }
   int row = static_cast<int>(lo);
   long long row_end = __ldg(indptr + row + 1);
-  typename DotT<kF64>::XV x =
-      xfrag<kF64>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane));
+  typename DotT<kF64>::XV x[VEC];
+  auto load_x = [&]() {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i)
+      x[i] = xfrag<kF64>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) +
+                                    lane * VEC + i));
+  };
+  load_x();
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncwarp(vmask);
 
-  const float4* Y4 = reinterpret_cast<const float4*>(Yt_) + lane;
-  const double2* Y8 = reinterpret_cast<const double2*>(Yt_) + 2 * lane;
+  const float4* Y4 = reinterpret_cast<const float4*>(Yt) + lane * VEC;
   const int d4 = static_cast<int>(d / 4);
   auto gather_y = [&](int col) -> YV {
-    if constexpr (kY64) {
-      const double2* p = Y8 + static_cast<long long>(col) * (2 * d4);
-      const double2 a = __ldg(p), b = __ldg(p + 1);
-      return make_double4(a.x, a.y, b.x, b.y);
+    YV y;
+    const float4* p = Y4 + static_cast<long long>(col) * d4;
+    if constexpr (VEC == 2) {  // Yt is the call's own 256-byte aligned workspace
+      asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=f"(y.v[0].x), "=f"(y.v[0].y), "=f"(y.v[0].z), "=f"(y.v[0].w),
+                     "=f"(y.v[1].x), "=f"(y.v[1].y), "=f"(y.v[1].z), "=f"(y.v[1].w)
+                   : "l"(p));
     } else {
-      return ld_gather4(Y4 + static_cast<long long>(col) * d4);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) y.v[i] = ld_gather4(p + i);
     }
+    return y;
   };
   for (int g = 0; g < ne; g += L) {
     const int n = min(L, ne - g);
@@ -192,10 +201,16 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
         const int cc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
         for (int v = 0; v < 4; ++v)
-          yv[u + v] = (u0 + u + v < n) ? gather_y(cc[v]) : YV{};
+          if (u0 + u + v < n) yv[u + v] = gather_y(cc[v]);
+          else
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) yv[u + v].v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       auto dot = [&](const YV& y) -> T {
-        if constexpr (kY64) return dot4(x, y); else return dot4<kF64>(x, y);
+        T r = dot4<kF64>(x[0], y.v[0]);
+#pragma unroll
+        for (int i = 1; i < VEC; ++i) r += dot4<kF64>(x[i], y.v[i]);
+        return r;
       };
       if (one_row) {
 #pragma unroll
@@ -207,7 +222,7 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
             const long long e = e0 + g + u0 + u;
             if (e >= row_end) {  // next non-empty row containing e
               do { ++row; row_end = __ldg(indptr + row + 1); } while (e >= row_end);
-              x = xfrag<kF64>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) + lane));
+              load_x();
             }
           }
           part[u0 + u] = dot(yv[u]);
@@ -424,15 +439,11 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
                       int64_t nnz, int64_t d, cudaStream_t s) {
   if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "sddmm: d must be >= 1");
   if (nnz == 0) return;
-  // Y[d][n] -> Yt[n][d] once per call (f64 with STRATA_SDDMM_YT64 for the vectorised kernels;
-  // the scalar fallback always reads f32).
-  const bool vec = (d == 32 || d == 64 || d == 128);
-  const bool y64 = STRATA_SDDMM_YT64 && vec;
-  void* Yt = workspace_alloc((y64 ? sizeof(double) : sizeof(float)) * cols * d, s);
+  // Y[d][n] -> Yt[n][d] once per call (f32; the vectorised kernels gather 128- / 256-bit slices)
+  float* Yt = static_cast<float*>(workspace_alloc(sizeof(float) * cols * d, s));
   {
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((d + 31) / 32));
-    if (y64) transpose_kernel<double><<<grid, dim3(32, 8), 0, s>>>(Y, static_cast<double*>(Yt), d, cols);
-    else transpose_kernel<float><<<grid, dim3(32, 8), 0, s>>>(Y, static_cast<float*>(Yt), d, cols);
+    transpose_kernel<float><<<grid, dim3(32, 8), 0, s>>>(Y, Yt, d, cols);
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
   const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0;
@@ -444,20 +455,22 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
   auto smem_for = [&](int L) { return (kBlock / L) * 2 * kNnzPerChunk * 4; };
   const bool staged = aligned && reinterpret_cast<uintptr_t>(indices) % 16 == 0 &&
                       reinterpret_cast<uintptr_t>(A) % 16 == 0;
-  static PerDeviceOnce once;  // d = 32: 64 KB per block
+  static PerDeviceOnce once;  // 8 lanes per VW (d = 32, and d = 64 in 256-bit slices): 64 KB
   once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8)));
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8)));
   });
-  if (y64 && !staged) throw ApiError(STRATA_ERR_INTERNAL, "sddmm: f64 Yt needs 16-byte aligned operands");
   if (staged && d == 32)
     sddmm_kernel<8><<<blocks_for(8), kBlock, smem_for(8), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  else if (staged && d == 64 && STRATA_SDDMM_VEC64 == 2)
+    sddmm_kernel<8, 2><<<blocks_for(8), kBlock, smem_for(8), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   else if (staged && d == 64)
     sddmm_kernel<16><<<blocks_for(16), kBlock, smem_for(16), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   else if (staged && d == 128)
     sddmm_kernel<32><<<blocks_for(32), kBlock, smem_for(32), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   else {
     const unsigned blocks = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, 148 * 32));
-    sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, static_cast<const float*>(Yt), B, rows, nnz, d);
+    sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
   }
   STRATA_CUDA_CHECK(cudaGetLastError());
   STRATA_CUDA_CHECK(cudaFreeAsync(Yt, s));

@@ -62,7 +62,7 @@ struct SpmmArgs {
   long long d;
   long long total_chunks;
   int nparts;
-  int pad_;
+  int w256;  // X 32-byte aligned: 256-bit slice loads for VEC >= 2
   SpmmPartDev parts[kMaxParts];
 };
 
@@ -78,18 +78,31 @@ struct Frag {
 // Gather one X row fragment owned by this lane.
 template <int L, int VEC, bool kScalar>
 __device__ __forceinline__ void gather(Frag<VEC, kScalar>& f, const float* __restrict__ X,
-                                       long long col, long long d, int lane, long long feat0) {
+                                       long long col, long long d, int lane, long long feat0,
+                                       bool w256) {
   if constexpr (kScalar) {
     const long long fi = feat0 + lane;
     f.v[0].x = fi < d ? ld_gather(X + col * d + fi) : 0.f;
   } else {
     // Vector variants are launched only for d == 4 * L * VEC, so the row stride is a
     // compile-time power of two: one shift instead of a 64-bit multiply per gathered slot.
+    // A lane owns VEC consecutive float4 of the row (feature 4*VEC*lane ..): with VEC = 2 one
+    // 256-bit load (sm_100 LDG.256), with VEC = 4 two.
     (void)d;
     const float4* xp = reinterpret_cast<const float4*>(X) +
-                       (static_cast<unsigned long long>(static_cast<uint32_t>(col)) * (L * VEC)) + lane;
+                       (static_cast<unsigned long long>(static_cast<uint32_t>(col)) * (L * VEC)) + lane * VEC;
+    // L < 32 VEC variants (d = 64) are launched only on 32-byte aligned X; d = 256 / 512 check
+    if (VEC % 2 == 0 && (L < 32 || w256)) {  // warp-uniform
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) f.v[i] = ld_gather4(xp + i * L);
+      for (int i = 0; i + 1 < VEC; i += 2)
+        asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=f"(f.v[i].x), "=f"(f.v[i].y), "=f"(f.v[i].z), "=f"(f.v[i].w),
+                       "=f"(f.v[i + 1].x), "=f"(f.v[i + 1].y), "=f"(f.v[i + 1].z), "=f"(f.v[i + 1].w)
+                     : "l"(xp + i));
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) f.v[i] = ld_gather4(xp + i);
+    }
   }
 }
 
@@ -184,10 +197,10 @@ __device__ __forceinline__ void put_row(float* __restrict__ row, const Acc<VEC, 
     const long long fi = feat0 + lane;
     if (fi < d) row[fi] = static_cast<float>(acc.v[0]);
   } else {
-    float4* rp = reinterpret_cast<float4*>(row) + lane;
+    float4* rp = reinterpret_cast<float4*>(row) + lane * VEC;
 #pragma unroll
     for (int i = 0; i < VEC; ++i)
-      st_stream4(rp + i * L, make_float4(static_cast<float>(acc.v[4 * i]), static_cast<float>(acc.v[4 * i + 1]),
+      st_stream4(rp + i, make_float4(static_cast<float>(acc.v[4 * i]), static_cast<float>(acc.v[4 * i + 1]),
                                          static_cast<float>(acc.v[4 * i + 2]), static_cast<float>(acc.v[4 * i + 3])));
   }
 }
@@ -200,21 +213,27 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
     const long long fi = feat0 + lane;
     if (fi < d) row[fi] = kAdd ? row[fi] + acc.v[0] : acc.v[0];
   } else {
-    double2* rp = reinterpret_cast<double2*>(row) + 2 * lane;
+    double2* rp = reinterpret_cast<double2*>(row) + 2 * lane * VEC;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
       double2 a0 = make_double2(acc.v[4 * i], acc.v[4 * i + 1]);
       double2 a1 = make_double2(acc.v[4 * i + 2], acc.v[4 * i + 3]);
       if constexpr (kAdd) {
-        const double2 o0 = rp[2 * i * L], o1 = rp[2 * i * L + 1];
+        const double2 o0 = rp[2 * i], o1 = rp[2 * i + 1];
         a0.x += o0.x; a0.y += o0.y; a1.x += o1.x; a1.y += o1.y;
       }
-      rp[2 * i * L] = a0;
-      rp[2 * i * L + 1] = a1;
+      rp[2 * i] = a0;
+      rp[2 * i + 1] = a1;
     }
   }
 }
 
+#ifndef STRATA_SPMM_VEC64  // A/B knob: d = 64 as 8 lanes x 256-bit slices (2) or 16 x 128-bit (1)
+#define STRATA_SPMM_VEC64 2    // (C2: 3.30 -> 2.91 ms)
+#endif
+#ifndef STRATA_SPMM_VEC128  // A/B knob: d = 128 as 16 lanes x 256-bit slices (2) or 32 x 128-bit (1)
+#define STRATA_SPMM_VEC128 1   // (C5: 5.05 -> 5.54 ms with 2: the DRAM-bound case keeps 32 lanes)
+#endif
 #ifndef STRATA_SPMM_MINB16  // CTAs/SM the d=64 variant is register-budgeted for (A/B knob)
 #define STRATA_SPMM_MINB16 2
 #endif
@@ -234,7 +253,7 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 template <int L, int VEC, bool kScalar, bool kMulti>
 // (the multi-destination instantiation keeps the 3-CTA budget only for one destination's worth
 // of registers: it gets the 2-CTA budget, so its replica stores do not spill)
-__global__ void __launch_bounds__(kBlock, VEC > 1 ? 1 : ((L == 32 && !kScalar && !kMulti) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2)))
+__global__ void __launch_bounds__(kBlock, (VEC > 1 && L == 32) ? 1 : (VEC > 1 ? 2 : ((L == 32 && !kScalar && !kMulti) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2))))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int kT = 8;  // real slots per consume batch / slots per lane per compaction round
 #ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
@@ -414,7 +433,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
           Frag<VEC, kScalar> xv[UG];
 #pragma unroll
           for (int u = 0; u < UG; ++u)
-            gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0);
+            gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0, a.w256);
 #pragma unroll
           for (int u = 0; u < UG; ++u) fma_acc((ub + u) & 1 ? a1 : acc, sV[e0 + ub + u], xv[u]);
         }
@@ -427,7 +446,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
           Frag<VEC, kScalar> xv[UG];
 #pragma unroll
           for (int u = 0; u < UG; ++u)
-            gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0);
+            gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0, a.w256);
 #pragma unroll
           for (int u = 0; u < UG; ++u) fma_part((ub + u) & 1 ? p1 : part, sV[e0 + ub + u], xv[u]);
         }
@@ -441,7 +460,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
         Frag<VEC, kScalar> xv[UG];
 #pragma unroll
         for (int u = 0; u < UG; ++u)
-          if (ub + u < n) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u] & 0x7fffffff, d, lane, feat0);
+          if (ub + u < n) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u] & 0x7fffffff, d, lane, feat0, a.w256);
 #pragma unroll
         for (int u = 0; u < UG; ++u) {
           const int uu = ub + u;
@@ -631,9 +650,17 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
   int L = 32, VEC = 1;
   bool scalar = true;
   if (aligned) {
+    // 256-bit slices for d = 64 only with 32-byte aligned X (d = 256 / 512 fall back to two
+    // 128-bit loads per slice inside the kernel)
+    const bool a32 = reinterpret_cast<uintptr_t>(X) % 32 == 0;
     if (d == 32) { L = 8; scalar = false; }
-    else if (d == 64) { L = 16; scalar = false; }
-    else if (d == 128) { L = 32; scalar = false; }
+    else if (d == 64) {
+      const int v = (STRATA_SPMM_VEC64 == 2 && a32) ? 2 : 1;
+      L = 16 / v; VEC = v; scalar = false;
+    } else if (d == 128) {
+      const int v = (STRATA_SPMM_VEC128 == 2 && a32) ? 2 : 1;
+      L = 32 / v; VEC = v; scalar = false;
+    }
     else if (d == 256) { L = 32; VEC = 2; scalar = false; }
     else if (d == 512) { L = 32; VEC = 4; scalar = false; }
   }
@@ -668,6 +695,7 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     SpmmArgs args{};
     args.I = h.I.p; args.J = h.J.p; args.V = h.V.p; args.X = X; args.Y = Y;
     args.carry = carry; args.yacc = yacc; args.d = d;
+    args.w256 = reinterpret_cast<uintptr_t>(X) % 32 == 0 ? 1 : 0;
     long long chunks = 0;
     int np = 0;
     for (; pi < h.parts.size() && h.parts[pi].partition == part_id; ++pi) {
@@ -683,8 +711,14 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     args.total_chunks = chunks;
     if (chunks > 0) {
       if (scalar) launch_variant<32, 1, true>(args, chunks, d, s);
-      else if (L == 8) launch_variant<8, 1, false>(args, chunks, d, s);
-      else if (L == 16) launch_variant<16, 1, false>(args, chunks, d, s);
+      else if (L == 8 && VEC == 1) launch_variant<8, 1, false>(args, chunks, d, s);
+#if STRATA_SPMM_VEC64 == 2
+      else if (L == 8 && VEC == 2) launch_variant<8, 2, false>(args, chunks, d, s);
+#endif
+      else if (L == 16 && VEC == 1) launch_variant<16, 1, false>(args, chunks, d, s);
+#if STRATA_SPMM_VEC128 == 2
+      else if (L == 16 && VEC == 2) launch_variant<16, 2, false>(args, chunks, d, s);
+#endif
       else if (VEC == 1) launch_variant<32, 1, false>(args, chunks, d, s);
       else if (VEC == 2) launch_variant<32, 2, false>(args, chunks, d, s);
       else launch_variant<32, 4, false>(args, chunks, d, s);

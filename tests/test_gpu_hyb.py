@@ -143,6 +143,22 @@ def test_spmm_feature_sizes(cuda, d):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("d", [64, 256, 512])
+def test_spmm_x_16_byte_aligned(cuda, d):
+    """X at a 16-byte-only aligned address: d = 64 takes the 128-bit-slice variant, d = 256 / 512
+    the VEC kernels' two-128-bit-load fallback; bitwise equal to the 32-byte-aligned call."""
+    import torch
+    m = S.generate_matrix("powerlaw", 3000, 2800, 0, 0, 0, 20.0, 5)
+    h = S.decompose_hyb(m.to_device(cuda), 1, 3)
+    X = torch.from_numpy(S.dense_int((m.cols, d), 6)).to(cuda)
+    buf = torch.empty(m.cols * d + 4, device=cuda)
+    X16 = buf[4: 4 + m.cols * d].view(m.cols, d)
+    X16.copy_(X)
+    ya, yu = S.spmm(h, X).cpu().numpy(), S.spmm(h, X16).cpu().numpy()
+    assert np.array_equal(ya, yu)
+    assert np.array_equal(ya, port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, X.cpu().numpy()))
+
+
 def test_spmm_long_split_rows_deterministic(cuda):
     """Rows far above 2^k split into many bucket-k segments spanning many chunks (the
     carry + fix-up path); results must be exact on integer data and bitwise reproducible."""
