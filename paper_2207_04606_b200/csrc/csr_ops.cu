@@ -72,7 +72,7 @@ __device__ __forceinline__ T reduce_scatter(T (&v)[L], int lane, unsigned mask) 
 #define STRATA_SDDMM_F64 1
 #endif
 #ifndef STRATA_SDDMM_VEC64  // A/B knob: d = 64 as 8 lanes x 256-bit slices (2) or 16 x 128-bit (1)
-#define STRATA_SDDMM_VEC64 2
+#define STRATA_SDDMM_VEC64 1  // (2 measured 7.93 vs 4.12 ms at C2: 8-non-zero groups halve the work per reduce-scatter)
 #endif
 
 // Dot-product numerics.  The reference accumulates sum_k A*X*Y in f64 and rounds each partial
