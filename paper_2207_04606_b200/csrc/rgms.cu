@@ -521,34 +521,13 @@ __device__ __forceinline__ void t_row_consumed(const float* T, long long q, int 
 #endif
 }
 
-#ifndef STRATA_RGMS_SUM_VEC  // A/B knob: 2 = each lane owns 2 consecutive float4 of a T row
-#define STRATA_RGMS_SUM_VEC 1    // (one 256-bit load), half the lanes per row
-#endif
 template <int DOUT>
 struct RowSumShape {
   static constexpr int kF4 = DOUT / 4;
-  static constexpr int kV = (STRATA_RGMS_SUM_VEC == 2 && kF4 >= 2) ? 2 : 1;
-  static constexpr int kL = kF4 / kV < 32 ? kF4 / kV : 32;
+  static constexpr int kL = kF4 < 32 ? kF4 : 32;
   static constexpr int kF = kF4 / kL;
   static constexpr int kGrp = 32 / kL;
-  // float4 f of lane l's slice of a row: strided (lane l owns l, l + kL, ...) or, with kV = 2,
-  // contiguous (l * kF ..), so a lane's slice is one 256-bit access when kF = 2
-  static __device__ __forceinline__ int at(int l, int f) { return kV == 2 ? l * kF + f : f * kL + l; }
 };
-
-// kF float4 of a streamed T row slice (evict-first): one 256-bit load when kF == 2 and kV == 2.
-template <class RS>
-__device__ __forceinline__ void ld_t_slice(const float4* __restrict__ p, float4* v) {
-  if constexpr (RS::kV == 2 && RS::kF == 2) {
-    asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[0].z), "=f"(v[0].w), "=f"(v[1].x),
-                   "=f"(v[1].y), "=f"(v[1].z), "=f"(v[1].w)
-                 : "l"(p));
-  } else {
-#pragma unroll
-    for (int f = 0; f < RS::kF; ++f) v[f] = __ldcs(p + (RS::kV == 2 ? f : f * RS::kL));
-  }
-}
 
 // Short rows: a warp takes a block of 32 consecutive rows (bounds: one coalesced load, kept in
 // smem); lane group g owns rows g*kRPV .. g*kRPV + kRPV - 1, whose T rows are contiguous, and
@@ -572,7 +551,7 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
   const int lane = threadIdx.x & 31, l = lane % kL, g = lane / kL, w = threadIdx.x >> 5;
   int* bnd = sbnd[w];
   const long long nwarps = nblk * (blockDim.x >> 5);
-  const float4* T4 = reinterpret_cast<const float4*>(T) + RS::at(l, 0);
+  const float4* T4 = reinterpret_cast<const float4*>(T) + l;
   // The next block's bounds are loaded while this block's T rows stream (one DRAM latency
   // less on every block's dependency chain).
   long long b = blk * (blockDim.x >> 5) + w;
@@ -612,7 +591,7 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
         const long long yr = kCompact ? static_cast<long long>(srow[w][r]) : i0 + r;
 #pragma unroll
         for (int f = 0; f < kF; ++f) {
-          st_stream4(reinterpret_cast<float4*>(Y + yr * DOUT) + RS::at(l, f), acc[f]);
+          st_stream4(reinterpret_cast<float4*>(Y + yr * DOUT) + f * kL + l, acc[f]);
           acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
@@ -628,14 +607,11 @@ __device__ __forceinline__ void row_sum_body(const int32_t* __restrict__ dptr, c
       }
       float4 u[kB][kF];
 #pragma unroll
-      for (int j = 0; j < kB; ++j) {
-        if (q + j < qend) {
-          ld_t_slice<RS>(T4 + static_cast<long long>(q + j) * kF4, u[j]);
-        } else {
+      for (int j = 0; j < kB; ++j)
 #pragma unroll
-          for (int f = 0; f < kF; ++f) u[j][f] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
+        for (int f = 0; f < kF; ++f)
+          u[j][f] = q + j < qend ? __ldcs(T4 + static_cast<long long>(q + j) * kF4 + f * kL)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
       int used = kB;
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
@@ -710,7 +686,7 @@ __device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr
 #pragma unroll
         for (int g = 0; g < kF; ++g)
           u[j][g] = __ldcs(reinterpret_cast<const float4*>(T) +
-                           static_cast<long long>(q + j * kGrp) * kF4 + RS::at(l, g));
+                           static_cast<long long>(q + j * kGrp) * kF4 + g * kL + l);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -724,7 +700,7 @@ __device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr
 #pragma unroll
       for (int g = 0; g < kF; ++g)
         acc[g] = add4(acc[g], __ldcs(reinterpret_cast<const float4*>(T) +
-                                     static_cast<long long>(q) * kF4 + RS::at(l, g)));
+                                     static_cast<long long>(q) * kF4 + g * kL + l));
 #if STRATA_RGMS_T_L2
       t_row_consumed<DOUT>(T, q, l);
 #endif
@@ -732,7 +708,7 @@ __device__ __forceinline__ void long_chunk_body(const int32_t* __restrict__ dptr
 #pragma unroll
     for (int g = 0; g < kF; ++g) {
       const float4 v = reduce_groups<kL>(acc[g]);
-      if (grp == 0) reinterpret_cast<float4*>(partial + static_cast<long long>(c) * DOUT)[RS::at(l, g)] = v;
+      if (grp == 0) reinterpret_cast<float4*>(partial + static_cast<long long>(c) * DOUT)[g * kL + l] = v;
     }
   }
 }
@@ -773,13 +749,13 @@ rgms_long_finish_kernel(const int32_t* __restrict__ long_rows, const int32_t* __
     for (int c = c0 + grp; c < c1; c += kGrp) {
 #pragma unroll
       for (int g = 0; g < kF; ++g)
-        acc[g] = add4(acc[g], reinterpret_cast<const float4*>(partial + static_cast<long long>(c) * DOUT)[RS::at(l, g)]);
+        acc[g] = add4(acc[g], reinterpret_cast<const float4*>(partial + static_cast<long long>(c) * DOUT)[g * kL + l]);
     }
     const long long row = __ldg(long_rows + li);
 #pragma unroll
     for (int g = 0; g < kF; ++g) {
       const float4 v = reduce_groups<kL>(acc[g]);
-      if (grp == 0) st_stream4(reinterpret_cast<float4*>(Y + row * DOUT) + RS::at(l, g), v);
+      if (grp == 0) st_stream4(reinterpret_cast<float4*>(Y + row * DOUT) + g * kL + l, v);
     }
   }
 }
