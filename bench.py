@@ -617,6 +617,45 @@ def extra_tensor_core(S, torch, dev, stream, hbm_peak, bf16_peak):
     return out
 
 
+def extra_mtx_ingest(S, torch, dev):
+    """Device Matrix Market ingest: the C5 graph (61.9 M entries, values
+    1..9 as the reference writer prints them) as text in host memory -> strata_mtx_parse
+    (newline scan + per-line parse on the GPU) -> strata_csr_from_coo; wall clock, warm."""
+    m = S.generate_matrix("powerlaw", 2449029, 2449029, 0, 0, 0, 25.3, 1)
+    # entry lines "RRRRRRR CCCCCCC V\n": 7-digit zero-padded indices (istream reads leading
+    # zeros as the same integer), built with vectorised digit arithmetic
+    rows = np.repeat(np.arange(m.rows, dtype=np.int64), np.diff(m.indptr)) + 1
+    cols = m.indices.astype(np.int64) + 1
+    lines = np.empty((m.nnz, 18), np.uint8)
+    for k in range(7):
+        p10 = 10 ** (6 - k)
+        lines[:, k] = (rows // p10) % 10 + 48
+        lines[:, 8 + k] = (cols // p10) % 10 + 48
+    lines[:, 7] = lines[:, 15] = 32
+    lines[:, 16] = m.values.astype(np.int64) % 10 + 48
+    lines[:, 17] = 10
+    del rows, cols
+    text = (f"%%MatrixMarket matrix coordinate real general\n{m.rows} {m.cols} {m.nnz}\n".encode()
+            + lines.tobytes())
+    del lines
+    out = {"bytes": len(text), "entries": m.nnz}
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        mm = S.read_matrix_market(text)
+        t1 = time.perf_counter()
+        csr = mm.to_csr(dev)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        ok = bool(torch.equal(csr.indptr.cpu(), torch.from_numpy(m.indptr))) and \
+            bool(torch.equal(csr.indices.cpu(), torch.from_numpy(m.indices)))
+        del mm, csr
+    out.update({"parse_ms": round((t1 - t0) * 1e3, 1), "csr_ms": round((t2 - t1) * 1e3, 1),
+                "parse_gbs": round(len(text) / (t1 - t0) / 1e9, 2), "csr_equals_generator": ok,
+                "note": "text in pageable host memory: the H2D copy of the entry region is inside"})
+    return out
+
+
 def extra_c1_same_config(S, torch, dev, stream):
     """BASELINE configs[0] (C1) end to end on both executors, same workload, same operands:
     power-law 65,536 nodes, avg 16, seed 1 (1,048,664 nnz), hyb:c=1 (k=5), d = 32, X from the
@@ -904,6 +943,10 @@ def run_ours(args):
             extra["c1_same_config"] = extra_c1_same_config(S, torch, dev, stream)
         except Exception as e:  # informational only
             extra["c1_error"] = str(e)
+        try:
+            extra["c5_mtx_ingest"] = extra_mtx_ingest(S, torch, dev)
+        except Exception as e:  # informational only
+            extra["mtx_error"] = str(e)
     if rank == 0 and not args.no_cpu_baseline:  # every N: the other ranks wait at the barrier
         try:
             cpu = cpu_baseline_single(m, d)
