@@ -56,6 +56,19 @@ def test_sharded_spmm_sddmm_world1(cuda, comm1, chunks, use_comm):
     assert torch.equal(B, S.sddmm(dm, Xs, Yd))
 
 
+@pytest.mark.parametrize("c,k", [(2, 3), (3, 1)])
+def test_sharded_column_partitions(cuda, comm1, c, k):
+    """Chunks decomposed with c > 1 column partitions (f64 partition accumulation per chunk)
+    and small k (split rows): the sharded SpMM equals the single-GPU hyb(c, k) SpMM bitwise."""
+    m = S.generate_matrix("powerlaw", 9000, 8000, 0, 0, 0, 15.0, 2)
+    dm = m.to_device(cuda)
+    plan = ShardPlan(dm, 0, 1, chunks=3, c=c, k=k)
+    X = torch.from_numpy(S.dense_int((m.cols, 64), 7)).to(cuda)
+    Y = torch.full((m.rows, 64), float("nan"), device=cuda)
+    plan.spmm(X, Y, comm1)
+    assert torch.equal(Y, S.spmm(S.decompose_hyb(dm, c, k), X))
+
+
 def test_sharded_errors(cuda, comm1):
     m = S.generate_matrix("powerlaw", 3000, 3000, 0, 0, 0, 6.0, 2)
     dm = m.to_device(cuda)

@@ -241,6 +241,14 @@ def test_rgms_hyb_parts_equal_csr_plan(cuda, c, k):
         dst, src, a = rel.dst[lo:hi], rel.src[lo:hi], rel.A[lo:hi]
         indptr = np.r_[0, np.cumsum(np.bincount(dst, minlength=rel.rows))].astype(np.int32)
         slices.append(S.CsrMatrix(rel.rows, rel.cols, indptr, src.astype(np.int32), a.astype(np.float32)))
+    # relation 3 emptied: a hyb with no parts, and its edges gone from the CSR reference too
+    lo3, hi3 = int(rel.rel_ptr[3]), int(rel.rel_ptr[4])
+    slices[3] = S.CsrMatrix(rel.rows, rel.cols, np.zeros(rel.rows + 1, np.int32),
+                            np.zeros(0, np.int32), np.zeros(0, np.float32))
+    keep = np.r_[np.arange(0, lo3), np.arange(hi3, rel.nnz)]
+    rel = S.RelSparse(7, rel.rows, rel.cols,
+                      np.r_[rel.rel_ptr[:4], rel.rel_ptr[4:] - (hi3 - lo3)].astype(np.int32),
+                      rel.dst[keep], rel.src[keep], rel.A[keep])
     hybs = [S.decompose_hyb(sl.to_device(cuda), c, k) for sl in slices]
     X = bf16(torch.from_numpy(S.dense_int((rel.cols, 32), 4)).to(cuda))
     W = bf16(torch.from_numpy(S.dense_int((7, 32, 32), 5)).to(cuda))
