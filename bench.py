@@ -350,9 +350,41 @@ def load_traffic(key):
     return None
 
 
+def load_l2_peak():
+    """Measured L2 read bandwidth (GB/s) of this B200 model: tools/peaks.cu (256-bit loads over
+    an L2-resident buffer, every SM), committed as profiles/peaks.json.  None when absent."""
+    p = os.path.join(ROOT, "profiles", "peaks.json")
+    try:
+        return float(json.load(open(p))["l2_read_peak_gbs"])
+    except Exception:
+        return None
+
+
+def copy_bound_ms(torch, dev, host_in, host_out, reps=3):
+    """The e2e path's floor on this box: the same pinned H2D and D2H byte counts issued
+    concurrently on two streams (what strata_spmm_hyb_f32_host_batch overlaps), wall clock,
+    best of `reps`."""
+    d_in = torch.empty(host_in.shape, dtype=host_in.dtype, device=dev)
+    d_out = torch.zeros(host_out.shape, dtype=host_out.dtype, device=dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = float("inf")
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            d_in.copy_(host_in, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            host_out.copy_(d_out, non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, (time.perf_counter() - t0) * 1e3)
+    del d_in, d_out
+    return best
+
+
 def extra_reddit(S, torch, dev, stream, peak):
     """C2 (Reddit shape): hyb SpMM and CSR SDDMM, device-timed (informational)."""
     cfg = REDDIT
+    l2_peak = load_l2_peak()
     m = S.generate_matrix(cfg["kind"], cfg["n"], cfg["m"], 0, 0, 0, cfg["avg"], cfg["seed"])
     d = cfg["d"]
     dcsr = m.to_device(dev)
@@ -382,6 +414,8 @@ def extra_reddit(S, torch, dev, stream, peak):
         out[name] = {"ms": round(ms, 4), "gflops": round(flops / (ms * 1e-3) / 1e9, 2),
                      "b_alg_gbs": round(gbs, 1), "frac_of_hbm": round(gbs / peak, 3),
                      "note": "X is L2-resident (59.6 MB < 126 MB L2): frac is L2-assisted"}
+        if l2_peak:  # the gathers' real ceiling: measured L2 read bandwidth
+            out[name]["frac_of_l2_peak"] = round(gbs / l2_peak, 3)
     out["reddit_nnz"] = m.nnz
     # Fused SDDMM -> edge softmax -> SpMM (GAT-style layer step), d = 64.
     plan = S.AttentionPlan(dcsr)
@@ -395,6 +429,10 @@ def extra_reddit(S, torch, dev, stream, peak):
         "ms": round(ms_a, 4), "gflops": round(4.0 * m.nnz * d / (ms_a * 1e-3) / 1e9, 1),
         "b_alg_gbs": round(b_a / (ms_a * 1e-3) / 1e9, 1),
         "note": "one pass (online softmax); K, V rows gathered per edge, L2-resident at C2"}
+    if l2_peak:
+        out["reddit_fused_attention"]["frac_of_l2_peak"] = round(b_a / (ms_a * 1e-3) / 1e9 / l2_peak, 3)
+    if l2_peak:
+        out["l2_read_peak_gbs"] = {"value": l2_peak, "source": "profiles/peaks.json (tools/peaks.cu)"}
     # The reference tuner's c-grid (tune.cpp:19-36) on the device: csr + hyb(c in 1..16) timed,
     # gated bitwise against the CSR format on integer operands.
     from paper_2207_04606_b200 import tune as T
@@ -901,10 +939,15 @@ def run_ours(args):
     t0 = time.perf_counter()
     S.spmm_host(h_e2e, Xh[0], Yh[0], stream=stream)
     single_ms = (time.perf_counter() - t0) * 1e3
+    floor_ms = copy_bound_ms(torch, dev, Xh[0], Yh[1])
     e2e = {"value": round(flops / float(te[0]) / 1e9, 3), "unit": "GFLOP/s",
            "h2d_bytes_per_step": int(Xh[0].numel() * 4), "d2h_bytes_per_step": int(Yh[0].numel() * 4),
            "ms_per_step": round(float(te[0]) * 1e3, 3), "steps": e2e_steps,
            "single_call_ms": round(single_ms, 3),
+           "copy_bound_ms": round(floor_ms, 3),
+           "frac_of_copy_bound": round(floor_ms / (float(te[0]) * 1e3), 4),
+           "copy_bound_note": "the same pinned H2D + D2H bytes issued concurrently on two "
+                              "streams, no compute (the link's bidirectional floor)",
            "path": "strata_spmm_hyb_f32_host_batch (pinned host X in, host Y rows out, per "
                    "step; copy-in/compute/copy-out pipelined across steps, wall clock)"}
     del Xh, Yh

@@ -361,45 +361,32 @@ int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_ho
       if (H.stage_x[k].n < xn) H.stage_x[k].alloc(xn);
       if (H.stage_y[k].n < yn) H.stage_y[k].alloc(yn);
     }
-    cudaStream_t cin = nullptr, cout = nullptr;
-    cudaEvent_t ev[9] = {};  // entry, x_ready[2], x_free[2], y_ready[2], y_free[2]
-    auto cleanup = [&] {
-      for (auto& e : ev) if (e) cudaEventDestroy(e);
-      if (cin) cudaStreamDestroy(cin);
-      if (cout) cudaStreamDestroy(cout);
-    };
-    try {
-      STRATA_CUDA_CHECK(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-      STRATA_CUDA_CHECK(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
-      for (auto& e : ev) STRATA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      cudaEvent_t entry = ev[0], *x_ready = ev + 1, *x_free = ev + 3, *y_ready = ev + 5,
-                  *y_free = ev + 7;
-      STRATA_CUDA_CHECK(cudaEventRecord(entry, s));  // everything follows prior work on `s`
-      STRATA_CUDA_CHECK(cudaStreamWaitEvent(cin, entry, 0));
-      STRATA_CUDA_CHECK(cudaStreamWaitEvent(cout, entry, 0));
-      for (int64_t b = 0; b < nbatch; ++b) {
-        const int k = static_cast<int>(b % nslots);
-        float* sx = H.stage_x[k].p;
-        float* sy = H.stage_y[k].p;
-        if (b >= nslots) STRATA_CUDA_CHECK(cudaStreamWaitEvent(cin, x_free[k], 0));
-        if (xn) STRATA_CUDA_CHECK(cudaMemcpyAsync(sx, X_host[b], xn * 4, cudaMemcpyHostToDevice, cin));
-        STRATA_CUDA_CHECK(cudaEventRecord(x_ready[k], cin));
-        STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, x_ready[k], 0));
-        if (b >= nslots) STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, y_free[k], 0));
-        spmm_hyb_launch(H, sx, &sy, 1, d, s);
-        STRATA_CUDA_CHECK(cudaEventRecord(x_free[k], s));
-        STRATA_CUDA_CHECK(cudaEventRecord(y_ready[k], s));
-        STRATA_CUDA_CHECK(cudaStreamWaitEvent(cout, y_ready[k], 0));
-        if (yn) STRATA_CUDA_CHECK(cudaMemcpyAsync(Y_host[b], sy, yn * 4, cudaMemcpyDeviceToHost, cout));
-        STRATA_CUDA_CHECK(cudaEventRecord(y_free[k], cout));
-      }
-      STRATA_CUDA_CHECK(cudaStreamSynchronize(cout));
-      STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
-    } catch (...) {
-      cleanup();
-      throw;
+    H.e2e.ensure();
+    cudaStream_t cin = H.e2e.cin, cout = H.e2e.cout;
+    cudaEvent_t* ev = H.e2e.ev;
+    cudaEvent_t entry = ev[0], *x_ready = ev + 1, *x_free = ev + 3, *y_ready = ev + 5,
+                *y_free = ev + 7;
+    STRATA_CUDA_CHECK(cudaEventRecord(entry, s));  // everything follows prior work on `s`
+    STRATA_CUDA_CHECK(cudaStreamWaitEvent(cin, entry, 0));
+    STRATA_CUDA_CHECK(cudaStreamWaitEvent(cout, entry, 0));
+    for (int64_t b = 0; b < nbatch; ++b) {
+      const int k = static_cast<int>(b % nslots);
+      float* sx = H.stage_x[k].p;
+      float* sy = H.stage_y[k].p;
+      if (b >= nslots) STRATA_CUDA_CHECK(cudaStreamWaitEvent(cin, x_free[k], 0));
+      if (xn) STRATA_CUDA_CHECK(cudaMemcpyAsync(sx, X_host[b], xn * 4, cudaMemcpyHostToDevice, cin));
+      STRATA_CUDA_CHECK(cudaEventRecord(x_ready[k], cin));
+      STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, x_ready[k], 0));
+      if (b >= nslots) STRATA_CUDA_CHECK(cudaStreamWaitEvent(s, y_free[k], 0));
+      spmm_hyb_launch(H, sx, &sy, 1, d, s);
+      STRATA_CUDA_CHECK(cudaEventRecord(x_free[k], s));
+      STRATA_CUDA_CHECK(cudaEventRecord(y_ready[k], s));
+      STRATA_CUDA_CHECK(cudaStreamWaitEvent(cout, y_ready[k], 0));
+      if (yn) STRATA_CUDA_CHECK(cudaMemcpyAsync(Y_host[b], sy, yn * 4, cudaMemcpyDeviceToHost, cout));
+      STRATA_CUDA_CHECK(cudaEventRecord(y_free[k], cout));
     }
-    cleanup();
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(cout));
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
   });
 }
 

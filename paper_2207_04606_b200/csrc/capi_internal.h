@@ -180,6 +180,24 @@ struct strata_hyb_impl {
   // pool for each SpMM, so one handle may serve several streams / threads at once.
   mutable std::mutex stage_mu;                   // guards the e2e staging buffers below
   mutable DevBuf<float> stage_x[2], stage_y[2];  // e2e staging (double-buffered)
+  // The e2e path's copy streams and hand-off events, made on first use and kept with the
+  // handle (creating them per call cost more than a C1-sized copy).
+  struct E2eSync {
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t ev[9] = {};  // entry, x_ready[2], x_free[2], y_ready[2], y_free[2]
+    void ensure() {
+      if (!cin) STRATA_CUDA_CHECK(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+      if (!cout) STRATA_CUDA_CHECK(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+      for (auto& e : ev)
+        if (!e) STRATA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    ~E2eSync() {
+      for (auto& e : ev) if (e) cudaEventDestroy(e);
+      if (cin) cudaStreamDestroy(cin);
+      if (cout) cudaStreamDestroy(cout);
+    }
+  };
+  mutable E2eSync e2e;  // guarded by stage_mu
 };
 
 // Kernel launchers (defined in .cu files).

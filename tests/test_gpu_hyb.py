@@ -159,6 +159,55 @@ def test_spmm_x_16_byte_aligned(cuda, d):
     assert np.array_equal(ya, port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, X.cpu().numpy()))
 
 
+def special_x(shape, seed):
+    """Integer operand with IEEE specials planted: +-inf, NaN, -0, f32 subnormals (the kernels'
+    integer-pipe f32 -> f64 conversion must route inf / NaN to the F2F path and keep subnormals
+    exact)."""
+    X = S.dense_int(shape, seed)
+    r = np.random.default_rng(seed)
+    rows = r.choice(shape[0], size=min(shape[0], 40), replace=False)
+    kinds = [np.inf, -np.inf, np.nan, -0.0, 1e-40, -3e-42, 2 ** -149]
+    for q, i in enumerate(rows):
+        X[i, r.integers(shape[1])] = kinds[q % len(kinds)]
+    X[rows[-1], :] = np.float32(1.5e-39)  # a whole subnormal row
+    return X
+
+
+def check_special(got, want32, want64):
+    """Non-finite outputs exactly where the reference F32 pipeline has them (NaN, and inf with
+    its sign); every finite output within the strict 1e-5 bar of the F64 pipeline (the f32
+    reference rounds each partial sum, which in the subnormal range is coarser than our single
+    rounding of the exact sum)."""
+    assert np.array_equal(np.isnan(got), np.isnan(want32))
+    inf = np.isinf(want32)
+    assert np.array_equal(np.isinf(got), inf) and np.array_equal(got[inf], want32[inf])
+    fin = np.isfinite(want32)
+    assert close_to_f64(got[fin], want64[fin])
+    return True
+
+
+@pytest.mark.parametrize("d", [32, 64, 128, 256])
+@pytest.mark.parametrize("c", [1, 2])
+def test_spmm_nonfinite_and_subnormal_x(cuda, d, c):
+    """inf / NaN in X propagate as in the reference's sums (IEEE); -0 and subnormals exact;
+    integer rows bitwise.  (Pad slots are skipped, not multiplied by 0: a non-finite x at a
+    padded column yields the CSR result, where the reference's hyb nest would give 0 * inf =
+    NaN, storage.cpp:528 / kernels.cpp:85-108.)"""
+    import torch
+    m = S.generate_matrix("powerlaw", 3000, 2500, 0, 0, 0, 18.0, 4)
+    X = special_x((m.cols, d), 11)
+    with np.errstate(invalid="ignore", over="ignore"):
+        want = port.spmm_csr_refnum(m.rows, m.indptr, m.indices, m.values, X)
+        want64 = port.spmm_csr_f64(m.rows, m.indptr, m.indices, m.values, X)
+    assert np.isnan(want).any() and np.isinf(want).any()
+    dm = m.to_device(cuda)
+    for k in (S.hyb_auto_k(m), 1):
+        got = S.spmm(S.decompose_hyb(dm, c, k), torch.from_numpy(X).to(cuda)).cpu().numpy()
+        assert check_special(got, want, want64), (d, c, k)
+    got = S.spmm_csr(dm, torch.from_numpy(X).to(cuda)).cpu().numpy()
+    assert check_special(got, want, want64), d
+
+
 def test_spmm_long_split_rows_deterministic(cuda):
     """Rows far above 2^k split into many bucket-k segments spanning many chunks (the
     carry + fix-up path); results must be exact on integer data and bitwise reproducible."""

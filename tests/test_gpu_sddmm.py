@@ -7,7 +7,7 @@ import pytest
 import paper_2207_04606_b200 as S
 from oracle import port
 
-from test_gpu_hyb import close_to_f64, csr_of
+from test_gpu_hyb import check_special, close_to_f64, csr_of, special_x
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.npz")
@@ -42,6 +42,24 @@ def test_sddmm_integer_exact(cuda, d):
     got = S.sddmm(m.to_device(cuda), torch.from_numpy(X).to(cuda),
                   torch.from_numpy(Yd).to(cuda)).cpu().numpy()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("d", [32, 64, 128, 16])
+def test_sddmm_nonfinite_and_subnormal(cuda, d):
+    """inf / NaN / -0 / subnormals in X and Y: the gathered-Y integer-pipe conversion falls back
+    to F2F for a group holding a non-finite value; specials where the oracle has them, finite
+    values within 1e-5 of the F64 pipeline."""
+    import torch
+    m = S.generate_matrix("powerlaw", 3000, 2600, 0, 0, 0, 25.0, 3)
+    X = special_x((m.rows, d), 5)
+    Yd = np.ascontiguousarray(special_x((m.cols, d), 6).T)
+    with np.errstate(invalid="ignore", over="ignore"):
+        want = port.sddmm_csr_refnum(m.rows, m.cols, m.indptr, m.indices, m.values, X, Yd)
+        want64 = port.sddmm_csr_f64(m.rows, m.cols, m.indptr, m.indices, m.values, X, Yd)
+    assert np.isnan(want).any() and np.isinf(want).any()
+    got = S.sddmm(m.to_device(cuda), torch.from_numpy(X).to(cuda),
+                  torch.from_numpy(Yd).to(cuda)).cpu().numpy()
+    assert check_special(got, want, want64)
 
 
 @pytest.mark.parametrize("seed", range(8))
