@@ -32,6 +32,9 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kNnzPerChunk = 256;
+// SDDMM non-zeros per virtual warp: 256, halved for 4-lane VWs so the staged indices / values of
+// a CTA's 64 VWs stay at 64 KB of shared memory.
+__host__ __device__ constexpr int sddmm_chunk(int L) { return L >= 8 ? kNnzPerChunk : kNnzPerChunk / 2; }
 constexpr long long kCsrLong = 2048;  // row-split CSR SpMM: longer rows are chunked
 constexpr long long kCsrChunk = 256;  // non-zeros per chunk of a long row
 constexpr long long kCsrGroup = 64;   // chunk partials summed per level-1 group
@@ -71,8 +74,18 @@ __device__ __forceinline__ T reduce_scatter(T (&v)[L], int lane, unsigned mask) 
 #ifndef STRATA_SDDMM_F64  // A/B knob: 1 = f64 dot products (default), 0 = f32
 #define STRATA_SDDMM_F64 1
 #endif
-#ifndef STRATA_SDDMM_VEC64  // A/B knob: d = 64 as 8 lanes x 256-bit slices (2) or 16 x 128-bit (1)
-#define STRATA_SDDMM_VEC64 1  // (2 measured 7.93 vs 4.12 ms at C2: 8-non-zero groups halve the work per reduce-scatter)
+// A/B knobs: float4s per lane (VEC) for d = 32 / 64 / 128; lanes per non-zero L = d / (4 VEC).
+// C2 graph (114.6M nnz), VEC = 2 everywhere (256-bit gathers, U = 4 in flight, 2 CTAs/SM):
+//   d = 32: 4 lanes 1.89 -> 1.71 ms; d = 64: 8 lanes 4.12 -> 3.21 ms (at U = 8 it needed 170
+//   registers, 1 CTA/SM: 7.93 ms); d = 128: 16 lanes 17.20 -> 7.30 ms.  VEC = 4 spills.
+#ifndef STRATA_SDDMM_VEC32
+#define STRATA_SDDMM_VEC32 2
+#endif
+#ifndef STRATA_SDDMM_VEC64
+#define STRATA_SDDMM_VEC64 2
+#endif
+#ifndef STRATA_SDDMM_VEC128
+#define STRATA_SDDMM_VEC128 2
 #endif
 
 // Dot-product numerics.  The reference accumulates sum_k A*X*Y in f64 and rounds each partial
@@ -116,31 +129,36 @@ struct YSlice {
   float4 v[VEC];
 };
 
+#ifndef STRATA_SDDMM_U2  // gathers in flight per lane for the 256-bit variant (A/B knob)
+#define STRATA_SDDMM_U2 4
+#endif
+
 template <int L, int VEC = 1, bool kF64 = STRATA_SDDMM_F64>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, VEC > 1 ? 2 : 1)
 sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
              const float* __restrict__ A, const float* __restrict__ X,
              const float* __restrict__ Yt, float* __restrict__ B, long long rows, long long nnz,
              long long d) {
   using T = typename DotT<kF64>::T;
   using YV = YSlice<VEC>;
-  constexpr int U = 8;
+  constexpr int U = VEC > 1 ? STRATA_SDDMM_U2 : 8;  // (VEC = 2, U = 8 needed 170 registers: 1 CTA/SM)
   const int wl = threadIdx.x & 31;
   const int lane = threadIdx.x & (L - 1);
   const int vbase = wl & ~(L - 1);
   const unsigned vmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << vbase);
   const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
-  const long long e0 = vw * kNnzPerChunk;
+  constexpr int kChunk = sddmm_chunk(L);
+  const long long e0 = vw * kChunk;
   if (e0 >= nnz) return;
-  const int ne = static_cast<int>(min64(kNnzPerChunk, nnz - e0));
+  const int ne = static_cast<int>(min64(kChunk, nnz - e0));
 
   // Stage the chunk's column indices and A values in this VW's shared-memory slice (one
   // memory round trip; read back as broadcasts, no per-non-zero shuffles).
   extern __shared__ int4 sddmm_smem[];
-  int32_t* sJ = reinterpret_cast<int32_t*>(sddmm_smem) + (threadIdx.x / L) * (2 * kNnzPerChunk);
-  float* sA = reinterpret_cast<float*>(sJ + kNnzPerChunk);
-  if (ne == kNnzPerChunk) {
-    for (int q = lane; q < kNnzPerChunk / 4; q += L) {
+  int32_t* sJ = reinterpret_cast<int32_t*>(sddmm_smem) + (threadIdx.x / L) * (2 * kChunk);
+  float* sA = reinterpret_cast<float*>(sJ + kChunk);
+  if (ne == kChunk) {
+    for (int q = lane; q < kChunk / 4; q += L) {
       ::strata_b200::tc::cp_async16(sJ + 4 * q, indices + e0 + 4 * q);
       ::strata_b200::tc::cp_async16(sA + 4 * q, A + e0 + 4 * q);
     }
@@ -177,11 +195,13 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   auto gather_y = [&](int col) -> YV {
     YV y;
     const float4* p = Y4 + static_cast<long long>(col) * d4;
-    if constexpr (VEC == 2) {  // Yt is the call's own 256-byte aligned workspace
-      asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                   : "=f"(y.v[0].x), "=f"(y.v[0].y), "=f"(y.v[0].z), "=f"(y.v[0].w),
-                     "=f"(y.v[1].x), "=f"(y.v[1].y), "=f"(y.v[1].z), "=f"(y.v[1].w)
-                   : "l"(p));
+    if constexpr (VEC % 2 == 0) {  // Yt is the call's own 256-byte aligned workspace
+#pragma unroll
+      for (int i = 0; i < VEC; i += 2)
+        asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=f"(y.v[i].x), "=f"(y.v[i].y), "=f"(y.v[i].z), "=f"(y.v[i].w),
+                       "=f"(y.v[i + 1].x), "=f"(y.v[i + 1].y), "=f"(y.v[i + 1].z), "=f"(y.v[i + 1].w)
+                     : "l"(p + i));
     } else {
 #pragma unroll
       for (int i = 0; i < VEC; ++i) y.v[i] = ld_gather4(p + i);
@@ -447,27 +467,29 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
   const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0;
-  const long long chunks = (nnz + kNnzPerChunk - 1) / kNnzPerChunk;
   auto blocks_for = [&](int L) {
+    const long long chunks = (nnz + sddmm_chunk(L) - 1) / sddmm_chunk(L);
     return static_cast<unsigned>((chunks * L + kBlock - 1) / kBlock);
   };
-  // per virtual warp: column indices + A values of one chunk (2 KB)
-  auto smem_for = [&](int L) { return (kBlock / L) * 2 * kNnzPerChunk * 4; };
+  // per virtual warp: column indices + A values of one chunk (2 KB; 1 KB for 4-lane VWs)
+  auto smem_for = [&](int L) { return (kBlock / L) * 2 * sddmm_chunk(L) * 4; };
   const bool staged = aligned && reinterpret_cast<uintptr_t>(indices) % 16 == 0 &&
                       reinterpret_cast<uintptr_t>(A) % 16 == 0;
-  static PerDeviceOnce once;  // 8 lanes per VW (d = 32, and d = 64 in 256-bit slices): 64 KB
+  // Lanes per non-zero: each lane owns 4 * VEC consecutive features (256-bit gathers for VEC >= 2)
+  // so a non-zero's dot is reduced across L = d / (4 VEC) lanes; fewer lanes, fewer reduce steps.
+  constexpr int v32 = STRATA_SDDMM_VEC32, v64 = STRATA_SDDMM_VEC64, v128 = STRATA_SDDMM_VEC128;
+  static PerDeviceOnce once;  // VWs of <= 8 lanes stage 64 KB per CTA
   once([&] {
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8)));
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8)));
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<32 / (4 * v32), v32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(32 / (4 * v32))));
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<64 / (4 * v64), v64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(64 / (4 * v64))));
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<128 / (4 * v128), v128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(128 / (4 * v128))));
   });
-  if (staged && d == 32)
-    sddmm_kernel<8><<<blocks_for(8), kBlock, smem_for(8), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
-  else if (staged && d == 64 && STRATA_SDDMM_VEC64 == 2)
-    sddmm_kernel<8, 2><<<blocks_for(8), kBlock, smem_for(8), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
-  else if (staged && d == 64)
-    sddmm_kernel<16><<<blocks_for(16), kBlock, smem_for(16), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
-  else if (staged && d == 128)
-    sddmm_kernel<32><<<blocks_for(32), kBlock, smem_for(32), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  auto run = [&](auto kern, int L) {
+    kern<<<blocks_for(L), kBlock, smem_for(L), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  };
+  if (staged && d == 32) run(sddmm_kernel<32 / (4 * v32), v32>, 32 / (4 * v32));
+  else if (staged && d == 64) run(sddmm_kernel<64 / (4 * v64), v64>, 64 / (4 * v64));
+  else if (staged && d == 128) run(sddmm_kernel<128 / (4 * v128), v128>, 128 / (4 * v128));
   else {
     const unsigned blocks = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, 148 * 32));
     sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);

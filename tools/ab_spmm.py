@@ -40,6 +40,10 @@ def main():
             Yd = torch.randint(-3, 4, (d, m.cols), device=dev, dtype=torch.float32)
             B = torch.empty((m.nnz,), device=dev)
             out["C2_sddmm_ms"] = round(timeit(lambda: S.sddmm(dcsr, Xs, Yd, B)), 4)
+            for dd in (32, 128):
+                Xs = torch.randint(-3, 4, (m.rows, dd), device=dev, dtype=torch.float32)
+                Yd = torch.randint(-3, 4, (dd, m.cols), device=dev, dtype=torch.float32)
+                out[f"C2_sddmm_d{dd}_ms"] = round(timeit(lambda: S.sddmm(dcsr, Xs, Yd, B)), 4)
         del h, X, Y, dcsr
         torch.cuda.empty_cache()
     # dense transform of the GNN layer at C5 shape (strata_gemm_f32, 3xTF32 tcgen05)
