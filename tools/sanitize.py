@@ -31,11 +31,12 @@ if want("hyb"):  # spmm_hyb_kernel (cp.async staging) + split-run fix-up, c = 1 
 
 if want("sddmm"):
     m = S.generate_matrix("powerlaw", 2000, 2100, 0, 0, 0, 10.0, 5)
-    Xs = torch.from_numpy(S.dense_int((m.rows, 64), 2)).to(dev)
-    Yd = torch.from_numpy(S.dense_int((64, m.cols), 3)).to(dev)
-    B = S.sddmm(m.to_device(dev), Xs, Yd).cpu().numpy()
-    assert np.array_equal(B, port.sddmm_csr_refnum(m.rows, m.cols, m.indptr, m.indices, m.values,
-                                                   Xs.cpu().numpy(), Yd.cpu().numpy()))
+    for d in (32, 64, 128):  # 4-, 8- and 16-lane 256-bit variants
+        Xs = torch.from_numpy(S.dense_int((m.rows, d), 2)).to(dev)
+        Yd = torch.from_numpy(S.dense_int((d, m.cols), 3)).to(dev)
+        B = S.sddmm(m.to_device(dev), Xs, Yd).cpu().numpy()
+        assert np.array_equal(B, port.sddmm_csr_refnum(m.rows, m.cols, m.indptr, m.indices, m.values,
+                                                       Xs.cpu().numpy(), Yd.cpu().numpy()))
     print("sddmm ok")
 
 if want("bsr"):  # tcgen05 + TMA BSR SpMM (PDL launch) and the block-sparse SDDMM
