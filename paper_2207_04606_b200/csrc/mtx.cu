@@ -28,8 +28,10 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <mutex>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "capi_internal.h"
@@ -408,6 +410,85 @@ long long read_preamble(const char* text, long long bytes, bool& pattern, bool& 
   return p;
 }
 
+// Host text -> device for large pageable buffers: host threads copy 32 MB chunks into a ring of
+// pinned buffers (two sets of kStageThreads) while the copy engine drains the other set, so the
+// transfer runs at the threads' memcpy rate overlapped with DMA instead of the driver's
+// single-threaded pageable staging (C5 text, 1.1 GB: ~100 ms pageable).  The ring is allocated
+// once per process (portable pinned memory) and serialised by a mutex.
+constexpr int kStageThreads = 4;
+constexpr size_t kStageChunk = size_t(32) << 20;
+
+struct StageRing {
+  std::mutex mu;
+  char* buf[2 * kStageThreads] = {};
+  bool ok = false, tried = false;
+  bool ensure() {
+    if (tried) return ok;
+    tried = true;
+    for (int i = 0; i < 2 * kStageThreads; ++i) {
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, kStageChunk, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return ok = false;
+      }
+      buf[i] = static_cast<char*>(p);
+    }
+    return ok = true;
+  }
+};
+
+StageRing& stage_ring() {
+  static StageRing* r = new StageRing;  // process lifetime (no teardown-order CUDA calls)
+  return *r;
+}
+
+void copy_text_h2d(uint8_t* dst, const char* src, long long n, cudaStream_t s) {
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  StageRing& R = stage_ring();
+  std::unique_lock<std::mutex> lock(R.mu);
+  // small, already page-locked (strata_mtx_read_file's buffer) or no pinned memory: one copy
+  if (pinned || n < static_cast<long long>(4 * kStageChunk) || !R.ensure()) {
+    lock.unlock();
+    STRATA_CUDA_CHECK(cudaMemcpyAsync(dst, src, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+    return;
+  }
+  cudaEvent_t ev[2 * kStageThreads];
+  for (auto& e : ev) STRATA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const long long nchunks = (n + static_cast<long long>(kStageChunk) - 1) / static_cast<long long>(kStageChunk);
+  bool used[2 * kStageThreads] = {};
+  try {
+    for (long long w = 0; w * kStageThreads < nchunks; ++w) {
+      const int set = static_cast<int>(w & 1) * kStageThreads;
+      const long long c0 = w * kStageThreads;
+      const int nc = static_cast<int>(std::min<long long>(kStageThreads, nchunks - c0));
+      for (int t = 0; t < nc; ++t)  // the set's previous DMA must have drained
+        if (used[set + t]) STRATA_CUDA_CHECK(cudaEventSynchronize(ev[set + t]));
+      std::thread th[kStageThreads];
+      for (int t = 0; t < nc; ++t) {
+        const long long o = (c0 + t) * static_cast<long long>(kStageChunk);
+        const size_t len = static_cast<size_t>(std::min<long long>(kStageChunk, n - o));
+        th[t] = std::thread([&R, set, t, src, o, len] { std::memcpy(R.buf[set + t], src + o, len); });
+      }
+      for (int t = 0; t < nc; ++t) th[t].join();
+      for (int t = 0; t < nc; ++t) {
+        const long long o = (c0 + t) * static_cast<long long>(kStageChunk);
+        const size_t len = static_cast<size_t>(std::min<long long>(kStageChunk, n - o));
+        STRATA_CUDA_CHECK(cudaMemcpyAsync(dst + o, R.buf[set + t], len, cudaMemcpyHostToDevice, s));
+        STRATA_CUDA_CHECK(cudaEventRecord(ev[set + t], s));
+        used[set + t] = true;
+      }
+    }
+    STRATA_CUDA_CHECK(cudaStreamSynchronize(s));  // the ring is free for the next caller
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    for (auto& e : ev) cudaEventDestroy(e);
+    throw;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
 std::string line_at(const char* text, long long bytes, long long start) {
   const void* nl = memchr(text + start, '\n', static_cast<size_t>(bytes - start));
   const long long e = nl ? static_cast<const char*>(nl) - text : bytes;
@@ -430,7 +511,7 @@ void mtx_parse(const char* text, long long bytes, strata_mtx& h, cudaStream_t s)
   if (n <= 0) throw ApiError(STRATA_ERR_USAGE, "truncated matrix market entries");
 
   auto* buf = static_cast<uint8_t*>(workspace_alloc(static_cast<size_t>(n) + 16, s));
-  STRATA_CUDA_CHECK(cudaMemcpyAsync(buf, text + off, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+  copy_text_h2d(buf, text + off, n, s);
   const long long nblk = (n + kBlockBytes - 1) / kBlockBytes;
   auto* cnt = static_cast<long long*>(workspace_alloc(sizeof(long long) * (nblk + 1) * 2, s));
   long long* base = cnt + nblk + 1;
@@ -453,8 +534,14 @@ void mtx_parse(const char* text, long long bytes, strata_mtx& h, cudaStream_t s)
   long long nlines = std::min(nl_total, nnz);
   if (nl_total < nnz && n - (last_nl + 1) > 0) ++nlines;
 
-  DevBuf<int32_t> r(nlines), c(nlines), mult(symmetric ? nlines + 1 : 0);
-  DevBuf<double> v(nlines);
+  // Outputs from the stream-ordered pool (persistent: freed with the handle); cudaMalloc /
+  // cudaFree of ~1 GB per parse cost more than the parse kernels at C5.
+  DevBuf<int32_t> r, c, mult;
+  DevBuf<double> v;
+  r.alloc_async(nlines, s, true);
+  c.alloc_async(nlines, s, true);
+  v.alloc_async(nlines, s, true);
+  if (symmetric) mult.alloc_async(nlines + 1, s, true);
   auto* bad = static_cast<unsigned long long*>(workspace_alloc(sizeof(unsigned long long), s));
   STRATA_CUDA_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
   if (nlines > 0)
@@ -496,26 +583,26 @@ void mtx_parse(const char* text, long long bytes, strata_mtx& h, cudaStream_t s)
     h.col = std::move(c);
     h.v64 = std::move(v);
     h.ntrip = nlines;
-    h.v32.alloc(nlines);
+    h.v32.alloc_async(nlines, s, true);
     to_f32_kernel<<<grid_for(nlines), 256, 0, s>>>(h.v64.p, nlines, h.v32.p);
     STRATA_CUDA_CHECK(cudaGetLastError());
     STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
     return;
   }
-  DevBuf<int32_t> offs(nlines + 1);
+  DevBuf<int32_t> offs(nlines + 1, s);
   STRATA_CUDA_CHECK(cudaMemsetAsync(mult.p + nlines, 0, sizeof(int32_t), s));
   tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, mult.p, offs.p, nlines + 1, s);
-  DevBuf<uint8_t> t2(tb);
+  DevBuf<uint8_t> t2(tb, s);
   cub::DeviceScan::ExclusiveSum(t2.p, tb, mult.p, offs.p, nlines + 1, s);
   int32_t total = 0;
   STRATA_CUDA_CHECK(cudaMemcpyAsync(&total, offs.p + nlines, sizeof(total), cudaMemcpyDeviceToHost, s));
   STRATA_CUDA_CHECK(cudaStreamSynchronize(s));
   h.ntrip = total;
-  h.row.alloc(total);
-  h.col.alloc(total);
-  h.v64.alloc(total);
-  h.v32.alloc(total);
+  h.row.alloc_async(total, s, true);
+  h.col.alloc_async(total, s, true);
+  h.v64.alloc_async(total, s, true);
+  h.v32.alloc_async(total, s, true);
   mtx_mirror_kernel<<<grid_for(nlines), 256, 0, s>>>(r.p, c.p, v.p, offs.p, nlines, h.row.p, h.col.p,
                                                       h.v64.p, h.v32.p);
   STRATA_CUDA_CHECK(cudaGetLastError());
