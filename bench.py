@@ -691,6 +691,22 @@ def extra_mtx_ingest(S, torch, dev):
     out.update({"parse_ms": round((t1 - t0) * 1e3, 1), "csr_ms": round((t2 - t1) * 1e3, 1),
                 "parse_gbs": round(len(text) / (t1 - t0) / 1e9, 2), "csr_equals_generator": ok,
                 "note": "text in pageable host memory: the H2D copy of the entry region is inside"})
+    # read_matrix_market_file (mmio.cpp:57-61): the same text from a file (page cache warm)
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".mtx", delete=False) as f:
+        f.write(text)
+        path = f.name
+    try:
+        for rep in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            mm = S.read_matrix_market_file(path)
+            torch.cuda.synchronize()
+            file_ms = (time.perf_counter() - t0) * 1e3
+            del mm
+        out["file_ms"] = round(file_ms, 1)
+    finally:
+        os.unlink(path)
     return out
 
 

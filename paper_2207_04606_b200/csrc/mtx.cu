@@ -23,6 +23,10 @@
 // build_csr stores for the F32 pipeline, storage.cpp:57-61 / :117), ready for
 // strata_csr_from_coo.
 #include <cub/cub.cuh>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <cfloat>
 #include <cstdio>
@@ -640,23 +644,27 @@ int strata_mtx_parse(const char* text, int64_t bytes, strata_mtx** out, void* st
 int strata_mtx_read_file(const char* path, strata_mtx** out, void* stream) {
   return guarded([&] {
     if (!out || !path) throw ApiError(STRATA_ERR_USAGE, "null argument");
-    std::ifstream f(path, std::ios::binary);
-    if (!f) throw ApiError(STRATA_ERR_USAGE, std::string("cannot open ") + path);  // mmio.cpp:59
-    f.seekg(0, std::ios::end);
-    const long long bytes = static_cast<long long>(f.tellg());
-    f.seekg(0, std::ios::beg);
-    // Pinned staging so the entry region reaches HBM at full PCIe rate (pageable memory where
-    // no device is present: only the host-side preamble errors can be produced then).
-    char* pinned = nullptr;
-    std::vector<char> pageable;
-    if (cudaMallocHost(&pinned, static_cast<size_t>(std::max(bytes, 1ll))) != cudaSuccess) {
-      cudaGetLastError();
-      pinned = nullptr;
-      pageable.resize(static_cast<size_t>(std::max(bytes, 1ll)));
+    // The file is mapped, not read: the page cache is the host copy (a fresh 1 GB read buffer
+    // cost ~0.3 s of first-touch page faults alone), and mtx_parse's staging threads fault the
+    // mapped pages in parallel while they copy them to pinned buffers.
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) throw ApiError(STRATA_ERR_USAGE, std::string("cannot open ") + path);  // mmio.cpp:59
+    struct stat st {};
+    if (fstat(fd, &st) != 0) {
+      close(fd);
+      throw ApiError(STRATA_ERR_USAGE, std::string("cannot open ") + path);
     }
-    std::unique_ptr<char, cudaError_t (*)(void*)> hold(pinned, cudaFreeHost);
-    char* text = pinned ? pinned : pageable.data();
-    if (bytes > 0 && !f.read(text, bytes)) throw ApiError(STRATA_ERR_USAGE, std::string("cannot open ") + path);
+    const long long bytes = static_cast<long long>(st.st_size);
+    void* map = bytes > 0 ? mmap(nullptr, static_cast<size_t>(bytes), PROT_READ, MAP_PRIVATE, fd, 0) : nullptr;
+    close(fd);
+    if (bytes > 0 && map == MAP_FAILED) throw ApiError(STRATA_ERR_USAGE, std::string("cannot open ") + path);
+    if (map) madvise(map, static_cast<size_t>(bytes), MADV_SEQUENTIAL);
+    struct Unmap {
+      void* p;
+      size_t n;
+      ~Unmap() { if (p) munmap(p, n); }
+    } hold{map, static_cast<size_t>(bytes)};
+    const char* text = static_cast<const char*>(map);
     auto h = std::make_unique<strata_mtx>();
     mtx_parse(text, bytes, *h, static_cast<cudaStream_t>(stream));
     *out = h.release();

@@ -42,3 +42,16 @@ for rep in range(3):
     t4 = time.perf_counter()
     print(f"pageable_h2d_ms {1e3*(t1-t0):.1f} parse_ms {1e3*(t2-t1):.1f} pin_ms {1e3*(t3-t2):.1f} pinned_h2d_ms {1e3*(t4-t3):.1f}")
     del g, mm, pin, g2
+
+import tempfile  # noqa: E402
+with tempfile.NamedTemporaryFile(suffix=".mtx", delete=False) as f:
+    f.write(text)
+    path = f.name
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mm = S.read_matrix_market_file(path)
+    torch.cuda.synchronize()
+    print(f"file_ms {1e3*(time.perf_counter()-t0):.1f}")
+    del mm
+os.unlink(path)
