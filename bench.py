@@ -707,6 +707,23 @@ def extra_mtx_ingest(S, torch, dev):
         out["file_ms"] = round(file_ms, 1)
     finally:
         os.unlink(path)
+    # The reference's parser (oracle/_ref: mmio.cpp:17-55, istream per line) on a 2M-line
+    # prefix of the same text, one core: its line rate and the full-text estimate.
+    try:
+        from oracle import ref
+        k = 2_000_000
+        head = f"%%MatrixMarket matrix coordinate real general\n{m.rows} {m.cols} {k}\n".encode()
+        body_off = text.index(b"\n", text.index(b"\n") + 1) + 1
+        sample = head + text[body_off: body_off + 18 * k]
+        t0 = time.perf_counter()
+        coo = ref.Coo.read_matrix_market(sample)
+        t_ref = time.perf_counter() - t0
+        assert coo.nnz == k
+        out["reference_sample"] = {"lines": k, "ms": round(t_ref * 1e3, 1), "cores": 1,
+                                   "full_text_est_ms": round(t_ref * 1e3 * m.nnz / k, 0),
+                                   "speedup_vs_parse_est": round(t_ref * 1e3 * m.nnz / k / out["parse_ms"], 1)}
+    except Exception as e:  # informational only (no oracle/_ref on this box)
+        out["reference_sample"] = {"unavailable": str(e)[:200]}
     return out
 
 
