@@ -39,16 +39,24 @@ constexpr long long kCsrLong = 2048;  // row-split CSR SpMM: longer rows are chu
 constexpr long long kCsrChunk = 256;  // non-zeros per chunk of a long row
 constexpr long long kCsrGroup = 64;   // chunk partials summed per level-1 group
 
+// nonfinite != nullptr: set to 1 when any element is inf / NaN (for the SDDMM's integer-pipe
+// conversion twins; zeroed by the caller).
 template <class TO>
 __global__ void transpose_kernel(const float* __restrict__ in, TO* __restrict__ out,
-                                 long long rows, long long cols) {
+                                 long long rows, long long cols, int* __restrict__ nonfinite = nullptr) {
   // in[rows][cols] -> out[cols][rows]
   __shared__ float tile[32][33];
   const long long c0 = static_cast<long long>(blockIdx.x) * 32, r0 = static_cast<long long>(blockIdx.y) * 32;
+  bool bad = false;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const long long r = r0 + i, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[i][threadIdx.x] = __ldcs(in + r * cols + c);
+    if (r < rows && c < cols) {
+      const float v = __ldcs(in + r * cols + c);
+      tile[i][threadIdx.x] = v;
+      bad |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+    }
   }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && threadIdx.x == 0) *nonfinite = 1;
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const long long c = c0 + i, r = r0 + threadIdx.x;
@@ -78,6 +86,9 @@ __device__ __forceinline__ T reduce_scatter(T (&v)[L], int lane, unsigned mask) 
 // C2 graph (114.6M nnz), VEC = 2 everywhere (256-bit gathers, U = 4 in flight, 2 CTAs/SM):
 //   d = 32: 4 lanes 1.89 -> 1.71 ms; d = 64: 8 lanes 4.12 -> 3.21 ms (at U = 8 it needed 170
 //   registers, 1 CTA/SM: 7.93 ms); d = 128: 16 lanes 17.20 -> 7.30 ms.  VEC = 4 spills.
+#ifndef STRATA_SDDMM_ICVT  // A/B knob: gathered Yt values converted on the integer pipes, with an
+#define STRATA_SDDMM_ICVT 0  // F2F twin for inf / NaN (C2 d = 64: 3.255 vs 3.224 ms — off)
+#endif
 #ifndef STRATA_SDDMM_VEC32
 #define STRATA_SDDMM_VEC32 2
 #endif
@@ -100,23 +111,32 @@ template <>
 struct DotT<true> { using T = double; using XV = double4; };
 
 // The row's X fragment in the dot's precision: converted once per row, not per non-zero.
-template <bool kF64>
+// kUp: scaled by 2^896 to pair with the integer-pipe conversion of the gathered Yt values
+// (cvt_down, common.cuh) — the products x * y are unchanged.
+template <bool kF64, bool kUp = false>
 __device__ __forceinline__ typename DotT<kF64>::XV xfrag(const float4& x) {
   if constexpr (kF64) {
-    return make_double4(static_cast<double>(x.x), static_cast<double>(x.y), static_cast<double>(x.z),
-                        static_cast<double>(x.w));
+    constexpr double sc = kUp ? 0x1p896 : 1.0;
+    return make_double4(static_cast<double>(x.x) * sc, static_cast<double>(x.y) * sc,
+                        static_cast<double>(x.z) * sc, static_cast<double>(x.w) * sc);
   } else {
     return x;
   }
 }
 
-template <bool kF64>
+template <bool kUp>
+__device__ __forceinline__ double ycvt(float y) {
+  if constexpr (kUp) return cvt_down(y);
+  else return static_cast<double>(y);
+}
+
+template <bool kF64, bool kUp = false>
 __device__ __forceinline__ typename DotT<kF64>::T dot4(const typename DotT<kF64>::XV& x, const float4& y) {
   if constexpr (kF64) {
-    double s = x.x * static_cast<double>(y.x);
-    s = fma(x.y, static_cast<double>(y.y), s);
-    s = fma(x.z, static_cast<double>(y.z), s);
-    return fma(x.w, static_cast<double>(y.w), s);
+    double s = x.x * ycvt<kUp>(y.x);
+    s = fma(x.y, ycvt<kUp>(y.y), s);
+    s = fma(x.z, ycvt<kUp>(y.z), s);
+    return fma(x.w, ycvt<kUp>(y.w), s);
   } else {
     return x.x * y.x + x.y * y.y + x.z * y.z + x.w * y.w;
   }
@@ -133,12 +153,23 @@ struct YSlice {
 #define STRATA_SDDMM_U2 4
 #endif
 
-template <int L, int VEC = 1, bool kF64 = STRATA_SDDMM_F64>
-__global__ void __launch_bounds__(kBlock, VEC > 1 ? 2 : 1)
+#ifndef STRATA_SDDMM_MINB  // CTAs/SM the 256-bit variants are register-budgeted for (A/B knob)
+#define STRATA_SDDMM_MINB 2
+#endif
+
+// kCvt: 0 = F2F conversions of the gathered Yt values; 1 = integer-pipe conversions (exits when
+// Yt holds an inf / NaN, *yflag != 0); 2 = F2F, exits when Yt is all finite (the twin of 1).
+template <int L, int VEC = 1, bool kF64 = STRATA_SDDMM_F64, int kCvt = 0>
+__global__ void __launch_bounds__(kBlock, VEC > 1 ? STRATA_SDDMM_MINB : 1)
 sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
              const float* __restrict__ A, const float* __restrict__ X,
              const float* __restrict__ Yt, float* __restrict__ B, long long rows, long long nnz,
-             long long d) {
+             long long d, const int* __restrict__ yflag) {
+  if constexpr (kCvt != 0) {
+    const bool nonfinite = *yflag != 0;
+    if (nonfinite == (kCvt == 1)) return;
+  }
+  constexpr bool kUp = kF64 && kCvt == 1;
   using T = typename DotT<kF64>::T;
   using YV = YSlice<VEC>;
   constexpr int U = VEC > 1 ? STRATA_SDDMM_U2 : 8;  // (VEC = 2, U = 8 needed 170 registers: 1 CTA/SM)
@@ -183,7 +214,7 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   auto load_x = [&]() {
 #pragma unroll
     for (int i = 0; i < VEC; ++i)
-      x[i] = xfrag<kF64>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) +
+      x[i] = xfrag<kF64, kUp>(ld_gather4(reinterpret_cast<const float4*>(X + static_cast<long long>(row) * d) +
                                     lane * VEC + i));
   };
   load_x();
@@ -227,9 +258,9 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
             for (int i = 0; i < VEC; ++i) yv[u + v].v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       auto dot = [&](const YV& y) -> T {
-        T r = dot4<kF64>(x[0], y.v[0]);
+        T r = dot4<kF64, kUp>(x[0], y.v[0]);
 #pragma unroll
-        for (int i = 1; i < VEC; ++i) r += dot4<kF64>(x[i], y.v[i]);
+        for (int i = 1; i < VEC; ++i) r += dot4<kF64, kUp>(x[i], y.v[i]);
         return r;
       };
       if (one_row) {
@@ -459,11 +490,14 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
                       int64_t nnz, int64_t d, cudaStream_t s) {
   if (d <= 0) throw ApiError(STRATA_ERR_USAGE, "sddmm: d must be >= 1");
   if (nnz == 0) return;
-  // Y[d][n] -> Yt[n][d] once per call (f32; the vectorised kernels gather 128- / 256-bit slices)
-  float* Yt = static_cast<float*>(workspace_alloc(sizeof(float) * cols * d, s));
+  // Y[d][n] -> Yt[n][d] once per call (f32; the vectorised kernels gather 128- / 256-bit slices),
+  // noting whether Y holds an inf / NaN (selects the integer-pipe or the F2F twin below)
+  float* Yt = static_cast<float*>(workspace_alloc(sizeof(float) * cols * d + 256, s));
+  int* yflag = reinterpret_cast<int*>(Yt + cols * d);
+  if (STRATA_SDDMM_ICVT) STRATA_CUDA_CHECK(cudaMemsetAsync(yflag, 0, sizeof(int), s));
   {
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((d + 31) / 32));
-    transpose_kernel<float><<<grid, dim3(32, 8), 0, s>>>(Y, Yt, d, cols);
+    transpose_kernel<float><<<grid, dim3(32, 8), 0, s>>>(Y, Yt, d, cols, STRATA_SDDMM_ICVT ? yflag : nullptr);
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
   const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0;
@@ -478,18 +512,31 @@ void sddmm_csr_launch(const int32_t* indptr, const int32_t* indices, const float
   // Lanes per non-zero: each lane owns 4 * VEC consecutive features (256-bit gathers for VEC >= 2)
   // so a non-zero's dot is reduced across L = d / (4 VEC) lanes; fewer lanes, fewer reduce steps.
   constexpr int v32 = STRATA_SDDMM_VEC32, v64 = STRATA_SDDMM_VEC64, v128 = STRATA_SDDMM_VEC128;
+  constexpr bool kF = STRATA_SDDMM_F64 != 0;
+  // (kCvt 1 + 2: the integer-pipe kernel and its F2F twin, one of which exits at once)
+  constexpr int c1 = (kF && STRATA_SDDMM_ICVT) ? 1 : 0, c2 = c1 ? 2 : 0;
   static PerDeviceOnce once;  // VWs of <= 8 lanes stage 64 KB per CTA
-  once([&] {
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<32 / (4 * v32), v32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(32 / (4 * v32))));
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<64 / (4 * v64), v64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(64 / (4 * v64))));
-    STRATA_CUDA_CHECK(cudaFuncSetAttribute(sddmm_kernel<128 / (4 * v128), v128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(128 / (4 * v128))));
-  });
-  auto run = [&](auto kern, int L) {
-    kern<<<blocks_for(L), kBlock, smem_for(L), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);
+  auto attr = [&](auto kern, int L) {
+    STRATA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(L)));
   };
-  if (staged && d == 32) run(sddmm_kernel<32 / (4 * v32), v32>, 32 / (4 * v32));
-  else if (staged && d == 64) run(sddmm_kernel<64 / (4 * v64), v64>, 64 / (4 * v64));
-  else if (staged && d == 128) run(sddmm_kernel<128 / (4 * v128), v128>, 128 / (4 * v128));
+  once([&] {
+    attr(sddmm_kernel<32 / (4 * v32), v32, kF, c1>, 32 / (4 * v32));
+    attr(sddmm_kernel<32 / (4 * v32), v32, kF, c2>, 32 / (4 * v32));
+    attr(sddmm_kernel<64 / (4 * v64), v64, kF, c1>, 64 / (4 * v64));
+    attr(sddmm_kernel<64 / (4 * v64), v64, kF, c2>, 64 / (4 * v64));
+    attr(sddmm_kernel<128 / (4 * v128), v128, kF, c1>, 128 / (4 * v128));
+    attr(sddmm_kernel<128 / (4 * v128), v128, kF, c2>, 128 / (4 * v128));
+  });
+  auto run = [&](auto k1, auto k2, int L) {
+    k1<<<blocks_for(L), kBlock, smem_for(L), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d, yflag);
+    if (c2) k2<<<blocks_for(L), kBlock, smem_for(L), s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d, yflag);
+  };
+  if (staged && d == 32)
+    run(sddmm_kernel<32 / (4 * v32), v32, kF, c1>, sddmm_kernel<32 / (4 * v32), v32, kF, c2>, 32 / (4 * v32));
+  else if (staged && d == 64)
+    run(sddmm_kernel<64 / (4 * v64), v64, kF, c1>, sddmm_kernel<64 / (4 * v64), v64, kF, c2>, 64 / (4 * v64));
+  else if (staged && d == 128)
+    run(sddmm_kernel<128 / (4 * v128), v128, kF, c1>, sddmm_kernel<128 / (4 * v128), v128, kF, c2>, 128 / (4 * v128));
   else {
     const unsigned blocks = static_cast<unsigned>(std::min<long long>((nnz + 255) / 256, 148 * 32));
     sddmm_scalar_kernel<<<blocks, 256, 0, s>>>(indptr, indices, A, X, Yt, B, rows, nnz, d);

@@ -63,6 +63,7 @@ struct SpmmArgs {
   long long total_chunks;
   int nparts;
   int w256;  // X 32-byte aligned: 256-bit slice loads for VEC >= 2
+  const int* xflag;  // kCvt != 0 variants: 1 when X holds an inf / NaN (x_nonfinite_kernel)
   SpmmPartDev parts[kMaxParts];
 };
 
@@ -129,6 +130,23 @@ struct Acc {
 #ifndef STRATA_SPMM_F64
 #define STRATA_SPMM_F64 1
 #endif
+
+// Exact products with X converted on the integer pipes (cvt_down, common.cuh).
+template <bool kUp, int VEC, bool kScalar>
+__device__ __forceinline__ void fma_acc(Acc<VEC, kScalar>& acc, float a, const Frag<VEC, kScalar>& x) {
+  if constexpr (kUp && !kScalar) {
+    const double au = static_cast<double>(a) * 0x1p896;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      acc.v[4 * i + 0] = fma(au, cvt_down(x.v[i].x), acc.v[4 * i + 0]);
+      acc.v[4 * i + 1] = fma(au, cvt_down(x.v[i].y), acc.v[4 * i + 1]);
+      acc.v[4 * i + 2] = fma(au, cvt_down(x.v[i].z), acc.v[4 * i + 2]);
+      acc.v[4 * i + 3] = fma(au, cvt_down(x.v[i].w), acc.v[4 * i + 3]);
+    }
+  } else {
+    fma_acc(acc, a, x);
+  }
+}
 
 template <int VEC, bool kScalar>
 __device__ __forceinline__ void fma_acc(Acc<VEC, kScalar>& acc, float a, const Frag<VEC, kScalar>& x) {
@@ -234,6 +252,9 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 #ifndef STRATA_SPMM_VEC128  // A/B knob: d = 128 as 16 lanes x 256-bit slices (2) or 32 x 128-bit (1)
 #define STRATA_SPMM_VEC128 1   // (C5: 5.05 -> 5.54 ms with 2: the DRAM-bound case keeps 32 lanes)
 #endif
+#ifndef STRATA_SPMM_ICVT  // A/B knob: d = 64 gathers converted on the integer pipes (C2 2.91 -> 2.56 ms)
+#define STRATA_SPMM_ICVT 1
+#endif
 #ifndef STRATA_SPMM_MINB16  // CTAs/SM the d=64 variant is register-budgeted for (A/B knob)
 #define STRATA_SPMM_MINB16 2
 #endif
@@ -250,11 +271,18 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 //      slot of every ELL row is flagged in bit 31 of its column;
 //   3. consume: batches of 8 real slots are read with broadcast 128-bit shared loads (no
 //      shuffles), their X rows gathered UG at a time (128-bit per lane), and accumulated.
-template <int L, int VEC, bool kScalar, bool kMulti>
+// kCvt: 0 = F2F conversions; 1 = integer-pipe conversions (cvt_down), exits when the call's X
+// holds an inf / NaN (*a.xflag != 0); 2 = F2F, exits when X is all finite (the twin of 1).
+template <int L, int VEC, bool kScalar, bool kMulti, int kCvt = 0>
 // (the multi-destination instantiation keeps the 3-CTA budget only for one destination's worth
 // of registers: it gets the 2-CTA budget, so its replica stores do not spill)
 __global__ void __launch_bounds__(kBlock, (VEC > 1 && L == 32) ? 1 : (VEC > 1 ? 2 : ((L == 32 && !kScalar && !kMulti) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2))))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
+  if constexpr (kCvt != 0) {
+    const bool nonfinite = *a.xflag != 0;
+    if (nonfinite == (kCvt == 1)) return;
+  }
+  constexpr bool kUp = kCvt == 1;
   constexpr int kT = 8;  // real slots per consume batch / slots per lane per compaction round
 #ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
 #define STRATA_SPMM_UG 8
@@ -435,7 +463,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
           for (int u = 0; u < UG; ++u)
             gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0, a.w256);
 #pragma unroll
-          for (int u = 0; u < UG; ++u) fma_acc((ub + u) & 1 ? a1 : acc, sV[e0 + ub + u], xv[u]);
+          for (int u = 0; u < UG; ++u) fma_acc<kUp>((ub + u) & 1 ? a1 : acc, sV[e0 + ub + u], xv[u]);
         }
         add_acc(acc, a1);
 #else
@@ -467,7 +495,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
           if (uu < n) {
             if ((starts >> uu) & 1u) row_start(sD[++row - row_lo]);
 #if STRATA_SPMM_F64
-            fma_acc(acc, sV[e0 + uu], xv[u]);  // broadcast LDS
+            fma_acc<kUp>(acc, sV[e0 + uu], xv[u]);  // broadcast LDS
 #else
             fma_part(part, sV[e0 + uu], xv[u]);  // broadcast LDS
 #endif
@@ -609,13 +637,35 @@ __global__ void zero_rows_kernel(const int32_t* __restrict__ rows, long long n,
   }
 }
 
-template <int L, int VEC, bool kScalar, bool kMulti>
+// Any inf / NaN among X's n floats -> *flag = 1 (flag zeroed by the caller).  256-bit loads of
+// a 32-byte aligned X; one store per warp that saw one.
+__global__ void __launch_bounds__(256) x_nonfinite_kernel(const float* __restrict__ X, long long n,
+                                                          int* __restrict__ flag) {
+  const long long n8 = n / 8;
+  bool bad = false;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    uint32_t v[8];
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "l"(X + i * 8));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) bad |= (v[k] & 0x7f800000u) == 0x7f800000u;
+  }
+  if (blockIdx.x == 0)
+    for (long long i = n8 * 8 + threadIdx.x; i < n; i += blockDim.x)
+      bad |= (__float_as_uint(X[i]) & 0x7f800000u) == 0x7f800000u;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+template <int L, int VEC, bool kScalar, bool kMulti, int kCvt = 0>
 void launch_variant_m(const SpmmArgs& args, long long total_chunks, long long d, cudaStream_t s) {
   const long long threads = total_chunks * L;
   const unsigned blocks = static_cast<unsigned>((threads + kBlock - 1) / kBlock);
   dim3 grid(blocks, kScalar ? static_cast<unsigned>((d + 31) / 32) : 1u);
   constexpr int smem = (kBlock / L) * 3 * kPiece * 4;  // 3 KB staging per virtual warp
-  auto* kern = spmm_hyb_kernel<L, VEC, kScalar, kMulti>;
+  auto* kern = spmm_hyb_kernel<L, VEC, kScalar, kMulti, kCvt>;
   static PerDeviceOnce once;  // per instantiation and device
   once([&] {
     STRATA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -687,6 +737,20 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
 
+  // d = 64 in 256-bit slices (L = 8, VEC = 2), one destination: scan X for inf / NaN once per
+  // call (X is L2-resident at C2; ~10 us) so the integer-pipe conversion variant can run.
+  int* xflag = nullptr;
+#if STRATA_SPMM_ICVT
+  if (!scalar && L == 8 && VEC == 2 && ndst == 1 && h.cols > 0) {
+    xflag = static_cast<int*>(workspace_alloc(sizeof(int), s));
+    STRATA_CUDA_CHECK(cudaMemsetAsync(xflag, 0, sizeof(int), s));
+    const long long n = h.cols * d;
+    const unsigned blocks = static_cast<unsigned>(std::min<long long>((n / 8 + 255) / 256 + 1, 148 * 8));
+    x_nonfinite_kernel<<<blocks, 256, 0, s>>>(X, n, xflag);
+    STRATA_CUDA_CHECK(cudaGetLastError());
+  }
+#endif
+
   // One launch (plus the fix-up pair) per column partition, partitions in order.
   size_t pi = 0, fr = 0;
   const bool vec2 = d % 2 == 0;
@@ -713,6 +777,11 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
       if (scalar) launch_variant<32, 1, true>(args, chunks, d, s);
       else if (L == 8 && VEC == 1) launch_variant<8, 1, false>(args, chunks, d, s);
 #if STRATA_SPMM_VEC64 == 2
+      else if (L == 8 && VEC == 2 && xflag) {  // integer-pipe conversions, F2F twin for inf / NaN
+        args.xflag = xflag;
+        launch_variant_m<8, 2, false, false, 1>(args, chunks, d, s);
+        launch_variant_m<8, 2, false, false, 2>(args, chunks, d, s);
+      }
       else if (L == 8 && VEC == 2) launch_variant<8, 2, false>(args, chunks, d, s);
 #endif
       else if (L == 16 && VEC == 1) launch_variant<16, 1, false>(args, chunks, d, s);
@@ -755,6 +824,7 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
   if (scratch) STRATA_CUDA_CHECK(cudaFreeAsync(scratch, s));
+  if (xflag) STRATA_CUDA_CHECK(cudaFreeAsync(xflag, s));
 }
 
 }  // namespace strata_b200
