@@ -677,7 +677,8 @@ def extra_mtx_ingest(S, torch, dev):
             + lines.tobytes())
     del lines
     out = {"bytes": len(text), "entries": m.nnz}
-    for rep in range(2):
+    parse_s, csr_s = [], []
+    for rep in range(4):  # first call warms the pinned ring and the pool; best of the rest
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         mm = S.read_matrix_market(text)
@@ -685,12 +686,17 @@ def extra_mtx_ingest(S, torch, dev):
         csr = mm.to_csr(dev)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
+        if rep:
+            parse_s.append(t1 - t0)
+            csr_s.append(t2 - t1)
         ok = bool(torch.equal(csr.indptr.cpu(), torch.from_numpy(m.indptr))) and \
             bool(torch.equal(csr.indices.cpu(), torch.from_numpy(m.indices)))
         del mm, csr
-    out.update({"parse_ms": round((t1 - t0) * 1e3, 1), "csr_ms": round((t2 - t1) * 1e3, 1),
-                "parse_gbs": round(len(text) / (t1 - t0) / 1e9, 2), "csr_equals_generator": ok,
-                "note": "text in pageable host memory: the H2D copy of the entry region is inside"})
+    out.update({"parse_ms": round(min(parse_s) * 1e3, 1), "parse_ms_reps": [round(x * 1e3, 1) for x in parse_s],
+                "csr_ms": round(min(csr_s) * 1e3, 1),
+                "parse_gbs": round(len(text) / min(parse_s) / 1e9, 2), "csr_equals_generator": ok,
+                "note": "text in pageable host memory: the H2D copy of the entry region is inside "
+                        "(wall clock, best of 3 warm calls)"})
     # read_matrix_market_file (mmio.cpp:57-61): the same text from a file (page cache warm)
     import tempfile
     with tempfile.NamedTemporaryFile(suffix=".mtx", delete=False) as f:

@@ -29,6 +29,7 @@
 #include <unistd.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -452,8 +453,12 @@ void copy_text_h2d(uint8_t* dst, const char* src, long long n, cudaStream_t s) {
   cudaGetLastError();
   StageRing& R = stage_ring();
   std::unique_lock<std::mutex> lock(R.mu);
-  // small, already page-locked (strata_mtx_read_file's buffer) or no pinned memory: one copy
-  if (pinned || n < static_cast<long long>(4 * kStageChunk) || !R.ensure()) {
+  // small, already page-locked or no pinned memory: one copy
+  const bool ring = !pinned && n >= static_cast<long long>(4 * kStageChunk) && R.ensure();
+  if (std::getenv("STRATA_MTX_DEBUG"))
+    std::fprintf(stderr, "[strata mtx] %lld bytes: %s\n", n,
+                 ring ? "pinned staging ring" : (pinned ? "page-locked source" : "driver pageable copy"));
+  if (!ring) {
     lock.unlock();
     STRATA_CUDA_CHECK(cudaMemcpyAsync(dst, src, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
     return;
