@@ -478,9 +478,14 @@ void copy_text_h2d(uint8_t* dst, const char* src, long long n, cudaStream_t s) {
       for (int t = 0; t < nc; ++t) {
         const long long o = (c0 + t) * static_cast<long long>(kStageChunk);
         const size_t len = static_cast<size_t>(std::min<long long>(kStageChunk, n - o));
-        th[t] = std::thread([&R, set, t, src, o, len] { std::memcpy(R.buf[set + t], src + o, len); });
+        try {
+          th[t] = std::thread([&R, set, t, src, o, len] { std::memcpy(R.buf[set + t], src + o, len); });
+        } catch (...) {  // no thread: copy on this one
+          std::memcpy(R.buf[set + t], src + o, len);
+        }
       }
-      for (int t = 0; t < nc; ++t) th[t].join();
+      for (int t = 0; t < nc; ++t)
+        if (th[t].joinable()) th[t].join();
       for (int t = 0; t < nc; ++t) {
         const long long o = (c0 + t) * static_cast<long long>(kStageChunk);
         const size_t len = static_cast<size_t>(std::min<long long>(kStageChunk, n - o));
