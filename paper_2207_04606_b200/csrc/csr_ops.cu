@@ -225,7 +225,13 @@ sddmm_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ ind
   const int d4 = static_cast<int>(d / 4);
   auto gather_y = [&](int col) -> YV {
     YV y;
-    const float4* p = Y4 + static_cast<long long>(col) * d4;
+    // the staged variants run only for d == 4 * L * VEC: a compile-time row stride, one wide
+    // multiply-add per gathered row address (col >= 0)
+    const float4* p;
+    asm("mad.wide.u32 %0, %1, %2, %3;"
+        : "=l"(p)
+        : "r"(static_cast<uint32_t>(col)), "r"(static_cast<uint32_t>(L * VEC * 16)), "l"(Y4));
+    (void)d4;
     if constexpr (VEC % 2 == 0) {  // Yt is the call's own 256-byte aligned workspace
 #pragma unroll
       for (int i = 0; i < VEC; i += 2)

@@ -34,6 +34,10 @@ namespace strata_b200 {
 
 namespace {
 
+#ifndef STRATA_SPMM_XG  // A/B knob: lane-offset gather base + one wide multiply-add per row address
+#define STRATA_SPMM_XG 1
+#endif
+
 constexpr int kMaxParts = 32;
 constexpr int kBlock = 256;
 constexpr int kPiece = 256;  // ELL slots staged in shared memory per virtual warp at a time
@@ -89,9 +93,19 @@ __device__ __forceinline__ void gather(Frag<VEC, kScalar>& f, const float* __res
     // compile-time power of two: one shift instead of a 64-bit multiply per gathered slot.
     // A lane owns VEC consecutive float4 of the row (feature 4*VEC*lane ..): with VEC = 2 one
     // 256-bit load (sm_100 LDG.256), with VEC = 4 two.
+    // X is the lane-offset base (X + 4 * VEC * lane floats, hoisted out of the loop): one
+    // 32 x 32 -> 64-bit multiply-add per gathered row instead of a shift / merge / LEA chain.
     (void)d;
+#if STRATA_SPMM_XG
+    (void)lane;
+    const float4* xp;
+    asm("mad.wide.u32 %0, %1, %2, %3;"
+        : "=l"(xp)
+        : "r"(static_cast<uint32_t>(col)), "r"(static_cast<uint32_t>(L * VEC * 16)), "l"(X));
+#else
     const float4* xp = reinterpret_cast<const float4*>(X) +
                        (static_cast<unsigned long long>(static_cast<uint32_t>(col)) * (L * VEC)) + lane * VEC;
+#endif
     // L < 32 VEC variants (d = 64) are launched only on 32-byte aligned X; d = 256 / 512 check
     if (VEC % 2 == 0 && (L < 32 || w256)) {  // warp-uniform
 #pragma unroll
@@ -294,6 +308,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   const long long vw = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) / L;
   if (vw >= a.total_chunks) return;
   const long long feat0 = kScalar ? static_cast<long long>(blockIdx.y) * 32 : 0;
+  const float* __restrict__ Xg = (kScalar || !STRATA_SPMM_XG) ? a.X : a.X + 4 * VEC * lane;  // gather base
 
   int pi = 0;
   while (pi + 1 < a.nparts && vw >= a.parts[pi + 1].chunk_begin) ++pi;
@@ -461,7 +476,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
           Frag<VEC, kScalar> xv[UG];
 #pragma unroll
           for (int u = 0; u < UG; ++u)
-            gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0, a.w256);
+            gather<L, VEC, kScalar>(xv[u], Xg, col[ub + u], d, lane, feat0, a.w256);
 #pragma unroll
           for (int u = 0; u < UG; ++u) fma_acc<kUp>((ub + u) & 1 ? a1 : acc, sV[e0 + ub + u], xv[u]);
         }
@@ -474,7 +489,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
           Frag<VEC, kScalar> xv[UG];
 #pragma unroll
           for (int u = 0; u < UG; ++u)
-            gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u], d, lane, feat0, a.w256);
+            gather<L, VEC, kScalar>(xv[u], Xg, col[ub + u], d, lane, feat0, a.w256);
 #pragma unroll
           for (int u = 0; u < UG; ++u) fma_part((ub + u) & 1 ? p1 : part, sV[e0 + ub + u], xv[u]);
         }
@@ -488,7 +503,7 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
         Frag<VEC, kScalar> xv[UG];
 #pragma unroll
         for (int u = 0; u < UG; ++u)
-          if (ub + u < n) gather<L, VEC, kScalar>(xv[u], a.X, col[ub + u] & 0x7fffffff, d, lane, feat0, a.w256);
+          if (ub + u < n) gather<L, VEC, kScalar>(xv[u], Xg, col[ub + u] & 0x7fffffff, d, lane, feat0, a.w256);
 #pragma unroll
         for (int u = 0; u < UG; ++u) {
           const int uu = ub + u;
