@@ -108,6 +108,12 @@ void* workspace_alloc(size_t bytes, cudaStream_t s) {
   return p;
 }
 
+long long l2_bytes() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrL2CacheSize, dev);
+  return n > 0 ? n : (126ll << 20);
+}
+
 int num_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)

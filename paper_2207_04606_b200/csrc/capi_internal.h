@@ -228,6 +228,7 @@ void ell_from_csr_launch(const int32_t* indptr, const int32_t* indices, const fl
                          cudaStream_t s);
 
 int num_sms();
+long long l2_bytes();  // the current device's L2 capacity
 // 2D bf16 TMA descriptor over a row-major [rows][cols] array with a {box_cols, box_rows} box
 // (cuTensorMapEncodeTiled through the runtime's driver entry point).
 CUtensorMap make_tensor_map_bf16_2d(const void* base, long long rows, long long cols,

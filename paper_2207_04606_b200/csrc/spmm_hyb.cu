@@ -752,11 +752,14 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
 
-  // d = 64 in 256-bit slices (L = 8, VEC = 2), one destination: scan X for inf / NaN once per
-  // call (X is L2-resident at C2; ~10 us) so the integer-pipe conversion variant can run.
+  // d = 64 in 256-bit slices (L = 8, VEC = 2), one destination, X small enough to stay in L2
+  // (the XU-bound case; a DRAM-bound gather gains nothing and the scan would cost X's bytes
+  // again): scan X for inf / NaN once per call (~10 us at C2) so the integer-pipe conversion
+  // variant can run.
   int* xflag = nullptr;
 #if STRATA_SPMM_ICVT
-  if (!scalar && L == 8 && VEC == 2 && ndst == 1 && h.cols > 0) {
+  if (!scalar && L == 8 && VEC == 2 && ndst == 1 && h.cols > 0 &&
+      static_cast<long long>(h.cols) * d * 4 <= l2_bytes()) {
     xflag = static_cast<int*>(workspace_alloc(sizeof(int), s));
     STRATA_CUDA_CHECK(cudaMemsetAsync(xflag, 0, sizeof(int), s));
     const long long n = h.cols * d;
