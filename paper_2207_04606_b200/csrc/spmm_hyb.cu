@@ -269,6 +269,9 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 #ifndef STRATA_SPMM_ICVT  // A/B knob: d = 64 gathers converted on the integer pipes (C2 2.91 -> 2.56 ms)
 #define STRATA_SPMM_ICVT 1
 #endif
+#ifndef STRATA_SPMM_MINB_V2  // CTAs/SM the 256-bit d = 64 variant is register-budgeted for
+#define STRATA_SPMM_MINB_V2 2
+#endif
 #ifndef STRATA_SPMM_MINB16  // CTAs/SM the d=64 variant is register-budgeted for (A/B knob)
 #define STRATA_SPMM_MINB16 2
 #endif
@@ -290,7 +293,7 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 template <int L, int VEC, bool kScalar, bool kMulti, int kCvt = 0>
 // (the multi-destination instantiation keeps the 3-CTA budget only for one destination's worth
 // of registers: it gets the 2-CTA budget, so its replica stores do not spill)
-__global__ void __launch_bounds__(kBlock, (VEC > 1 && L == 32) ? 1 : (VEC > 1 ? 2 : ((L == 32 && !kScalar && !kMulti) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2))))
+__global__ void __launch_bounds__(kBlock, (VEC > 1 && L == 32) ? 1 : (VEC > 1 ? STRATA_SPMM_MINB_V2 : ((L == 32 && !kScalar && !kMulti) ? STRATA_SPMM_MINB32 : (L == 16 && !kScalar ? STRATA_SPMM_MINB16 : 2))))
 spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
   if constexpr (kCvt != 0) {
     const bool nonfinite = *a.xflag != 0;
@@ -301,7 +304,10 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
 #ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
 #define STRATA_SPMM_UG 8
 #endif
-  constexpr int UG = kScalar ? 8 : (VEC == 1 ? STRATA_SPMM_UG : (VEC == 2 ? 4 : 2));
+#ifndef STRATA_SPMM_UG2  // ... for the 256-bit (VEC = 2) variants
+#define STRATA_SPMM_UG2 2  // (C2: UG = 1 / 2 / 4 / 8 -> 2.48 / 2.45 / 2.51 / 3.75 ms; 3 CTAs/SM spill)
+#endif
+  constexpr int UG = kScalar ? 8 : (VEC == 1 ? STRATA_SPMM_UG : (VEC == 2 ? STRATA_SPMM_UG2 : 2));
   constexpr int kRound = kT * L;  // slots examined per compaction round
   constexpr int32_t kRowFlag = static_cast<int32_t>(0x80000000u);
   const int lane = threadIdx.x & (L - 1);
