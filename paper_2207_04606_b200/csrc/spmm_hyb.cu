@@ -90,9 +90,8 @@ __device__ __forceinline__ void gather(Frag<VEC, kScalar>& f, const float* __res
     f.v[0].x = fi < d ? ld_gather(X + col * d + fi) : 0.f;
   } else {
     // Vector variants are launched only for d == 4 * L * VEC, so the row stride is a
-    // compile-time power of two: one shift instead of a 64-bit multiply per gathered slot.
-    // A lane owns VEC consecutive float4 of the row (feature 4*VEC*lane ..): with VEC = 2 one
-    // 256-bit load (sm_100 LDG.256), with VEC = 4 two.
+    // compile-time constant.  A lane owns VEC consecutive float4 of the row (feature
+    // 4*VEC*lane ..): with VEC = 2 one 256-bit load (sm_100 LDG.256), with VEC = 4 two.
     // X is the lane-offset base (X + 4 * VEC * lane floats, hoisted out of the loop): one
     // 32 x 32 -> 64-bit multiply-add per gathered row instead of a shift / merge / LEA chain.
     (void)d;
@@ -266,7 +265,7 @@ __device__ __forceinline__ void put_f64(double* __restrict__ row, const Acc<VEC,
 #ifndef STRATA_SPMM_VEC128  // A/B knob: d = 128 as 16 lanes x 256-bit slices (2) or 32 x 128-bit (1)
 #define STRATA_SPMM_VEC128 1   // (C5: 5.05 -> 5.54 ms with 2: the DRAM-bound case keeps 32 lanes)
 #endif
-#ifndef STRATA_SPMM_ICVT  // A/B knob: d = 64 gathers converted on the integer pipes (C2 2.91 -> 2.56 ms)
+#ifndef STRATA_SPMM_ICVT  // A/B knob: d = 64 gathers converted on the integer pipes (C2 2.91 -> 2.59 ms)
 #define STRATA_SPMM_ICVT 1
 #endif
 #ifndef STRATA_SPMM_MINB_V2  // CTAs/SM the 256-bit d = 64 variant is register-budgeted for
@@ -769,7 +768,7 @@ void spmm_hyb_launch(const strata_hyb_impl& h, const float* X, float* const* Yds
     xflag = static_cast<int*>(workspace_alloc(sizeof(int), s));
     STRATA_CUDA_CHECK(cudaMemsetAsync(xflag, 0, sizeof(int), s));
     const long long n = h.cols * d;
-    const unsigned blocks = static_cast<unsigned>(std::min<long long>((n / 8 + 255) / 256 + 1, 148 * 8));
+    const unsigned blocks = static_cast<unsigned>(std::min<long long>((n / 8 + 255) / 256 + 1, num_sms() * 8ll));
     x_nonfinite_kernel<<<blocks, 256, 0, s>>>(X, n, xflag);
     STRATA_CUDA_CHECK(cudaGetLastError());
   }
