@@ -106,3 +106,52 @@ def test_read_file(cuda, tmp_path):
     wr, wc, wv = ref.Coo.read_matrix_market(text).triplets()
     gr, gc, gv = m.triplets()
     assert np.array_equal(gr, wr) and np.array_equal(gc, wc) and np.array_equal(gv, wv)
+
+
+def test_read_file_errors(cuda, tmp_path):
+    """Empty and missing files give the reference's messages (mmio.cpp:21 / :59)."""
+    p = tmp_path / "empty.mtx"
+    p.write_bytes(b"")
+    with pytest.raises(S.StrataError) as e:
+        S.read_matrix_market_file(str(p))
+    with pytest.raises(ref.RefError) as w:
+        ref.Coo.read_matrix_market(b"")
+    assert str(e.value) == str(w.value)
+    with pytest.raises(S.StrataError) as e:
+        S.read_matrix_market_file(str(tmp_path / "missing.mtx"))
+    assert "cannot open" in str(e.value)
+
+
+def test_large_text_staged_copy(cuda, tmp_path):
+    """A text above the 128 MB staging threshold goes through the multi-threaded pinned ring
+    (pageable bytes) and the mapped-file path: triplets equal the generated values, and the
+    reference parser agrees on a prefix."""
+    n = 9_000_000  # 18-byte lines: 162 MB
+    r = np.random.default_rng(3)
+    rows = r.integers(1, 10_000_000, n)
+    cols = r.integers(1, 10_000_000, n)
+    vals = r.integers(1, 10, n)
+    lines = np.empty((n, 18), np.uint8)
+    for k in range(7):
+        p10 = 10 ** (6 - k)
+        lines[:, k] = (rows // p10) % 10 + 48
+        lines[:, 8 + k] = (cols // p10) % 10 + 48
+    lines[:, 7] = lines[:, 15] = 32
+    lines[:, 16] = vals + 48
+    lines[:, 17] = 10
+    text = (f"%%MatrixMarket matrix coordinate real general\n9999999 9999999 {n}\n".encode()
+            + lines.tobytes())
+    del lines
+    for m in (S.read_matrix_market(text), None):
+        if m is None:
+            p = tmp_path / "big.mtx"
+            p.write_bytes(text)
+            m = S.read_matrix_market_file(str(p))
+        gr, gc, gv = m.triplets()
+        assert np.array_equal(gr, rows - 1) and np.array_equal(gc, cols - 1)
+        assert np.array_equal(gv, vals.astype(np.float64))
+    head = text[:text.index(b"\n", text.index(b"\n") + 1) + 1 + 18 * 1000]
+    head = head.replace(f" {n}\n".encode(), b" 1000\n", 1)
+    wr2, wc2, wv2 = ref.Coo.read_matrix_market(head).triplets()
+    assert np.array_equal(gr[:1000], wr2) and np.array_equal(gc[:1000], wc2)
+    assert np.array_equal(gv[:1000], wv2)
