@@ -303,10 +303,15 @@ spmm_hyb_kernel(const __grid_constant__ SpmmArgs a) {
 #ifndef STRATA_SPMM_UG  // gathers in flight per lane for the float4 variants (A/B knob)
 #define STRATA_SPMM_UG 8
 #endif
-#ifndef STRATA_SPMM_UG2  // ... for the 256-bit (VEC = 2) variants
-#define STRATA_SPMM_UG2 2  // (C2: UG = 1 / 2 / 4 / 8 -> 2.48 / 2.45 / 2.51 / 3.75 ms; 3 CTAs/SM spill)
+#ifndef STRATA_SPMM_UG2  // ... for the 256-bit (VEC = 2) variants: the L2-resident (integer-pipe
+#define STRATA_SPMM_UG2 2  // conversion, kCvt != 0) kernels (C2: UG = 1 / 2 / 4 / 8 -> 2.48 /
+#endif                     // 2.45 / 2.51 / 3.75 ms) and the DRAM-bound F2F one (C5-shape d = 64:
+#ifndef STRATA_SPMM_UG2_DRAM  // UG 2 -> 4: 4.07 -> 3.73 ms GNN layer 128 -> 64)
+#define STRATA_SPMM_UG2_DRAM 4
 #endif
-  constexpr int UG = kScalar ? 8 : (VEC == 1 ? STRATA_SPMM_UG : (VEC == 2 ? STRATA_SPMM_UG2 : 2));
+  constexpr int UG = kScalar ? 8
+                             : (VEC == 1 ? STRATA_SPMM_UG
+                                         : (VEC == 2 ? (kCvt != 0 ? STRATA_SPMM_UG2 : STRATA_SPMM_UG2_DRAM) : 2));
   constexpr int kRound = kT * L;  // slots examined per compaction round
   constexpr int32_t kRowFlag = static_cast<int32_t>(0x80000000u);
   const int lane = threadIdx.x & (L - 1);
