@@ -53,6 +53,11 @@ def b_alg_spmm(nnz, m, n, d):
     return nnz * (4 + 4) + (m + 1) * 4 + nnz * d * 4 + m * d * 4
 
 
+def b_min_spmm(nnz, m, n, d):
+    """SURVEY §8d's B_min: the same with X read once (n rows) instead of once per non-zero."""
+    return nnz * (4 + 4) + (m + 1) * 4 + n * d * 4 + m * d * 4
+
+
 def b_alg_sddmm(nnz, m, n, d):
     return nnz * (4 + 4 + 4) + (m + 1) * 4 + m * d * 4 + nnz * d * 4
 
@@ -416,6 +421,9 @@ def extra_reddit(S, torch, dev, stream, peak):
                      "note": "X is L2-resident (59.6 MB < 126 MB L2): frac is L2-assisted"}
         if l2_peak:  # the gathers' real ceiling: measured L2 read bandwidth
             out[name]["frac_of_l2_peak"] = round(gbs / l2_peak, 3)
+        if name == "reddit_hyb_spmm":  # also B_min (X read once)
+            out[name]["b_min_frac_of_hbm"] = round(
+                b_min_spmm(m.nnz, m.rows, m.cols, d) / (ms * 1e-3) / 1e9 / peak, 3)
     out["reddit_nnz"] = m.nnz
     # Fused SDDMM -> edge softmax -> SpMM (GAT-style layer step), d = 64.
     plan = S.AttentionPlan(dcsr)
@@ -947,7 +955,11 @@ def run_ours(args):
             "peak_kind": peak_kind, "kernel": "spmm_hyb_kernel (+ split-run fix-up)",
             "kernel_ms": round(spmm_ms, 4),
             "algorithmic_bytes_per_launch": int(b_alg),
-            "bytes_model": "nnz*8 + (m+1)*4 + nnz*d*4 (one X row per non-zero) + m*d*4"}
+            "bytes_model": "nnz*8 + (m+1)*4 + nnz*d*4 (one X row per non-zero) + m*d*4",
+            # B_min (X read once): how far the step is from perfect X reuse, which at C5 (X
+            # 1.25 GB, 10x L2) no schedule can approach
+            "b_min_bytes": int(b_min_spmm(shard.nnz, shard.rows, m.cols, d)),
+            "b_min_frac": round(b_min_spmm(shard.nnz, shard.rows, m.cols, d) / (spmm_ms * 1e-3) / 1e9 / hbm_peak, 4)}
     if traffic:  # measured DRAM bytes (ncu, profiles/) over the same launch time: frac > 1 on
         # the algorithmic model means L2 served part of the X gathers (~10 % at C5)
         roof["dram_traffic_frac"] = round(traffic / 1e9 / (spmm_ms * 1e-3) / hbm_peak, 4)
