@@ -357,6 +357,7 @@ int strata_spmm_hyb_f32_host_batch(const strata_hyb* h, const float* const* X_ho
     require(d >= 1, STRATA_ERR_USAGE, "spmm: d must be >= 1");
     require(nbatch >= 0 && (nbatch == 0 || (X_host && Y_host)), STRATA_ERR_USAGE,
             "spmm_host_batch: bad batch arguments");
+    DeviceGuard dg(H.device);  // host buffers in, host buffers out: run on the handle's device
     require_device();
     if (nbatch == 0) return;
     cudaStream_t s = as_stream(stream);
