@@ -92,6 +92,11 @@ int strata_hyb_part_info(const strata_hyb* h, int part, int* partition, int* buc
  * (build_ell_bucket, storage.cpp:229-269).  Any pointer may be NULL to skip it. */
 int strata_hyb_part_read(const strata_hyb* h, int part, int32_t* I_indptr, int32_t* I_indices,
                          int32_t* J_indices, float* values);
+/* The two above in one call (the readback SURVEY §8b names): EllBucketPart's partition /
+ * bucket / width / nrows and the part's arrays copied to HOST buffers; any output may be NULL. */
+int strata_hyb_get_part(const strata_hyb* h, int part, int* partition, int* bucket, int64_t* width,
+                        int64_t* nrows, int32_t* I_indptr, int32_t* I_indices, int32_t* J_indices,
+                        float* values);
 /* Device views of one part (owned by the handle; valid until destroy). */
 int strata_hyb_part_device(const strata_hyb* h, int part, const int32_t** I_indices,
                            const int32_t** J_indices, const float** values);

@@ -74,6 +74,7 @@ _sig("strata_hyb_num_parts", C.c_int, vp, C.POINTER(C.c_int))
 _sig("strata_hyb_part_info", C.c_int, vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
      i64p, i64p, i64p, i64p, i64p, i64p)
 _sig("strata_hyb_part_read", C.c_int, vp, C.c_int, vp, vp, vp, vp)
+_sig("strata_hyb_get_part", C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp)
 _sig("strata_hyb_part_device", C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp))
 _sig("strata_hyb_padding_ratio", C.c_int, vp, C.POINTER(C.c_double))
 _sig("strata_hyb_dims", C.c_int, vp, i64p, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int))
@@ -146,7 +147,7 @@ EXPORTED = [
     "strata_csr_host_values", "strata_csr_host_destroy", "strata_csr_host_row_order",
     "strata_dense_int",
     "strata_hyb_decompose", "strata_hyb_auto_k", "strata_hyb_num_parts", "strata_hyb_part_info",
-    "strata_hyb_part_read", "strata_hyb_part_device", "strata_hyb_padding_ratio",
+    "strata_hyb_part_read", "strata_hyb_get_part", "strata_hyb_part_device", "strata_hyb_padding_ratio",
     "strata_hyb_dims", "strata_hyb_destroy", "strata_hyb_schedule_info",
     "strata_hyb_row_work_balance", "strata_spmm_hyb_f32", "strata_spmm_hyb_f32_host",
     "strata_spmm_hyb_f32_host_batch", "strata_spmm_hyb_f32_multi", "strata_gnn_layer_work_floats",

@@ -265,6 +265,14 @@ int strata_hyb_part_read(const strata_hyb* h, int part, int32_t* I_indptr, int32
   });
 }
 
+int strata_hyb_get_part(const strata_hyb* h, int part, int* partition, int* bucket, int64_t* width,
+                        int64_t* nrows, int32_t* I_indptr, int32_t* I_indices, int32_t* J_indices,
+                        float* values) {
+  const int rc = strata_hyb_part_info(h, part, partition, bucket, width, nrows, nullptr, nullptr,
+                                      nullptr, nullptr);
+  return rc != STRATA_OK ? rc : strata_hyb_part_read(h, part, I_indptr, I_indices, J_indices, values);
+}
+
 int strata_hyb_part_device(const strata_hyb* h, int part, const int32_t** I_indices,
                            const int32_t** J_indices, const float** values) {
   return guard([&] {

@@ -96,6 +96,33 @@ def test_decompose_c1_shape_vs_oracle(cuda, c, k):
         assert np.array_equal(arrs["values"], R["values"])
 
 
+def test_get_part_readback(cuda):
+    """strata_hyb_get_part (SURVEY 8b's readback name) = part_info + part_read in one call."""
+    import ctypes as C
+    from paper_2207_04606_b200._lib import check, lib
+    m = S.generate_matrix("powerlaw", 3000, 2900, 0, 0, 0, 12.0, 3)
+    h = S.decompose_hyb(m.to_device(cuda), 2, 3)
+    assert len(h.parts) > 2
+    for i, P in enumerate(h.parts):
+        part, bucket = C.c_int(), C.c_int()
+        width, nrows = C.c_int64(), C.c_int64()
+        iptr = np.empty(2, np.int32)
+        ii = np.empty(P.nrows, np.int32)
+        jj = np.empty(P.nrows * P.width, np.int32)
+        vv = np.empty(P.nrows * P.width, np.float32)
+        check(lib.strata_hyb_get_part(h._h, i, C.byref(part), C.byref(bucket), C.byref(width),
+                                      C.byref(nrows), iptr.ctypes.data, ii.ctypes.data,
+                                      jj.ctypes.data, vv.ctypes.data))
+        assert (part.value, bucket.value, width.value, nrows.value) == (P.partition, P.bucket, P.width, P.nrows)
+        want = h.part_arrays(i)
+        got = [iptr, ii, jj, vv]
+        for g, w in zip(got, want.values()):
+            assert np.array_equal(g.view(np.uint32), np.asarray(w).view(np.uint32))
+    with pytest.raises(S.StrataError) as e:
+        check(lib.strata_hyb_get_part(h._h, len(h.parts), None, None, None, None, None, None, None, None))
+    assert e.value.kind == "Lookup"
+
+
 def test_decompose_usage_errors(cuda):
     m = S.generate_matrix("powerlaw", 100, 100, 0, 0, 0, 4.0, 1).to_device(cuda)
     with pytest.raises(S.StrataError) as e:
