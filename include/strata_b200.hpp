@@ -725,6 +725,90 @@ struct FormatRewriteRule {
   TensorStorage storage;
 };
 
+// ---- rule generators (transform.hpp:92-103, transform.cpp:432-557) --------------------------
+// The converted storage (device conversion, arrays read back under the reference's aux names)
+// with the reference's rule / buffer names: rule `name`, buffer "A_" + name, arrays prefixed
+// name + "_".  (The IR fields of the reference's rules — axes, index maps — belong to the
+// lowering passes, which are out of scope.)
+inline FormatRewriteRule identity_rule(const TensorStorage& csr, const std::string& name = "csr") {
+  FormatRewriteRule r;
+  r.name = name;
+  r.new_buffer = "A_" + name;
+  r.storage = csr;  // build_csr(csr_to_coo(csr), name + "_"): the same arrays, renamed
+  r.storage.aux.clear();
+  for (const auto& [key, arr] : csr.aux) {
+    for (const char* base : {"J_indptr", "J_indices"}) {
+      const std::string b(base);
+      if (key.size() >= b.size() && key.compare(key.size() - b.size(), b.size(), b) == 0)
+        r.storage.aux[name + "_" + b] = arr;
+    }
+  }
+  return r;
+}
+
+inline FormatRewriteRule ell_rule(const TensorStorage& csr, int64_t w, const std::string& name = "ell") {
+  FormatRewriteRule r;
+  r.name = name;
+  r.new_buffer = "A_" + name;
+  r.storage = csr_to_ell(csr, w, name + "_");
+  return r;
+}
+
+inline FormatRewriteRule bsr_rule(const TensorStorage& csr, int64_t b, const std::string& name = "bsr") {
+  FormatRewriteRule r;
+  r.name = name;
+  r.new_buffer = "A_" + name;
+  r.storage = csr_to_bsr(csr, b, name + "_");
+  return r;
+}
+
+// c * (k + 1) rules, one per (partition, bucket) ELL sub-matrix, empty buckets included
+// (build_ell_bucket with no segments: I_indptr {0, 0}, empty arrays).
+inline std::vector<FormatRewriteRule> hyb_rules(const TensorStorage& csr, int c, int k,
+                                                const std::string& name = "hyb") {
+  HybDecomposition h = decompose_hyb(csr, c, k, name + "_");
+  std::vector<FormatRewriteRule> rules;
+  for (int p = 0; p < c; ++p) {
+    for (int b = 0; b <= k; ++b) {
+      FormatRewriteRule r;
+      r.name = name + "_p" + std::to_string(p) + "_b" + std::to_string(b);
+      r.new_buffer = "A_" + r.name;
+      const EllBucketPart* part = nullptr;
+      for (const auto& q : h.parts)
+        if (q.partition == p && q.bucket == b) part = &q;
+      if (part) {
+        r.storage = part->ell;
+      } else {
+        const std::string pre = name + "_hyb_p" + std::to_string(p) + "_b" + std::to_string(b) + "_";
+        r.storage.kind = FormatKind::EllBucket;
+        r.storage.rows = csr.rows;
+        r.storage.cols = csr.cols;
+        r.storage.width = int64_t{1} << b;
+        r.storage.aux[pre + "I_indptr"] = {0, 0};
+        r.storage.aux[pre + "I_indices"] = {};
+        r.storage.aux[pre + "J_indices"] = {};
+      }
+      rules.push_back(std::move(r));
+    }
+  }
+  return rules;
+}
+
+// bind_storage (interp.hpp:63, interp.cpp:554-562): aux arrays as I32 buffers under their own
+// names, the values under buffer_name.
+inline void bind_storage(Bindings& b, const std::string& buffer_name, const TensorStorage& s) {
+  for (const auto& [key, arr] : s.aux) {
+    TensorData d;
+    d.dtype = DType::I32;
+    d.i32 = arr;
+    b.buffers[key] = std::move(d);
+  }
+  TensorData v;
+  v.dtype = DType::F32;
+  v.f32 = s.values;
+  b.buffers[buffer_name] = std::move(v);
+}
+
 enum class Stage { I, II, III };
 inline const char* stage_name(Stage s) { return s == Stage::I ? "I" : s == Stage::II ? "II" : "III"; }
 

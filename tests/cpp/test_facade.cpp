@@ -589,6 +589,45 @@ TEST_CASE("sharded SpMM / SDDMM through the C ABI with an NCCL communicator (wor
   check(strata_nccl_comm_destroy(&comm));
 }
 
+// transform.hpp:92-103 rule generators + bind_storage (interp.cpp:554-562): names, buffer
+// names and array sizes equal the reference's (golden.npz "rules/example_c2_k2").
+TEST_CASE("rule generators and bind_storage") {
+  const TensorStorage csr = build_csr(example_m());
+  const std::vector<std::string> want = {
+      "hyb_p0_b0|A_hyb_p0_b0|hyb_hyb_p0_b0_I_indices:1,hyb_hyb_p0_b0_I_indptr:2,hyb_hyb_p0_b0_J_indices:1",
+      "hyb_p0_b1|A_hyb_p0_b1|hyb_hyb_p0_b1_I_indices:1,hyb_hyb_p0_b1_I_indptr:2,hyb_hyb_p0_b1_J_indices:2",
+      "hyb_p0_b2|A_hyb_p0_b2|hyb_hyb_p0_b2_I_indices:0,hyb_hyb_p0_b2_I_indptr:2,hyb_hyb_p0_b2_J_indices:0",
+      "hyb_p1_b0|A_hyb_p1_b0|hyb_hyb_p1_b0_I_indices:2,hyb_hyb_p1_b0_I_indptr:2,hyb_hyb_p1_b0_J_indices:2",
+      "hyb_p1_b1|A_hyb_p1_b1|hyb_hyb_p1_b1_I_indices:1,hyb_hyb_p1_b1_I_indptr:2,hyb_hyb_p1_b1_J_indices:2",
+      "hyb_p1_b2|A_hyb_p1_b2|hyb_hyb_p1_b2_I_indices:0,hyb_hyb_p1_b2_I_indptr:2,hyb_hyb_p1_b2_J_indices:0"};
+  const auto rules = hyb_rules(csr, 2, 2, "hyb");
+  REQUIRE(rules.size() == want.size());
+  for (size_t i = 0; i < rules.size(); ++i) {
+    std::string got = rules[i].name + "|" + rules[i].new_buffer + "|";
+    bool first = true;
+    for (const auto& [key, arr] : rules[i].storage.aux) {  // std::map: sorted like the golden
+      got += (first ? "" : ",") + key + ":" + std::to_string(arr.size());
+      first = false;
+    }
+    CHECK(got == want[i]);
+  }
+  const FormatRewriteRule b = bsr_rule(csr, 2);
+  CHECK(b.name == "bsr" && b.new_buffer == "A_bsr" && b.storage.kind == FormatKind::Bsr);
+  CHECK(b.storage.aux.count("bsr_JO_indptr") == 1 && b.storage.aux.count("bsr_JO_indices") == 1);
+  CHECK(b.storage.arr("bsr_JO_indptr") == csr_to_bsr(csr, 2, "x_").arr("x_JO_indptr"));
+  const FormatRewriteRule e = ell_rule(csr, 4);
+  CHECK(e.new_buffer == "A_ell" && e.storage.aux.count("ell_J_indices") == 1);
+  CHECK(e.storage.values.size() == 16);
+  const FormatRewriteRule id = identity_rule(csr);
+  CHECK(id.new_buffer == "A_csr" && id.storage.arr("csr_J_indptr") == csr.arr("J_indptr"));
+  CHECK(id.storage.arr("csr_J_indices") == csr.arr("J_indices") && id.storage.values == csr.values);
+  Bindings bb;
+  bind_storage(bb, "A_bsr", b.storage);
+  CHECK(bb.buffers.at("A_bsr").dtype == DType::F32 && bb.buffers.at("A_bsr").f32 == b.storage.values);
+  CHECK(bb.buffers.at("bsr_JO_indices").dtype == DType::I32 &&
+        bb.buffers.at("bsr_JO_indices").i32 == b.storage.arr("bsr_JO_indices"));
+}
+
 int main() {
   int failed_cases = 0;
   for (auto& c : cases()) {
