@@ -91,13 +91,14 @@ struct DenseMatrix {
   double at(int64_t i, int64_t j) const { return v[i * cols + j]; }
 };
 
-enum class FormatKind { Csr, Bsr, Ell, EllBucket };
+enum class FormatKind { Csr, Bsr, Ell, Dbsr, SrBcrs, EllBucket };  // storage.hpp:66
 
 struct TensorStorage {
   FormatKind kind = FormatKind::Csr;
   std::map<std::string, IntArray> aux;
   std::vector<float> values;
   int64_t rows = 0, cols = 0, nnz = 0, pad_slots = 0, block = 1, width = 0;
+  int64_t group = 1;  // SR-BCRS: tiles per group (g); block = tile height (t)
   const IntArray& arr(const std::string& name) const {
     auto it = aux.find(name);
     if (it == aux.end()) fail(ErrKind::Lookup, "storage has no aux array: " + name);
@@ -324,6 +325,31 @@ void for_each_stored_cell(const TensorStorage& s, F&& fn) {
               fn(br * b + ii, ix[p] * b + ji, double{s.values[(p * b + ii) * b + ji]});
       break;
     }
+    case FormatKind::Dbsr: {  // stored block rows only (IO_indices)
+      const int64_t b = s.block;
+      const IntArray& rmap = detail::need_suffix(s, "IO_indices");
+      const IntArray& jp = detail::need_suffix(s, "JO_indptr");
+      const IntArray& jx = detail::need_suffix(s, "JO_indices");
+      for (size_t r = 0; r < rmap.size(); ++r)
+        for (int32_t p = jp[r]; p < jp[r + 1]; ++p)
+          for (int64_t ii = 0; ii < b; ++ii)
+            for (int64_t ji = 0; ji < b; ++ji)
+              fn(rmap[r] * b + ii, jx[p] * b + ji, double{s.values[(p * b + ii) * b + ji]});
+      break;
+    }
+    case FormatKind::SrBcrs: {  // tile rows of t rows, groups of g column tiles, tail padded
+      const int64_t t = s.block, g = s.group;
+      const IntArray& gp = detail::need_suffix(s, "G_indptr");
+      const IntArray& jx = detail::need_suffix(s, "JT_indices");
+      for (int64_t r = 0; r < s.rows / t; ++r)
+        for (int32_t q = gp[r]; q < gp[r + 1]; ++q)
+          for (int64_t sl = 0; sl < g; ++sl) {
+            const int64_t tile = q * g + sl;
+            if (tile > int64_t{gp[r]} * g && jx[tile] == jx[tile - 1]) continue;  // padding tile
+            for (int64_t e = 0; e < t; ++e) fn(r * t + e, int64_t{jx[tile]}, double{s.values[tile * t + e]});
+          }
+      break;
+    }
     case FormatKind::Ell:
     case FormatKind::EllBucket: {
       const IntArray& jx = detail::need_suffix(s, "J_indices");
@@ -410,6 +436,35 @@ inline std::vector<std::string> validate_storage(const TensorStorage& s) {
       check_segments("JO", ix, s.block > 0 ? s.cols / s.block : 0, segs, false);
       if (static_cast<int64_t>(s.values.size()) != static_cast<int64_t>(ix.size()) * s.block * s.block)
         out.push_back("JO: values size != blocks * b * b");
+      break;
+    }
+    case FormatKind::Dbsr: {
+      const int64_t b = s.block > 0 ? s.block : 1;
+      const IntArray& rmap = detail::need_suffix(s, "IO_indices");
+      if (const IntArray* ip = detail::find_suffix(s, "IO_indptr"))
+        check_indptr("IO", *ip, static_cast<int64_t>(rmap.size()));
+      check_segments("IO", rmap, s.rows / b, {{0, static_cast<int64_t>(rmap.size())}}, false);
+      const IntArray& ip = detail::need_suffix(s, "JO_indptr");
+      const IntArray& ix = detail::need_suffix(s, "JO_indices");
+      check_indptr("JO", ip, static_cast<int64_t>(ix.size()));
+      if (ip.size() != rmap.size() + 1) out.push_back("JO: indptr length != stored rows + 1");
+      for (size_t i = 0; i + 1 < ip.size(); ++i) segs.emplace_back(ip[i], std::min<int64_t>(ip[i + 1], ix.size()));
+      check_segments("JO", ix, s.cols / b, segs, false);
+      if (static_cast<int64_t>(s.values.size()) != static_cast<int64_t>(ix.size()) * b * b)
+        out.push_back("JO: values size != blocks * b * b");
+      break;
+    }
+    case FormatKind::SrBcrs: {
+      const int64_t t = s.block > 0 ? s.block : 1, g = s.group > 0 ? s.group : 1;
+      const IntArray& gp = detail::need_suffix(s, "G_indptr");
+      const IntArray& jx = detail::need_suffix(s, "JT_indices");
+      check_indptr("G", gp, static_cast<int64_t>(jx.size()) / g);
+      if (static_cast<int64_t>(gp.size()) != s.rows / t + 1) out.push_back("G: indptr length != tile rows + 1");
+      for (size_t i = 0; i + 1 < gp.size(); ++i)
+        segs.emplace_back(int64_t{gp[i]} * g, std::min<int64_t>(int64_t{gp[i + 1]} * g, jx.size()));
+      check_segments("JT", jx, s.cols, segs, true);
+      if (static_cast<int64_t>(s.values.size()) != static_cast<int64_t>(jx.size()) * t)
+        out.push_back("JT: values size != tiles * t");
       break;
     }
     case FormatKind::Ell:
@@ -504,6 +559,68 @@ inline TensorStorage csr_to_ell(const TensorStorage& csr, int64_t w, const std::
   t.aux[prefix + "J_indices"] = std::move(jj);
   t.values = std::move(vv);
   return t;
+}
+
+// csr_to_dbsr (storage.cpp:336-370): the BSR plus its stored block rows, on the device.
+inline TensorStorage csr_to_dbsr(const TensorStorage& csr, int64_t b, const std::string& prefix = "") {
+  if (b < 1) fail(ErrKind::Usage, "block size must be >= 1");
+  DeviceCsr d(csr);
+  strata_dbsr* h = nullptr;
+  check(strata_dbsr_from_csr(d.indptr.data(), d.indices.data(), d.values.data(), csr.rows, csr.cols,
+                             csr.nnz, b, nullptr, &h));
+  std::unique_ptr<strata_dbsr, int (*)(strata_dbsr*)> hold(h, strata_dbsr_destroy);
+  int64_t mb = 0, nb = 0, bb = 0, nstored = 0, nblocks = 0, pad = 0;
+  check(strata_dbsr_info(h, &mb, &nb, &bb, &nstored, &nblocks, &pad));
+  IntArray io(std::max<int64_t>(nstored, 1)), jp(nstored + 1), jx(std::max<int64_t>(nblocks, 1));
+  std::vector<float> v(std::max<int64_t>(nblocks * b * b, 1));
+  check(strata_dbsr_read(h, io.data(), jp.data(), jx.data(), v.data()));
+  io.resize(nstored);
+  jx.resize(nblocks);
+  v.resize(nblocks * b * b);
+  TensorStorage t;
+  t.kind = FormatKind::Dbsr;
+  t.rows = mb * b;
+  t.cols = nb * b;
+  t.nnz = csr.nnz;
+  t.block = b;
+  t.pad_slots = pad;
+  t.aux[prefix + "IO_indptr"] = {0, static_cast<int32_t>(nstored)};
+  t.aux[prefix + "IO_indices"] = std::move(io);
+  t.aux[prefix + "JO_indptr"] = std::move(jp);
+  t.aux[prefix + "JO_indices"] = std::move(jx);
+  t.values = std::move(v);
+  return t;
+}
+
+// csr_to_srbcrs (storage.cpp:372-440): t-row tiles, distinct columns grouped by g (the last
+// group padded with its last column), values slot-major [groups * g][t], on the device.
+inline TensorStorage csr_to_srbcrs(const TensorStorage& csr, int64_t t, int64_t g,
+                                   const std::string& prefix = "") {
+  if (t < 1 || g < 1) fail(ErrKind::Usage, "SR-BCRS requires t >= 1 and g >= 1");
+  DeviceCsr d(csr);
+  strata_srbcrs* h = nullptr;
+  check(strata_srbcrs_from_csr(d.indptr.data(), d.indices.data(), d.values.data(), csr.rows,
+                               csr.cols, csr.nnz, t, g, nullptr, &h));
+  std::unique_ptr<strata_srbcrs, int (*)(strata_srbcrs*)> hold(h, strata_srbcrs_destroy);
+  int64_t mb = 0, tt = 0, gg = 0, groups = 0, pad = 0;
+  check(strata_srbcrs_info(h, &mb, &tt, &gg, &groups, &pad));
+  IntArray gp(mb + 1), jx(std::max<int64_t>(groups * g, 1));
+  std::vector<float> v(std::max<int64_t>(groups * g * t, 1));
+  check(strata_srbcrs_read(h, gp.data(), jx.data(), v.data()));
+  jx.resize(groups * g);
+  v.resize(groups * g * t);
+  TensorStorage s;
+  s.kind = FormatKind::SrBcrs;
+  s.rows = mb * t;
+  s.cols = csr.cols;
+  s.nnz = csr.nnz;
+  s.block = t;
+  s.group = g;
+  s.pad_slots = pad;
+  s.aux[prefix + "G_indptr"] = std::move(gp);
+  s.aux[prefix + "JT_indices"] = std::move(jx);
+  s.values = std::move(v);
+  return s;
 }
 
 // generate_matrix (driver.cpp:365-416): identical graph, as triplets in CSR order.
@@ -1133,7 +1250,7 @@ inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m_in, int64_
     int64_t mb = 0, nb = 0, b = 0, nstored = 0, nblocks = 0, pad = 0;
     check(strata_dbsr_info(h, &mb, &nb, &b, &nstored, &nblocks, &pad));
     plan->work_slots = nblocks * b * b;
-    FormatRewriteRule* r = rule("dbsr", FormatKind::Bsr);
+    FormatRewriteRule* r = rule("dbsr", FormatKind::Dbsr);
     r->storage.block = fmt.b;
     r->storage.nnz = csr.nnz;
     r->storage.pad_slots = pad;
@@ -1147,7 +1264,7 @@ inline Pipeline build_matrix_pipeline(KernelOp op, const CooMatrix& m_in, int64_
     int64_t mb = 0, t = 0, g = 0, ngroups = 0, pad = 0;
     check(strata_srbcrs_info(h, &mb, &t, &g, &ngroups, &pad));
     plan->work_slots = ngroups * t * g;
-    FormatRewriteRule* r = rule("srbcrs", FormatKind::Bsr);
+    FormatRewriteRule* r = rule("srbcrs", FormatKind::SrBcrs);
     r->storage.nnz = csr.nnz;
     r->storage.pad_slots = pad;
   } else if (fmt.kind == "ell") {

@@ -589,6 +589,91 @@ TEST_CASE("sharded SpMM / SDDMM through the C ABI with an NCCL communicator (wor
   check(strata_nccl_comm_destroy(&comm));
 }
 
+// test_storage.cpp:156-237: DBSR / SR-BCRS builders (device conversion, host read-back).
+TEST_CASE("csr_to_dbsr keeps only non-empty block rows") {  // :156-165
+  CooMatrix m;
+  m.rows = m.cols = 6;
+  m.triplets = {{0, 0, 1}, {4, 2, 2}};
+  TensorStorage dbsr = csr_to_dbsr(build_csr(m), 2);
+  CHECK(dbsr.arr("IO_indices") == IntArray{0, 2});
+  CHECK(validate_storage(dbsr).empty());
+  CHECK(reconstruct_dense(dbsr).v == dense_from_coo(m).v);
+}
+
+TEST_CASE("csr_to_dbsr equals bsr reconstruction when no row is empty") {  // :167-172
+  std::mt19937 rng(7);
+  CooMatrix m = random_coo(rng, 8, 8, 0.6);
+  TensorStorage csr = build_csr(m);
+  CHECK(reconstruct_dense(csr_to_dbsr(csr, 2)).v == reconstruct_dense(csr_to_bsr(csr, 2)).v);
+}
+
+TEST_CASE("csr_to_dbsr of a zero matrix stores nothing") {  // :174-179
+  CooMatrix m;
+  m.rows = m.cols = 4;
+  TensorStorage dbsr = csr_to_dbsr(build_csr(m), 2);
+  CHECK(dbsr.arr("IO_indices").empty());
+}
+
+TEST_CASE("csr_to_srbcrs single full column tile") {  // :181-191
+  CooMatrix m;
+  m.rows = 2;
+  m.cols = 3;
+  m.triplets = {{0, 1, 1}, {1, 1, 2}};
+  TensorStorage s = csr_to_srbcrs(build_csr(m), 2, 1);
+  CHECK(s.arr("G_indptr") == IntArray{0, 1});
+  CHECK(s.arr("JT_indices") == IntArray{1});
+  CHECK(s.values.size() == 2);
+  CHECK(padding_ratio(s) == 0.0);
+}
+
+TEST_CASE("csr_to_srbcrs groups tiles and pads the tail") {  // :193-204
+  CooMatrix m;
+  m.rows = 2;
+  m.cols = 8;
+  m.triplets = {{0, 1, 1}, {0, 4, 2}, {1, 6, 3}};
+  TensorStorage s = csr_to_srbcrs(build_csr(m), 2, 2);
+  CHECK(s.arr("G_indptr") == IntArray{0, 2});
+  CHECK(s.values.size() == 2 * 2 * 2);
+  CHECK(s.pad_slots == 8 - 3);
+  CHECK(reconstruct_dense(s).v == dense_from_coo(m).v);
+  CHECK(validate_storage(s).empty());
+}
+
+TEST_CASE("srbcrs reconstruction pads rows to a multiple of t") {  // :206-215
+  TensorStorage s = csr_to_srbcrs(build_csr(example_m()), 3, 2);
+  DenseMatrix d = reconstruct_dense(s);
+  CHECK(d.rows == 6);
+  DenseMatrix orig = dense_from_coo(example_m());
+  for (int64_t i = 0; i < 4; ++i)
+    for (int64_t j = 0; j < 4; ++j) CHECK(d.at(i, j) == orig.at(i, j));
+  for (int64_t i = 4; i < 6; ++i)
+    for (int64_t j = 0; j < 4; ++j) CHECK(d.at(i, j) == 0.0);
+}
+
+TEST_CASE("round trip: DBSR and SR-BCRS reconstruct random matrices exactly") {  // :217-237
+  std::mt19937 rng(42);
+  for (int trial = 0; trial < 40; ++trial) {
+    const int64_t rows = 1 + static_cast<int64_t>(rng() % 64);
+    const int64_t cols = 1 + static_cast<int64_t>(rng() % 64);
+    CooMatrix m = random_coo(rng, rows, cols, 0.25);
+    const DenseMatrix want = dense_from_coo(m);
+    TensorStorage csr = build_csr(m);
+    auto check_padded = [&](const DenseMatrix& got) {
+      for (int64_t i = 0; i < got.rows; ++i)
+        for (int64_t j = 0; j < got.cols; ++j) {
+          const double expect = (i < rows && j < cols) ? want.at(i, j) : 0.0;
+          if (got.at(i, j) != expect) return false;
+        }
+      return got.rows >= rows && got.cols >= cols;
+    };
+    const TensorStorage dbsr = csr_to_dbsr(csr, 3), sr = csr_to_srbcrs(csr, 2, 2);
+    CHECK(check_padded(reconstruct_dense(dbsr)));
+    CHECK(check_padded(reconstruct_dense(sr)));
+    CHECK(validate_storage(dbsr).empty());
+    CHECK(validate_storage(sr).empty());
+  }
+}
+
 // transform.hpp:92-103 rule generators + bind_storage (interp.cpp:554-562): names, buffer
 // names and array sizes equal the reference's (golden.npz "rules/example_c2_k2").
 TEST_CASE("rule generators and bind_storage") {
