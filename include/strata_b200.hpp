@@ -93,6 +93,18 @@ struct DenseMatrix {
 
 enum class FormatKind { Csr, Bsr, Ell, Dbsr, SrBcrs, EllBucket };  // storage.hpp:66
 
+inline const char* format_kind_name(FormatKind k) {  // storage.cpp:16-26
+  switch (k) {
+    case FormatKind::Csr: return "csr";
+    case FormatKind::Bsr: return "bsr";
+    case FormatKind::Ell: return "ell";
+    case FormatKind::Dbsr: return "dbsr";
+    case FormatKind::SrBcrs: return "srbcrs";
+    case FormatKind::EllBucket: return "ell_bucket";
+  }
+  return "?";
+}
+
 struct TensorStorage {
   FormatKind kind = FormatKind::Csr;
   std::map<std::string, IntArray> aux;
@@ -283,6 +295,33 @@ inline double padding_ratio(const HybDecomposition& h) { return h.padding_ratio;
 inline double padding_ratio(const TensorStorage& s) {
   if (s.kind == FormatKind::Csr) fail(ErrKind::Usage, "padding ratio not applicable to CSR storage");
   return s.values.empty() ? 0.0 : static_cast<double>(s.pad_slots) / static_cast<double>(s.values.size());
+}
+
+// csr_to_coo (storage.cpp:126-136): the CSR's entries as triplets in row-major order.
+inline CooMatrix csr_to_coo(const TensorStorage& s) {
+  if (s.kind != FormatKind::Csr) fail(ErrKind::Usage, "csr_to_coo needs CSR storage");
+  const IntArray* ip = nullptr;
+  const IntArray* ix = nullptr;
+  for (const auto& kv : s.aux) {  // the CSR's arrays under any prefix
+    const std::string& k = kv.first;
+    if (k.size() >= 8 && k.compare(k.size() - 8, 8, "J_indptr") == 0) ip = &kv.second;
+    if (k.size() >= 9 && k.compare(k.size() - 9, 9, "J_indices") == 0) ix = &kv.second;
+  }
+  if (!ip || !ix) fail(ErrKind::Lookup, "storage has no aux array: J_indptr / J_indices");
+  CooMatrix m;
+  m.rows = s.rows;
+  m.cols = s.cols;
+  for (int64_t i = 0; i < s.rows; ++i)
+    for (int32_t p = (*ip)[i]; p < (*ip)[i + 1]; ++p)
+      m.triplets.push_back({i, int64_t{(*ix)[p]}, double{s.values[p]}});
+  return m;
+}
+
+// dense_from_coo (storage.cpp:449-453): duplicates add up.
+inline DenseMatrix dense_from_coo(const CooMatrix& m) {
+  DenseMatrix d(m.rows, m.cols);
+  for (const auto& t : m.triplets) d.at(t.row, t.col) += t.value;
+  return d;
 }
 
 // ---- invariants / accounting (storage.cpp:455-630), host-side on read-back storage ---------
@@ -924,6 +963,70 @@ inline void bind_storage(Bindings& b, const std::string& buffer_name, const Tens
   v.dtype = DType::F32;
   v.f32 = s.values;
   b.buffers[buffer_name] = std::move(v);
+}
+
+// ---- RelSparse (kernels.hpp:33-43, kernels.cpp:19-83): the RGMS operand -------------------
+// Relation-major: I_indptr[R+1] over the rows active in each relation, I_indices those rows,
+// J_indptr / J_indices their neighbours (ascending columns), values in the same order.
+struct RelSparse {
+  int64_t relations = 0, rows = 0, cols = 0, nnz = 0;
+  std::map<std::string, IntArray> aux;
+  TensorData values;
+};
+
+inline RelSparse build_rel_sparse(const std::vector<CooMatrix>& per_relation, DType dtype) {
+  if (per_relation.empty()) fail(ErrKind::Usage, "need at least one relation");
+  RelSparse r;
+  r.relations = static_cast<int64_t>(per_relation.size());
+  r.rows = per_relation[0].rows;
+  r.cols = per_relation[0].cols;
+  IntArray i_indptr = {0}, i_indices, j_indptr = {0}, j_indices;
+  std::vector<double> vals;
+  for (const auto& m : per_relation) {
+    if (m.rows != r.rows || m.cols != r.cols) fail(ErrKind::Usage, "all relations must share dims");
+    std::vector<Triplet> t = m.triplets;
+    std::sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
+      return a.row != b.row ? a.row < b.row : a.col < b.col;
+    });
+    for (size_t q = 0; q < t.size();) {
+      const int64_t row = t[q].row;
+      i_indices.push_back(static_cast<int32_t>(row));
+      for (; q < t.size() && t[q].row == row; ++q) {
+        j_indices.push_back(static_cast<int32_t>(t[q].col));
+        vals.push_back(t[q].value);
+      }
+      j_indptr.push_back(static_cast<int32_t>(j_indices.size()));
+    }
+    i_indptr.push_back(static_cast<int32_t>(i_indices.size()));
+  }
+  r.nnz = static_cast<int64_t>(vals.size());
+  r.aux["I_indptr"] = std::move(i_indptr);
+  r.aux["I_indices"] = std::move(i_indices);
+  r.aux["J_indptr"] = std::move(j_indptr);
+  r.aux["J_indices"] = std::move(j_indices);
+  r.values = TensorData::of(vals, dtype);
+  return r;
+}
+
+inline void bind_rel_sparse(Bindings& b, const std::string& buffer_name, const RelSparse& r) {
+  for (const auto& [key, arr] : r.aux) {
+    TensorData d;
+    d.dtype = DType::I32;
+    d.i32 = arr;
+    b.buffers[key] = std::move(d);
+  }
+  b.buffers[buffer_name] = r.values;
+}
+
+inline DenseMatrix relation_dense(const RelSparse& r, int64_t rel) {
+  DenseMatrix d(r.rows, r.cols);
+  const IntArray& ip = r.aux.at("I_indptr");
+  const IntArray& ii = r.aux.at("I_indices");
+  const IntArray& jp = r.aux.at("J_indptr");
+  const IntArray& ji = r.aux.at("J_indices");
+  for (int32_t q = ip[rel]; q < ip[rel + 1]; ++q)
+    for (int32_t e = jp[q]; e < jp[q + 1]; ++e) d.at(ii[q], ji[e]) += r.values.get(e);
+  return d;
 }
 
 enum class Stage { I, II, III };

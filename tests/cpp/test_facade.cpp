@@ -72,12 +72,6 @@ CooMatrix random_coo(std::mt19937& rng, int64_t rows, int64_t cols, double densi
   return m;
 }
 
-DenseMatrix dense_from_coo(const CooMatrix& m) {
-  DenseMatrix d(m.rows, m.cols);
-  for (const auto& t : m.triplets) d.at(t.row, t.col) += t.value;
-  return d;
-}
-
 DenseMatrix random_dense(std::mt19937& rng, int64_t r, int64_t c) {
   DenseMatrix d(r, c);
   std::uniform_int_distribution<int> val(-4, 4);
@@ -672,6 +666,34 @@ TEST_CASE("round trip: DBSR and SR-BCRS reconstruct random matrices exactly") { 
     CHECK(validate_storage(dbsr).empty());
     CHECK(validate_storage(sr).empty());
   }
+}
+
+// storage.cpp:16-26 / :126-136, kernels.cpp:19-83 host helpers.
+TEST_CASE("format names, csr_to_coo, RelSparse") {
+  CHECK(std::string(format_kind_name(FormatKind::EllBucket)) == "ell_bucket");
+  CHECK(std::string(format_kind_name(FormatKind::SrBcrs)) == "srbcrs");
+  const CooMatrix m = example_m();
+  const CooMatrix back = csr_to_coo(build_csr(m));
+  CHECK(dense_from_coo(back).v == dense_from_coo(m).v && back.triplets.size() == m.triplets.size());
+  // two relations of the 4 x 4 example: the reference's relation-major layout
+  CooMatrix r0, r1;
+  r0.rows = r1.rows = r0.cols = r1.cols = 4;
+  r0.triplets = {{2, 3, 7}, {0, 2, 2}, {2, 0, 4}};
+  r1.triplets = {{1, 3, 3}, {0, 0, 1}};
+  const RelSparse rs = build_rel_sparse({r0, r1}, DType::F32);
+  CHECK(rs.aux.at("I_indptr") == IntArray({0, 2, 4}));
+  CHECK(rs.aux.at("I_indices") == IntArray({0, 2, 0, 1}));
+  CHECK(rs.aux.at("J_indptr") == IntArray({0, 1, 3, 4, 5}));
+  CHECK(rs.aux.at("J_indices") == IntArray({2, 0, 3, 0, 3}));
+  CHECK(rs.values.dtype == DType::F32 && rs.values.f32 == std::vector<float>({2, 4, 7, 1, 3}));
+  CHECK(relation_dense(rs, 0).v == dense_from_coo(r0).v);
+  CHECK(relation_dense(rs, 1).v == dense_from_coo(r1).v);
+  Bindings b;
+  bind_rel_sparse(b, "A", rs);
+  CHECK(b.buffers.at("A").f32 == rs.values.f32 && b.buffers.at("J_indices").i32 == rs.aux.at("J_indices"));
+  CooMatrix bad = r1;
+  bad.rows = 5;
+  CHECK_THROWS_KIND(build_rel_sparse({r0, bad}, DType::F32), ErrKind::Usage, "share dims");
 }
 
 // transform.hpp:92-103 rule generators + bind_storage (interp.cpp:554-562): names, buffer
