@@ -950,6 +950,39 @@ inline std::vector<FormatRewriteRule> hyb_rules(const TensorStorage& csr, int c,
   return rules;
 }
 
+// verify_coverage (transform.hpp:85-90, transform.cpp:396-426): every original non-zero is
+// claimed by exactly one rule and the rule storages add up to the original (toy sizes: dense).
+inline std::vector<std::string> verify_coverage(const TensorStorage& original,
+                                                const std::vector<FormatRewriteRule>& rules) {
+  std::vector<std::string> out;
+  const DenseMatrix orig = reconstruct_dense(original);
+  DenseMatrix sum(orig.rows, orig.cols);
+  std::vector<int> claims(static_cast<size_t>(orig.rows * orig.cols), 0);
+  for (const auto& rule : rules) {
+    for_each_stored_cell(rule.storage, [&](int64_t i, int64_t j, double v) {
+      if (i < orig.rows && j < orig.cols) {
+        sum.at(i, j) += v;
+        claims[i * orig.cols + j] += 1;
+      } else if (v != 0.0) {
+        out.push_back(rule.name + ": non-zero value in padding region");
+      }
+    });
+  }
+  for (int64_t i = 0; i < orig.rows; ++i)
+    for (int64_t j = 0; j < orig.cols; ++j) {
+      if (sum.at(i, j) != orig.at(i, j)) {
+        out.push_back("value mismatch at (" + std::to_string(i) + ", " + std::to_string(j) + ")");
+        return out;
+      }
+      if (orig.at(i, j) != 0.0 && claims[i * orig.cols + j] != 1) {
+        out.push_back("non-zero (" + std::to_string(i) + ", " + std::to_string(j) + ") claimed by " +
+                      std::to_string(claims[i * orig.cols + j]) + " rules");
+        return out;
+      }
+    }
+  return out;
+}
+
 // bind_storage (interp.hpp:63, interp.cpp:554-562): aux arrays as I32 buffers under their own
 // names, the values under buffer_name.
 inline void bind_storage(Bindings& b, const std::string& buffer_name, const TensorStorage& s) {

@@ -728,6 +728,14 @@ TEST_CASE("rule generators and bind_storage") {
   const FormatRewriteRule id = identity_rule(csr);
   CHECK(id.new_buffer == "A_csr" && id.storage.arr("csr_J_indptr") == csr.arr("J_indptr"));
   CHECK(id.storage.arr("csr_J_indices") == csr.arr("J_indices") && id.storage.values == csr.values);
+  // verify_coverage (transform.cpp:396-426): hyb / bsr / ell / identity rules each cover
+  // the matrix exactly; two copies of a rule claim every non-zero twice
+  CHECK(verify_coverage(csr, rules).empty());
+  CHECK(verify_coverage(csr, {b}).empty());
+  CHECK(verify_coverage(csr, {e}).empty());
+  CHECK(verify_coverage(csr, {id}).empty());
+  const auto twice = verify_coverage(csr, {id, id});
+  CHECK(twice.size() == 1 && twice[0].find("value mismatch") == 0);
   Bindings bb;
   bind_storage(bb, "A_bsr", b.storage);
   CHECK(bb.buffers.at("A_bsr").dtype == DType::F32 && bb.buffers.at("A_bsr").f32 == b.storage.values);
