@@ -1,6 +1,10 @@
-REF=1 bash tools/gpu_round.sh
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/launches_bench.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra > gpurun_out/ncu_bench.log 2>&1
-WORKLOADS="reddit_spmm" bash tools/gpu_prof.sh > /dev/null 2>&1
-SAN_ONLY="hyb sddmm" bash tools/gpu_sanitize.sh > /dev/null 2>&1
-ls gpurun_out
+for i in 1 2; do
+python tools/ab_spmm.py
+for v in ab/*/; do STRATA_B200_LIB=$v/libstrata_b200.so python tools/ab_spmm.py; done
+done > gpurun_out/ab.jsonl 2>&1
+python - <<'P'
+import json
+for l in open('gpurun_out/ab.jsonl'):
+    if l.startswith('{'):
+        d=json.loads(l); print(d['lib'], d['C5_spmm_ms'], d['C2_spmm_ms'], d['C1_spmm_ms'], d['C2_sddmm_ms'])
+P
