@@ -608,6 +608,16 @@ TEST_CASE("csr_to_dbsr of a zero matrix stores nothing") {  // :174-179
   CHECK(dbsr.arr("IO_indices").empty());
 }
 
+TEST_CASE("csr_to_srbcrs of a zero matrix stores nothing") {
+  CooMatrix m;
+  m.rows = m.cols = 4;
+  TensorStorage s = csr_to_srbcrs(build_csr(m), 2, 2);
+  CHECK(s.arr("G_indptr") == IntArray({0, 0, 0}));
+  CHECK(s.arr("JT_indices").empty() && s.values.empty());
+  CHECK(validate_storage(s).empty());
+  CHECK(padding_ratio(s) == 0.0);
+}
+
 TEST_CASE("csr_to_srbcrs single full column tile") {  // :181-191
   CooMatrix m;
   m.rows = 2;
